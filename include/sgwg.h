@@ -1,0 +1,231 @@
+/*
+ * sgwg.h -- C ABI of the B200-native sparse-grid WENO5 hot path.
+ *
+ * The reference (`sgweno`, header-only C++20, /root/reference/proj/include/sgweno)
+ * has no FFI: its operator boundary is the duck-typed Model concept consumed by
+ * `evolve_family` plus the free functions `make_family`, `initialize_family`,
+ * `prolong` and `combine`.  A GPU backend has to replace the whole
+ * evolve + combine pipeline (a per-member, per-stage host `rhs` callback would
+ * force a host<->device copy per stage), so this ABI exports exactly the
+ * entry points a maintainer would bind to replace those calls.  Each function
+ * cites the reference interface it replaces (paths relative to
+ * proj/include/sgweno/).  Plain C types only: no torch, no C++.
+ *
+ * Conventions
+ *   - Member order is the reference's: levels sorted lexicographically
+ *     (grid.hpp:57-79, combine.hpp:71-72).  Member states are packed one after
+ *     another in that order, each row-major with dimension 0 slowest
+ *     (grid.hpp:102-108).  This is also the device layout.
+ *   - Every function returns SGWG_OK (0) or a nonzero status; the message of
+ *     the last failure on the calling thread is sgwg_last_error().  There is no
+ *     CPU fallback: without a usable sm_100 device sgwg_init fails.
+ */
+#ifndef SGWG_H
+#define SGWG_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGWG_MAXD 4
+
+/* status codes (errors of the reference map as noted) */
+enum {
+  SGWG_OK = 0,
+  SGWG_EINVAL = 1,     /* std::invalid_argument / std::out_of_range            */
+  SGWG_ENONFINITE = 2, /* FamilyIntegratorFailure{level,step,stage}, timestep.hpp:31-40 */
+  SGWG_ECUDA = 3,      /* CUDA runtime error (no device, OOM, launch failure)   */
+  SGWG_ENCCL = 4,      /* NCCL error in a sharded family                       */
+  SGWG_EUNSUPPORTED = 5
+};
+
+/* grid.hpp:14 BoundaryKind */
+enum { SGWG_PERIODIC = 0, SGWG_ZERO = 1 };
+/* models.hpp:19 ModelKind (+ the Vlasov-Poisson model of BASELINE C4/C5) */
+enum { SGWG_ADVECTION = 0, SGWG_BURGERS = 1, SGWG_VLASOV_BOLTZMANN = 2, SGWG_VLASOV_POISSON = 3 };
+/* weno.hpp:17 WenoMode */
+enum { SGWG_WENO_NONLINEAR = 0, SGWG_WENO_LINEAR = 1 };
+/* interp.hpp:16 InterpMode */
+enum { SGWG_INTERP_LAGRANGE = 0, SGWG_INTERP_WENO = 1 };
+/* timestep.hpp:15 DtMode */
+enum { SGWG_DT_CFL = 0, SGWG_DT_ACCURACY = 1 };
+/* arithmetic of the device kernels */
+enum {
+  SGWG_ARITH_EXACT = 0, /* reference expression order, no FMA contraction, IEEE divides:
+                           bitwise equal to the reference built without FMA */
+  SGWG_ARITH_FAST = 1   /* FMA contraction, one divide per reconstruction, reciprocal
+                           spacings: within 1e-10 of the reference */
+};
+
+/* DomainBox + root cells + boundaries + N_L: the arguments of make_family
+ * (combine.hpp:69-70, grid.hpp:17-37). */
+typedef struct {
+  int d;                      /* 1..4 */
+  int nl;                     /* finest level N_L (>= d-1) */
+  double lower[SGWG_MAXD];
+  double upper[SGWG_MAXD];
+  int root_cells[SGWG_MAXD];
+  int bc[SGWG_MAXD];          /* SGWG_PERIODIC / SGWG_ZERO */
+} sgwg_domain;
+
+/* ProblemSpec's physics (models.hpp:23-41, 568-580) + WenoParams (weno.hpp:19-22). */
+typedef struct {
+  int kind;                   /* SGWG_ADVECTION ... */
+  int weno_mode;              /* SGWG_WENO_NONLINEAR / LINEAR */
+  double epsilon;             /* WENO epsilon, reference default 1e-6 (weno.hpp:20) */
+  double speeds[SGWG_MAXD];   /* advection speeds a_k (models.hpp:25) */
+  int space_dim;              /* kinetic models: phase space has 2*space_dim dims */
+  double theta, tau;          /* Vlasov-Boltzmann relaxation (models.hpp:37-41) */
+} sgwg_model;
+
+/* StepPolicy (timestep.hpp:17-21) + the accuracy-mode multiplier that BASELINE
+ * C1 needs (dt = 0.5 h^{5/3}).  dt_scale = 1 is the reference rule. */
+typedef struct {
+  int mode;                   /* SGWG_DT_CFL / SGWG_DT_ACCURACY */
+  double cfl;                 /* cfl_number */
+  double reference_spacing;   /* minimum spacing of the finest grid */
+  double dt_scale;
+} sgwg_policy;
+
+/* FamilyIntegratorFailure (timestep.hpp:31-40): member index (sorted order),
+ * step index and RK stage (1..3) of the first non-finite tendency. */
+typedef struct {
+  int member;
+  long long step;
+  int stage;
+} sgwg_failure;
+
+/* Device-timed statistics of the last sgwg_evolve / sgwg_combine. */
+typedef struct {
+  double evolve_ms;           /* CUDA-event time of the whole evolve (all stops, no combines) */
+  double combine_ms;          /* CUDA-event time of the last combine */
+  long long steps;            /* RK steps taken */
+  long long kernel_launches;  /* device kernels launched by the last evolve (incl. early-exit) */
+  long long combine_launches; /* device kernels launched by the last combine */
+  double pass_ms_sum;         /* profile mode: summed event time of the WENO pass kernels */
+  long long pass_launches;    /* profile mode: number of timed WENO pass launches */
+  double pass_flops;          /* algorithmic flops of those launches (SURVEY 8(d) counting) */
+  double pass_bytes;          /* algorithmic HBM bytes of those launches */
+} sgwg_stats;
+
+typedef struct sgwg_ctx sgwg_ctx;
+typedef struct sgwg_family sgwg_family;
+
+/* on_stop(t) of evolve_family (timestep.hpp:129,171). Called on the host after
+ * the device has landed exactly on stop time t; the callback may call
+ * sgwg_combine / sgwg_download on the same family. */
+typedef void (*sgwg_stop_cb)(double t, void* user);
+
+/* ---- context ------------------------------------------------------------ */
+/* Bind a CUDA device (one process per GPU).  Replaces nothing in the
+ * reference (it is single-process CPU; parallel.hpp:12-31 thread fan-out). */
+int sgwg_init(int device, sgwg_ctx** out);
+int sgwg_shutdown(sgwg_ctx* ctx);
+const char* sgwg_last_error(void);
+int sgwg_version(void);
+/* arithmetic mode for families created afterwards (default SGWG_ARITH_EXACT) */
+int sgwg_set_arith(sgwg_ctx* ctx, int arith);
+/* profile mode: time every WENO pass launch with CUDA events, no CUDA graphs */
+int sgwg_set_profile(sgwg_ctx* ctx, int on);
+/* the cudaStream_t all work of this context is issued on (as void*) */
+void* sgwg_stream(sgwg_ctx* ctx);
+
+/* ---- family: make_family (combine.hpp:69-83) ------------------------------ */
+/* Full family: every combination level of (d, nl), sorted. */
+int sgwg_family_create(sgwg_ctx* ctx, const sgwg_domain* dom, sgwg_family** out);
+/* Shard of a family: only the listed members (indices into the sorted full
+ * family, ascending).  Evolve and combine act on these members only; a
+ * sharded combine returns this shard's partial combination sum. */
+int sgwg_family_create_shard(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members,
+                             int count, sgwg_family** out);
+int sgwg_family_destroy(sgwg_family* fam);
+/* enumerate_combination_levels (grid.hpp:57-79), sorted: count, then levels[count*d] */
+int sgwg_enumerate_levels(int d, int nl, int* levels, int cap, int* count);
+int sgwg_family_num_members(const sgwg_family* fam, int* count);
+/* global (full-family) index, level tuple and point extents of local member mi */
+int sgwg_family_member(const sgwg_family* fam, int mi, int* global_index, int* levels,
+                       int* points);
+/* total packed points of the local members; finest-grid points (finest_geometry,
+ * combine.hpp:85-91) */
+int sgwg_family_sizes(const sgwg_family* fam, size_t* member_points, size_t* finest_points);
+
+/* ---- state transfer: initialize_family (models.hpp:855-871) / member.state ---- */
+/* Upload/download the packed states of all local members (host pointers). */
+int sgwg_family_upload(sgwg_family* fam, const double* host, size_t n);
+int sgwg_family_download(sgwg_family* fam, double* host, size_t n);
+/* Same, device pointers (cudaMemcpyDeviceToDevice on the family stream). */
+int sgwg_family_upload_device(sgwg_family* fam, const double* dev, size_t n);
+int sgwg_family_download_device(sgwg_family* fam, double* dev, size_t n);
+
+/* ---- physics: FamilyModel (models.hpp:754-851) ---------------------------- */
+int sgwg_set_model(sgwg_family* fam, const sgwg_model* model);
+
+/* ---- multi-GPU: NCCL communicator over the shards (one rank per process) ---- */
+/* id: 128-byte ncclUniqueId made by sgwg_nccl_unique_id on rank 0 and
+ * broadcast by the caller (e.g. torch.distributed).  Used for the per-step
+ * family wave-speed all-reduce(max) and the combine reduction. */
+int sgwg_nccl_unique_id(void* id128);
+int sgwg_family_set_comm(sgwg_family* fam, const void* id128, int nranks, int rank);
+
+/* ---- evolve_family (timestep.hpp:126-174) --------------------------------- */
+/* March the (local) family from its current time to tfinal in lockstep with
+ * the reference's stop list / landing / dt rules.  dts (capacity cap, may be
+ * NULL) receives the dt sequence, *nsteps its length.  On a non-finite
+ * tendency returns SGWG_ENONFINITE and fills *fail.  The family's time starts
+ * at 0 when it is created / uploaded. */
+int sgwg_evolve(sgwg_family* fam, const sgwg_policy* policy, double tfinal, const double* stops,
+                int nstops, sgwg_stop_cb on_stop, void* user, double* dts, size_t cap,
+                size_t* nsteps, sgwg_failure* fail);
+
+/* ---- combine (combine.hpp:95-122) with prolong (interp.hpp:197-250) -------- */
+/* acc = sum over members in sorted order of c_m * P_m(u_m) on the finest grid.
+ * out: finest_points doubles, host (out_is_device = 0) or device pointer.  In a
+ * sharded family with a communicator the partial sums are all-reduced (sum)
+ * so every rank receives the combined field. */
+int sgwg_combine(sgwg_family* fam, int interp_mode, double eps, double* out, size_t n,
+                 int out_is_device);
+/* prolong (interp.hpp:197-250) of one local member onto the finest grid. */
+int sgwg_prolong(sgwg_family* fam, int mi, int interp_mode, double eps, double* out, size_t n,
+                 int out_is_device);
+
+/* ---- single-stage entry points (unit-level parity) ------------ */
+/* FamilyModel::rhs (models.hpp:772-788) of every local member: tendency of the
+ * current states into out (packed like the states). */
+int sgwg_rhs(sgwg_family* fam, double* out, size_t n, int out_is_device);
+/* One SspRk3::step (timestep.hpp:83-108) of every local member with a given dt. */
+int sgwg_rk3_step(sgwg_family* fam, double dt, sgwg_failure* fail);
+
+int sgwg_get_stats(const sgwg_family* fam, sgwg_stats* stats);
+
+/* ---- host-side initial data: initialize_family (models.hpp:855-871) ------- */
+/* Initial-condition presets of BASELINE C1-C5 and the paper examples,
+ * evaluated with the host libm at the reference's coordinates
+ * (restrict_to_grid, grid.hpp:166-186; normalize_initial models.hpp:97-102 for
+ * the kinetic examples), then uploaded.  Bitwise equal to initialize_family. */
+enum {
+  SGWG_IC_C1 = 0,   /* sin(pi(x+y))                                   */
+  SGWG_IC_C2 = 1,   /* 0.5 + sin(pi(x+y))                             */
+  SGWG_IC_C3 = 2,   /* sin(pi(x+y+z))                                 */
+  SGWG_IC_C4 = 3,   /* (1+0.01 cos(x/2)) exp(-v^2/2)/sqrt(2pi)        */
+  SGWG_IC_C5 = 4,   /* (1+0.05(cos(x1/2)+cos(x2/2))) exp(-|v|^2/2)/2pi */
+  SGWG_IC_EX1 = 5,  /* 0.3 + 0.7 sin(pi/2 (x+y))      models.hpp:605  */
+  SGWG_IC_EX3 = 6,  /* 1 + 0.5 sin(sum x)             models.hpp:647  */
+  SGWG_IC_EX5A = 7, /* models.hpp:690-694, mass-normalised            */
+  SGWG_IC_EX5B = 8, /* models.hpp:709-714, mass-normalised            */
+  SGWG_IC_EX2 = 9   /* 1 + 0.5 sin(x+y+z)             models.hpp:625  */
+};
+int sgwg_family_init_preset(sgwg_family* fam, int preset);
+/* General initial data: ic(x, d, user) evaluated on the host at every grid
+ * point of every local member (restrict_to_grid order), then uploaded. */
+typedef double (*sgwg_ic_fn)(const double* x, int d, void* user);
+int sgwg_family_init_fn(sgwg_family* fam, sgwg_ic_fn ic, void* user, int normalize_mass);
+
+/* DFMA throughput probe (TFLOP/s) used as the measured fp64 roofline peak. */
+int sgwg_fp64_peak(sgwg_ctx* ctx, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGWG_H */

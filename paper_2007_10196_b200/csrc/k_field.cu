@@ -1,0 +1,168 @@
+// k_field.cu -- Vlasov-Poisson field of every member (BASELINE C4/C5).
+//
+// NEW PHYSICS: the reference has no Poisson solver.  This
+// follows the kinetic template of vb_rhs_into (models.hpp:334-363): the
+// charge density uses the reference's trapezoid weights over the contiguous
+// velocity block (moment_density models.hpp:294-306, block_weights 240-257,
+// trapezoid_weights_1d 64-71), rho(x) = 1 - sum_v w_v f(x, v); the field solves
+// -lap(phi) = rho, E = -grad(phi) spectrally on the member's own periodic
+// x-grid (mean and Nyquist modes dropped), as the oracle restatement
+// oracle/sgw_oracle.c:spectral_poisson does with a direct DFT.
+//
+// One CTA per member: the x-grid has <= 2048 points (C4: 32*2^l; C5:
+// (8*2^l1)x(8*2^l2), l1+l2 <= 5), so the whole 2D FFT lives in shared memory.
+#include <math.h>
+
+#include "sgwg_internal.h"
+
+namespace sgwg {
+
+constexpr int kFieldThreads = 512;
+constexpr int kFieldMaxX = 2048;
+
+__device__ __forceinline__ int bitrev(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }
+
+// radix-2 FFTs of all lines of an n1 x n2 complex array along `axis` (1 = x2,
+// contiguous).  sign -1: forward e^{-i...}; +1: inverse (unnormalised).
+__device__ void fft_lines(double* re, double* im, int n1, int n2, int axis, int sign) {
+  const int len = axis ? n2 : n1;
+  if (len <= 1) return;
+  const int nx = n1 * n2;
+  const int stride = axis ? 1 : n2;
+  const int bits = __ffs(len) - 1;
+  for (int idx = threadIdx.x; idx < nx; idx += blockDim.x) {
+    const int line = idx / len, pos = idx - line * len;
+    const int rev = bitrev(pos, bits);
+    if (pos < rev) {
+      const int base = axis ? line * n2 : line;
+      const int a = base + pos * stride, b = base + rev * stride;
+      const double tr = re[a], ti = im[a];
+      re[a] = re[b];
+      im[a] = im[b];
+      re[b] = tr;
+      im[b] = ti;
+    }
+  }
+  __syncthreads();
+  for (int half = 1; half < len; half <<= 1) {
+    for (int bfly = threadIdx.x; bfly < nx / 2; bfly += blockDim.x) {
+      const int per = len / 2;
+      const int line = bfly / per, q = bfly - line * per;
+      const int grp = q / half, pos = q - grp * half;
+      const int base = axis ? line * n2 : line;
+      const int i0 = base + (grp * 2 * half + pos) * stride;
+      const int i1 = i0 + half * stride;
+      double s, c;
+      sincospi(sign * (double)pos / (double)half, &s, &c);
+      const double br = re[i1] * c - im[i1] * s;
+      const double bi = re[i1] * s + im[i1] * c;
+      const double ar = re[i0], ai = im[i0];
+      re[i0] = ar + br;
+      im[i0] = ai + bi;
+      re[i1] = ar - br;
+      im[i1] = ai - bi;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams p) {
+  if (p.ctl != nullptr && !p.ctl->active) return;
+  const MemberDesc* M = p.mem + blockIdx.x;
+  const int dx = p.space_dim;
+  const int n1 = M->xext[0], n2 = M->xext[1];
+  const int nx = M->nx;
+  const int vn = M->vn;
+  extern __shared__ double sh[];
+  double* rr = sh;
+  double* ri = sh + nx;
+  double* er = sh + 2 * nx;
+  double* ei = sh + 3 * nx;
+  __shared__ double red[kFieldThreads / 32][2];
+
+  // rho(x) = 1 - sum_v w_v f(x, v): one warp per x point
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int ev0 = M->ext[dx], ev1 = (dx == 2) ? M->ext[dx + 1] : 1;
+  const double hv0 = M->h[dx], hv1 = (dx == 2) ? M->h[dx + 1] : 1.0;
+  const int zb0 = M->bc[dx], zb1 = (dx == 2) ? M->bc[dx + 1] : 0;
+  const double* f = p.f + M->offset;
+  for (int xi = warp; xi < nx; xi += nwarps) {
+    const double* block = f + (long long)xi * vn;
+    double acc = 0.0;
+    for (int vi = lane; vi < vn; vi += 32) {
+      const int i0 = vi / ev1, i1 = vi - i0 * ev1;
+      double w0 = hv0, w1 = hv1;
+      if (zb0 == 1 && (i0 == 0 || i0 == ev0 - 1)) w0 *= 0.5;
+      if (dx == 2 && zb1 == 1 && (i1 == 0 || i1 == ev1 - 1)) w1 *= 0.5;
+      const double w = (dx == 2) ? w0 * w1 : w0;
+      acc = fma(w, block[vi], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      rr[xi] = 1.0 - acc;
+      ri[xi] = 0.0;
+      p.rho[M->xoff + xi] = 1.0 - acc;
+    }
+  }
+  __syncthreads();
+  fft_lines(rr, ri, n1, n2, 1, -1);
+  fft_lines(rr, ri, n1, n2, 0, -1);
+
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int comp = 0; comp < dx; ++comp) {
+    for (int id = threadIdx.x; id < nx; id += blockDim.x) {
+      const int k1 = id / n2, k2 = id - k1 * n2;
+      const int s1 = (k1 <= n1 / 2) ? k1 : k1 - n1;
+      const int s2 = (k2 <= n2 / 2) ? k2 : k2 - n2;
+      const bool nyq = ((n1 % 2 == 0) && k1 == n1 / 2 && n1 > 1) ||
+                       ((n2 % 2 == 0) && k2 == n2 / 2 && n2 > 1);
+      const double kap1 = two_pi * (double)s1 / p.L[0];
+      const double kap2 = (dx == 2) ? two_pi * (double)s2 / p.L[1] : 0.0;
+      const double k2s = kap1 * kap1 + kap2 * kap2;
+      if ((s1 == 0 && s2 == 0) || nyq) {
+        er[id] = 0.0;
+        ei[id] = 0.0;
+      } else {
+        const double kc = (comp == 0) ? kap1 : kap2;
+        er[id] = kc * ri[id] / k2s;  // -i kc rhat / |k|^2
+        ei[id] = -kc * rr[id] / k2s;
+      }
+    }
+    __syncthreads();
+    fft_lines(er, ei, n1, n2, 1, +1);
+    fft_lines(er, ei, n1, n2, 0, +1);
+    double lmax = 0.0;
+    const double inv_n = 1.0 / (double)nx;
+    double* E = p.efield + M->xoff * dx + (long long)comp * nx;
+    for (int id = threadIdx.x; id < nx; id += blockDim.x) {
+      const double e = er[id] * inv_n;
+      E[id] = e;
+      lmax = fmax(lmax, fabs(e));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    if (lane == 0) red[warp][0] = lmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int q = 0; q < nwarps; ++q) m = fmax(m, red[q][0]);
+      p.emax[blockIdx.x * dx + comp] = m;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t configure_field() {
+  return cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(4 * kFieldMaxX * sizeof(double)));
+}
+
+cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s) {
+  if (nmembers <= 0) return cudaSuccess;
+  const size_t smem = 4 * kFieldMaxX * sizeof(double);
+  field_kernel<<<nmembers, kFieldThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace sgwg

@@ -1,0 +1,433 @@
+// kernels.cuh -- sm_100a fp64 kernels of the sparse-grid WENO5 hot path.
+//
+// Included twice: k_exact.cu (SGWG_FAST=0, compiled with --fmad=false) keeps
+// the reference's expression order and IEEE divides so results are bitwise
+// equal to the reference built without FMA; k_fast.cu (SGWG_FAST=1) contracts
+// to DFMA, uses one divide per reconstruction (common denominator of the three
+// nonlinear weights) and reciprocal spacings -- within 1e-10 of the reference.
+//
+// Kernels
+//   pass_kernel<BURGERS>  one dimension-by-dimension WENO5 sweep of every member
+//                         of the family (batched), accumulating the tendency in
+//                         the reference's order; the last pass of an RK stage
+//                         fuses the SSP-RK3 stage update, the non-finite check
+//                         and the per-member max|u| of the stage output.
+//                         Replaces advective_sweep / flux_sweep (models.hpp:142-177)
+//                         -> advect_derivative_line / weno_derivative_line
+//                         (weno.hpp:118-192) and SspRk3::step (timestep.hpp:86-104).
+//   upsample_kernel       one dimension of prolong (interp.hpp:217-244) for all
+//                         members at once (upsample_line, interp.hpp:151-189).
+//   final_kernel          the last dimension of prolong fused with the signed
+//                         combination sum in sorted member order (combine.hpp:113-120).
+#pragma once
+#include "sgwg_internal.h"
+
+#ifndef SGWG_FAST
+#error "define SGWG_FAST"
+#endif
+
+namespace sgwg {
+namespace SGWG_NS {
+
+constexpr double kSixth = 1.0 / 6.0;  // weno.hpp:30
+
+__device__ __forceinline__ double sq(double x) { return x * x; }
+
+// weno5_flux_positive (weno.hpp:60-72) with smoothness_indicators (weno.hpp:36-44),
+// reference expression order.
+__device__ __forceinline__ double recon_ref(double s0, double s1, double s2, double s3, double s4,
+                                            double eps, int linear) {
+  const double c0 = kSixth * (2.0 * s0 - 7.0 * s1 + 11.0 * s2);
+  const double c1 = kSixth * (-s1 + 5.0 * s2 + 2.0 * s3);
+  const double c2 = kSixth * (2.0 * s2 + 5.0 * s3 - s4);
+  if (linear) return 0.1 * c0 + 0.6 * c1 + 0.3 * c2;
+  const double b0 = (13.0 / 12.0) * sq(s0 - 2.0 * s1 + s2) + 0.25 * sq(s0 - 4.0 * s1 + 3.0 * s2);
+  const double b1 = (13.0 / 12.0) * sq(s1 - 2.0 * s2 + s3) + 0.25 * sq(s1 - s3);
+  const double b2 = (13.0 / 12.0) * sq(s2 - 2.0 * s3 + s4) + 0.25 * sq(3.0 * s2 - 4.0 * s3 + s4);
+  const double a0 = 0.1 / sq(eps + b0);
+  const double a1 = 0.6 / sq(eps + b1);
+  const double a2 = 0.3 / sq(eps + b2);
+  return (a0 * c0 + a1 * c1 + a2 * c2) / (a0 + a1 + a2);
+}
+
+#if SGWG_FAST
+// Same reconstruction with the three weights over a common denominator:
+//   sum_r d_r c_r / q_r / sum_r d_r / q_r = sum_r d_r c_r Q_r / sum_r d_r Q_r,
+//   q_r = (eps+b_r)^2, Q_0 = q_1 q_2, Q_1 = q_0 q_2, Q_2 = q_0 q_1.
+// One divide instead of four.  Q_r overflows only for b_r ~ 1e77; then the
+// reference form is used.
+__device__ __forceinline__ double recon(double s0, double s1, double s2, double s3, double s4,
+                                        double eps, int linear) {
+  const double c0 = fma(2.0, s0, fma(-7.0, s1, 11.0 * s2));
+  const double c1 = fma(5.0, s2, fma(2.0, s3, -s1));
+  const double c2 = fma(2.0, s2, fma(5.0, s3, -s4));
+  if (linear) return kSixth * fma(0.1, c0, fma(0.6, c1, 0.3 * c2));
+  const double d0 = s0 - 2.0 * s1 + s2, g0 = s0 - 4.0 * s1 + 3.0 * s2;
+  const double d1 = s1 - 2.0 * s2 + s3, g1 = s1 - s3;
+  const double d2 = s2 - 2.0 * s3 + s4, g2 = 3.0 * s2 - 4.0 * s3 + s4;
+  const double e0 = fma(13.0 / 12.0 * d0, d0, fma(0.25 * g0, g0, eps));
+  const double e1 = fma(13.0 / 12.0 * d1, d1, fma(0.25 * g1, g1, eps));
+  const double e2 = fma(13.0 / 12.0 * d2, d2, fma(0.25 * g2, g2, eps));
+  const double q0 = e0 * e0, q1 = e1 * e1, q2 = e2 * e2;
+  const double w0 = 0.1 * (q1 * q2), w1 = 0.6 * (q0 * q2), w2 = 0.3 * (q0 * q1);
+  const double den = 6.0 * (w0 + w1 + w2);
+  if (!(den < 1.0e300)) return recon_ref(s0, s1, s2, s3, s4, eps, linear);
+  return fma(w0, c0, fma(w1, c1, w2 * c2)) / den;
+}
+#else
+__device__ __forceinline__ double recon(double s0, double s1, double s2, double s3, double s4,
+                                        double eps, int linear) {
+  return recon_ref(s0, s1, s2, s3, s4, eps, linear);
+}
+#endif
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Lines of dimension k of a member: line L -> (outer o, inner i), base offset
+// o*n*inner + i, element j at base + j*inner (grid.hpp:202-217, line_at order).
+template <bool BURGERS>
+__global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) {
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  const int4 tk = p.tasks[blockIdx.x];
+  const MemberDesc* M = p.mem + tk.x;
+  const int k = p.kdim;
+  const int n = M->ext[k];
+  const long long inner = M->stride[k];
+  const int S = M->segS[k], P = M->runP[k], W = M->linesW[k], pitch = M->pitch[k];
+  const long long nlines = M->npts / n;
+  const long long L0 = tk.y;
+  const int seg0 = tk.z;
+  const int Weff = (int)min((long long)W, nlines - L0);
+  const int Seff = min(S, n - seg0);
+  const int bc = M->bc[k];
+  const int tid = threadIdx.x;
+
+  extern __shared__ double smem[];
+  double* sfp = smem;
+  double* sfm = smem + p.dyn_smem_doubles;
+  double* scoef = smem + (BURGERS ? 2 : 1) * p.dyn_smem_doubles;
+  long long* sbase = reinterpret_cast<long long*>(scoef + W);
+
+  if (p.amax_zero != nullptr && blockIdx.x == 0)
+    for (int i = tid; i < p.nmembers; i += blockDim.x) p.amax_zero[i] = 0ull;
+
+  // line bases and per-line coefficients (advective_sweep coef_of_line)
+  for (int w = tid; w < Weff; w += blockDim.x) {
+    const long long L = L0 + w;
+    const long long o = L / inner, i = L % inner;
+    const long long base = o * (long long)n * inner + i;
+    sbase[w] = base;
+    double c = p.c_const;
+    if (p.flux == kFluxKinX) {  // models.hpp:341-344: coefficient v_j
+      const int q = p.space_dim + k;
+      const int idx = (int)((base / M->stride[q]) % M->ext[q]);
+      c = M->lower[q] + idx * M->h[q];
+    } else if (p.flux == kFluxKinVB) {  // models.hpp:346-349: coefficient -x_j
+      const int q = k - p.space_dim;
+      const int idx = (int)((base / M->stride[q]) % M->ext[q]);
+      c = -(M->lower[q] + idx * M->h[q]);
+    } else if (p.flux == kFluxKinVP) {  // -E_j(x) of this member's Poisson field
+      const int comp = k - p.space_dim;
+      const long long xi = base / M->vn;
+      c = -p.efield[M->xoff * p.space_dim + (long long)comp * M->nx + xi];
+    }
+    scoef[w] = c;
+  }
+  __syncthreads();
+
+  // gather the padded segment [seg0-3, seg0+Seff+3) of every line; periodic
+  // wrap ((j%n)+n)%n or zero ghosts (weno.hpp:131-141); split fluxes.
+  const double* u = p.uin + M->offset;
+  const int len = Seff + 6;
+  const double alpha = BURGERS ? __longlong_as_double((long long)p.amax_in[tk.x]) : 0.0;
+  for (int q = tid; q < Weff * len; q += blockDim.x) {
+    int w, jj;
+    if (inner > 1) {
+      w = q % Weff;
+      jj = q / Weff;
+    } else {
+      jj = q % len;
+      w = q / len;
+    }
+    const int j = seg0 - 3 + jj;
+    double uj;
+    if (bc == 0) {
+      int jw = j % n;
+      if (jw < 0) jw += n;
+      uj = __ldg(u + sbase[w] + (long long)jw * inner);
+    } else {
+      uj = (j >= 0 && j < n) ? __ldg(u + sbase[w] + (long long)j * inner) : 0.0;
+    }
+    if (BURGERS) {
+      const double f = 0.5 * uj * uj;           // models.hpp:194
+      const double fpj = 0.5 * (f + alpha * uj);  // weno.hpp:138-140
+      sfp[w * pitch + jj] = fpj;
+      sfm[w * pitch + jj] = f - fpj;
+    } else {
+      sfp[w * pitch + jj] = scoef[w] * uj;  // weno.hpp:176
+    }
+  }
+  __syncthreads();
+
+  // interfaces and flux differences: thread (w, r) owns points [r*P, r*P+P)
+  // of line w and recomputes the interface left of its run.
+  const int R = (S + P - 1) / P;
+  const int w = tid % W;
+  const int r = tid / W;
+  const int j0 = r * P;
+  const bool mine = (r < R) && (w < Weff) && (j0 < Seff);
+  double du[kMaxRun];
+  const double eps = p.eps;
+  const int linear = p.linear;
+  if (mine) {
+    const double* fp = sfp + w * pitch;
+    const double* fm = sfm + w * pitch;
+    const double c = scoef[w];
+    const int bdir = (c < 0.0) ? 5 : 0;  // downwind: reversed window (weno.hpp:178-183)
+    const int sdir = (c < 0.0) ? -1 : 1;
+    auto flux_at = [&](int jl) -> double {  // interface jl+1/2 (local index)
+      if (BURGERS) {
+        const double* a = fp + jl + 1;
+        const double* b = fm + jl + 2;
+        return recon(a[0], a[1], a[2], a[3], a[4], eps, linear) +
+               recon(b[4], b[3], b[2], b[1], b[0], eps, linear);
+      } else {
+        const double* a = fp + jl + 1 + bdir;
+        return recon(a[0], a[sdir], a[2 * sdir], a[3 * sdir], a[4 * sdir], eps, linear);
+      }
+    };
+#if SGWG_FAST
+    const double inv_h = M->inv_h[k];
+#else
+    const double h = M->h[k];
+#endif
+    double fprev = flux_at(j0 - 1);
+#pragma unroll
+    for (int t = 0; t < kMaxRun; ++t) {
+      const int jl = j0 + t;
+      if (t < P && jl < Seff) {
+        const double f = flux_at(jl);
+#if SGWG_FAST
+        du[t] = (f - fprev) * inv_h;
+#else
+        du[t] = (f - fprev) / h;  // weno.hpp:147,152
+#endif
+        fprev = f;
+      }
+    }
+  }
+  __syncthreads();
+  if (mine) {
+#pragma unroll
+    for (int t = 0; t < kMaxRun; ++t)
+      if (t < P && j0 + t < Seff) sfp[w * S + j0 + t] = du[t];
+  }
+  __syncthreads();
+
+  // accumulate out -= du in dimension order (models.hpp:155,175,187-197) and,
+  // on the last pass, the SSP-RK3 stage update (timestep.hpp:93,98,103).
+  double lmax = 0.0;
+  const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
+  for (int q = tid; q < Weff * Seff; q += blockDim.x) {
+    int ww, jl;
+    if (inner > 1) {
+      ww = q % Weff;
+      jl = q / Weff;
+    } else {
+      jl = q % Seff;
+      ww = q / Seff;
+    }
+    const long long gi = M->offset + sbase[ww] + (long long)(seg0 + jl) * inner;
+    const double d = sfp[ww * S + jl];
+    const double kv = p.first ? (0.0 - d) : (p.kbuf[gi] - d);
+    if (!p.last) {
+      p.kbuf[gi] = kv;
+      continue;
+    }
+    double o;
+    if (p.stage == 0) {
+      o = kv;
+    } else {
+      if (!isfinite(kv)) {  // tendency_finite (timestep.hpp:71-75)
+        const unsigned long long code =
+            (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
+        atomicMin(p.fail + tk.x, code);
+      }
+      const double ui = p.uin[gi];
+      if (p.stage == 1) {
+        o = ui + dt * kv;
+      } else if (p.stage == 2) {
+        o = 0.75 * p.un[gi] + 0.25 * (ui + dt * kv);
+      } else {
+        o = (1.0 / 3.0) * p.un[gi] + (2.0 / 3.0) * (ui + dt * kv);
+      }
+    }
+    p.out[gi] = o;
+    lmax = fmax(lmax, fabs(o));
+  }
+  if (p.last && p.track_max) {
+    lmax = warp_max(lmax);
+    if ((tid & 31) == 0)
+      atomicMax(p.amax_out + tk.x, (unsigned long long)__double_as_longlong(lmax));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prolongation / combination
+// ---------------------------------------------------------------------------
+
+// One point of upsample_line (interp.hpp:151-189) with OffsetTable::make
+// (interp.hpp:124-146): fine index j of a line of n_src source values at
+// src[base + i*stride], refinement 2^m.
+__device__ __forceinline__ double interp_point(const double* __restrict__ src, long long base,
+                                               long long stride, int n_src, int j, int m, int bc,
+                                               int mode, double eps) {
+  const int f = 1 << m;
+  const int r = j & (f - 1);
+  if (r == 0) return src[base + (long long)((j >> m) % n_src) * stride];
+  int di;
+  double t;
+  if (mode == 1) {  // InterpMode::weno
+    di = (r >= f / 2) ? 1 : 0;
+    t = (double)r / f - di;
+  } else {
+    di = 0;
+    t = (double)r / f;
+  }
+  const double c0 = (t - 1.0) * (t - 2.0) / 12.0;  // interp.hpp:39 / 120-121
+  const double c1 = (4.0 - t * t) / 6.0;
+  const double c2 = (t + 2.0) * (t + 1.0) / 12.0;
+  const int i = (j >> m) + di;
+  double s[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int ii = i - 2 + q;
+    if (bc == 0) {
+      int iw = ii % n_src;
+      if (iw < 0) iw += n_src;
+      s[q] = src[base + (long long)iw * stride];
+    } else {
+      s[q] = (ii >= 0 && ii < n_src) ? src[base + (long long)ii * stride] : 0.0;
+    }
+  }
+  // substencil_values (interp.hpp:45-53)
+  const double p0 = s[0] * 0.5 * (t + 1.0) * t - s[1] * (t + 2.0) * t +
+                    s[2] * 0.5 * (t + 2.0) * (t + 1.0);
+  const double p1 = s[1] * 0.5 * t * (t - 1.0) - s[2] * (t + 1.0) * (t - 1.0) +
+                    s[3] * 0.5 * (t + 1.0) * t;
+  const double p2 = s[2] * 0.5 * (t - 1.0) * (t - 2.0) - s[3] * t * (t - 2.0) +
+                    s[4] * 0.5 * t * (t - 1.0);
+  if (mode == 0) return c0 * p0 + c1 * p1 + c2 * p2;
+  const double b0 = (13.0 / 12.0) * sq(s[0] - 2.0 * s[1] + s[2]) +
+                    0.25 * sq(s[0] - 4.0 * s[1] + 3.0 * s[2]);
+  const double b1 = (13.0 / 12.0) * sq(s[1] - 2.0 * s[2] + s[3]) + 0.25 * sq(s[1] - s[3]);
+  const double b2 = (13.0 / 12.0) * sq(s[2] - 2.0 * s[3] + s[4]) +
+                    0.25 * sq(3.0 * s[2] - 4.0 * s[3] + s[4]);
+#if SGWG_FAST
+  const double q0 = sq(eps + b0), q1 = sq(eps + b1), q2 = sq(eps + b2);
+  const double w0 = c0 * (q1 * q2), w1 = c1 * (q0 * q2), w2 = c2 * (q0 * q1);
+  const double den = w0 + w1 + w2;
+  if (den < 1.0e300)  // else: fall through to the reference form
+    return fma(w0, p0, fma(w1, p1, w2 * p2)) / den;
+#endif
+  const double a0 = c0 / sq(eps + b0);
+  const double a1 = c1 / sq(eps + b1);
+  const double a2 = c2 / sq(eps + b2);
+  return (a0 * p0 + a1 * p1 + a2 * p2) / (a0 + a1 + a2);
+}
+
+// dimension k of prolong for a batch of members: dst has finest extent along
+// k, src the member's current extents (finest for dims < k).
+__global__ void __launch_bounds__(256) upsample_kernel(const UpsampleParams p) {
+  const int2 tk = p.tasks[blockIdx.x];
+  const int slot = tk.x;
+  const int mi = p.slot_member[slot];
+  const MemberDesc* M = p.mem + mi;
+  const int k = p.kdim;
+  const int* ext = p.slot_ext + 4 * slot;
+  long long inner = 1;
+  for (int q = k + 1; q < 4; ++q) inner *= ext[q];
+  const int n_src = ext[k];
+  const int n_dst = p.fine_ext;
+  const int m = p.nl - M->level[k];
+  const double* src = p.src[slot];
+  double* dst = p.dst[slot];
+  const long long ndst = p.slot_n[slot];
+  const long long start = (long long)tk.y * p.chunk;
+  const long long end = min(start + (long long)p.chunk, ndst);
+  for (long long q = start + threadIdx.x; q < end; q += blockDim.x) {
+    const long long o = q / ((long long)n_dst * inner);
+    const long long rem = q - o * (long long)n_dst * inner;
+    const int j = (int)(rem / inner);
+    const long long i = rem - (long long)j * inner;
+    const long long base = o * (long long)n_src * inner + i;
+    dst[q] = interp_point(src, base, inner, n_src, j, m, p.bc, p.mode, p.eps);
+  }
+}
+
+// last dimension of prolong fused with acc += c*p over members in sorted order.
+__global__ void __launch_bounds__(256) final_kernel(const FinalParams p) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long first = p.row0 * (long long)p.fine_last;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < p.nfine; q += stride) {
+    const long long idx = first + q;
+    const long long o = idx / p.fine_last;
+    const int j = (int)(idx - o * p.fine_last);
+    double acc = 0.0;
+    for (int mi = 0; mi < p.nm; ++mi) {
+      const int m = p.mrefine[mi];
+      const double* src = p.src[mi];
+      double v;
+      if (m == 0) {
+        v = src[idx];
+      } else {
+        const int n_src = p.msrc_ext[mi];
+        v = interp_point(src, o * (long long)n_src, 1, n_src, j, m, p.bc_last, p.mode, p.eps);
+      }
+      if (p.assign)
+        acc = v;
+      else
+        acc = acc + p.coef[mi] * v;  // combine.hpp:119
+    }
+    p.out[q] = acc;
+  }
+}
+
+cudaError_t configure() {
+  cudaError_t e = cudaFuncSetAttribute(pass_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              160 * 1024);
+}
+
+cudaError_t launch_pass(const PassParams& p, int nblocks, size_t smem, cudaStream_t s) {
+  if (nblocks <= 0) return cudaSuccess;
+  if (p.flux == kFluxBurgers)
+    pass_kernel<true><<<nblocks, kPassThreads, smem, s>>>(p);
+  else
+    pass_kernel<false><<<nblocks, kPassThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s) {
+  if (nblocks <= 0) return cudaSuccess;
+  upsample_kernel<<<nblocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final(const FinalParams& p, cudaStream_t s) {
+  if (p.nfine <= 0) return cudaSuccess;
+  long long blocks = (p.nfine + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  final_kernel<<<(int)blocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace SGWG_NS
+}  // namespace sgwg

@@ -1,0 +1,1326 @@
+// sgwg_api.cu -- host runtime of the C ABI (include/sgwg.h).
+//
+// Owns the device family (packed member states, step-control block, pass
+// task tables), sequences the batched WENO pass kernels into SSP-RK3 steps,
+// captures chunks of steps into CUDA graphs with device-side dt and stop
+// landing (no host sync per step), and runs prolongation + combination.
+// Reference interfaces replaced: make_family (combine.hpp:69-83),
+// FamilyModel (models.hpp:754-851), evolve_family (timestep.hpp:126-174),
+// prolong (interp.hpp:197-250), combine (combine.hpp:95-122).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/sgwg.h"
+#include "sgwg_internal.h"
+
+using namespace sgwg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail_with(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail_with(SGWG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKN(call)                                                                    \
+  do {                                                                               \
+    ncclResult_t r_ = (call);                                                        \
+    if (r_ != ncclSuccess)                                                           \
+      return fail_with(SGWG_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define TRY(call)          \
+  do {                     \
+    int s_ = (call);       \
+    if (s_ != SGWG_OK) return s_; \
+  } while (0)
+
+long long binomial(int n, int k) {  // combine.hpp:27-32
+  if (k < 0 || k > n) return 0;
+  long long r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
+// enumerate_combination_levels (grid.hpp:57-79): lexicographic by construction
+void enum_rec(int d, int nl, int lo, int k, int used, std::array<int, 4>& cur,
+              std::vector<std::array<int, 4>>& out) {
+  if (k == d - 1) {
+    for (int last = std::max(0, lo - used); last + used <= nl; ++last) {
+      cur[k] = last;
+      if (used + last >= lo) out.push_back(cur);
+    }
+    return;
+  }
+  for (int l = 0; l + used <= nl; ++l) {
+    cur[k] = l;
+    enum_rec(d, nl, lo, k + 1, used + l, cur, out);
+  }
+}
+
+std::vector<std::array<int, 4>> enumerate_levels(int d, int nl) {
+  std::vector<std::array<int, 4>> out;
+  std::array<int, 4> cur{0, 0, 0, 0};
+  enum_rec(d, nl, std::max(0, nl - d + 1), 0, 0, cur, out);
+  std::sort(out.begin(), out.end());  // combine.hpp:71-72 (already sorted)
+  return out;
+}
+
+struct PassCfg {
+  int S, P, W, pitch;
+};
+
+// tiling of one line direction of length n: segments of <= 64 points, runs of
+// <= kMaxRun points per thread, as many lines per CTA as the 256 threads allow.
+PassCfg pass_cfg(int n) {
+  PassCfg c;
+  c.S = std::min(n, 64);
+  c.P = (c.S + 7) / 8;
+  if (c.P > kMaxRun) c.P = kMaxRun;
+  const int R = (c.S + c.P - 1) / c.P;
+  c.W = kPassThreads / R;
+  c.pitch = c.S + 6;
+  if (c.pitch % 2 == 0) c.pitch += 1;
+  return c;
+}
+
+}  // namespace
+
+struct sgwg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int arith = SGWG_ARITH_EXACT;
+  int profile = 0;
+  int sm_count = 148;
+};
+
+struct StageBufs {
+  const double* uin;
+  const double* un;
+  double* out;
+};
+
+struct PassDesc {
+  int kdim;
+  int flux;
+  double c_const;
+};
+
+struct ProlongPlan {
+  // per dimension k in 0..d-2: slot tables of members with refinement > 0
+  struct Dim {
+    int nslots = 0;
+    int ntasks = 0;
+    int2* tasks = nullptr;
+    const double** src = nullptr;
+    double** dst = nullptr;
+    int* slot_member = nullptr;
+    long long* slot_n = nullptr;
+    int* slot_ext = nullptr;
+  } dims[kMaxD];
+  std::vector<double*> owned;
+  // final pass
+  const double** fsrc = nullptr;
+  double* fcoef = nullptr;
+  int* fext = nullptr;
+  int* fref = nullptr;
+  int nm = 0;
+};
+
+struct sgwg_family {
+  sgwg_ctx* ctx = nullptr;
+  sgwg_domain dom{};
+  int d = 0, nl = 0;
+  int nm = 0;   // local members
+  int nfull = 0;
+  std::vector<int> gidx;
+  std::vector<std::array<int, 4>> levels;
+  std::vector<MemberDesc> hmem;
+  MemberDesc* dmem = nullptr;
+  long long total = 0;
+  long long finest = 0;
+  int fine_ext[kMaxD] = {1, 1, 1, 1};
+  double fine_h[kMaxD] = {0, 0, 0, 0};
+  double *u = nullptr, *A = nullptr, *B = nullptr, *K = nullptr;
+  int4* dtasks[kMaxD] = {nullptr, nullptr, nullptr, nullptr};
+  int ntasks[kMaxD] = {0, 0, 0, 0};
+  int smem_doubles[kMaxD] = {0, 0, 0, 0};
+  int maxW[kMaxD] = {0, 0, 0, 0};
+  int2* dmax_tasks = nullptr;
+  int nmax_tasks = 0;
+  unsigned long long* amax = nullptr;  // 3 slots x nm
+  unsigned long long* fail = nullptr;  // nm
+  StepCtl* ctl = nullptr;
+  StepCtl* hctl = nullptr;  // pinned mirror
+  double* dts = nullptr;
+  long long dts_cap = 0;
+  sgwg_model model{};
+  bool has_model = false;
+  // Vlasov-Poisson
+  double *rho = nullptr, *E = nullptr, *emax = nullptr;
+  long long nx_total = 0;
+  // graphs: steps per chunk -> exec
+  std::map<int, cudaGraphExec_t> graphs;
+  long long graph_key_policy = -1;
+  // prolongation plans
+  ProlongPlan* full_plan = nullptr;
+  double* fine_buf = nullptr;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  sgwg_stats stats{};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // current policy for graph building
+  DtParams dtp{};
+};
+
+namespace {
+
+int arith_of(const sgwg_family* f) { return f->ctx->arith; }
+
+cudaError_t do_launch_pass(const sgwg_family* f, const PassParams& p, int kdim) {
+  const size_t nsplit = (p.flux == kFluxBurgers) ? 2 : 1;
+  const size_t smem =
+      (nsplit * (size_t)f->smem_doubles[kdim] + 2 * (size_t)f->maxW[kdim]) * sizeof(double);
+  if (arith_of(f) == SGWG_ARITH_FAST) return fast::launch_pass(p, f->ntasks[kdim], smem, f->ctx->stream);
+  return exact::launch_pass(p, f->ntasks[kdim], smem, f->ctx->stream);
+}
+
+std::vector<PassDesc> pass_order(const sgwg_family* f) {
+  std::vector<PassDesc> v;
+  const sgwg_model& m = f->model;
+  if (m.kind == SGWG_ADVECTION || m.kind == SGWG_BURGERS) {
+    for (int k = 0; k < f->d; ++k)
+      v.push_back({k, m.kind == SGWG_BURGERS ? (int)kFluxBurgers : (int)kFluxAdvect,
+                   m.kind == SGWG_ADVECTION ? m.speeds[k] : 0.0});
+  } else {  // vb_rhs_into order: x_0, v_0, x_1, v_1 (models.hpp:339-350)
+    const int dx = m.space_dim;
+    for (int j = 0; j < dx; ++j) {
+      v.push_back({j, (int)kFluxKinX, 0.0});
+      v.push_back({dx + j, m.kind == SGWG_VLASOV_POISSON ? (int)kFluxKinVP : (int)kFluxKinVB, 0.0});
+    }
+  }
+  return v;
+}
+
+// One RK stage (stage 1..3) or a bare tendency evaluation (stage 0).
+int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool with_field = true) {
+  const sgwg_model& m = f->model;
+  const bool burgers = (m.kind == SGWG_BURGERS);
+  if (m.kind == SGWG_VLASOV_POISSON && with_field) {
+    FieldParams fp{};
+    fp.mem = f->dmem;
+    fp.f = b.uin;
+    fp.rho = f->rho;
+    fp.efield = f->E;
+    fp.emax = f->emax;
+    fp.space_dim = m.space_dim;
+    fp.stage = stage;
+    fp.L[0] = f->dom.upper[0] - f->dom.lower[0];
+    fp.L[1] = (m.space_dim == 2) ? f->dom.upper[1] - f->dom.lower[1] : 1.0;
+    fp.ctl = f->ctl;
+    CK(launch_field(fp, f->nm, f->ctx->stream));
+    f->stats.kernel_launches++;
+  }
+  const auto order = pass_order(f);
+  const int in_slot = (stage == 0) ? 0 : stage - 1;
+  const int out_slot = (stage == 0) ? 0 : stage % 3;
+  for (size_t pi = 0; pi < order.size(); ++pi) {
+    const PassDesc& pd = order[pi];
+    PassParams p{};
+    p.mem = f->dmem;
+    p.tasks = f->dtasks[pd.kdim];
+    p.kdim = pd.kdim;
+    p.flux = pd.flux;
+    p.first = (pi == 0);
+    p.last = (pi + 1 == order.size());
+    p.stage = stage;
+    p.linear = (m.weno_mode == SGWG_WENO_LINEAR);
+    p.eps = m.epsilon;
+    p.c_const = pd.c_const;
+    p.space_dim = m.space_dim;
+    p.uin = b.uin;
+    p.un = b.un;
+    p.out = b.out;
+    p.kbuf = f->K;
+    p.efield = f->E;
+    p.ctl = f->ctl;
+    p.amax_in = f->amax + (size_t)in_slot * f->nm;
+    p.amax_out = f->amax + (size_t)out_slot * f->nm;
+    p.amax_zero = (stage == 2 && pi == 0 && burgers) ? f->amax : nullptr;
+    p.nmembers = f->nm;
+    p.track_max = burgers && stage != 0;
+    p.fail = f->fail;
+    p.dyn_smem_doubles = f->smem_doubles[pd.kdim];
+    if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
+    CK(do_launch_pass(f, p, pd.kdim));
+    if (timed) {
+      CK(cudaEventRecord(f->ev1, f->ctx->stream));
+      CK(cudaEventSynchronize(f->ev1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+      f->stats.pass_ms_sum += ms;
+      f->stats.pass_launches++;
+      // algorithmic counts: per point and direction
+      // advective 70 flops, Burgers 142; RK stage update 2/5/5 flops;
+      // stage bytes 16 (stage 1) / 24 (stages 2, 3) per point, on the last pass.
+      const double pts = (double)f->total;
+      f->stats.pass_flops += pts * (burgers ? 142.0 : 70.0);
+      if (p.last && stage > 0) {
+        f->stats.pass_flops += pts * (stage == 1 ? 2.0 : 5.0);
+        f->stats.pass_bytes += pts * (stage == 1 ? 16.0 : 24.0);
+      }
+    }
+    f->stats.kernel_launches++;
+  }
+  return SGWG_OK;
+}
+
+int launch_member_max_slot0(sgwg_family* f) {
+  CK(cudaMemsetAsync(f->amax, 0, sizeof(unsigned long long) * 3 * f->nm, f->ctx->stream));
+  CK(launch_member_max(f->dmem, f->nm, f->dmax_tasks, f->nmax_tasks, f->u, f->amax,
+                       f->ctx->stream));
+  return SGWG_OK;
+}
+
+// one full step: (VP field of u^n), speeds (+ all-reduce), dt, three stages
+int launch_step(sgwg_family* f, bool timed) {
+  const bool vp = f->model.kind == SGWG_VLASOV_POISSON;
+  if (vp) {
+    FieldParams fp{};
+    fp.mem = f->dmem;
+    fp.f = f->u;
+    fp.rho = f->rho;
+    fp.efield = f->E;
+    fp.emax = f->emax;
+    fp.space_dim = f->model.space_dim;
+    fp.stage = 1;
+    fp.L[0] = f->dom.upper[0] - f->dom.lower[0];
+    fp.L[1] = (f->model.space_dim == 2) ? f->dom.upper[1] - f->dom.lower[1] : 1.0;
+    fp.ctl = f->ctl;
+    CK(launch_field(fp, f->nm, f->ctx->stream));
+    f->stats.kernel_launches++;
+  }
+  DtParams dp = f->dtp;
+  if (f->comm != nullptr) {
+    CK(launch_local_speeds(dp, f->ctx->stream));
+    CKN(ncclAllReduce(f->ctl->speeds, f->ctl->speeds, kMaxD + 1, ncclDouble, ncclMax, f->comm,
+                      f->ctx->stream));
+    dp.use_reduced = 1;
+    f->stats.kernel_launches++;
+  }
+  CK(launch_dt(dp, f->ctx->stream));
+  f->stats.kernel_launches++;
+  if (f->model.kind == SGWG_BURGERS) {
+    // clear the stage-2/3 input slots (read in the previous step)
+    CK(cudaMemsetAsync(f->amax + f->nm, 0, sizeof(unsigned long long) * 2 * f->nm,
+                       f->ctx->stream));
+  }
+  // stage 1: u -> A; stage 2: (A, u) -> B; stage 3: (B, u) -> u (timestep.hpp:91-103)
+  StageBufs s1{f->u, f->u, f->A}, s2{f->A, f->u, f->B}, s3{f->B, f->u, f->u};
+  // VP: the stage-1 field was computed above (it feeds dt); stages 2, 3 recompute it
+  TRY(launch_stage(f, 1, s1, timed, /*with_field=*/!vp));
+  TRY(launch_stage(f, 2, s2, timed));
+  TRY(launch_stage(f, 3, s3, timed));
+  return SGWG_OK;
+}
+
+int build_tasks(sgwg_family* f) {
+  for (int k = 0; k < f->d; ++k) {
+    std::vector<int4> t;
+    int smax = 0, wmax = 0;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      MemberDesc& M = f->hmem[mi];
+      const int n = M.ext[k];
+      const PassCfg c = pass_cfg(n);
+      M.segS[k] = c.S;
+      M.runP[k] = c.P;
+      M.linesW[k] = c.W;
+      M.pitch[k] = c.pitch;
+      smax = std::max(smax, c.W * c.pitch);
+      wmax = std::max(wmax, c.W);
+      const long long nlines = M.npts / n;
+      for (long long L0 = 0; L0 < nlines; L0 += c.W)
+        for (int s0 = 0; s0 < n; s0 += c.S) t.push_back(make_int4(mi, (int)L0, s0, 0));
+    }
+    f->ntasks[k] = (int)t.size();
+    f->smem_doubles[k] = smax;
+    f->maxW[k] = wmax;
+    CK(cudaMalloc(&f->dtasks[k], sizeof(int4) * std::max<size_t>(1, t.size())));
+    CK(cudaMemcpy(f->dtasks[k], t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice));
+  }
+  std::vector<int2> mt;
+  for (int mi = 0; mi < f->nm; ++mi)
+    for (long long c = 0; c * 4096 < f->hmem[mi].npts; ++c) mt.push_back(make_int2(mi, (int)c));
+  f->nmax_tasks = (int)mt.size();
+  CK(cudaMalloc(&f->dmax_tasks, sizeof(int2) * std::max<size_t>(1, mt.size())));
+  CK(cudaMemcpy(f->dmax_tasks, mt.data(), sizeof(int2) * mt.size(), cudaMemcpyHostToDevice));
+  return SGWG_OK;
+}
+
+int check_domain(const sgwg_domain* dom) {
+  if (dom == nullptr) return fail_with(SGWG_EINVAL, "null domain");
+  if (dom->d < 1 || dom->d > 4)
+    return fail_with(SGWG_EINVAL, "enumerate_combination_levels: d must be 1..4");
+  if (dom->nl < dom->d - 1)
+    return fail_with(SGWG_EINVAL, "enumerate_combination_levels: need N_L >= d-1");
+  for (int k = 0; k < dom->d; ++k) {
+    if (!(dom->upper[k] > dom->lower[k]))
+      return fail_with(SGWG_EINVAL, "DomainBox: upper must exceed lower");
+    if (dom->root_cells[k] < 1)
+      return fail_with(SGWG_EINVAL, "GridGeometry: root cells must be >= 1");
+    if (dom->bc[k] != SGWG_PERIODIC && dom->bc[k] != SGWG_ZERO)
+      return fail_with(SGWG_EINVAL, "unknown boundary kind");
+  }
+  return SGWG_OK;
+}
+
+int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int count,
+                  sgwg_family** out) {
+  if (ctx == nullptr || out == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  TRY(check_domain(dom));
+  CK(cudaSetDevice(ctx->device));
+  auto all = enumerate_levels(dom->d, dom->nl);
+  std::vector<int> sel;
+  if (members == nullptr) {
+    for (int i = 0; i < (int)all.size(); ++i) sel.push_back(i);
+  } else {
+    for (int i = 0; i < count; ++i) {
+      if (members[i] < 0 || members[i] >= (int)all.size() || (i > 0 && members[i] <= members[i - 1]))
+        return fail_with(SGWG_EINVAL, "shard members must be ascending valid indices");
+      sel.push_back(members[i]);
+    }
+  }
+  sgwg_family* f = new sgwg_family();
+  f->ctx = ctx;
+  f->dom = *dom;
+  f->d = dom->d;
+  f->nl = dom->nl;
+  f->nfull = (int)all.size();
+  f->nm = (int)sel.size();
+  const int d = f->d;
+  for (int k = 0; k < d; ++k) {  // finest_geometry (combine.hpp:85-91)
+    const int cells = dom->root_cells[k] << dom->nl;
+    f->fine_ext[k] = cells + (dom->bc[k] == SGWG_ZERO ? 1 : 0);
+    f->fine_h[k] = std::ldexp((dom->upper[k] - dom->lower[k]) / dom->root_cells[k], -dom->nl);
+  }
+  f->finest = 1;
+  for (int k = 0; k < d; ++k) f->finest *= f->fine_ext[k];
+  long long off = 0;
+  for (int gi : sel) {
+    MemberDesc M{};
+    const auto& lv = all[gi];
+    M.offset = off;
+    M.npts = 1;
+    for (int k = 0; k < kMaxD; ++k) {
+      M.ext[k] = 1;
+      M.h[k] = 1.0;
+      M.inv_h[k] = 1.0;
+    }
+    for (int k = 0; k < d; ++k) {  // GridGeometry::make (grid.hpp:110-133)
+      const int cells = dom->root_cells[k] << lv[k];
+      M.ext[k] = cells + (dom->bc[k] == SGWG_ZERO ? 1 : 0);
+      M.bc[k] = dom->bc[k];
+      M.level[k] = lv[k];
+      M.h[k] = std::ldexp((dom->upper[k] - dom->lower[k]) / dom->root_cells[k], -lv[k]);
+      M.inv_h[k] = 1.0 / M.h[k];
+      M.lower[k] = dom->lower[k];
+      M.npts *= M.ext[k];
+    }
+    M.stride[d - 1] = 1;
+    for (int k = d - 2; k >= 0; --k) M.stride[k] = M.stride[k + 1] * M.ext[k + 1];
+    for (int k = d; k < kMaxD; ++k) M.stride[k] = 1;
+    f->hmem.push_back(M);
+    f->gidx.push_back(gi);
+    f->levels.push_back(lv);
+    off += M.npts;
+  }
+  f->total = off;
+  CK(cudaEventCreate(&f->ev0));
+  CK(cudaEventCreate(&f->ev1));
+  int st = build_tasks(f);
+  if (st != SGWG_OK) return st;
+  CK(cudaMalloc(&f->dmem, sizeof(MemberDesc) * std::max(1, f->nm)));
+  CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
+  const size_t bytes = sizeof(double) * std::max<long long>(1, f->total);
+  CK(cudaMalloc(&f->u, bytes));
+  CK(cudaMalloc(&f->A, bytes));
+  CK(cudaMalloc(&f->B, bytes));
+  CK(cudaMalloc(&f->K, bytes));
+  CK(cudaMemset(f->u, 0, bytes));  // make_family: zero states (combine.hpp:79)
+  CK(cudaMalloc(&f->amax, sizeof(unsigned long long) * 3 * std::max(1, f->nm)));
+  CK(cudaMalloc(&f->fail, sizeof(unsigned long long) * std::max(1, f->nm)));
+  CK(cudaMalloc(&f->ctl, sizeof(StepCtl)));
+  CK(cudaMallocHost(&f->hctl, sizeof(StepCtl)));
+  std::memset(f->hctl, 0, sizeof(StepCtl));
+  *out = f;
+  return SGWG_OK;
+}
+
+int setup_vp(sgwg_family* f) {
+  const int dx = f->model.space_dim;
+  if (dx < 1 || dx > 2 || f->d != 2 * dx)
+    return fail_with(SGWG_EINVAL, "kinetic model: grid rank must be twice the space dimension");
+  long long xoff = 0;
+  for (auto& M : f->hmem) {
+    M.nx = 1;
+    for (int k = 0; k < dx; ++k) M.nx *= M.ext[k];
+    M.vn = (int)(M.npts / M.nx);
+    M.xext[0] = M.ext[0];
+    M.xext[1] = (dx == 2) ? M.ext[1] : 1;
+    M.xoff = xoff;
+    xoff += M.nx;
+    if (f->model.kind == SGWG_VLASOV_POISSON) {
+      for (int k = 0; k < dx; ++k)
+        if (M.bc[k] != SGWG_PERIODIC)
+          return fail_with(SGWG_EINVAL, "Vlasov-Poisson: x directions must be periodic");
+      if (M.nx > 2048) return fail_with(SGWG_EUNSUPPORTED, "Vlasov-Poisson: x-grid > 2048 points");
+      for (int k = 0; k < dx; ++k)
+        if ((M.ext[k] & (M.ext[k] - 1)) != 0)
+          return fail_with(SGWG_EUNSUPPORTED, "Vlasov-Poisson: x extents must be powers of two");
+    }
+  }
+  f->nx_total = xoff;
+  CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
+  if (f->model.kind == SGWG_VLASOV_POISSON && f->rho == nullptr) {
+    CK(cudaMalloc(&f->rho, sizeof(double) * std::max<long long>(1, xoff)));
+    CK(cudaMalloc(&f->E, sizeof(double) * std::max<long long>(1, xoff * dx)));
+    CK(cudaMalloc(&f->emax, sizeof(double) * std::max(1, f->nm * dx)));
+  }
+  return SGWG_OK;
+}
+
+void clear_graphs(sgwg_family* f) {
+  for (auto& kv : f->graphs) cudaGraphExecDestroy(kv.second);
+  f->graphs.clear();
+}
+
+int get_graph(sgwg_family* f, int nsteps, cudaGraphExec_t* exec) {
+  auto it = f->graphs.find(nsteps);
+  if (it != f->graphs.end()) {
+    *exec = it->second;
+    return SGWG_OK;
+  }
+  cudaGraph_t g;
+  const long long saved = f->stats.kernel_launches;
+  CK(cudaStreamBeginCapture(f->ctx->stream, cudaStreamCaptureModeThreadLocal));
+  for (int s = 0; s < nsteps; ++s) {
+    int st = launch_step(f, false);
+    if (st != SGWG_OK) {
+      cudaStreamEndCapture(f->ctx->stream, &g);
+      return st;
+    }
+  }
+  CK(cudaStreamEndCapture(f->ctx->stream, &g));
+  f->stats.kernel_launches = saved;
+  cudaGraphExec_t e;
+  CK(cudaGraphInstantiate(&e, g, 0));
+  CK(cudaGraphDestroy(g));
+  f->graphs[nsteps] = e;
+  *exec = e;
+  return SGWG_OK;
+}
+
+int launches_per_step(const sgwg_family* f) {
+  const int np = (int)pass_order(f).size();
+  int n = 1 + 3 * np;
+  if (f->model.kind == SGWG_VLASOV_POISSON) n += 3;
+  if (f->comm != nullptr) n += 1;
+  return n;
+}
+
+int read_failure(sgwg_family* f, sgwg_failure* fail) {
+  std::vector<unsigned long long> h(f->nm);
+  CK(cudaMemcpy(h.data(), f->fail, sizeof(unsigned long long) * f->nm, cudaMemcpyDeviceToHost));
+  // evolve_family steps members serially, so the reported failure is the
+  // lowest member index among those failing at the earliest step
+  unsigned long long best_step = ULLONG_MAX;
+  for (auto c : h)
+    if (c != ULLONG_MAX) best_step = std::min(best_step, c / 4);
+  for (int mi = 0; mi < f->nm; ++mi)
+    if (h[mi] != ULLONG_MAX && h[mi] / 4 == best_step) {
+      if (fail) {
+        fail->member = f->gidx[mi];
+        fail->step = (long long)(h[mi] / 4);
+        fail->stage = (int)(h[mi] % 4);
+      }
+      return fail_with(SGWG_ENONFINITE, "integrator failure at step " + std::to_string(best_step));
+    }
+  if (fail) {  // failure on another rank (propagated through the all-reduce)
+    fail->member = -1;
+    fail->step = -1;
+    fail->stage = 0;
+  }
+  return fail_with(SGWG_ENONFINITE, "integrator failure on another rank");
+}
+
+// ---- prolongation / combination plans ----
+
+void free_plan(ProlongPlan* pl) {
+  if (pl == nullptr) return;
+  for (auto& dm : pl->dims) {
+    cudaFree(dm.tasks);
+    cudaFree(dm.src);
+    cudaFree(dm.dst);
+    cudaFree(dm.slot_member);
+    cudaFree(dm.slot_n);
+    cudaFree(dm.slot_ext);
+  }
+  for (double* p : pl->owned) cudaFree(p);
+  cudaFree(pl->fsrc);
+  cudaFree(pl->fcoef);
+  cudaFree(pl->fext);
+  cudaFree(pl->fref);
+  delete pl;
+}
+
+template <class T>
+int upload_vec(T** dptr, const std::vector<T>& v) {
+  CK(cudaMalloc(dptr, sizeof(T) * std::max<size_t>(1, v.size())));
+  if (!v.empty()) CK(cudaMemcpy(*dptr, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return SGWG_OK;
+}
+
+constexpr int kUpsampleChunk = 2048;
+
+int build_plan(sgwg_family* f, const std::vector<int>& mis, ProlongPlan** out) {
+  ProlongPlan* pl = new ProlongPlan();
+  const int d = f->d;
+  std::vector<long long> coefs(d);
+  for (int j = 0; j < d; ++j) coefs[j] = (j % 2 == 0 ? 1 : -1) * binomial(d - 1, j);
+  // current array and extents per member
+  std::vector<const double*> cur(mis.size());
+  std::vector<std::array<int, 4>> ext(mis.size());
+  for (size_t s = 0; s < mis.size(); ++s) {
+    const MemberDesc& M = f->hmem[mis[s]];
+    cur[s] = f->u + M.offset;
+    for (int q = 0; q < 4; ++q) ext[s][q] = (q < d) ? M.ext[q] : 1;
+  }
+  for (int k = 0; k + 1 < d; ++k) {
+    std::vector<int2> tasks;
+    std::vector<const double*> src;
+    std::vector<double*> dst;
+    std::vector<int> smember, sext;
+    std::vector<long long> sn;
+    for (size_t s = 0; s < mis.size(); ++s) {
+      const MemberDesc& M = f->hmem[mis[s]];
+      if (f->nl - M.level[k] == 0) continue;  // interp.hpp:219
+      long long n = 1;
+      for (int q = 0; q < d; ++q) n *= (q == k) ? f->fine_ext[k] : ext[s][q];
+      double* buf = nullptr;
+      CK(cudaMalloc(&buf, sizeof(double) * n));
+      pl->owned.push_back(buf);
+      const int slot = (int)src.size();
+      src.push_back(cur[s]);
+      dst.push_back(buf);
+      smember.push_back(mis[s]);
+      for (int q = 0; q < 4; ++q) sext.push_back(ext[s][q]);
+      sn.push_back(n);
+      for (long long c = 0; c * kUpsampleChunk < n; ++c) tasks.push_back(make_int2(slot, (int)c));
+      cur[s] = buf;
+      ext[s][k] = f->fine_ext[k];
+    }
+    auto& dm = pl->dims[k];
+    dm.nslots = (int)src.size();
+    dm.ntasks = (int)tasks.size();
+    TRY(upload_vec(&dm.tasks, tasks));
+    TRY(upload_vec(&dm.src, src));
+    TRY(upload_vec(&dm.dst, dst));
+    TRY(upload_vec(&dm.slot_member, smember));
+    TRY(upload_vec(&dm.slot_n, sn));
+    TRY(upload_vec(&dm.slot_ext, sext));
+  }
+  std::vector<const double*> fsrc;
+  std::vector<double> fcoef;
+  std::vector<int> fext, fref;
+  for (size_t s = 0; s < mis.size(); ++s) {
+    const MemberDesc& M = f->hmem[mis[s]];
+    int lsum = 0;
+    for (int q = 0; q < d; ++q) lsum += M.level[q];
+    fsrc.push_back(cur[s]);
+    fcoef.push_back((double)coefs[f->nl - lsum]);  // combine.hpp:116
+    fext.push_back(ext[s][d - 1]);
+    fref.push_back(f->nl - M.level[d - 1]);
+  }
+  pl->nm = (int)mis.size();
+  TRY(upload_vec(&pl->fsrc, fsrc));
+  TRY(upload_vec(&pl->fcoef, fcoef));
+  TRY(upload_vec(&pl->fext, fext));
+  TRY(upload_vec(&pl->fref, fref));
+  *out = pl;
+  return SGWG_OK;
+}
+
+int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, double* out) {
+  const int d = f->d;
+  const bool fast_mode = arith_of(f) == SGWG_ARITH_FAST;
+  for (int k = 0; k + 1 < d; ++k) {
+    auto& dm = pl->dims[k];
+    if (dm.ntasks == 0) continue;
+    UpsampleParams p{};
+    p.mem = f->dmem;
+    p.tasks = dm.tasks;
+    p.src = dm.src;
+    p.dst = dm.dst;
+    p.slot_member = dm.slot_member;
+    p.slot_n = dm.slot_n;
+    p.slot_ext = dm.slot_ext;
+    p.kdim = k;
+    p.nl = f->nl;
+    p.fine_ext = f->fine_ext[k];
+    p.bc = f->dom.bc[k];
+    p.mode = mode;
+    p.eps = eps;
+    p.chunk = kUpsampleChunk;
+    CK(fast_mode ? fast::launch_upsample(p, dm.ntasks, f->ctx->stream)
+                 : exact::launch_upsample(p, dm.ntasks, f->ctx->stream));
+    f->stats.combine_launches++;
+  }
+  FinalParams fp{};
+  fp.mem = f->dmem;
+  fp.src = pl->fsrc;
+  fp.coef = pl->fcoef;
+  fp.msrc_ext = pl->fext;
+  fp.mrefine = pl->fref;
+  fp.nm = pl->nm;
+  fp.d = d;
+  fp.nl = f->nl;
+  fp.fine_last = f->fine_ext[d - 1];
+  fp.nfine = f->finest;
+  fp.row0 = 0;
+  fp.bc_last = f->dom.bc[d - 1];
+  fp.mode = mode;
+  fp.eps = eps;
+  fp.assign = assign;
+  fp.out = out;
+  CK(fast_mode ? fast::launch_final(fp, f->ctx->stream) : exact::launch_final(fp, f->ctx->stream));
+  f->stats.combine_launches++;
+  return SGWG_OK;
+}
+
+int copy_out(sgwg_family* f, const double* dev, double* out, size_t n, int out_is_device) {
+  if (out_is_device) {
+    if (out != dev)
+      CK(cudaMemcpyAsync(out, dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, f->ctx->stream));
+  } else {
+    CK(cudaMemcpyAsync(out, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, f->ctx->stream));
+  }
+  CK(cudaStreamSynchronize(f->ctx->stream));
+  return SGWG_OK;
+}
+
+int ensure_fine_buf(sgwg_family* f) {
+  if (f->fine_buf == nullptr) CK(cudaMalloc(&f->fine_buf, sizeof(double) * f->finest));
+  return SGWG_OK;
+}
+
+int require_model(const sgwg_family* f) {
+  if (!f->has_model) return fail_with(SGWG_EINVAL, "sgwg_set_model not called");
+  return SGWG_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+// C ABI
+// =========================================================================
+extern "C" {
+
+const char* sgwg_last_error(void) { return g_err.c_str(); }
+int sgwg_version(void) { return 1; }
+
+int sgwg_init(int device, sgwg_ctx** out) {
+  if (out == nullptr) return fail_with(SGWG_EINVAL, "null ctx pointer");
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail_with(SGWG_ECUDA, "no such CUDA device");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail_with(SGWG_ECUDA, std::string("sm_100a build needs a Blackwell device, got ") +
+                                     prop.name);
+  sgwg_ctx* c = new sgwg_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(exact::configure());
+  CK(fast::configure());
+  CK(configure_field());
+  *out = c;
+  return SGWG_OK;
+}
+
+int sgwg_shutdown(sgwg_ctx* ctx) {
+  if (ctx == nullptr) return SGWG_OK;
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return SGWG_OK;
+}
+
+int sgwg_set_arith(sgwg_ctx* ctx, int arith) {
+  if (ctx == nullptr || (arith != SGWG_ARITH_EXACT && arith != SGWG_ARITH_FAST))
+    return fail_with(SGWG_EINVAL, "bad arith mode");
+  ctx->arith = arith;
+  return SGWG_OK;
+}
+
+int sgwg_set_profile(sgwg_ctx* ctx, int on) {
+  if (ctx == nullptr) return fail_with(SGWG_EINVAL, "null ctx");
+  ctx->profile = on ? 1 : 0;
+  return SGWG_OK;
+}
+
+void* sgwg_stream(sgwg_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int sgwg_enumerate_levels(int d, int nl, int* levels, int cap, int* count) {
+  if (d < 1 || d > 4) return fail_with(SGWG_EINVAL, "enumerate_combination_levels: d must be 1..4");
+  if (nl < d - 1) return fail_with(SGWG_EINVAL, "enumerate_combination_levels: need N_L >= d-1");
+  auto v = enumerate_levels(d, nl);
+  if (count) *count = (int)v.size();
+  if (levels)
+    for (int i = 0; i < (int)v.size() && i < cap; ++i)
+      for (int k = 0; k < d; ++k) levels[i * d + k] = v[i][k];
+  return SGWG_OK;
+}
+
+int sgwg_family_create(sgwg_ctx* ctx, const sgwg_domain* dom, sgwg_family** out) {
+  return family_create(ctx, dom, nullptr, 0, out);
+}
+
+int sgwg_family_create_shard(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members,
+                             int count, sgwg_family** out) {
+  if (members == nullptr || count < 0) return fail_with(SGWG_EINVAL, "bad shard member list");
+  return family_create(ctx, dom, members, count, out);
+}
+
+int sgwg_family_destroy(sgwg_family* f) {
+  if (f == nullptr) return SGWG_OK;
+  cudaSetDevice(f->ctx->device);
+  cudaStreamSynchronize(f->ctx->stream);
+  clear_graphs(f);
+  free_plan(f->full_plan);
+  if (f->comm) ncclCommDestroy(f->comm);
+  for (int k = 0; k < kMaxD; ++k) cudaFree(f->dtasks[k]);
+  cudaFree(f->dmax_tasks);
+  cudaFree(f->dmem);
+  cudaFree(f->u);
+  cudaFree(f->A);
+  cudaFree(f->B);
+  cudaFree(f->K);
+  cudaFree(f->amax);
+  cudaFree(f->fail);
+  cudaFree(f->ctl);
+  cudaFreeHost(f->hctl);
+  cudaFree(f->dts);
+  cudaFree(f->rho);
+  cudaFree(f->E);
+  cudaFree(f->emax);
+  cudaFree(f->fine_buf);
+  cudaEventDestroy(f->ev0);
+  cudaEventDestroy(f->ev1);
+  delete f;
+  return SGWG_OK;
+}
+
+int sgwg_family_num_members(const sgwg_family* f, int* count) {
+  if (f == nullptr || count == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  *count = f->nm;
+  return SGWG_OK;
+}
+
+int sgwg_family_member(const sgwg_family* f, int mi, int* global_index, int* levels, int* points) {
+  if (f == nullptr || mi < 0 || mi >= f->nm) return fail_with(SGWG_EINVAL, "bad member index");
+  if (global_index) *global_index = f->gidx[mi];
+  for (int k = 0; k < f->d; ++k) {
+    if (levels) levels[k] = f->levels[mi][k];
+    if (points) points[k] = f->hmem[mi].ext[k];
+  }
+  return SGWG_OK;
+}
+
+int sgwg_family_sizes(const sgwg_family* f, size_t* member_points, size_t* finest_points) {
+  if (f == nullptr) return fail_with(SGWG_EINVAL, "null family");
+  if (member_points) *member_points = (size_t)f->total;
+  if (finest_points) *finest_points = (size_t)f->finest;
+  return SGWG_OK;
+}
+
+int sgwg_family_upload(sgwg_family* f, const double* host, size_t n) {
+  if (f == nullptr || host == nullptr || n != (size_t)f->total)
+    return fail_with(SGWG_EINVAL, "upload: size must equal the packed member points");
+  CK(cudaSetDevice(f->ctx->device));
+  CK(cudaMemcpyAsync(f->u, host, sizeof(double) * n, cudaMemcpyHostToDevice, f->ctx->stream));
+  CK(cudaStreamSynchronize(f->ctx->stream));
+  return SGWG_OK;
+}
+
+int sgwg_family_download(sgwg_family* f, double* host, size_t n) {
+  if (f == nullptr || host == nullptr || n != (size_t)f->total)
+    return fail_with(SGWG_EINVAL, "download: size must equal the packed member points");
+  CK(cudaSetDevice(f->ctx->device));
+  CK(cudaMemcpyAsync(host, f->u, sizeof(double) * n, cudaMemcpyDeviceToHost, f->ctx->stream));
+  CK(cudaStreamSynchronize(f->ctx->stream));
+  return SGWG_OK;
+}
+
+int sgwg_family_upload_device(sgwg_family* f, const double* dev, size_t n) {
+  if (f == nullptr || dev == nullptr || n != (size_t)f->total)
+    return fail_with(SGWG_EINVAL, "upload: size must equal the packed member points");
+  CK(cudaMemcpyAsync(f->u, dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, f->ctx->stream));
+  CK(cudaStreamSynchronize(f->ctx->stream));
+  return SGWG_OK;
+}
+
+int sgwg_family_download_device(sgwg_family* f, double* dev, size_t n) {
+  if (f == nullptr || dev == nullptr || n != (size_t)f->total)
+    return fail_with(SGWG_EINVAL, "download: size must equal the packed member points");
+  CK(cudaMemcpyAsync(dev, f->u, sizeof(double) * n, cudaMemcpyDeviceToDevice, f->ctx->stream));
+  CK(cudaStreamSynchronize(f->ctx->stream));
+  return SGWG_OK;
+}
+
+int sgwg_set_model(sgwg_family* f, const sgwg_model* m) {
+  if (f == nullptr || m == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  if (m->kind < SGWG_ADVECTION || m->kind > SGWG_VLASOV_POISSON)
+    return fail_with(SGWG_EINVAL, "unknown model kind");
+  if (m->kind == SGWG_VLASOV_BOLTZMANN)
+    return fail_with(SGWG_EUNSUPPORTED,
+                     "Vlasov-Boltzmann relaxation is outside the B200 hot path (SURVEY 2.1)");
+  if (!(m->epsilon > 0.0)) return fail_with(SGWG_EINVAL, "WENO epsilon must be positive");
+  // weno_derivative_line: periodic lines need >= 6 points (weno.hpp:122-123)
+  for (const auto& M : f->hmem)
+    for (int k = 0; k < f->d; ++k)
+      if (M.bc[k] == SGWG_PERIODIC && M.ext[k] < 6)
+        return fail_with(SGWG_EINVAL, "weno_derivative_line: periodic line too short");
+  f->model = *m;
+  f->has_model = true;
+  if (m->kind == SGWG_VLASOV_POISSON) TRY(setup_vp(f));
+  clear_graphs(f);
+  return SGWG_OK;
+}
+
+int sgwg_nccl_unique_id(void* id128) {
+  if (id128 == nullptr) return fail_with(SGWG_EINVAL, "null id");
+  ncclUniqueId id;
+  CKN(ncclGetUniqueId(&id));
+  std::memcpy(id128, &id, sizeof(id));
+  return SGWG_OK;
+}
+
+int sgwg_family_set_comm(sgwg_family* f, const void* id128, int nranks, int rank) {
+  if (f == nullptr || id128 == nullptr || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail_with(SGWG_EINVAL, "bad communicator arguments");
+  CK(cudaSetDevice(f->ctx->device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  if (f->comm) ncclCommDestroy(f->comm);
+  CKN(ncclCommInitRank(&f->comm, nranks, id, rank));
+  f->nranks = nranks;
+  f->rank = rank;
+  clear_graphs(f);
+  return SGWG_OK;
+}
+
+int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const double* stops_in,
+                int nstops, sgwg_stop_cb on_stop, void* user, double* dts, size_t cap,
+                size_t* nsteps, sgwg_failure* fail) {
+  if (f == nullptr || pol == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  TRY(require_model(f));
+  if (tfinal < 0.0) return fail_with(SGWG_EINVAL, "evolve_family: negative final time");
+  if (pol->mode == SGWG_DT_ACCURACY && !(pol->reference_spacing > 0.0))
+    return fail_with(SGWG_EINVAL, "compute_dt: reference spacing must be positive");
+  if (pol->mode == SGWG_DT_CFL && !(pol->cfl > 0.0))
+    return fail_with(SGWG_EINVAL, "compute_dt: cfl must be positive");
+  CK(cudaSetDevice(f->ctx->device));
+  cudaStream_t s = f->ctx->stream;
+  // stop list (timestep.hpp:133-142)
+  const double eps_dedupe = 1e-12 * std::max(1.0, tfinal);
+  std::vector<double> stops(stops_in, stops_in + std::max(0, nstops));
+  stops.push_back(tfinal);
+  std::sort(stops.begin(), stops.end());
+  stops.erase(std::remove_if(stops.begin(), stops.end(),
+                             [&](double x) { return x <= 0.0 || x > tfinal + eps_dedupe; }),
+              stops.end());
+  stops.erase(std::unique(stops.begin(), stops.end(),
+                          [&](double a, double b) { return std::abs(a - b) <= eps_dedupe; }),
+              stops.end());
+  if (stops.empty()) stops.push_back(tfinal);
+  const double eps_t = 1e-12 * std::max(1.0, tfinal);
+
+  // dt parameters (compute_dt, timestep.hpp:47-67; family_wave_speeds models.hpp:791-839)
+  DtParams dp{};
+  dp.ctl = f->ctl;
+  dp.kind = f->model.kind;
+  dp.mode = pol->mode;
+  dp.cfl = pol->cfl;
+  if (pol->mode == SGWG_DT_ACCURACY) {
+    double b = std::pow(pol->reference_spacing, 5.0 / 3.0);
+    if (pol->dt_scale != 1.0) b = pol->dt_scale * b;
+    dp.base_dt = b;
+  }
+  for (int k = 0; k < f->d; ++k) dp.fine_h[k] = f->fine_h[k];
+  if (f->model.kind == SGWG_ADVECTION) {
+    for (int k = 0; k < f->d; ++k) dp.const_speeds[k] = std::abs(f->model.speeds[k]);
+  } else if (f->model.kind == SGWG_VLASOV_POISSON) {
+    const int dx = f->model.space_dim;
+    for (int j = 0; j < dx; ++j)
+      dp.const_speeds[j] =
+          std::max(std::abs(f->dom.lower[dx + j]), std::abs(f->dom.upper[dx + j]));
+  }
+  dp.d = f->d;
+  dp.space_dim = f->model.space_dim;
+  dp.amax = f->amax;
+  dp.emax = f->emax;
+  dp.nmembers = f->nm;
+  dp.fail = f->fail;
+  // dt record buffer
+  const long long want_cap = (long long)std::max<size_t>(cap, 1);
+  if (f->dts_cap < want_cap) {
+    cudaFree(f->dts);
+    CK(cudaMalloc(&f->dts, sizeof(double) * want_cap));
+    f->dts_cap = want_cap;
+    clear_graphs(f);
+  }
+  dp.dts = f->dts;
+  dp.dts_cap = f->dts_cap;
+  // graphs bake the policy in: rebuild when it changes
+  const long long key = (long long)std::hash<std::string>()(
+      std::string((const char*)&dp, sizeof(DtParams) - 0));
+  if (key != f->graph_key_policy) {
+    clear_graphs(f);
+    f->graph_key_policy = key;
+  }
+  f->dtp = dp;
+
+  // initial state of the device loop
+  std::memset(f->hctl, 0, sizeof(StepCtl));
+  f->hctl->t = 0.0;
+  f->hctl->eps_t = eps_t;
+  f->hctl->active = 1;
+  CK(cudaMemcpyAsync(f->ctl, f->hctl, sizeof(StepCtl), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(f->fail, 0xff, sizeof(unsigned long long) * f->nm, s));
+  if (f->model.kind == SGWG_BURGERS) TRY(launch_member_max_slot0(f));
+
+  f->stats.evolve_ms = 0;
+  f->stats.steps = 0;
+  f->stats.kernel_launches = 0;
+  f->stats.pass_ms_sum = 0;
+  f->stats.pass_launches = 0;
+  f->stats.pass_flops = 0;
+  f->stats.pass_bytes = 0;
+  const int lps = launches_per_step(f);
+  double t_host = 0.0;
+  double last_dt = (pol->mode == SGWG_DT_ACCURACY) ? dp.base_dt : 0.0;
+  int status = SGWG_OK;
+  for (double stop : stops) {
+    if (stop > tfinal + eps_t) break;
+    // set stop, reactivate (t, step, failure state persist)
+    CK(cudaMemcpyAsync(&f->ctl->stop, &stop, sizeof(double), cudaMemcpyHostToDevice, s));
+    f->hctl->active = 1;
+    CK(cudaMemcpyAsync(&f->ctl->active, &f->hctl->active, sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(f->ev0, s));
+    double seg_ms = 0.0;
+    for (;;) {
+      // how many steps to launch before looking: exact in accuracy mode,
+      // estimated from the last dt in CFL mode (early-exit kernels absorb overshoot)
+      long long est = 1;
+      if (last_dt > 0.0) est = (long long)std::ceil((stop - t_host) / last_dt) + 1;
+      est = std::max(1LL, std::min(est, 256LL));
+      if (f->ctx->profile) {  // un-captured, every pass bracketed by events
+        for (long long q = 0; q < est; ++q) TRY(launch_step(f, true));
+      } else {
+        long long left = est;
+        while (left > 0) {
+          int chunk = 1;
+          while (chunk * 2 <= left && chunk < 64) chunk *= 2;
+          cudaGraphExec_t ge;
+          TRY(get_graph(f, chunk, &ge));
+          CK(cudaGraphLaunch(ge, s));
+          f->stats.kernel_launches += (long long)chunk * lps;
+          left -= chunk;
+        }
+      }
+      CK(cudaMemcpyAsync(f->hctl, f->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      t_host = f->hctl->t;
+      if (f->hctl->dt > 0.0) last_dt = f->hctl->dt;
+      if (f->hctl->failed) {
+        status = read_failure(f, fail);
+        break;
+      }
+      if (!f->hctl->active) break;
+    }
+    CK(cudaEventRecord(f->ev1, s));
+    CK(cudaEventSynchronize(f->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+    seg_ms += ms;
+    f->stats.evolve_ms += seg_ms;
+    if (status != SGWG_OK) break;
+    // land exactly on the stop (timestep.hpp:170)
+    f->hctl->t = stop;
+    t_host = stop;
+    CK(cudaMemcpyAsync(&f->ctl->t, &stop, sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    if (on_stop) on_stop(stop, user);
+  }
+  CK(cudaMemcpyAsync(f->hctl, f->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  f->stats.steps = f->hctl->step;
+  if (nsteps) *nsteps = (size_t)f->hctl->step;
+  if (dts && cap > 0) {
+    const size_t nn = std::min<size_t>(cap, (size_t)f->hctl->step);
+    if (nn > 0) CK(cudaMemcpy(dts, f->dts, sizeof(double) * nn, cudaMemcpyDeviceToHost));
+  }
+  return status;
+}
+
+int sgwg_rk3_step(sgwg_family* f, double dt, sgwg_failure* fail) {
+  if (f == nullptr) return fail_with(SGWG_EINVAL, "null family");
+  TRY(require_model(f));
+  if (!(dt > 0.0)) return fail_with(SGWG_EINVAL, "ssp_rk3_step: dt must be positive");
+  CK(cudaSetDevice(f->ctx->device));
+  cudaStream_t s = f->ctx->stream;
+  std::memset(f->hctl, 0, sizeof(StepCtl));
+  f->hctl->active = 1;
+  f->hctl->dt = dt;
+  CK(cudaMemcpyAsync(f->ctl, f->hctl, sizeof(StepCtl), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(f->fail, 0xff, sizeof(unsigned long long) * f->nm, s));
+  if (f->model.kind == SGWG_BURGERS) TRY(launch_member_max_slot0(f));
+  StageBufs s1{f->u, f->u, f->A}, s2{f->A, f->u, f->B}, s3{f->B, f->u, f->u};
+  TRY(launch_stage(f, 1, s1, false));
+  TRY(launch_stage(f, 2, s2, false));
+  TRY(launch_stage(f, 3, s3, false));
+  std::vector<unsigned long long> h(f->nm);
+  CK(cudaMemcpyAsync(h.data(), f->fail, sizeof(unsigned long long) * f->nm,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (auto c : h)
+    if (c != ULLONG_MAX) return read_failure(f, fail);
+  return SGWG_OK;
+}
+
+int sgwg_rhs(sgwg_family* f, double* out, size_t n, int out_is_device) {
+  if (f == nullptr || out == nullptr || n != (size_t)f->total)
+    return fail_with(SGWG_EINVAL, "rhs: size must equal the packed member points");
+  TRY(require_model(f));
+  CK(cudaSetDevice(f->ctx->device));
+  cudaStream_t s = f->ctx->stream;
+  std::memset(f->hctl, 0, sizeof(StepCtl));
+  f->hctl->active = 1;
+  CK(cudaMemcpyAsync(f->ctl, f->hctl, sizeof(StepCtl), cudaMemcpyHostToDevice, s));
+  if (f->model.kind == SGWG_BURGERS) TRY(launch_member_max_slot0(f));
+  StageBufs b{f->u, f->u, f->A};
+  TRY(launch_stage(f, 0, b, false));
+  return copy_out(f, f->A, out, n, out_is_device);
+}
+
+int sgwg_combine(sgwg_family* f, int mode, double eps, double* out, size_t n, int out_is_device) {
+  if (f == nullptr || out == nullptr || n != (size_t)f->finest)
+    return fail_with(SGWG_EINVAL, "combine: output size must equal the finest-grid points");
+  if (mode != SGWG_INTERP_WENO && mode != SGWG_INTERP_LAGRANGE)
+    return fail_with(SGWG_EINVAL, "unknown interpolation mode");
+  if (mode == SGWG_INTERP_WENO && !(eps > 0.0))
+    return fail_with(SGWG_EINVAL, "weno_interp5: epsilon must be positive");
+  if (f->nm == 0 && f->comm == nullptr) return fail_with(SGWG_EINVAL, "combine: empty family");
+  CK(cudaSetDevice(f->ctx->device));
+  if (f->full_plan == nullptr) {
+    std::vector<int> mis(f->nm);
+    for (int i = 0; i < f->nm; ++i) mis[i] = i;
+    TRY(build_plan(f, mis, &f->full_plan));
+  }
+  double* dst = out_is_device ? out : nullptr;
+  if (dst == nullptr) {
+    TRY(ensure_fine_buf(f));
+    dst = f->fine_buf;
+  }
+  f->stats.combine_launches = 0;
+  CK(cudaEventRecord(f->ev0, f->ctx->stream));
+  TRY(run_plan(f, f->full_plan, mode, eps, 0, dst));
+  if (f->comm != nullptr && f->nranks > 1) {
+    CKN(ncclAllReduce(dst, dst, (size_t)f->finest, ncclDouble, ncclSum, f->comm, f->ctx->stream));
+  }
+  CK(cudaEventRecord(f->ev1, f->ctx->stream));
+  CK(cudaEventSynchronize(f->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+  f->stats.combine_ms = ms;
+  return copy_out(f, dst, out, n, out_is_device);
+}
+
+int sgwg_prolong(sgwg_family* f, int mi, int mode, double eps, double* out, size_t n,
+                 int out_is_device) {
+  if (f == nullptr || out == nullptr || n != (size_t)f->finest)
+    return fail_with(SGWG_EINVAL, "prolong: output size must equal the finest-grid points");
+  if (mi < 0 || mi >= f->nm) return fail_with(SGWG_EINVAL, "bad member index");
+  if (mode != SGWG_INTERP_WENO && mode != SGWG_INTERP_LAGRANGE)
+    return fail_with(SGWG_EINVAL, "unknown interpolation mode");
+  CK(cudaSetDevice(f->ctx->device));
+  ProlongPlan* pl = nullptr;
+  TRY(build_plan(f, std::vector<int>{mi}, &pl));
+  double* dst = out_is_device ? out : nullptr;
+  if (dst == nullptr) {
+    int st = ensure_fine_buf(f);
+    if (st != SGWG_OK) {
+      free_plan(pl);
+      return st;
+    }
+    dst = f->fine_buf;
+  }
+  int st = run_plan(f, pl, mode, eps, 1, dst);
+  if (st == SGWG_OK) st = copy_out(f, dst, out, n, out_is_device);
+  free_plan(pl);
+  return st;
+}
+
+static double preset_value(int preset, const double* x, int d) {
+  const double pi = 3.14159265358979323846;  // std::numbers::pi
+  switch (preset) {
+    case SGWG_IC_C1: return std::sin(pi * (x[0] + x[1]));
+    case SGWG_IC_C2: return 0.5 + std::sin(pi * (x[0] + x[1]));
+    case SGWG_IC_C3: return std::sin(pi * (x[0] + x[1] + x[2]));
+    case SGWG_IC_C4:
+      return (1.0 + 0.01 * std::cos(0.5 * x[0])) / std::sqrt(2.0 * pi) *
+             std::exp(-0.5 * (x[1] * x[1]));
+    case SGWG_IC_C5:
+      return (1.0 + 0.05 * (std::cos(0.5 * x[0]) + std::cos(0.5 * x[1]))) / (2.0 * pi) *
+             std::exp(-0.5 * (x[2] * x[2] + x[3] * x[3]));
+    case SGWG_IC_EX1: return 0.3 + 0.7 * std::sin(0.5 * pi * (x[0] + x[1]));
+    case SGWG_IC_EX3: {
+      double s = 0.0;
+      for (int k = 0; k < d; ++k) s += x[k];
+      return 1.0 + 0.5 * std::sin(s);
+    }
+    case SGWG_IC_EX5A: {
+      const double xx = x[0], v = x[1];
+      const double s = std::sin(0.5 * xx * xx);
+      return s * s * std::exp(-0.5 * (xx * xx + v * v));
+    }
+    case SGWG_IC_EX5B: {
+      const double x1 = x[0], x2 = x[1], v1 = x[2], v2 = x[3];
+      const double s = std::sin(0.5 * x1 * x1);
+      const double c = std::cos(0.5 * x2 * x2);
+      return s * s * c * c * std::exp(-0.5 * (x1 * x1 + x2 * x2 + v1 * v1 + v2 * v2));
+    }
+    case SGWG_IC_EX2: return 1.0 + 0.5 * std::sin(x[0] + x[1] + x[2]);
+  }
+  return 0.0;
+}
+
+struct PresetIc {
+  int preset;
+};
+static double preset_cb(const double* x, int d, void* user) {
+  return preset_value(static_cast<PresetIc*>(user)->preset, x, d);
+}
+
+int sgwg_family_init_fn(sgwg_family* f, sgwg_ic_fn ic, void* user, int normalize_mass) {
+  if (f == nullptr || ic == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  std::vector<double> host((size_t)std::max<long long>(1, f->total));
+  const int d = f->d;
+  for (int mi = 0; mi < f->nm; ++mi) {
+    const MemberDesc& M = f->hmem[mi];
+    double* out = host.data() + M.offset;
+    int idx[kMaxD] = {0, 0, 0, 0};
+    double x[kMaxD];
+    for (int k = 0; k < d; ++k) x[k] = M.lower[k];
+    for (long long lin = 0; lin < M.npts; ++lin) {  // restrict_to_grid (grid.hpp:166-186)
+      out[lin] = ic(x, d, user);
+      for (int k = d - 1; k >= 0; --k) {
+        if (++idx[k] < M.ext[k]) {
+          x[k] = M.lower[k] + idx[k] * M.h[k];
+          break;
+        }
+        idx[k] = 0;
+        x[k] = M.lower[k];
+      }
+    }
+    if (normalize_mass) {  // normalize_initial / quadrature_mass (models.hpp:73-102)
+      int id2[kMaxD] = {0, 0, 0, 0};
+      double sum = 0.0, comp = 0.0;
+      for (long long lin = 0; lin < M.npts; ++lin) {
+        double wp = 1.0;
+        for (int k = 0; k < d; ++k) {
+          double w = M.h[k];
+          if (M.bc[k] == SGWG_ZERO && (id2[k] == 0 || id2[k] == M.ext[k] - 1)) w *= 0.5;
+          wp *= w;
+        }
+        const double term = wp * out[lin] - comp;
+        const double next = sum + term;
+        comp = (next - sum) - term;
+        sum = next;
+        for (int k = d - 1; k >= 0; --k) {
+          if (++id2[k] < M.ext[k]) break;
+          id2[k] = 0;
+        }
+      }
+      if (!(sum > 0.0)) return fail_with(SGWG_EINVAL, "normalize_initial: nonpositive mass");
+      for (long long lin = 0; lin < M.npts; ++lin) out[lin] /= sum;
+    }
+  }
+  return sgwg_family_upload(f, host.data(), (size_t)f->total);
+}
+
+int sgwg_family_init_preset(sgwg_family* f, int preset) {
+  if (preset < SGWG_IC_C1 || preset > SGWG_IC_EX2) return fail_with(SGWG_EINVAL, "unknown preset");
+  PresetIc p{preset};
+  const int norm = (preset == SGWG_IC_EX5A || preset == SGWG_IC_EX5B) ? 1 : 0;
+  return sgwg_family_init_fn(f, preset_cb, &p, norm);
+}
+
+int sgwg_get_stats(const sgwg_family* f, sgwg_stats* st) {
+  if (f == nullptr || st == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  *st = f->stats;
+  return SGWG_OK;
+}
+
+int sgwg_fp64_peak(sgwg_ctx* ctx, double* tflops) {
+  if (ctx == nullptr || tflops == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  double* buf;
+  CK(cudaMalloc(&buf, sizeof(double)));
+  const int iters = 1 << 16;
+  const int blocks = ctx->sm_count * 8;
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(launch_fp64_peak(buf, iters, blocks, ctx->stream));  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    CK(cudaEventRecord(a, ctx->stream));
+    CK(launch_fp64_peak(buf, iters, blocks, ctx->stream));
+    CK(cudaEventRecord(b, ctx->stream));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  const double flops = (double)blocks * 256.0 * iters * 8.0 * 2.0;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return SGWG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+// sgwg_internal.h -- device-side data layout shared by the kernel TUs and the
+// host runtime (sgwg_api.cu).  Not part of the public C ABI (include/sgwg.h).
+//
+// HBM layout of a family: every member's state is packed in
+// one contiguous fp64 buffer in the reference's sorted member order, each
+// member row-major with dimension 0 slowest (grid.hpp:102-108).  Three such
+// buffers (u^n, stage A, stage B) plus one tendency buffer K hold a step.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sgwg {
+
+constexpr int kMaxD = 4;
+constexpr int kPassThreads = 256;  // threads per WENO pass CTA
+constexpr int kMaxRun = 8;         // max points per thread run (registers)
+
+enum FluxKind : int {
+  kFluxAdvect = 0,   // c*u with c constant over the member (advection speeds)
+  kFluxBurgers = 1,  // 0.5 u^2 with Lax-Friedrichs split, alpha = max|u| of the member
+  kFluxKinX = 2,     // kinetic x_j line: c = v_j coordinate      (models.hpp:341-344)
+  kFluxKinVB = 3,    // kinetic v_j line: c = -x_j coordinate     (models.hpp:346-349)
+  kFluxKinVP = 4     // kinetic v_j line: c = -E_j(x) (Vlasov-Poisson, new physics)
+};
+
+// One component grid on the device (GridGeometry, grid.hpp:85-136).
+struct MemberDesc {
+  long long offset;        // first point in the packed state buffers
+  long long npts;
+  long long stride[kMaxD];
+  int ext[kMaxD];          // points per dimension
+  int bc[kMaxD];
+  int level[kMaxD];
+  double h[kMaxD];
+  double inv_h[kMaxD];
+  double lower[kMaxD];
+  // per-dimension WENO pass tiling: segment length S, run length P, lines W, smem pitch
+  int segS[kMaxD], runP[kMaxD], linesW[kMaxD], pitch[kMaxD];
+  // Vlasov-Poisson: x-grid of the member
+  long long xoff;          // offset of this member in the packed x-grid buffers (rho, E)
+  int nx;                  // x points
+  int vn;                  // points of the velocity block (contiguous)
+  int xext[2];             // x extents (dx=1: {n0, 1})
+};
+
+// Step control block (timestep.hpp:126-174 loop state), device resident.
+struct StepCtl {
+  double t;          // current time
+  double stop;       // current stop
+  double eps_t;      // 1e-12 * max(1, T)
+  double dt;         // dt of the current step
+  long long step;    // number of steps taken (also next step index)
+  long long cur_step;
+  int active;        // 1 while stop - t > eps_t and no failure
+  int failed;        // a member reported a non-finite tendency
+  double speeds[kMaxD + 1];  // family wave speeds of the step (+ failure flag slot)
+};
+
+struct PassParams {
+  const MemberDesc* mem;
+  const int4* tasks;       // (member, first line, segment start, -)
+  int kdim;                // dimension swept by this pass
+  int flux;                // FluxKind
+  int first, last;         // first / last pass of the stage (accumulation order)
+  int stage;               // 1..3 RK stage when last; 0: rhs only (out = tendency)
+  int linear;              // WenoMode::linear
+  double eps;
+  double c_const;          // advection speed of this dimension
+  int space_dim;           // kinetic models
+  const double* uin;       // stage input
+  const double* un;        // u^n (stages 2, 3)
+  double* out;             // stage output
+  double* kbuf;            // tendency accumulator
+  const double* efield;    // VP: E, packed per member [comp][xi]
+  const StepCtl* ctl;      // dt, active, step
+  const unsigned long long* amax_in;   // per member max|u_in| (Burgers alpha)
+  unsigned long long* amax_out;        // per member max|out| (next stage alpha)
+  unsigned long long* amax_zero;       // slot cleared by this pass (or null)
+  int nmembers;
+  int track_max;
+  unsigned long long* fail;            // per member: min(step*4 + stage)
+  int dyn_smem_doubles;    // doubles of dynamic smem per array
+};
+
+struct UpsampleParams {
+  const MemberDesc* mem;
+  const int2* tasks;       // (member-slot, first output index of the chunk)
+  const double* const* src;  // per member-slot source array
+  double* const* dst;        // per member-slot destination array
+  const int* slot_member;    // member-slot -> member index
+  const long long* slot_n;   // member-slot -> dst points
+  const int* slot_ext;       // member-slot -> src extents (4 per slot, dims > k original)
+  int kdim;
+  int nl;
+  int fine_ext;            // finest points along kdim
+  int bc;
+  int mode;                // InterpMode
+  double eps;
+  int chunk;
+};
+
+struct FinalParams {
+  const MemberDesc* mem;
+  const double* const* src;  // per local member: array after dims 0..d-2
+  const double* coef;        // per local member combination coefficient
+  const int* msrc_ext;       // per local member: source extent along the last dim
+  const int* mrefine;        // per local member: refinement exponent along the last dim
+  int nm;
+  int d;
+  int nl;
+  int fine_last;           // finest points along the last dim
+  long long nfine;         // finest points (or slab points)
+  long long row0;          // first finest row (dims 0..d-2 flattened) of this launch
+  int bc_last;
+  int mode;
+  double eps;
+  int assign;              // 1: out = p (prolong of one member, no accumulation)
+  double* out;
+};
+
+struct FieldParams {
+  const MemberDesc* mem;
+  const double* f;         // stage input (packed)
+  double* rho;             // packed per member (nx)
+  double* efield;          // packed per member (space_dim * nx)
+  double* emax;            // per member max|E_j| (space_dim per member), stage 1 only
+  int space_dim;
+  int stage;
+  double L[2];             // periodic x lengths
+  const StepCtl* ctl;
+};
+
+// launchers: one set per arithmetic TU (k_exact.cu, k_fast.cu)
+#define SGWG_DECLARE_LAUNCHERS(NS)                                                        \
+  namespace NS {                                                                          \
+  cudaError_t configure();                                                                \
+  cudaError_t launch_pass(const PassParams& p, int nblocks, size_t smem, cudaStream_t s); \
+  cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s);      \
+  cudaError_t launch_final(const FinalParams& p, cudaStream_t s);                         \
+  }
+SGWG_DECLARE_LAUNCHERS(exact)
+SGWG_DECLARE_LAUNCHERS(fast)
+
+// exact-arithmetic scalar kernels (k_exact.cu)
+struct DtParams {
+  StepCtl* ctl;
+  int kind;                // model kind
+  int mode;                // DtMode
+  double cfl;
+  double base_dt;          // accuracy mode: pow(h, 5/3) (x scale), computed on the host
+  double fine_h[kMaxD];    // finest spacings (finest_geometry)
+  double const_speeds[kMaxD];
+  int d;
+  int space_dim;
+  const unsigned long long* amax;  // Burgers: per member max|u^n| (slot 0)
+  const double* emax;              // VP: per member max|E_j|
+  int nmembers;
+  const unsigned long long* fail;
+  double* dts;
+  long long dts_cap;
+  int use_reduced;         // speeds already reduced across ranks into ctl->speeds
+};
+cudaError_t launch_local_speeds(const DtParams& p, cudaStream_t s);
+cudaError_t launch_dt(const DtParams& p, cudaStream_t s);
+cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* tasks, int ntasks,
+                              const double* u, unsigned long long* amax, cudaStream_t s);
+cudaError_t configure_field();
+cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s);
+cudaError_t launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t s);
+
+}  // namespace sgwg

@@ -1,0 +1,365 @@
+"""Python mirror of the reference ``sgweno`` solver interface over the C ABI.
+
+The reference is a header-only C++ library; its public entry points for this
+path are ``make_family`` (combine.hpp:69-83), ``initialize_family``
+(models.hpp:855-871), ``FamilyModel`` (models.hpp:754-851), ``evolve_family``
+(timestep.hpp:126-174), ``prolong`` (interp.hpp:197-250) and ``combine``
+(combine.hpp:95-122).  :class:`Family` exposes the same operations, with the
+same argument meaning and error behaviour (``ValueError`` for the reference's
+``std::invalid_argument``, :class:`FamilyIntegratorFailure` for
+``FamilyIntegratorFailure{level, step, stage}``), on top of ``libsgwg.so``
+(include/sgwg.h).  There is no CPU fallback: if the extension or a Blackwell
+GPU is missing every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import configs as _cfg
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsgwg.so")
+
+OK, EINVAL, ENONFINITE, ECUDA, ENCCL, EUNSUPPORTED = range(6)
+ARITH_EXACT, ARITH_FAST = 0, 1
+
+_lib = None
+
+
+class SgwgError(RuntimeError):
+    """CUDA / NCCL / unsupported-feature failure of the B200 path."""
+
+
+class FamilyIntegratorFailure(RuntimeError):
+    """timestep.hpp:31-40: non-finite tendency of member `level` at (step, stage)."""
+
+    def __init__(self, msg, member, level, step, stage):
+        super().__init__(msg)
+        self.member, self.level, self.step, self.stage = member, level, step, stage
+
+
+class Domain(C.Structure):
+    _fields_ = [("d", C.c_int), ("nl", C.c_int), ("lower", C.c_double * 4),
+                ("upper", C.c_double * 4), ("root_cells", C.c_int * 4), ("bc", C.c_int * 4)]
+
+
+class Model(C.Structure):
+    _fields_ = [("kind", C.c_int), ("weno_mode", C.c_int), ("epsilon", C.c_double),
+                ("speeds", C.c_double * 4), ("space_dim", C.c_int), ("theta", C.c_double),
+                ("tau", C.c_double)]
+
+
+class Policy(C.Structure):
+    _fields_ = [("mode", C.c_int), ("cfl", C.c_double), ("reference_spacing", C.c_double),
+                ("dt_scale", C.c_double)]
+
+
+class Failure(C.Structure):
+    _fields_ = [("member", C.c_int), ("step", C.c_longlong), ("stage", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("evolve_ms", C.c_double), ("combine_ms", C.c_double), ("steps", C.c_longlong),
+                ("kernel_launches", C.c_longlong), ("combine_launches", C.c_longlong),
+                ("pass_ms_sum", C.c_double), ("pass_launches", C.c_longlong),
+                ("pass_flops", C.c_double), ("pass_bytes", C.c_double)]
+
+
+STOP_CB = C.CFUNCTYPE(None, C.c_double, C.c_void_p)
+IC_CB = C.CFUNCTYPE(C.c_double, C.POINTER(C.c_double), C.c_int, C.c_void_p)
+_DP = C.POINTER(C.c_double)
+_IP = C.POINTER(C.c_int)
+_VP = C.c_void_p
+
+# name -> (restype, argtypes); must list every function of include/sgwg.h
+SIGNATURES = {
+    "sgwg_last_error": (C.c_char_p, []),
+    "sgwg_version": (C.c_int, []),
+    "sgwg_init": (C.c_int, [C.c_int, C.POINTER(_VP)]),
+    "sgwg_shutdown": (C.c_int, [_VP]),
+    "sgwg_set_arith": (C.c_int, [_VP, C.c_int]),
+    "sgwg_set_profile": (C.c_int, [_VP, C.c_int]),
+    "sgwg_stream": (_VP, [_VP]),
+    "sgwg_family_create": (C.c_int, [_VP, C.POINTER(Domain), C.POINTER(_VP)]),
+    "sgwg_family_create_shard": (C.c_int, [_VP, C.POINTER(Domain), _IP, C.c_int,
+                                           C.POINTER(_VP)]),
+    "sgwg_family_destroy": (C.c_int, [_VP]),
+    "sgwg_enumerate_levels": (C.c_int, [C.c_int, C.c_int, _IP, C.c_int, _IP]),
+    "sgwg_family_num_members": (C.c_int, [_VP, _IP]),
+    "sgwg_family_member": (C.c_int, [_VP, C.c_int, _IP, _IP, _IP]),
+    "sgwg_family_sizes": (C.c_int, [_VP, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "sgwg_family_upload": (C.c_int, [_VP, _DP, C.c_size_t]),
+    "sgwg_family_download": (C.c_int, [_VP, _DP, C.c_size_t]),
+    "sgwg_family_upload_device": (C.c_int, [_VP, _VP, C.c_size_t]),
+    "sgwg_family_download_device": (C.c_int, [_VP, _VP, C.c_size_t]),
+    "sgwg_set_model": (C.c_int, [_VP, C.POINTER(Model)]),
+    "sgwg_nccl_unique_id": (C.c_int, [_VP]),
+    "sgwg_family_set_comm": (C.c_int, [_VP, _VP, C.c_int, C.c_int]),
+    "sgwg_evolve": (C.c_int, [_VP, C.POINTER(Policy), C.c_double, _DP, C.c_int, STOP_CB, _VP,
+                              _DP, C.c_size_t, C.POINTER(C.c_size_t), C.POINTER(Failure)]),
+    "sgwg_combine": (C.c_int, [_VP, C.c_int, C.c_double, _VP, C.c_size_t, C.c_int]),
+    "sgwg_prolong": (C.c_int, [_VP, C.c_int, C.c_int, C.c_double, _VP, C.c_size_t, C.c_int]),
+    "sgwg_rhs": (C.c_int, [_VP, _VP, C.c_size_t, C.c_int]),
+    "sgwg_rk3_step": (C.c_int, [_VP, C.c_double, C.POINTER(Failure)]),
+    "sgwg_get_stats": (C.c_int, [_VP, C.POINTER(Stats)]),
+    "sgwg_family_init_preset": (C.c_int, [_VP, C.c_int]),
+    "sgwg_family_init_fn": (C.c_int, [_VP, IC_CB, _VP, C.c_int]),
+    "sgwg_fp64_peak": (C.c_int, [_VP, _DP]),
+}
+
+
+def load():
+    """Load the in-tree extension; raise (no fallback) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise SgwgError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+    lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(status, failure=None, family=None):
+    if status == OK:
+        return
+    msg = load().sgwg_last_error().decode()
+    if status == EINVAL:
+        raise ValueError(msg)
+    if status == ENONFINITE:
+        level = None
+        if failure is not None and family is not None and failure.member >= 0:
+            level = tuple(family.all_levels[failure.member])
+        raise FamilyIntegratorFailure(msg, failure.member if failure else -1, level,
+                                      failure.step if failure else -1,
+                                      failure.stage if failure else 0)
+    raise SgwgError(f"[{status}] {msg}")
+
+
+def enumerate_combination_levels(d: int, nl: int) -> np.ndarray:
+    """grid.hpp:57-79 (sorted lexicographically)."""
+    lib = load()
+    cnt = C.c_int(0)
+    _check(lib.sgwg_enumerate_levels(d, nl, None, 0, C.byref(cnt)))
+    out = np.zeros(cnt.value * d, dtype=np.int32)
+    _check(lib.sgwg_enumerate_levels(d, nl, out.ctypes.data_as(_IP), cnt.value, C.byref(cnt)))
+    return out.reshape(cnt.value, d)
+
+
+class Context:
+    """One CUDA device (one process per GPU)."""
+
+    def __init__(self, device: int = 0, arith: str = "exact", profile: bool = False):
+        lib = load()
+        h = _VP()
+        _check(lib.sgwg_init(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self.set_arith(arith)
+        self.set_profile(profile)
+
+    def set_arith(self, arith: str):
+        self.arith = arith
+        _check(load().sgwg_set_arith(self.h, ARITH_FAST if arith == "fast" else ARITH_EXACT))
+
+    def set_profile(self, on: bool):
+        _check(load().sgwg_set_profile(self.h, 1 if on else 0))
+
+    @property
+    def stream(self) -> int:
+        return load().sgwg_stream(self.h) or 0
+
+    def fp64_peak_tflops(self) -> float:
+        v = C.c_double(0)
+        _check(load().sgwg_fp64_peak(self.h, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if self.h:
+            load().sgwg_shutdown(self.h)
+            self.h = None
+
+
+def make_domain(d, nl, lower, upper, root, bc) -> Domain:
+    dom = Domain()
+    dom.d, dom.nl = d, nl
+    for k in range(d):
+        dom.lower[k], dom.upper[k] = lower[k], upper[k]
+        dom.root_cells[k], dom.bc[k] = root[k], bc[k]
+    return dom
+
+
+class Family:
+    """CombinationSet + FamilyModel on the device (make_family, combine.hpp:69-83)."""
+
+    def __init__(self, ctx: Context, d, nl, lower, upper, root_cells, bc,
+                 members: Optional[Sequence[int]] = None):
+        lib = load()
+        self.ctx = ctx
+        self.dom = make_domain(d, nl, lower, upper, root_cells, bc)
+        self.d, self.nl = d, nl
+        h = _VP()
+        if members is None:
+            _check(lib.sgwg_family_create(ctx.h, C.byref(self.dom), C.byref(h)))
+        else:
+            m = np.ascontiguousarray(members, dtype=np.int32)
+            _check(lib.sgwg_family_create_shard(ctx.h, C.byref(self.dom),
+                                                m.ctypes.data_as(_IP), len(m), C.byref(h)))
+        self.h = h
+        self.all_levels = enumerate_combination_levels(d, nl)
+        n = C.c_int(0)
+        _check(lib.sgwg_family_num_members(h, C.byref(n)))
+        self.num_members = n.value
+        self.global_index, self.levels, self.points = [], [], []
+        for mi in range(n.value):
+            g = C.c_int(0)
+            lv = (C.c_int * 4)()
+            pt = (C.c_int * 4)()
+            _check(lib.sgwg_family_member(h, mi, C.byref(g), lv, pt))
+            self.global_index.append(g.value)
+            self.levels.append(tuple(lv[:d]))
+            self.points.append(tuple(pt[:d]))
+        mp, fp = C.c_size_t(0), C.c_size_t(0)
+        _check(lib.sgwg_family_sizes(h, C.byref(mp), C.byref(fp)))
+        self.total_points, self.finest_points = mp.value, fp.value
+        self._keep = []
+
+    @classmethod
+    def from_config(cls, ctx: Context, cfg: dict, members=None) -> "Family":
+        f = cls(ctx, cfg["d"], cfg["nl"], cfg["lower"], cfg["upper"], cfg["root"], cfg["bc"],
+                members)
+        f.set_model(cfg["kind"], speeds=cfg["speeds"], epsilon=cfg["epsilon"],
+                    weno_mode=cfg["weno_mode"], space_dim=cfg["space_dim"],
+                    theta=cfg["theta"], tau=cfg["tau"])
+        return f
+
+    def member_offsets(self):
+        off, out = 0, []
+        for p in self.points:
+            out.append(off)
+            off += int(np.prod(p))
+        return out
+
+    # -- state -----------------------------------------------------------------
+    def initialize(self, preset: int):
+        """initialize_family (models.hpp:855-871) for a built-in preset."""
+        _check(load().sgwg_family_init_preset(self.h, preset))
+
+    def initialize_fn(self, fn: Callable[[np.ndarray], float], normalize_mass=False):
+        cb = IC_CB(lambda x, d, u: float(fn(np.ctypeslib.as_array(x, shape=(d,)))))
+        _check(load().sgwg_family_init_fn(self.h, cb, None, 1 if normalize_mass else 0))
+
+    def upload(self, states: np.ndarray):
+        s = np.ascontiguousarray(states, dtype=np.float64)
+        _check(load().sgwg_family_upload(self.h, s.ctypes.data_as(_DP), s.size))
+
+    def download(self) -> np.ndarray:
+        out = np.empty(self.total_points)
+        _check(load().sgwg_family_download(self.h, out.ctypes.data_as(_DP), out.size))
+        return out
+
+    def upload_device(self, ptr: int, n: int):
+        _check(load().sgwg_family_upload_device(self.h, _VP(ptr), n))
+
+    def download_device(self, ptr: int, n: int):
+        _check(load().sgwg_family_download_device(self.h, _VP(ptr), n))
+
+    # -- physics ---------------------------------------------------------------
+    def set_model(self, kind, speeds=(0, 0, 0, 0), epsilon=1e-6, weno_mode=0, space_dim=0,
+                  theta=1.0, tau=1.0):
+        m = Model()
+        m.kind, m.weno_mode, m.epsilon = kind, weno_mode, epsilon
+        for k, s in enumerate(list(speeds)[:4]):
+            m.speeds[k] = s
+        m.space_dim, m.theta, m.tau = space_dim, theta, tau
+        _check(load().sgwg_set_model(self.h, C.byref(m)))
+        self.model = m
+
+    def set_comm(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(load().sgwg_family_set_comm(self.h, buf, nranks, rank))
+
+    # -- evolve_family ------------------------------------------------------------
+    def evolve(self, mode, tfinal, stops=(), on_stop=None, cfl=0.4, reference_spacing=0.0,
+               dt_scale=1.0, cap=1 << 20) -> np.ndarray:
+        pol = Policy()
+        pol.mode, pol.cfl, pol.reference_spacing, pol.dt_scale = (mode, cfl, reference_spacing,
+                                                                  dt_scale)
+        st = np.ascontiguousarray(stops, dtype=np.float64)
+        dts = np.zeros(cap)
+        ns = C.c_size_t(0)
+        fail = Failure()
+
+        def _cb(t, user):
+            if on_stop is not None:
+                on_stop(t)
+
+        cb = STOP_CB(_cb)
+        status = load().sgwg_evolve(self.h, C.byref(pol), tfinal,
+                                    st.ctypes.data_as(_DP) if st.size else None, st.size, cb,
+                                    None, dts.ctypes.data_as(_DP), cap, C.byref(ns),
+                                    C.byref(fail))
+        _check(status, fail, self)
+        return dts[:min(ns.value, cap)].copy()
+
+    def evolve_config(self, cfg, tfinal=None, stops=None, on_stop=None):
+        return self.evolve(cfg["dt_mode"], cfg["tfinal"] if tfinal is None else tfinal,
+                           cfg["stops"] if stops is None else stops, on_stop, cfl=cfg["cfl"],
+                           reference_spacing=cfg["reference_spacing"], dt_scale=cfg["dt_scale"])
+
+    def rk3_step(self, dt):
+        fail = Failure()
+        _check(load().sgwg_rk3_step(self.h, dt, C.byref(fail)), fail, self)
+
+    def rhs(self) -> np.ndarray:
+        out = np.empty(self.total_points)
+        _check(load().sgwg_rhs(self.h, out.ctypes.data, out.size, 0))
+        return out
+
+    # -- combine / prolong -------------------------------------------------------
+    def combine(self, mode=1, eps=1e-6, out_device_ptr: Optional[int] = None) -> np.ndarray:
+        if out_device_ptr is not None:
+            _check(load().sgwg_combine(self.h, mode, eps, _VP(out_device_ptr),
+                                       self.finest_points, 1))
+            return None
+        out = np.empty(self.finest_points)
+        _check(load().sgwg_combine(self.h, mode, eps, out.ctypes.data, out.size, 0))
+        return out
+
+    def prolong(self, mi, mode=1, eps=1e-6) -> np.ndarray:
+        out = np.empty(self.finest_points)
+        _check(load().sgwg_prolong(self.h, mi, mode, eps, out.ctypes.data, out.size, 0))
+        return out
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(load().sgwg_get_stats(self.h, C.byref(s)))
+        return {n: getattr(s, n) for n, _ in Stats._fields_}
+
+    def close(self):
+        if self.h:
+            load().sgwg_family_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load().sgwg_nccl_unique_id(buf))
+    return buf.raw
+
+
+config = _cfg.config
