@@ -222,6 +222,12 @@ int sgwg_family_init_preset(sgwg_family* fam, int preset);
 typedef double (*sgwg_ic_fn)(const double* x, int d, void* user);
 int sgwg_family_init_fn(sgwg_family* fam, sgwg_ic_fn ic, void* user, int normalize_mass);
 
+/* Roofline probe: average device time of one WENO stage kernel launch (RK
+ * stage 1 of the current state, launched `reps` times back to back between
+ * CUDA events on the family stream), with the algorithmic flops / HBM bytes
+ * of one launch (SURVEY.md 8(d) counting). */
+int sgwg_time_stage(sgwg_family* fam, int reps, double* avg_ms, double* flops, double* bytes);
+
 /* DFMA throughput probe (TFLOP/s) used as the measured fp64 roofline peak. */
 int sgwg_fp64_peak(sgwg_ctx* ctx, double* tflops);
 

@@ -1,0 +1,106 @@
+// dt_device.cuh -- device-side compute_dt + stop landing, exact IEEE arithmetic
+// through explicit round-to-nearest intrinsics (never FMA-contracted, whatever
+// the TU's --fmad setting), so the dt sequence is bitwise the reference's.
+#pragma once
+#include <limits.h>
+
+#include "sgwg_internal.h"
+
+namespace sgwg {
+
+__device__ __forceinline__ double vload(const double* p) { return *(volatile const double*)p; }
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+  return *(volatile const unsigned long long*)p;
+}
+
+// FamilyModel::family_wave_speeds (models.hpp:791-839) over the local members;
+// sp[kMaxD] carries the failure flag so one all-reduce(max) propagates it.
+__device__ inline void device_local_speeds(const DtParams& p, double* sp) {
+  for (int k = 0; k < kMaxD + 1; ++k) sp[k] = 0.0;
+  if (p.kind == 1) {  // Burgers: family max|u^n| (models.hpp:798-802)
+    double umax = 0.0;
+    for (int m = 0; m < p.nmembers; ++m) {
+      const double a = __longlong_as_double((long long)vload(p.amax + m));
+      umax = (umax < a) ? a : umax;
+    }
+    for (int k = 0; k < p.d; ++k) sp[k] = umax;
+  } else {
+    for (int k = 0; k < p.d; ++k) sp[k] = p.const_speeds[k];
+    if (p.kind == 3) {  // Vlasov-Poisson: v-directions from the family max|E_j|
+      for (int m = 0; m < p.nmembers; ++m)
+        for (int j = 0; j < p.space_dim; ++j) {
+          const double a = vload(p.emax + m * p.space_dim + j);
+          sp[p.space_dim + j] = (sp[p.space_dim + j] < a) ? a : sp[p.space_dim + j];
+        }
+    }
+  }
+  double failed = 0.0;
+  for (int m = 0; m < p.nmembers; ++m)
+    if (vload(p.fail + m) != ULLONG_MAX) failed = 1.0;
+  sp[kMaxD] = failed;
+}
+
+// one iteration of evolve_family's step loop (timestep.hpp:152-168):
+// compute_dt (timestep.hpp:47-67) and the exact landing (timestep.hpp:155).
+__device__ inline void device_step_dt(const DtParams& p, bool use_reduced) {
+  StepCtl* c = p.ctl;
+  if (!c->active) return;
+  double sp[kMaxD + 1];
+  if (use_reduced) {
+    for (int k = 0; k < kMaxD + 1; ++k) sp[k] = vload(&c->speeds[k]);
+  } else {
+    device_local_speeds(p, sp);
+  }
+  if (sp[kMaxD] > 0.0) {
+    c->active = 0;
+    c->failed = 1;
+    return;
+  }
+  const double t = c->t, stop = c->stop;
+  if (!(__dsub_rn(stop, t) > c->eps_t)) {
+    c->active = 0;
+    return;
+  }
+  const double remaining = __dsub_rn(stop, t);
+  double dt;
+  if (p.mode == 0) {
+    double inv = 0.0;
+    for (int k = 0; k < p.d; ++k) inv = __dadd_rn(inv, __ddiv_rn(sp[k], p.fine_h[k]));
+    if (inv == 0.0) {
+      dt = remaining;
+    } else {
+      dt = __ddiv_rn(p.cfl, inv);
+      dt = (remaining < dt) ? remaining : dt;  // std::min(dt, remaining)
+    }
+  } else {
+    dt = p.base_dt;
+    dt = (remaining < dt) ? remaining : dt;
+  }
+  if (__dsub_rn(stop, __dadd_rn(t, dt)) <= c->eps_t) dt = __dsub_rn(stop, t);
+  c->dt = dt;
+  c->cur_step = c->step;
+  if (p.dts != nullptr && c->step < p.dts_cap) p.dts[c->step] = dt;
+  c->step = c->step + 1;
+  c->t = __dadd_rn(t, dt);
+}
+
+// Last-CTA-done epilogue of the stage-3 kernel: once every CTA of the grid
+// has published its max|u| / failure atomics, the last one computes the next
+// step's dt, so a step is three kernel launches.
+__device__ inline void fused_step_dt(const DtParams* dtp, unsigned int* counter) {
+  __shared__ unsigned int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(counter, 1u);
+    s_last = (prev == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    *counter = 0u;
+    device_step_dt(*dtp, false);
+  }
+}
+
+}  // namespace sgwg

@@ -9,82 +9,16 @@
 
 #include <limits.h>
 
-namespace sgwg {
+#include "dt_device.cuh"
 
-// FamilyModel::family_wave_speeds (models.hpp:791-839) over the local members;
-// speeds[d] carries the failure flag so one all-reduce(max) propagates it.
-__device__ void local_speeds(const DtParams& p, double* sp) {
-  for (int k = 0; k < kMaxD + 1; ++k) sp[k] = 0.0;
-  if (p.kind == 1) {  // Burgers: family max|u^n| (models.hpp:798-802)
-    double umax = 0.0;
-    for (int m = 0; m < p.nmembers; ++m) {
-      const double a = __longlong_as_double((long long)p.amax[m]);
-      umax = (umax < a) ? a : umax;
-    }
-    for (int k = 0; k < p.d; ++k) sp[k] = umax;
-  } else {
-    for (int k = 0; k < p.d; ++k) sp[k] = p.const_speeds[k];
-    if (p.kind == 3) {  // Vlasov-Poisson: v-directions from the family max|E_j|
-      for (int m = 0; m < p.nmembers; ++m)
-        for (int j = 0; j < p.space_dim; ++j) {
-          const double a = p.emax[m * p.space_dim + j];
-          sp[p.space_dim + j] = (sp[p.space_dim + j] < a) ? a : sp[p.space_dim + j];
-        }
-    }
-  }
-  double failed = 0.0;
-  for (int m = 0; m < p.nmembers; ++m)
-    if (p.fail[m] != ULLONG_MAX) failed = 1.0;
-  sp[kMaxD] = failed;
-}
+namespace sgwg {
 
 __global__ void local_speeds_kernel(const DtParams p) {
   if (!p.ctl->active) return;
-  local_speeds(p, p.ctl->speeds);
+  device_local_speeds(p, p.ctl->speeds);
 }
 
-// one iteration of evolve_family's step loop (timestep.hpp:152-168) with
-// compute_dt (timestep.hpp:47-67) and exact landing (timestep.hpp:155).
-__global__ void dt_kernel(const DtParams p) {
-  StepCtl* c = p.ctl;
-  if (!c->active) return;
-  double sp[kMaxD + 1];
-  if (p.use_reduced) {
-    for (int k = 0; k < kMaxD + 1; ++k) sp[k] = c->speeds[k];
-  } else {
-    local_speeds(p, sp);
-  }
-  if (sp[kMaxD] > 0.0) {
-    c->active = 0;
-    c->failed = 1;
-    return;
-  }
-  if (!(c->stop - c->t > c->eps_t)) {
-    c->active = 0;
-    return;
-  }
-  const double remaining = c->stop - c->t;
-  double dt;
-  if (p.mode == 0) {
-    double inv = 0.0;
-    for (int k = 0; k < p.d; ++k) inv += sp[k] / p.fine_h[k];
-    if (inv == 0.0) {
-      dt = remaining;
-    } else {
-      dt = p.cfl / inv;
-      dt = (remaining < dt) ? remaining : dt;  // std::min(dt, remaining)
-    }
-  } else {
-    dt = p.base_dt;
-    dt = (remaining < dt) ? remaining : dt;
-  }
-  if (c->stop - (c->t + dt) <= c->eps_t) dt = c->stop - c->t;
-  c->dt = dt;
-  c->cur_step = c->step;
-  if (p.dts != nullptr && c->step < p.dts_cap) p.dts[c->step] = dt;
-  c->step = c->step + 1;
-  c->t = c->t + dt;
-}
+__global__ void dt_kernel(const DtParams p) { device_step_dt(p, p.use_reduced != 0); }
 
 cudaError_t launch_local_speeds(const DtParams& p, cudaStream_t s) {
   local_speeds_kernel<<<1, 1, 0, s>>>(p);

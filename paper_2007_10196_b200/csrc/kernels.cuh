@@ -20,6 +20,7 @@
 //   final_kernel          the last dimension of prolong fused with the signed
 //                         combination sum in sorted member order (combine.hpp:113-120).
 #pragma once
+#include "dt_device.cuh"
 #include "sgwg_internal.h"
 
 #ifndef SGWG_FAST
@@ -275,7 +276,437 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
     if ((tid & 31) == 0)
       atomicMax(p.amax_out + tk.x, (unsigned long long)__double_as_longlong(lmax));
   }
+  if (p.last && p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
 }
+
+// ---------------------------------------------------------------------------
+// fused 2D stage: both sweeps + SSP-RK3 stage update in one launch
+// ---------------------------------------------------------------------------
+// A CTA owns a TX x TY tile of one member (thread per point).  It stages the
+// tile plus 3-point halos along each axis (no corners) in shared memory,
+// computes every x-interface flux F(i+1/2, j) and y-interface flux
+// G(i, j+1/2) of the tile exactly once, then forms
+//   k = (0 - (F(i+1/2)-F(i-1/2))/h0) - (G(j+1/2)-G(j-1/2))/h1
+// in the reference's accumulation order (models.hpp:187-197) and applies the
+// RK stage.  Same arithmetic per interface as pass_kernel, so both are
+// bitwise equal to the reference in the exact build.
+__device__ __forceinline__ double line_coef(int flux, const MemberDesc* M, int k, int space_dim,
+                                            int idx_other, double c_const,
+                                            const double* efield) {
+  if (flux == kFluxKinX) return M->lower[space_dim + k] + idx_other * M->h[space_dim + k];
+  if (flux == kFluxKinVB) return -(M->lower[k - space_dim] + idx_other * M->h[k - space_dim]);
+  if (flux == kFluxKinVP) return -efield[M->xoff * space_dim + (long long)(k - space_dim) * M->nx +
+                                         idx_other];
+  return c_const;
+}
+
+template <bool BURGERS>
+__global__ void __launch_bounds__(256) stage2d_kernel(const Stage2DParams p) {
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  const int4 tk = p.tiles[blockIdx.x];
+  const MemberDesc* M = p.mem + tk.x;
+  const int n0 = M->ext[0], n1 = M->ext[1];
+  const int TX = M->tx, TY = M->ty;
+  const int i0 = tk.y, j0 = tk.z;
+  const int TXe = min(TX, n0 - i0), TYe = min(TY, n1 - j0);
+  const int PY = TY + 6;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  extern __shared__ double sm[];
+  double* A = sm;                                      // fp (Burgers) or u
+  double* Bm = A + (TX + 6) * PY;                      // fm (Burgers)
+  double* Fx = BURGERS ? Bm + (TX + 6) * PY : Bm;      // (TX+1) x TY
+  double* Fy = Fx + (TX + 1) * TY;                     // TX x (TY+1)
+  double* cx = Fy + TX * (TY + 1);                     // per column (x-lines)
+  double* cy = cx + TY;                                // per row (y-lines)
+
+  if (p.amax_zero != nullptr && blockIdx.x == 0)
+    for (int i = tid; i < p.nmembers; i += nt) p.amax_zero[i] = 0ull;
+  if (!BURGERS) {
+    for (int j = tid; j < TYe; j += nt)
+      cx[j] = line_coef(p.flux0, M, 0, p.space_dim, j0 + j, p.c0, p.efield);
+    for (int i = tid; i < TXe; i += nt)
+      cy[i] = line_coef(p.flux1, M, 1, p.space_dim, i0 + i, p.c1, p.efield);
+  }
+  const double* u = p.uin + M->offset;
+  const double alpha = BURGERS ? __longlong_as_double((long long)p.amax_in[tk.x]) : 0.0;
+  const int bc0 = M->bc[0], bc1 = M->bc[1];
+  const int LX = TXe + 6, LY = TYe + 6;
+  for (int q = tid; q < LX * LY; q += nt) {
+    const int a = q / LY, b = q - a * LY;
+    if ((a < 3 || a >= TXe + 3) && (b < 3 || b >= TYe + 3)) continue;  // corners unused
+    int gi = i0 - 3 + a, gj = j0 - 3 + b;
+    bool zero = false;
+    if (bc0 == 0) {
+      gi %= n0;
+      if (gi < 0) gi += n0;
+    } else if (gi < 0 || gi >= n0) {
+      zero = true;
+    }
+    if (bc1 == 0) {
+      gj %= n1;
+      if (gj < 0) gj += n1;
+    } else if (gj < 0 || gj >= n1) {
+      zero = true;
+    }
+    const double uj = zero ? 0.0 : __ldg(u + (long long)gi * n1 + gj);
+    if (BURGERS) {
+      const double f = 0.5 * uj * uj;             // models.hpp:194
+      const double fpj = 0.5 * (f + alpha * uj);  // weno.hpp:138-140
+      A[a * PY + b] = fpj;
+      Bm[a * PY + b] = f - fpj;
+    } else {
+      A[a * PY + b] = uj;
+    }
+  }
+  __syncthreads();
+
+  const double eps = p.eps;
+  const int linear = p.linear;
+  // x-interfaces: (TXe+1) x TYe, F[ia][j] = flux at (i0+ia-1)+1/2, column j
+  for (int q = tid; q < (TXe + 1) * TYe; q += nt) {
+    const int ia = q / TYe, j = q - ia * TYe;
+    const double* col = A + j + 3;
+    double F;
+    if (BURGERS) {
+      const double* colm = Bm + j + 3;
+      F = recon(col[ia * PY], col[(ia + 1) * PY], col[(ia + 2) * PY], col[(ia + 3) * PY],
+                col[(ia + 4) * PY], eps, linear) +
+          recon(colm[(ia + 5) * PY], colm[(ia + 4) * PY], colm[(ia + 3) * PY],
+                colm[(ia + 2) * PY], colm[(ia + 1) * PY], eps, linear);
+    } else {
+      const double c = cx[j];
+      const int b0 = (c < 0.0) ? ia + 5 : ia;  // downwind: reversed window (weno.hpp:178-183)
+      const int s = (c < 0.0) ? -PY : PY;
+      const double* w = col + b0 * PY;
+      F = recon(c * w[0], c * w[s], c * w[2 * s], c * w[3 * s], c * w[4 * s], eps, linear);
+    }
+    Fx[ia * TY + j] = F;
+  }
+  // y-interfaces: TXe x (TYe+1), G[i][jb] = flux at row i, (j0+jb-1)+1/2
+  for (int q = tid; q < TXe * (TYe + 1); q += nt) {
+    const int i = q / (TYe + 1), jb = q - i * (TYe + 1);
+    const double* row = A + (i + 3) * PY;
+    double G;
+    if (BURGERS) {
+      const double* rowm = Bm + (i + 3) * PY;
+      G = recon(row[jb], row[jb + 1], row[jb + 2], row[jb + 3], row[jb + 4], eps, linear) +
+          recon(rowm[jb + 5], rowm[jb + 4], rowm[jb + 3], rowm[jb + 2], rowm[jb + 1], eps,
+                linear);
+    } else {
+      const double c = cy[i];
+      const int b0 = (c < 0.0) ? jb + 5 : jb;
+      const int s = (c < 0.0) ? -1 : 1;
+      const double* w = row + b0;
+      G = recon(c * w[0], c * w[s], c * w[2 * s], c * w[3 * s], c * w[4 * s], eps, linear);
+    }
+    Fy[i * (TY + 1) + jb] = G;
+  }
+  __syncthreads();
+
+  double lmax = 0.0;
+  const int ti = tid / TY, tj = tid - (tid / TY) * TY;
+  if (ti < TXe && tj < TYe) {
+#if SGWG_FAST
+    const double dux = (Fx[(ti + 1) * TY + tj] - Fx[ti * TY + tj]) * M->inv_h[0];
+    const double duy = (Fy[ti * (TY + 1) + tj + 1] - Fy[ti * (TY + 1) + tj]) * M->inv_h[1];
+#else
+    const double dux = (Fx[(ti + 1) * TY + tj] - Fx[ti * TY + tj]) / M->h[0];
+    const double duy = (Fy[ti * (TY + 1) + tj + 1] - Fy[ti * (TY + 1) + tj]) / M->h[1];
+#endif
+    const double kv = (0.0 - dux) - duy;
+    const long long gi = M->offset + (long long)(i0 + ti) * n1 + (j0 + tj);
+    double o;
+    if (p.stage == 0) {
+      o = kv;
+    } else {
+      if (!isfinite(kv)) {
+        const unsigned long long code =
+            (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
+        atomicMin(p.fail + tk.x, code);
+      }
+      const double dt = ctl->dt;
+      const double ui = p.uin[gi];
+      if (p.stage == 1)
+        o = ui + dt * kv;
+      else if (p.stage == 2)
+        o = 0.75 * p.un[gi] + 0.25 * (ui + dt * kv);
+      else
+        o = (1.0 / 3.0) * p.un[gi] + (2.0 / 3.0) * (ui + dt * kv);
+    }
+    p.out[gi] = o;
+    lmax = fabs(o);
+  }
+  if (p.track_max) {
+    lmax = warp_max(lmax);
+    if ((tid & 31) == 0) {
+      atomicMax(p.amax_out + tk.x, (unsigned long long)__double_as_longlong(lmax));
+    }
+  }
+  if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+
+#if SGWG_FAST
+// ---------------------------------------------------------------------------
+// fast 2D stage: sliding-window reconstructions with shared smoothness terms
+// ---------------------------------------------------------------------------
+// With D(j) = f_{j-1} - 2 f_j + f_{j+1} and d(j) = f_j - f_{j-1}, the
+// positive reconstruction at x_{i+1/2} (weno.hpp:60-72) is exactly
+//   f_i + sum_r w_r c_r / (6 sum_r w_r),
+//   c_0 = 2D(i-1) + 3d(i),  c_1 = -D(i) + 3d(i+1),  c_2 = -D(i+1) + 3d(i+1),
+//   4(eps+b_0) = (2d(i)+D(i-1))^2 + K(i-1),  4(eps+b_1) = (d(i)+d(i+1))^2 + K(i),
+//   4(eps+b_2) = (D(i+1)-2d(i+1))^2 + K(i+1),   K(j) = 13/3 D(j)^2 + 4 eps,
+//   w_r ~ (1, 6, 3)_r * prod_{s != r} (4(eps+b_s))^2,
+// and the negative one is its mirror about x_{i+1/2}.  D, d and K of a point
+// are shared by the three interfaces that see it, so a thread that slides
+// along RUN consecutive interfaces computes them once.  One reciprocal per
+// reconstruction (rcp.approx + Newton).  Rounding differs from the reference
+// at the 1e-16 level; the parity bar for this build is 1e-10.
+
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
+// generic role form: A,B,C = D at the three substencil centres, a,b = the two
+// first differences, fc = centre value; returns the reconstruction.
+__device__ __forceinline__ double recon_roles(double fc, double A, double B, double C, double KA,
+                                              double KB, double KC, double a, double b,
+                                              int linear) {
+  const double c0 = fma(3.0, a, 2.0 * A);
+  const double c1 = fma(3.0, b, -B);
+  const double c2 = fma(3.0, b, -C);
+  if (linear) return fc + kSixth * fma(0.1, c0, fma(0.6, c1, 0.3 * c2));
+  const double g0 = fma(2.0, a, A);
+  const double g1 = a + b;
+  const double g2 = fma(-2.0, b, C);
+  const double e0 = fma(g0, g0, KA), e1 = fma(g1, g1, KB), e2 = fma(g2, g2, KC);
+  const double q0 = e0 * e0, q1 = e1 * e1, q2 = e2 * e2;
+  const double w0 = q1 * q2;
+  const double w1 = (6.0 * q0) * q2;
+  const double w2 = (3.0 * q0) * q1;
+  const double num = fma(w0, c0, fma(w1, c1, w2 * c2));
+  const double den = 6.0 * (w0 + w1 + w2);
+  return fc + num * fast_rcp(den);
+}
+
+// du = (F(i+1/2) - F(i-1/2)) / h for RUN consecutive points of one line held
+// in shared memory (padded index q -> base[q * st]; the run's first point has
+// padded index p0+3).  BURGERS: F = pos(fp) + neg(fm); else F = upwind recon
+// of c*u (direction from the sign of c, weno.hpp:178-183).
+// Not inlined: one copy of the (large, fully unrolled) line sweep serves the
+// x and y sweeps of every tile shape, keeping the hot code in the i-cache.
+// du[t] is written to out[t * ost] (shared memory).
+template <bool BURGERS, int RUN>
+__device__ __noinline__ void sweep_run(const double* __restrict__ P,
+                                       const double* __restrict__ Mv, int st, int p0, double c,
+                                       double eps4, double inv_h, int linear,
+                                       double* __restrict__ out, int ost) {
+  double du[RUN];
+  constexpr int NV = RUN + 6;
+  double fp[NV], fm[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    fp[q] = P[(p0 + q) * st];
+    if (BURGERS) fm[q] = Mv[(p0 + q) * st];
+  }
+  if (!BURGERS) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) fp[q] *= c;
+  }
+  // D, d, K at padded positions (index into fp/fm)
+  auto D = [&](const double* f, int q) { return fma(-2.0, f[q], f[q - 1] + f[q + 1]); };
+  auto K = [&](double Dq) { return fma(13.0 / 3.0 * Dq, Dq, eps4); };
+  double Dp[NV], Kp[NV], dp[NV], Dm[NV], Km[NV], dm[NV];
+#pragma unroll
+  for (int q = 1; q < NV - 1; ++q) {
+    Dp[q] = D(fp, q);
+    Kp[q] = K(Dp[q]);
+    if (BURGERS) {
+      Dm[q] = D(fm, q);
+      Km[q] = K(Dm[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 1; q < NV; ++q) {
+    dp[q] = fp[q] - fp[q - 1];
+    if (BURGERS) dm[q] = fm[q] - fm[q - 1];
+  }
+  const bool down = (c < 0.0);
+  double fprev = 0.0;
+#pragma unroll
+  for (int t = 0; t <= RUN; ++t) {
+    const int i = t + 2;  // local point left of interface t (padded index)
+    double F;
+    if (BURGERS) {
+      const double fpos = recon_roles(fp[i], Dp[i - 1], Dp[i], Dp[i + 1], Kp[i - 1], Kp[i],
+                                      Kp[i + 1], dp[i], dp[i + 1], linear);
+      const int m = i + 1;
+      const double fneg = recon_roles(fm[m], Dm[m + 1], Dm[m], Dm[m - 1], Km[m + 1], Km[m],
+                                      Km[m - 1], -dm[m + 1], -dm[m], linear);
+      F = fpos + fneg;
+    } else {
+      const int m = i + 1;
+      const double fc = down ? fp[m] : fp[i];
+      const double A = down ? Dp[m + 1] : Dp[i - 1];
+      const double B = down ? Dp[m] : Dp[i];
+      const double C = down ? Dp[m - 1] : Dp[i + 1];
+      const double KA = down ? Kp[m + 1] : Kp[i - 1];
+      const double KB = down ? Kp[m] : Kp[i];
+      const double KC = down ? Kp[m - 1] : Kp[i + 1];
+      const double a = down ? -dp[m + 1] : dp[i];
+      const double b = down ? -dp[m] : dp[i + 1];
+      F = recon_roles(fc, A, B, C, KA, KB, KC, a, b, linear);
+    }
+    if (t > 0) du[t - 1] = (F - fprev) * inv_h;
+    fprev = F;
+  }
+#pragma unroll
+  for (int t = 0; t < RUN; ++t) out[t * ost] = du[t];
+}
+
+template <bool BURGERS, int TX, int TY>
+__device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const MemberDesc* M,
+                                                  int mi, int i0, int j0, double* sm) {
+  constexpr int RUN = 8;
+  constexpr int PY = ((TY + 6) % 2 == 0) ? TY + 7 : TY + 6;  // odd pitch
+  constexpr int DP = TY + 1;                                  // du pitch (odd for TY even)
+  constexpr int NS = TX * TY / RUN;  // threads per sweep; x and y sweeps run concurrently
+  constexpr int NT = 2 * NS;
+  double* FP = sm;
+  double* FM = FP + (TX + 6) * PY;
+  double* DX = FM + (BURGERS ? (TX + 6) * PY : 0);
+  double* DY = DX + TX * DP;
+  double* cx = DY + TX * DP;
+  double* cy = cx + TY;
+  const int n0 = M->ext[0], n1 = M->ext[1];
+  const int tid = threadIdx.x;
+  if (!BURGERS) {
+    for (int j = tid; j < TY; j += NT)
+      cx[j] = line_coef(p.flux0, M, 0, p.space_dim, min(j0 + j, n1 - 1), p.c0, p.efield);
+    for (int i = tid; i < TX; i += NT)
+      cy[i] = line_coef(p.flux1, M, 1, p.space_dim, min(i0 + i, n0 - 1), p.c1, p.efield);
+  }
+  const double* u = p.uin + M->offset;
+  const double alpha = BURGERS ? __longlong_as_double((long long)p.amax_in[mi]) : 0.0;
+  const int bc0 = M->bc[0], bc1 = M->bc[1];
+  constexpr int LY = TY + 6;
+  constexpr int NLOAD = ((TX + 6) * LY + NT - 1) / NT;
+  // all global loads of the thread issued back to back, then split + stored
+  double v[NLOAD];
+  int dst[NLOAD];
+#pragma unroll
+  for (int kq = 0; kq < NLOAD; ++kq) {
+    const int q = tid + kq * NT;
+    const int a = q / LY, b = q - (q / LY) * LY;
+    dst[kq] = -1;
+    v[kq] = 0.0;
+    if (q >= (TX + 6) * LY) continue;
+    if ((a < 3 || a >= TX + 3) && (b < 3 || b >= TY + 3)) continue;
+    dst[kq] = a * PY + b;
+    int gi = i0 - 3 + a, gj = j0 - 3 + b;
+    bool zero = false;
+    if (bc0 == 0) {
+      if (gi < 0 || gi >= n0) {  // periodic wrap ((j%n)+n)%n (tiles may exceed tiny lines)
+        gi %= n0;
+        if (gi < 0) gi += n0;
+      }
+    } else {
+      zero = (gi < 0 || gi >= n0);
+    }
+    if (bc1 == 0) {
+      if (gj < 0 || gj >= n1) {
+        gj %= n1;
+        if (gj < 0) gj += n1;
+      }
+    } else {
+      zero = zero || (gj < 0 || gj >= n1);
+    }
+    v[kq] = zero ? 0.0 : __ldg(u + gi * n1 + gj);
+  }
+#pragma unroll
+  for (int kq = 0; kq < NLOAD; ++kq) {
+    if (dst[kq] < 0) continue;
+    const double uj = v[kq];
+    if (BURGERS) {
+      const double f = 0.5 * uj * uj;
+      const double fpj = 0.5 * (f + alpha * uj);
+      FP[dst[kq]] = fpj;
+      FM[dst[kq]] = f - fpj;
+    } else {
+      FP[dst[kq]] = uj;
+    }
+  }
+  __syncthreads();
+  const double eps4 = 4.0 * p.eps;
+  if (tid < NS) {  // x-sweep warps: thread = (column j, run of RUN rows)
+    const int j = tid % TY, r = tid / TY;
+    const double c = BURGERS ? 0.0 : cx[j];
+    sweep_run<BURGERS, RUN>(FP + j + 3, FM + j + 3, PY, r * RUN, c, eps4, M->inv_h[0], p.linear,
+                            DX + r * RUN * DP + j, DP);
+  } else {  // y-sweep warps: thread = (row i, run of RUN columns)
+    const int i = (tid - NS) % TX, r = (tid - NS) / TX;
+    const double c = BURGERS ? 0.0 : cy[i];
+    sweep_run<BURGERS, RUN>(FP + (i + 3) * PY, FM + (i + 3) * PY, 1, r * RUN, c, eps4,
+                            M->inv_h[1], p.linear, DY + i * DP + r * RUN, 1);
+  }
+  __syncthreads();
+  // epilogue: k = (0 - du_x) - du_y, RK stage, coalesced along j
+  double lmax = 0.0;
+  const StepCtl* ctl = p.ctl;
+  const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
+  for (int q = tid; q < TX * TY; q += NT) {
+    const int ti = q / TY, tj = q % TY;
+    if (i0 + ti >= n0 || j0 + tj >= n1) continue;
+    const double kv = (0.0 - DX[ti * DP + tj]) - DY[ti * DP + tj];
+    const long long gi = M->offset + (long long)(i0 + ti) * n1 + (j0 + tj);
+    double o;
+    if (p.stage == 0) {
+      o = kv;
+    } else {
+      if (!isfinite(kv)) {
+        const unsigned long long code =
+            (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
+        atomicMin(p.fail + mi, code);
+      }
+      const double ui = p.uin[gi];
+      if (p.stage == 1)
+        o = fma(dt, kv, ui);
+      else if (p.stage == 2)
+        o = fma(0.75, p.un[gi], 0.25 * fma(dt, kv, ui));
+      else
+        o = fma(1.0 / 3.0, p.un[gi], (2.0 / 3.0) * fma(dt, kv, ui));
+    }
+    p.out[gi] = o;
+    lmax = fmax(lmax, fabs(o));
+  }
+  if (p.track_max) {
+    lmax = warp_max(lmax);
+    if ((tid & 31) == 0) atomicMax(p.amax_out + mi, (unsigned long long)__double_as_longlong(lmax));
+  }
+}
+
+template <bool BURGERS>
+__global__ void __launch_bounds__(512, 1) stage2d_fast_kernel(const Stage2DParams p) {
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  const int4 tk = p.tiles[blockIdx.x];
+  const MemberDesc* M = p.mem + tk.x;
+  extern __shared__ double sm[];
+  if (p.amax_zero != nullptr && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < p.nmembers; i += blockDim.x) p.amax_zero[i] = 0ull;
+  switch (tk.w) {  // tile shape (TX, TY), TX*TY = 2048, 256 threads
+    case 0: stage2d_fast_body<BURGERS, 32, 64>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 1: stage2d_fast_body<BURGERS, 64, 32>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 2: stage2d_fast_body<BURGERS, 16, 128>(p, M, tk.x, tk.y, tk.z, sm); break;
+    default: stage2d_fast_body<BURGERS, 128, 16>(p, M, tk.x, tk.y, tk.z, sm); break;
+  }
+  if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+#endif  // SGWG_FAST
 
 // ---------------------------------------------------------------------------
 // prolongation / combination
@@ -399,11 +830,35 @@ __global__ void __launch_bounds__(256) final_kernel(const FinalParams p) {
 }
 
 cudaError_t configure() {
+#if SGWG_FAST
+  cudaError_t e0 = cudaFuncSetAttribute(stage2d_fast_kernel<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage2d_fast_kernel<false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+#endif
   cudaError_t e = cudaFuncSetAttribute(pass_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               160 * 1024);
+}
+
+cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s) {
+  if (nblocks <= 0) return cudaSuccess;
+#if SGWG_FAST
+  if (p.burgers)
+    stage2d_fast_kernel<true><<<nblocks, 512, smem, s>>>(p);
+  else
+    stage2d_fast_kernel<false><<<nblocks, 512, smem, s>>>(p);
+#else
+  if (p.burgers)
+    stage2d_kernel<true><<<nblocks, 256, smem, s>>>(p);
+  else
+    stage2d_kernel<false><<<nblocks, 256, smem, s>>>(p);
+#endif
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pass(const PassParams& p, int nblocks, size_t smem, cudaStream_t s) {

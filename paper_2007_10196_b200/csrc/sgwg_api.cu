@@ -15,6 +15,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -191,6 +192,16 @@ struct sgwg_family {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // current policy for graph building
   DtParams dtp{};
+  DtParams* d_dtp = nullptr;       // device copy (fused dt)
+  unsigned int* counter = nullptr;  // CTA-done counter (fused dt)
+  // 2D fused-stage tiles
+  int4* dtiles2d = nullptr;
+  int ntiles2d = 0;
+  int smem2d = 0;
+  int4* dtiles2d_fast = nullptr;
+  int ntiles2d_fast = 0;
+  int smem2d_fast = 0;
+  bool no_fused2d = false;  // SGWG_NO_FUSED2D=1: use the per-dimension pass kernels
 };
 
 namespace {
@@ -222,28 +233,95 @@ std::vector<PassDesc> pass_order(const sgwg_family* f) {
   return v;
 }
 
+void account_timed(sgwg_family* f, int stage, int npass_dims, bool last, float ms) {
+  f->stats.pass_ms_sum += ms;
+  f->stats.pass_launches++;
+  // algorithmic counts: per point and direction
+  // advective 70 flops, Burgers 142; RK stage update 2/5/5 flops;
+  // stage bytes 16 (stage 1) / 24 (stages 2, 3) per point.
+  const double pts = (double)f->total;
+  const bool burgers = f->model.kind == SGWG_BURGERS;
+  f->stats.pass_flops += pts * (burgers ? 142.0 : 70.0) * npass_dims;
+  if (last && stage > 0) {
+    f->stats.pass_flops += pts * (stage == 1 ? 2.0 : 5.0);
+    f->stats.pass_bytes += pts * (stage == 1 ? 16.0 : 24.0);
+  }
+}
+
+int launch_field_for(sgwg_family* f, const double* state, int stage) {
+  const sgwg_model& m = f->model;
+  FieldParams fp{};
+  fp.mem = f->dmem;
+  fp.f = state;
+  fp.rho = f->rho;
+  fp.efield = f->E;
+  fp.emax = f->emax;
+  fp.space_dim = m.space_dim;
+  fp.stage = stage;
+  fp.L[0] = f->dom.upper[0] - f->dom.lower[0];
+  fp.L[1] = (m.space_dim == 2) ? f->dom.upper[1] - f->dom.lower[1] : 1.0;
+  fp.ctl = f->ctl;
+  CK(launch_field(fp, f->nm, f->ctx->stream));
+  f->stats.kernel_launches++;
+  return SGWG_OK;
+}
+
 // One RK stage (stage 1..3) or a bare tendency evaluation (stage 0).
-int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool with_field = true) {
+// fuse_dt: the stage-3 kernel also computes the next step's dt (last CTA).
+int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool with_field = true,
+                 bool fuse_dt = false) {
   const sgwg_model& m = f->model;
   const bool burgers = (m.kind == SGWG_BURGERS);
-  if (m.kind == SGWG_VLASOV_POISSON && with_field) {
-    FieldParams fp{};
-    fp.mem = f->dmem;
-    fp.f = b.uin;
-    fp.rho = f->rho;
-    fp.efield = f->E;
-    fp.emax = f->emax;
-    fp.space_dim = m.space_dim;
-    fp.stage = stage;
-    fp.L[0] = f->dom.upper[0] - f->dom.lower[0];
-    fp.L[1] = (m.space_dim == 2) ? f->dom.upper[1] - f->dom.lower[1] : 1.0;
-    fp.ctl = f->ctl;
-    CK(launch_field(fp, f->nm, f->ctx->stream));
-    f->stats.kernel_launches++;
-  }
+  if (m.kind == SGWG_VLASOV_POISSON && with_field) TRY(launch_field_for(f, b.uin, stage));
   const auto order = pass_order(f);
   const int in_slot = (stage == 0) ? 0 : stage - 1;
   const int out_slot = (stage == 0) ? 0 : stage % 3;
+  // stage s clears the slot stage s+1 will write: it was last read one stage ago
+  unsigned long long* zero_slot =
+      (burgers && stage > 0) ? f->amax + (size_t)((stage + 1) % 3) * f->nm : nullptr;
+  const DtParams* dtp = (fuse_dt && stage == 3) ? f->d_dtp : nullptr;
+  if (f->d == 2 && f->ntiles2d > 0) {
+    Stage2DParams p{};
+    const bool fastk = arith_of(f) == SGWG_ARITH_FAST;
+    p.mem = f->dmem;
+    p.tiles = fastk ? f->dtiles2d_fast : f->dtiles2d;
+    p.burgers = burgers;
+    p.flux0 = order[0].flux;
+    p.flux1 = order[1].flux;
+    p.c0 = order[0].c_const;
+    p.c1 = order[1].c_const;
+    p.stage = stage;
+    p.linear = (m.weno_mode == SGWG_WENO_LINEAR);
+    p.eps = m.epsilon;
+    p.space_dim = m.space_dim;
+    p.uin = b.uin;
+    p.un = b.un;
+    p.out = b.out;
+    p.efield = f->E;
+    p.ctl = f->ctl;
+    p.amax_in = f->amax + (size_t)in_slot * f->nm;
+    p.amax_out = f->amax + (size_t)out_slot * f->nm;
+    p.amax_zero = zero_slot;
+    p.nmembers = f->nm;
+    p.track_max = burgers && stage != 0;
+    p.fail = f->fail;
+    p.dtp = dtp;
+    p.counter = f->counter;
+    if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
+    CK(fastk ? fast::launch_stage2d(p, f->ntiles2d_fast,
+                                    (size_t)f->smem2d_fast * sizeof(double), f->ctx->stream)
+             : exact::launch_stage2d(p, f->ntiles2d, (size_t)f->smem2d * sizeof(double),
+                                     f->ctx->stream));
+    if (timed) {
+      CK(cudaEventRecord(f->ev1, f->ctx->stream));
+      CK(cudaEventSynchronize(f->ev1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+      account_timed(f, stage, 2, true, ms);
+    }
+    f->stats.kernel_launches++;
+    return SGWG_OK;
+  }
   for (size_t pi = 0; pi < order.size(); ++pi) {
     const PassDesc& pd = order[pi];
     PassParams p{};
@@ -266,11 +344,13 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     p.ctl = f->ctl;
     p.amax_in = f->amax + (size_t)in_slot * f->nm;
     p.amax_out = f->amax + (size_t)out_slot * f->nm;
-    p.amax_zero = (stage == 2 && pi == 0 && burgers) ? f->amax : nullptr;
+    p.amax_zero = (pi == 0) ? zero_slot : nullptr;
     p.nmembers = f->nm;
     p.track_max = burgers && stage != 0;
     p.fail = f->fail;
     p.dyn_smem_doubles = f->smem_doubles[pd.kdim];
+    p.dtp = p.last ? dtp : nullptr;
+    p.counter = f->counter;
     if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
     CK(do_launch_pass(f, p, pd.kdim));
     if (timed) {
@@ -278,17 +358,7 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
       CK(cudaEventSynchronize(f->ev1));
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
-      f->stats.pass_ms_sum += ms;
-      f->stats.pass_launches++;
-      // algorithmic counts: per point and direction
-      // advective 70 flops, Burgers 142; RK stage update 2/5/5 flops;
-      // stage bytes 16 (stage 1) / 24 (stages 2, 3) per point, on the last pass.
-      const double pts = (double)f->total;
-      f->stats.pass_flops += pts * (burgers ? 142.0 : 70.0);
-      if (p.last && stage > 0) {
-        f->stats.pass_flops += pts * (stage == 1 ? 2.0 : 5.0);
-        f->stats.pass_bytes += pts * (stage == 1 ? 16.0 : 24.0);
-      }
+      account_timed(f, stage, 1, p.last, ms);
     }
     f->stats.kernel_launches++;
   }
@@ -302,24 +372,14 @@ int launch_member_max_slot0(sgwg_family* f) {
   return SGWG_OK;
 }
 
-// one full step: (VP field of u^n), speeds (+ all-reduce), dt, three stages
-int launch_step(sgwg_family* f, bool timed) {
-  const bool vp = f->model.kind == SGWG_VLASOV_POISSON;
-  if (vp) {
-    FieldParams fp{};
-    fp.mem = f->dmem;
-    fp.f = f->u;
-    fp.rho = f->rho;
-    fp.efield = f->E;
-    fp.emax = f->emax;
-    fp.space_dim = f->model.space_dim;
-    fp.stage = 1;
-    fp.L[0] = f->dom.upper[0] - f->dom.lower[0];
-    fp.L[1] = (f->model.space_dim == 2) ? f->dom.upper[1] - f->dom.lower[1] : 1.0;
-    fp.ctl = f->ctl;
-    CK(launch_field(fp, f->nm, f->ctx->stream));
-    f->stats.kernel_launches++;
-  }
+// dt of the next step can be fused into the stage-3 kernel when nothing has to
+// happen between the end of a step and the dt (no field solve, no all-reduce)
+bool dt_fusable(const sgwg_family* f) {
+  return f->comm == nullptr && f->model.kind != SGWG_VLASOV_POISSON;
+}
+
+// the (unfused) dt of a step: speeds (+ NCCL all-reduce(max)), dt kernel
+int launch_dt_step(sgwg_family* f) {
   DtParams dp = f->dtp;
   if (f->comm != nullptr) {
     CK(launch_local_speeds(dp, f->ctx->stream));
@@ -330,17 +390,25 @@ int launch_step(sgwg_family* f, bool timed) {
   }
   CK(launch_dt(dp, f->ctx->stream));
   f->stats.kernel_launches++;
-  if (f->model.kind == SGWG_BURGERS) {
-    // clear the stage-2/3 input slots (read in the previous step)
-    CK(cudaMemsetAsync(f->amax + f->nm, 0, sizeof(unsigned long long) * 2 * f->nm,
-                       f->ctx->stream));
+  return SGWG_OK;
+}
+
+// one full step.  Unfused: (VP field of u^n), speeds (+ all-reduce), dt, three
+// stages.  Fused (dt_fusable): three stages, the dt of this step having been
+// computed by the previous step's stage-3 kernel (or the segment's first dt).
+int launch_step(sgwg_family* f, bool timed) {
+  const bool vp = f->model.kind == SGWG_VLASOV_POISSON;
+  const bool fused = dt_fusable(f);
+  if (!fused) {
+    if (vp) TRY(launch_field_for(f, f->u, 1));
+    TRY(launch_dt_step(f));
   }
   // stage 1: u -> A; stage 2: (A, u) -> B; stage 3: (B, u) -> u (timestep.hpp:91-103)
   StageBufs s1{f->u, f->u, f->A}, s2{f->A, f->u, f->B}, s3{f->B, f->u, f->u};
   // VP: the stage-1 field was computed above (it feeds dt); stages 2, 3 recompute it
   TRY(launch_stage(f, 1, s1, timed, /*with_field=*/!vp));
   TRY(launch_stage(f, 2, s2, timed));
-  TRY(launch_stage(f, 3, s3, timed));
+  TRY(launch_stage(f, 3, s3, timed, true, fused));
   return SGWG_OK;
 }
 
@@ -367,6 +435,52 @@ int build_tasks(sgwg_family* f) {
     f->maxW[k] = wmax;
     CK(cudaMalloc(&f->dtasks[k], sizeof(int4) * std::max<size_t>(1, t.size())));
     CK(cudaMemcpy(f->dtasks[k], t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice));
+  }
+  if (f->d == 2 && !f->no_fused2d) {  // fused 2D stage tiles: TX x TY = 256 points
+    std::vector<int4> t;
+    int smax = 0;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      MemberDesc& M = f->hmem[mi];
+      M.ty = (M.ext[1] >= 32) ? 32 : (M.ext[1] >= 16 ? 16 : 8);
+      M.tx = 256 / M.ty;
+      const int sm = 2 * (M.tx + 6) * (M.ty + 6) + (M.tx + 1) * M.ty + M.tx * (M.ty + 1) +
+                     M.tx + M.ty;
+      smax = std::max(smax, sm);
+      for (int i0 = 0; i0 < M.ext[0]; i0 += M.tx)
+        for (int j0 = 0; j0 < M.ext[1]; j0 += M.ty) t.push_back(make_int4(mi, i0, j0, 0));
+    }
+    f->ntiles2d = (int)t.size();
+    f->smem2d = smax;
+    CK(cudaMalloc(&f->dtiles2d, sizeof(int4) * std::max<size_t>(1, t.size())));
+    CK(cudaMemcpy(f->dtiles2d, t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice));
+    // fast build: 2048-point tiles of shape (TX, TY) in {(32,64),(64,32),(16,128),(128,16)},
+    // the one that wastes least on this member (kernels.cuh stage2d_fast_kernel)
+    static const int shp[4][2] = {{32, 64}, {64, 32}, {16, 128}, {128, 16}};
+    std::vector<int4> tf;
+    int sfmax = 0;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      const MemberDesc& M = f->hmem[mi];
+      int best = 0;
+      long long bw = -1;
+      for (int s = 0; s < 4; ++s) {
+        const long long cov = (long long)((M.ext[0] + shp[s][0] - 1) / shp[s][0]) * shp[s][0] *
+                              ((M.ext[1] + shp[s][1] - 1) / shp[s][1]) * shp[s][1];
+        if (bw < 0 || cov < bw) {
+          bw = cov;
+          best = s;
+        }
+      }
+      const int TX = shp[best][0], TY = shp[best][1];
+      const int PY = ((TY + 6) % 2 == 0) ? TY + 7 : TY + 6;
+      const int sm = 2 * (TX + 6) * PY + 2 * TX * (TY + 1) + TX + TY;
+      sfmax = std::max(sfmax, sm);
+      for (int i0 = 0; i0 < M.ext[0]; i0 += TX)
+        for (int j0 = 0; j0 < M.ext[1]; j0 += TY) tf.push_back(make_int4(mi, i0, j0, best));
+    }
+    f->ntiles2d_fast = (int)tf.size();
+    f->smem2d_fast = sfmax;
+    CK(cudaMalloc(&f->dtiles2d_fast, sizeof(int4) * std::max<size_t>(1, tf.size())));
+    CK(cudaMemcpy(f->dtiles2d_fast, tf.data(), sizeof(int4) * tf.size(), cudaMemcpyHostToDevice));
   }
   std::vector<int2> mt;
   for (int mi = 0; mi < f->nm; ++mi)
@@ -455,6 +569,7 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
     off += M.npts;
   }
   f->total = off;
+  f->no_fused2d = std::getenv("SGWG_NO_FUSED2D") != nullptr;
   CK(cudaEventCreate(&f->ev0));
   CK(cudaEventCreate(&f->ev1));
   int st = build_tasks(f);
@@ -470,6 +585,9 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   CK(cudaMalloc(&f->amax, sizeof(unsigned long long) * 3 * std::max(1, f->nm)));
   CK(cudaMalloc(&f->fail, sizeof(unsigned long long) * std::max(1, f->nm)));
   CK(cudaMalloc(&f->ctl, sizeof(StepCtl)));
+  CK(cudaMalloc(&f->d_dtp, sizeof(DtParams)));
+  CK(cudaMalloc(&f->counter, sizeof(unsigned int)));
+  CK(cudaMemset(f->counter, 0, sizeof(unsigned int)));
   CK(cudaMallocHost(&f->hctl, sizeof(StepCtl)));
   std::memset(f->hctl, 0, sizeof(StepCtl));
   *out = f;
@@ -541,8 +659,9 @@ int get_graph(sgwg_family* f, int nsteps, cudaGraphExec_t* exec) {
 }
 
 int launches_per_step(const sgwg_family* f) {
-  const int np = (int)pass_order(f).size();
-  int n = 1 + 3 * np;
+  const int np = (f->d == 2 && f->ntiles2d > 0) ? 1 : (int)pass_order(f).size();
+  int n = 3 * np;
+  if (!dt_fusable(f)) n += 1;
   if (f->model.kind == SGWG_VLASOV_POISSON) n += 3;
   if (f->comm != nullptr) n += 1;
   return n;
@@ -830,6 +949,10 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->amax);
   cudaFree(f->fail);
   cudaFree(f->ctl);
+  cudaFree(f->d_dtp);
+  cudaFree(f->counter);
+  cudaFree(f->dtiles2d);
+  cudaFree(f->dtiles2d_fast);
   cudaFreeHost(f->hctl);
   cudaFree(f->dts);
   cudaFree(f->rho);
@@ -1011,6 +1134,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
     f->graph_key_policy = key;
   }
   f->dtp = dp;
+  CK(cudaMemcpyAsync(f->d_dtp, &f->dtp, sizeof(DtParams), cudaMemcpyHostToDevice, s));
 
   // initial state of the device loop
   std::memset(f->hctl, 0, sizeof(StepCtl));
@@ -1039,6 +1163,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
     f->hctl->active = 1;
     CK(cudaMemcpyAsync(&f->ctl->active, &f->hctl->active, sizeof(int), cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(f->ev0, s));
+    if (dt_fusable(f)) TRY(launch_dt_step(f));  // first dt of the segment; then fused
     double seg_ms = 0.0;
     for (;;) {
       // how many steps to launch before looking: exact in accuracy mode,
@@ -1117,6 +1242,38 @@ int sgwg_rk3_step(sgwg_family* f, double dt, sgwg_failure* fail) {
   CK(cudaStreamSynchronize(s));
   for (auto c : h)
     if (c != ULLONG_MAX) return read_failure(f, fail);
+  return SGWG_OK;
+}
+
+int sgwg_time_stage(sgwg_family* f, int reps, double* avg_ms, double* flops, double* bytes) {
+  if (f == nullptr || reps < 1 || avg_ms == nullptr) return fail_with(SGWG_EINVAL, "bad argument");
+  TRY(require_model(f));
+  CK(cudaSetDevice(f->ctx->device));
+  cudaStream_t s = f->ctx->stream;
+  // RK stage 1 (u -> A) is idempotent: launch it back to back between two events
+  std::memset(f->hctl, 0, sizeof(StepCtl));
+  f->hctl->active = 1;
+  f->hctl->dt = 1e-9;
+  CK(cudaMemcpyAsync(f->ctl, f->hctl, sizeof(StepCtl), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(f->fail, 0xff, sizeof(unsigned long long) * f->nm, s));
+  if (f->model.kind == SGWG_BURGERS) TRY(launch_member_max_slot0(f));
+  StageBufs s1{f->u, f->u, f->A};
+  const long long saved = f->stats.kernel_launches;
+  TRY(launch_stage(f, 1, s1, false));  // warm-up
+  CK(cudaEventRecord(f->ev0, s));
+  for (int r = 0; r < reps; ++r) TRY(launch_stage(f, 1, s1, false));
+  CK(cudaEventRecord(f->ev1, s));
+  CK(cudaEventSynchronize(f->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+  const long long nl = (f->stats.kernel_launches - saved) / (reps + 1);
+  f->stats.kernel_launches = saved;
+  *avg_ms = ms / reps / std::max(1LL, nl);
+  const double pts = (double)f->total;
+  const bool burgers = f->model.kind == SGWG_BURGERS;
+  const int nd = (int)pass_order(f).size();
+  if (flops) *flops = pts * ((burgers ? 142.0 : 70.0) * nd + 2.0) / std::max(1LL, nl);
+  if (bytes) *bytes = pts * 16.0 / std::max(1LL, nl);
   return SGWG_OK;
 }
 

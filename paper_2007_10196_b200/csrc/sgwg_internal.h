@@ -41,6 +41,7 @@ struct MemberDesc {
   int nx;                  // x points
   int vn;                  // points of the velocity block (contiguous)
   int xext[2];             // x extents (dx=1: {n0, 1})
+  int tx, ty;              // 2D fused-stage tile (d == 2)
 };
 
 // Step control block (timestep.hpp:126-174 loop state), device resident.
@@ -80,6 +81,33 @@ struct PassParams {
   int track_max;
   unsigned long long* fail;            // per member: min(step*4 + stage)
   int dyn_smem_doubles;    // doubles of dynamic smem per array
+  const struct DtParams* dtp;  // stage 3, last pass: fused next-step dt (or null)
+  unsigned int* counter;       // CTA-done counter for the fused dt
+};
+
+struct Stage2DParams {
+  const MemberDesc* mem;
+  const int4* tiles;       // (member, i0, j0, -)
+  int burgers;
+  int flux0, flux1;        // FluxKind of the dimension-0 / dimension-1 sweep
+  double c0, c1;           // advection speeds
+  int stage;               // 1..3, 0 = tendency only
+  int linear;
+  double eps;
+  int space_dim;
+  const double* uin;
+  const double* un;
+  double* out;
+  const double* efield;
+  const StepCtl* ctl;
+  const unsigned long long* amax_in;
+  unsigned long long* amax_out;
+  unsigned long long* amax_zero;
+  int nmembers;
+  int track_max;
+  unsigned long long* fail;
+  const struct DtParams* dtp;
+  unsigned int* counter;
 };
 
 struct UpsampleParams {
@@ -135,6 +163,7 @@ struct FieldParams {
   namespace NS {                                                                          \
   cudaError_t configure();                                                                \
   cudaError_t launch_pass(const PassParams& p, int nblocks, size_t smem, cudaStream_t s); \
+  cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s); \
   cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s);      \
   cudaError_t launch_final(const FinalParams& p, cudaStream_t s);                         \
   }

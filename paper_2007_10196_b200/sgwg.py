@@ -109,6 +109,7 @@ SIGNATURES = {
     "sgwg_family_init_preset": (C.c_int, [_VP, C.c_int]),
     "sgwg_family_init_fn": (C.c_int, [_VP, IC_CB, _VP, C.c_int]),
     "sgwg_fp64_peak": (C.c_int, [_VP, _DP]),
+    "sgwg_time_stage": (C.c_int, [_VP, C.c_int, _DP, _DP, _DP]),
 }
 
 
@@ -338,6 +339,12 @@ class Family:
         out = np.empty(self.finest_points)
         _check(load().sgwg_prolong(self.h, mi, mode, eps, out.ctypes.data, out.size, 0))
         return out
+
+    def time_stage(self, reps=50):
+        """(avg ms per stage-kernel launch, algorithmic flops, bytes per launch)."""
+        ms, fl, by = C.c_double(0), C.c_double(0), C.c_double(0)
+        _check(load().sgwg_time_stage(self.h, reps, C.byref(ms), C.byref(fl), C.byref(by)))
+        return ms.value, fl.value, by.value
 
     def stats(self) -> dict:
         s = Stats()

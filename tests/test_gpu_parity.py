@@ -154,6 +154,25 @@ def test_evolve_c2_stops_bitwise(ctx, oracle):
         assert bitwise_equal(a, b), maxabs(a, b)
 
 
+def test_evolve_c2_per_dimension_passes_bitwise(ctx, oracle, monkeypatch):
+    """The per-dimension pass kernels (used for d != 2) on the 2D family too."""
+    monkeypatch.setenv("SGWG_NO_FUSED2D", "1")
+    cfg = configs.config("C2", nl=3, root=[16, 16])
+    got, want, gd, wd, gc, wc = _evolve_both(ctx, oracle, cfg, 0.03, stops=[0.01])
+    assert bitwise_equal(gd, wd)
+    assert bitwise_equal(got, want), maxabs(got, want)
+
+
+def test_evolve_c3_short_bitwise(ctx, oracle):
+    """BASELINE C3 family (3D, 31 members, dt = h^{5/3}) for a few steps."""
+    cfg = configs.config("C3")
+    T = 4 * cfg["reference_spacing"] ** (5.0 / 3.0)
+    got, want, gd, wd, gc, wc = _evolve_both(ctx, oracle, cfg, T)
+    assert len(gd) == len(wd) == 4
+    assert bitwise_equal(got, want), maxabs(got, want)
+    assert bitwise_equal(gc[-1], wc[-1]), maxabs(gc[-1], wc[-1])
+
+
 def test_evolve_fast_within_tol(ctx_fast, oracle):
     cfg = configs.config("C2", nl=4, root=[16, 16])
     got, want, gd, wd, gc, wc = _evolve_both(ctx_fast, oracle, cfg, 0.05)
