@@ -41,9 +41,17 @@ __device__ inline void device_local_speeds(const DtParams& p, double* sp) {
 }
 
 // one iteration of evolve_family's step loop (timestep.hpp:152-168):
-// compute_dt (timestep.hpp:47-67) and the exact landing (timestep.hpp:155).
+// compute_dt (timestep.hpp:47-67) and the exact landing (timestep.hpp:155),
+// applied to the step-control block c (global, or a CTA-local copy).
+__device__ inline void device_step_dt_on(const DtParams& p, StepCtl* c, bool use_reduced,
+                                         bool write_dts);
+
 __device__ inline void device_step_dt(const DtParams& p, bool use_reduced) {
-  StepCtl* c = p.ctl;
+  device_step_dt_on(p, p.ctl, use_reduced, true);
+}
+
+__device__ inline void device_step_dt_on(const DtParams& p, StepCtl* c, bool use_reduced,
+                                         bool write_dts) {
   if (!c->active) return;
   double sp[kMaxD + 1];
   if (use_reduced) {
@@ -79,7 +87,7 @@ __device__ inline void device_step_dt(const DtParams& p, bool use_reduced) {
   if (__dsub_rn(stop, __dadd_rn(t, dt)) <= c->eps_t) dt = __dsub_rn(stop, t);
   c->dt = dt;
   c->cur_step = c->step;
-  if (p.dts != nullptr && c->step < p.dts_cap) p.dts[c->step] = dt;
+  if (write_dts && p.dts != nullptr && c->step < p.dts_cap) p.dts[c->step] = dt;
   c->step = c->step + 1;
   c->t = __dadd_rn(t, dt);
 }

@@ -20,6 +20,8 @@
 //   final_kernel          the last dimension of prolong fused with the signed
 //                         combination sum in sorted member order (combine.hpp:113-120).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "dt_device.cuh"
 #include "sgwg_internal.h"
 
@@ -473,14 +475,14 @@ __device__ __forceinline__ double fast_rcp(double x) {
 
 // generic role form: A,B,C = D at the three substencil centres, a,b = the two
 // first differences, fc = centre value; returns the reconstruction.
+template <bool LINEAR>
 __device__ __forceinline__ double recon_roles(double fc, double A, double B, double C, double KA,
-                                              double KB, double KC, double a, double b,
-                                              int linear) {
-  const double c0 = fma(3.0, a, 2.0 * A);
+                                              double KB, double KC, double a, double b) {
+  const double g0 = fma(2.0, a, A);
+  const double c0 = fma(2.0, g0, -a);  // 2A + 3a
   const double c1 = fma(3.0, b, -B);
   const double c2 = fma(3.0, b, -C);
-  if (linear) return fc + kSixth * fma(0.1, c0, fma(0.6, c1, 0.3 * c2));
-  const double g0 = fma(2.0, a, A);
+  if (LINEAR) return fc + kSixth * fma(0.1, c0, fma(0.6, c1, 0.3 * c2));
   const double g1 = a + b;
   const double g2 = fma(-2.0, b, C);
   const double e0 = fma(g0, g0, KA), e1 = fma(g1, g1, KB), e2 = fma(g2, g2, KC);
@@ -500,34 +502,33 @@ __device__ __forceinline__ double recon_roles(double fc, double A, double B, dou
 // Not inlined: one copy of the (large, fully unrolled) line sweep serves the
 // x and y sweeps of every tile shape, keeping the hot code in the i-cache.
 // du[t] is written to out[t * ost] (shared memory).
-template <bool BURGERS, int RUN>
+template <bool BURGERS, int RUN, bool LINEAR>
 __device__ __noinline__ void sweep_run(const double* __restrict__ P,
                                        const double* __restrict__ Mv, int st, int p0, double c,
-                                       double eps4, double inv_h, int linear,
-                                       double* __restrict__ out, int ost) {
-  double du[RUN];
+                                       double eps4, double inv_h, double* __restrict__ out,
+                                       int ost) {
+  // Fully unrolled sliding window: interface t has left point q = t + 2
+  // (q = padded index relative to p0); D, d, K of a point are computed once and
+  // reused by the three interfaces that see it.  For advection Mv == P and the
+  // upwind side is selected per line.
   constexpr int NV = RUN + 6;
+  const double sc = BURGERS ? 1.0 : c;
   double fp[NV], fm[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    fp[q] = P[(p0 + q) * st];
+    fp[q] = sc * P[(p0 + q) * st];
     if (BURGERS) fm[q] = Mv[(p0 + q) * st];
   }
-  if (!BURGERS) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q) fp[q] *= c;
-  }
-  // D, d, K at padded positions (index into fp/fm)
-  auto D = [&](const double* f, int q) { return fma(-2.0, f[q], f[q - 1] + f[q + 1]); };
-  auto K = [&](double Dq) { return fma(13.0 / 3.0 * Dq, Dq, eps4); };
+  auto Dof = [](const double* f, int q) { return fma(-2.0, f[q], f[q - 1] + f[q + 1]); };
+  auto Kof = [&](double Dq) { return fma(13.0 / 3.0 * Dq, Dq, eps4); };
   double Dp[NV], Kp[NV], dp[NV], Dm[NV], Km[NV], dm[NV];
 #pragma unroll
   for (int q = 1; q < NV - 1; ++q) {
-    Dp[q] = D(fp, q);
-    Kp[q] = K(Dp[q]);
+    Dp[q] = Dof(fp, q);
+    Kp[q] = Kof(Dp[q]);
     if (BURGERS) {
-      Dm[q] = D(fm, q);
-      Km[q] = K(Dm[q]);
+      Dm[q] = Dof(fm, q);
+      Km[q] = Kof(Dm[q]);
     }
   }
 #pragma unroll
@@ -539,36 +540,30 @@ __device__ __noinline__ void sweep_run(const double* __restrict__ P,
   double fprev = 0.0;
 #pragma unroll
   for (int t = 0; t <= RUN; ++t) {
-    const int i = t + 2;  // local point left of interface t (padded index)
+    const int i = t + 2, m = t + 3;
     double F;
     if (BURGERS) {
-      const double fpos = recon_roles(fp[i], Dp[i - 1], Dp[i], Dp[i + 1], Kp[i - 1], Kp[i],
-                                      Kp[i + 1], dp[i], dp[i + 1], linear);
-      const int m = i + 1;
-      const double fneg = recon_roles(fm[m], Dm[m + 1], Dm[m], Dm[m - 1], Km[m + 1], Km[m],
-                                      Km[m - 1], -dm[m + 1], -dm[m], linear);
-      F = fpos + fneg;
-    } else {
-      const int m = i + 1;
-      const double fc = down ? fp[m] : fp[i];
-      const double A = down ? Dp[m + 1] : Dp[i - 1];
-      const double B = down ? Dp[m] : Dp[i];
-      const double C = down ? Dp[m - 1] : Dp[i + 1];
-      const double KA = down ? Kp[m + 1] : Kp[i - 1];
-      const double KB = down ? Kp[m] : Kp[i];
-      const double KC = down ? Kp[m - 1] : Kp[i + 1];
-      const double a = down ? -dp[m + 1] : dp[i];
-      const double b = down ? -dp[m] : dp[i + 1];
-      F = recon_roles(fc, A, B, C, KA, KB, KC, a, b, linear);
+      F = recon_roles<LINEAR>(fp[i], Dp[i - 1], Dp[i], Dp[i + 1], Kp[i - 1], Kp[i], Kp[i + 1],
+                              dp[i], dp[i + 1]) +
+          recon_roles<LINEAR>(fm[m], Dm[m + 1], Dm[m], Dm[m - 1], Km[m + 1], Km[m], Km[m - 1],
+                              -dm[m + 1], -dm[m]);
+    } else {  // downwind: the mirror window centred one point right (weno.hpp:178-183)
+      F = recon_roles<LINEAR>(
+          down ? fp[m] : fp[i], down ? Dp[m + 1] : Dp[i - 1], down ? Dp[m] : Dp[i],
+          down ? Dp[m - 1] : Dp[i + 1], down ? Kp[m + 1] : Kp[i - 1], down ? Kp[m] : Kp[i],
+          down ? Kp[m - 1] : Kp[i + 1], down ? -dp[m + 1] : dp[i], down ? -dp[m] : dp[i + 1]);
     }
-    if (t > 0) du[t - 1] = (F - fprev) * inv_h;
+    if (t > 0) out[(t - 1) * ost] = (F - fprev) * inv_h;
     fprev = F;
   }
-#pragma unroll
-  for (int t = 0; t < RUN; ++t) out[t * ost] = du[t];
 }
 
-template <bool BURGERS, int TX, int TY>
+template <bool PERSIST>
+__device__ __forceinline__ double ldx(const double* p) {
+  return PERSIST ? __ldcg(p) : __ldg(p);
+}
+
+template <bool BURGERS, bool PERSIST, int TX, int TY>
 __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const MemberDesc* M,
                                                   int mi, int i0, int j0, double* sm) {
   constexpr int RUN = 8;
@@ -593,72 +588,100 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   const double* u = p.uin + M->offset;
   const double alpha = BURGERS ? __longlong_as_double((long long)p.amax_in[mi]) : 0.0;
   const int bc0 = M->bc[0], bc1 = M->bc[1];
-  constexpr int LY = TY + 6;
-  constexpr int NLOAD = ((TX + 6) * LY + NT - 1) / NT;
-  // all global loads of the thread issued back to back, then split + stored
-  double v[NLOAD];
-  int dst[NLOAD];
-#pragma unroll
-  for (int kq = 0; kq < NLOAD; ++kq) {
-    const int q = tid + kq * NT;
-    const int a = q / LY, b = q - (q / LY) * LY;
-    dst[kq] = -1;
-    v[kq] = 0.0;
-    if (q >= (TX + 6) * LY) continue;
-    if ((a < 3 || a >= TX + 3) && (b < 3 || b >= TY + 3)) continue;
-    dst[kq] = a * PY + b;
+  // global index of tile-relative padded position (a, b) with the boundary
+  // treatment of weno.hpp:131-136 (periodic wrap / zero ghosts); -1 = zero.
+  auto gindex = [&](int a, int b) -> int {
     int gi = i0 - 3 + a, gj = j0 - 3 + b;
-    bool zero = false;
-    if (bc0 == 0) {
-      if (gi < 0 || gi >= n0) {  // periodic wrap ((j%n)+n)%n (tiles may exceed tiny lines)
-        gi %= n0;
-        if (gi < 0) gi += n0;
-      }
-    } else {
-      zero = (gi < 0 || gi >= n0);
+    if (gi < 0 || gi >= n0) {
+      if (bc0 != 0) return -1;
+      gi %= n0;
+      if (gi < 0) gi += n0;
     }
-    if (bc1 == 0) {
-      if (gj < 0 || gj >= n1) {
-        gj %= n1;
-        if (gj < 0) gj += n1;
-      }
-    } else {
-      zero = zero || (gj < 0 || gj >= n1);
+    if (gj < 0 || gj >= n1) {
+      if (bc1 != 0) return -1;
+      gj %= n1;
+      if (gj < 0) gj += n1;
     }
-    v[kq] = zero ? 0.0 : __ldg(u + gi * n1 + gj);
+    return gi * n1 + gj;
+  };
+  auto split_store = [&](int a, int b, double uj) {
+    if (BURGERS) {
+      const double f = 0.5 * uj * uj;              // models.hpp:194
+      const double fpj = 0.5 * (f + alpha * uj);   // weno.hpp:138-140
+      FP[a * PY + b] = fpj;
+      FM[a * PY + b] = f - fpj;
+    } else {
+      FP[a * PY + b] = uj;
+    }
+  };
+  // tile interior: NE points per thread (also the epilogue's u_in), then the
+  // 3-wide halos of the two axes; all loads issued before any use
+  constexpr int NE = TX * TY / NT;
+  constexpr int NH = 6 * (TX + TY);
+  constexpr int NHL = (NH + NT - 1) / NT;
+  double vin[NE], pre_n[NE], vh[NHL];
+  int ih[NHL];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int q = tid + e * NT;
+    const int g = gindex(q / TY + 3, q % TY + 3);
+    vin[e] = (g >= 0) ? ldx<PERSIST>(u + g) : 0.0;
+    pre_n[e] = (p.stage > 1 && g >= 0) ? ldx<PERSIST>(p.un + M->offset + g) : 0.0;
   }
 #pragma unroll
-  for (int kq = 0; kq < NLOAD; ++kq) {
-    if (dst[kq] < 0) continue;
-    const double uj = v[kq];
-    if (BURGERS) {
-      const double f = 0.5 * uj * uj;
-      const double fpj = 0.5 * (f + alpha * uj);
-      FP[dst[kq]] = fpj;
-      FM[dst[kq]] = f - fpj;
+  for (int e = 0; e < NHL; ++e) {
+    const int h = tid + e * NT;
+    int a = 0, b = 0;
+    if (h < 6 * TY) {
+      const int r6 = h / TY;
+      a = (r6 < 3) ? r6 : TX + r6;
+      b = h % TY + 3;
     } else {
-      FP[dst[kq]] = uj;
+      const int h2 = h - 6 * TY, c6 = h2 % 6;
+      a = h2 / 6 + 3;
+      b = (c6 < 3) ? c6 : TY + c6;
     }
+    ih[e] = (h < NH) ? a * 1024 + b : -1;
+    const int g = (h < NH) ? gindex(a, b) : -1;
+    vh[e] = (g >= 0) ? ldx<PERSIST>(u + g) : 0.0;
   }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int q = tid + e * NT;
+    split_store(q / TY + 3, q % TY + 3, vin[e]);
+  }
+#pragma unroll
+  for (int e = 0; e < NHL; ++e)
+    if (ih[e] >= 0) split_store(ih[e] >> 10, ih[e] & 1023, vh[e]);
   __syncthreads();
   const double eps4 = 4.0 * p.eps;
   if (tid < NS) {  // x-sweep warps: thread = (column j, run of RUN rows)
     const int j = tid % TY, r = tid / TY;
     const double c = BURGERS ? 0.0 : cx[j];
-    sweep_run<BURGERS, RUN>(FP + j + 3, FM + j + 3, PY, r * RUN, c, eps4, M->inv_h[0], p.linear,
-                            DX + r * RUN * DP + j, DP);
+    if (p.linear)
+      sweep_run<BURGERS, RUN, true>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
+                                    eps4, M->inv_h[0], DX + r * RUN * DP + j, DP);
+    else
+      sweep_run<BURGERS, RUN, false>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
+                                     eps4, M->inv_h[0], DX + r * RUN * DP + j, DP);
   } else {  // y-sweep warps: thread = (row i, run of RUN columns)
     const int i = (tid - NS) % TX, r = (tid - NS) / TX;
     const double c = BURGERS ? 0.0 : cy[i];
-    sweep_run<BURGERS, RUN>(FP + (i + 3) * PY, FM + (i + 3) * PY, 1, r * RUN, c, eps4,
-                            M->inv_h[1], p.linear, DY + i * DP + r * RUN, 1);
+    if (p.linear)
+      sweep_run<BURGERS, RUN, true>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
+                                    r * RUN, c, eps4, M->inv_h[1], DY + i * DP + r * RUN, 1);
+    else
+      sweep_run<BURGERS, RUN, false>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
+                                     r * RUN, c, eps4, M->inv_h[1], DY + i * DP + r * RUN, 1);
   }
   __syncthreads();
   // epilogue: k = (0 - du_x) - du_y, RK stage, coalesced along j
   double lmax = 0.0;
   const StepCtl* ctl = p.ctl;
-  const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
-  for (int q = tid; q < TX * TY; q += NT) {
+  const double dt = PERSIST ? p.dt_value : ((ctl != nullptr) ? ctl->dt : 0.0);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int q = tid + e * NT;
     const int ti = q / TY, tj = q % TY;
     if (i0 + ti >= n0 || j0 + tj >= n1) continue;
     const double kv = (0.0 - DX[ti * DP + tj]) - DY[ti * DP + tj];
@@ -668,17 +691,16 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
       o = kv;
     } else {
       if (!isfinite(kv)) {
-        const unsigned long long code =
-            (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
-        atomicMin(p.fail + mi, code);
+        const unsigned long long cs = PERSIST ? p.cur_step : (unsigned long long)ctl->cur_step;
+        atomicMin(p.fail + mi, cs * 4ull + (unsigned long long)p.stage);
       }
-      const double ui = p.uin[gi];
+      const double ui = vin[e];
       if (p.stage == 1)
         o = fma(dt, kv, ui);
       else if (p.stage == 2)
-        o = fma(0.75, p.un[gi], 0.25 * fma(dt, kv, ui));
+        o = fma(0.75, pre_n[e], 0.25 * fma(dt, kv, ui));
       else
-        o = fma(1.0 / 3.0, p.un[gi], (2.0 / 3.0) * fma(dt, kv, ui));
+        o = fma(1.0 / 3.0, pre_n[e], (2.0 / 3.0) * fma(dt, kv, ui));
     }
     p.out[gi] = o;
     lmax = fmax(lmax, fabs(o));
@@ -686,6 +708,17 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   if (p.track_max) {
     lmax = warp_max(lmax);
     if ((tid & 31) == 0) atomicMax(p.amax_out + mi, (unsigned long long)__double_as_longlong(lmax));
+  }
+}
+
+template <bool BURGERS, bool PERSIST>
+__device__ __forceinline__ void tile_body(const Stage2DParams& p, const MemberDesc* M, int4 tk,
+                                          double* sm) {
+  switch (tk.w) {  // tile shape (TX, TY), TX*TY = 2048, 512 threads (x and y sweep warps)
+    case 0: stage2d_fast_body<BURGERS, PERSIST, 32, 64>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 1: stage2d_fast_body<BURGERS, PERSIST, 64, 32>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 2: stage2d_fast_body<BURGERS, PERSIST, 16, 128>(p, M, tk.x, tk.y, tk.z, sm); break;
+    default: stage2d_fast_body<BURGERS, PERSIST, 128, 16>(p, M, tk.x, tk.y, tk.z, sm); break;
   }
 }
 
@@ -698,13 +731,86 @@ __global__ void __launch_bounds__(512, 1) stage2d_fast_kernel(const Stage2DParam
   extern __shared__ double sm[];
   if (p.amax_zero != nullptr && blockIdx.x == 0)
     for (int i = threadIdx.x; i < p.nmembers; i += blockDim.x) p.amax_zero[i] = 0ull;
-  switch (tk.w) {  // tile shape (TX, TY), TX*TY = 2048, 256 threads
-    case 0: stage2d_fast_body<BURGERS, 32, 64>(p, M, tk.x, tk.y, tk.z, sm); break;
-    case 1: stage2d_fast_body<BURGERS, 64, 32>(p, M, tk.x, tk.y, tk.z, sm); break;
-    case 2: stage2d_fast_body<BURGERS, 16, 128>(p, M, tk.x, tk.y, tk.z, sm); break;
-    default: stage2d_fast_body<BURGERS, 128, 16>(p, M, tk.x, tk.y, tk.z, sm); break;
-  }
+  tile_body<BURGERS, false>(p, M, tk, sm);
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+
+// Persistent cooperative variant for small families (C1/C2/C4-sized): one
+// launch runs up to `nsteps` RK steps.  Stages are separated by grid-wide
+// barriers; every CTA computes the step's dt redundantly from the same
+// post-barrier data (deterministic, so all CTAs agree) on its own copy of the
+// step-control block, and CTA 0 publishes it.  Loads of data written by other
+// CTAs in this launch go through L2 (ld.global.cg).
+template <bool BURGERS>
+__global__ void __launch_bounds__(512, 1) evolve2d_persistent_kernel(const PersistParams pp) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  __shared__ StepCtl sctl;
+  __shared__ DtParams sdt;
+  if (threadIdx.x == 0) {
+    sdt = *pp.base.dtp;
+    const volatile unsigned long long* src = (const volatile unsigned long long*)pp.base.ctl;
+    unsigned long long* dst = (unsigned long long*)&sctl;
+    for (int w = 0; w < (int)(sizeof(StepCtl) / 8); ++w) dst[w] = src[w];
+  }
+  __syncthreads();
+  const int nm = pp.base.nmembers;
+  for (int step = 0; step < pp.nsteps; ++step) {
+    if (threadIdx.x == 0) device_step_dt_on(sdt, &sctl, false, blockIdx.x == 0);
+    __syncthreads();
+    if (!sctl.active) break;  // identical decision in every CTA
+    for (int s = 1; s <= 3; ++s) {
+      Stage2DParams p = pp.base;
+      p.stage = s;
+      p.uin = (s == 1) ? pp.u : (s == 2 ? pp.A : pp.B);
+      p.un = pp.u;
+      p.out = (s == 1) ? pp.A : (s == 2 ? pp.B : pp.u);
+      p.amax_in = pp.base.amax_in + (size_t)(s - 1) * nm;
+      p.amax_out = pp.base.amax_zero + (size_t)(s % 3) * nm;
+      p.dt_value = sctl.dt;
+      p.cur_step = (unsigned long long)sctl.cur_step;
+      if (BURGERS && blockIdx.x == 0)  // stage s clears the slot stage s+1 writes
+        for (int i = threadIdx.x; i < nm; i += blockDim.x)
+          pp.base.amax_zero[(size_t)((s + 1) % 3) * nm + i] = 0ull;
+      for (int t = blockIdx.x; t < pp.base.ntiles; t += gridDim.x) {
+        const int4 tk = pp.base.tiles[t];
+        tile_body<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
+        __syncthreads();
+      }
+      grid.sync();
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    StepCtl* g = const_cast<StepCtl*>(pp.base.ctl);
+    g->t = sctl.t;
+    g->dt = sctl.dt;
+    g->step = sctl.step;
+    g->cur_step = sctl.cur_step;
+    g->active = sctl.active;
+    g->failed = sctl.failed;
+  }
+}
+
+cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s) {
+  void* args[] = {(void*)&p};
+  if (p.base.burgers)
+    return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<true>, nblocks, 512,
+                                       args, smem, s);
+  return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<false>, nblocks, 512, args,
+                                     smem, s);
+}
+
+int persist2d_max_blocks(int burgers, size_t smem) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, burgers ? (const void*)evolve2d_persistent_kernel<true>
+                       : (const void*)evolve2d_persistent_kernel<false>,
+      512, smem);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms;
 }
 #endif  // SGWG_FAST
 
@@ -835,6 +941,12 @@ cudaError_t configure() {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(stage2d_fast_kernel<false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
 #endif

@@ -1153,6 +1153,39 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   f->stats.pass_flops = 0;
   f->stats.pass_bytes = 0;
   const int lps = launches_per_step(f);
+  // small 2D families (fast build, single rank): persistent cooperative kernel
+  PersistParams pp{};
+  int persist_blocks = 0;
+  const size_t persist_smem = (size_t)f->smem2d_fast * sizeof(double);
+  if (arith_of(f) == SGWG_ARITH_FAST && f->d == 2 && f->ntiles2d_fast > 0 && dt_fusable(f) &&
+      !f->ctx->profile && std::getenv("SGWG_NO_PERSIST") == nullptr) {
+    const int maxb = fast::persist2d_max_blocks(f->model.kind == SGWG_BURGERS, persist_smem);
+    persist_blocks = std::min(f->ntiles2d_fast, maxb);
+    const auto order = pass_order(f);
+    Stage2DParams& p = pp.base;
+    p.mem = f->dmem;
+    p.tiles = f->dtiles2d_fast;
+    p.ntiles = f->ntiles2d_fast;
+    p.burgers = f->model.kind == SGWG_BURGERS;
+    p.flux0 = order[0].flux;
+    p.flux1 = order[1].flux;
+    p.c0 = order[0].c_const;
+    p.c1 = order[1].c_const;
+    p.linear = (f->model.weno_mode == SGWG_WENO_LINEAR);
+    p.eps = f->model.epsilon;
+    p.space_dim = f->model.space_dim;
+    p.efield = f->E;
+    p.ctl = f->ctl;
+    p.amax_in = f->amax;
+    p.amax_zero = f->amax;
+    p.nmembers = f->nm;
+    p.track_max = p.burgers;
+    p.fail = f->fail;
+    p.dtp = f->d_dtp;
+    pp.u = f->u;
+    pp.A = f->A;
+    pp.B = f->B;
+  }
   double t_host = 0.0;
   double last_dt = (pol->mode == SGWG_DT_ACCURACY) ? dp.base_dt : 0.0;
   int status = SGWG_OK;
@@ -1163,7 +1196,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
     f->hctl->active = 1;
     CK(cudaMemcpyAsync(&f->ctl->active, &f->hctl->active, sizeof(int), cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(f->ev0, s));
-    if (dt_fusable(f)) TRY(launch_dt_step(f));  // first dt of the segment; then fused
+    if (dt_fusable(f) && persist_blocks == 0) TRY(launch_dt_step(f));  // then fused
     double seg_ms = 0.0;
     for (;;) {
       // how many steps to launch before looking: exact in accuracy mode,
@@ -1171,7 +1204,11 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
       long long est = 1;
       if (last_dt > 0.0) est = (long long)std::ceil((stop - t_host) / last_dt) + 1;
       est = std::max(1LL, std::min(est, 256LL));
-      if (f->ctx->profile) {  // un-captured, every pass bracketed by events
+      if (persist_blocks > 0) {
+        pp.nsteps = (int)std::min<long long>(est, 512);
+        CK(fast::launch_persist2d(pp, persist_blocks, persist_smem, s));
+        f->stats.kernel_launches++;
+      } else if (f->ctx->profile) {  // un-captured, every pass bracketed by events
         for (long long q = 0; q < est; ++q) TRY(launch_step(f, true));
       } else {
         long long left = est;

@@ -108,6 +108,19 @@ struct Stage2DParams {
   unsigned long long* fail;
   const struct DtParams* dtp;
   unsigned int* counter;
+  // persistent mode (evolve2d_persistent_kernel): dt from the CTA's own copy of
+  // the step control, cache-global loads of data written by other CTAs
+  double dt_value;
+  unsigned long long cur_step;
+  int ntiles;
+};
+
+struct PersistParams {
+  Stage2DParams base;      // tiles, physics, amax, fail (stage/uin/un/out set per stage)
+  double* u;
+  double* A;
+  double* B;
+  int nsteps;              // steps of this launch (early exit when the stop is reached)
 };
 
 struct UpsampleParams {
@@ -169,6 +182,10 @@ struct FieldParams {
   }
 SGWG_DECLARE_LAUNCHERS(exact)
 SGWG_DECLARE_LAUNCHERS(fast)
+namespace fast {
+cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s);
+int persist2d_max_blocks(int burgers, size_t smem);
+}  // namespace fast
 
 // exact-arithmetic scalar kernels (k_exact.cu)
 struct DtParams {
