@@ -90,6 +90,14 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+#if SGWG_FAST
+template <bool BURGERS, int RUN, bool LINEAR>
+__device__ __noinline__ void sweep_run(const double* __restrict__ P,
+                                       const double* __restrict__ Mv, int st, int p0, double c,
+                                       double eps4, double inv_h, double* __restrict__ out,
+                                       int ost);
+#endif
+
 // Lines of dimension k of a member: line L -> (outer o, inner i), base offset
 // o*n*inner + i, element j at base + j*inner (grid.hpp:202-217, line_at order).
 template <bool BURGERS>
@@ -172,7 +180,11 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
       sfp[w * pitch + jj] = fpj;
       sfm[w * pitch + jj] = f - fpj;
     } else {
+#if SGWG_FAST
+      sfp[w * pitch + jj] = uj;  // sweep_run applies the line coefficient
+#else
       sfp[w * pitch + jj] = scoef[w] * uj;  // weno.hpp:176
+#endif
     }
   }
   __syncthreads();
@@ -184,9 +196,35 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
   const int r = tid / W;
   const int j0 = r * P;
   const bool mine = (r < R) && (w < Weff) && (j0 < Seff);
-  double du[kMaxRun];
   const double eps = p.eps;
   const int linear = p.linear;
+#if SGWG_FAST
+  // shared-term sliding sweep over whole runs of P (4 or 8) points; outputs
+  // past the segment end are computed on padding and discarded
+  double* sdu = reinterpret_cast<double*>(sbase + W);
+  if (mine) {
+    const double c = BURGERS ? 0.0 : scoef[w];
+    const double* Pl = sfp + w * pitch;
+    const double* Ml = (BURGERS ? sfm : sfp) + w * pitch;
+    double* o = sdu + w * pitch + j0;
+    const double eps4 = 4.0 * eps, inv_h = M->inv_h[k];
+    if (P == 8) {
+      if (linear)
+        sweep_run<BURGERS, 8, true>(Pl, Ml, 1, j0, c, eps4, inv_h, o, 1);
+      else
+        sweep_run<BURGERS, 8, false>(Pl, Ml, 1, j0, c, eps4, inv_h, o, 1);
+    } else {
+      if (linear)
+        sweep_run<BURGERS, 4, true>(Pl, Ml, 1, j0, c, eps4, inv_h, o, 1);
+      else
+        sweep_run<BURGERS, 4, false>(Pl, Ml, 1, j0, c, eps4, inv_h, o, 1);
+    }
+  }
+  __syncthreads();
+  const double* dub = sdu;
+  const int dpitch = pitch;
+#else
+  double du[kMaxRun];
   if (mine) {
     const double* fp = sfp + w * pitch;
     const double* fm = sfm + w * pitch;
@@ -231,6 +269,9 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
       if (t < P && j0 + t < Seff) sfp[w * S + j0 + t] = du[t];
   }
   __syncthreads();
+  const double* dub = sfp;
+  const int dpitch = S;
+#endif
 
   // accumulate out -= du in dimension order (models.hpp:155,175,187-197) and,
   // on the last pass, the SSP-RK3 stage update (timestep.hpp:93,98,103).
@@ -246,7 +287,7 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
       ww = q / Seff;
     }
     const long long gi = M->offset + sbase[ww] + (long long)(seg0 + jl) * inner;
-    const double d = sfp[ww * S + jl];
+    const double d = dub[ww * dpitch + jl];
     const double kv = p.first ? (0.0 - d) : (p.kbuf[gi] - d);
     if (!p.last) {
       p.kbuf[gi] = kv;

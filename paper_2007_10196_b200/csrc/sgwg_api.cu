@@ -92,14 +92,16 @@ struct PassCfg {
 
 // tiling of one line direction of length n: segments of <= 64 points, runs of
 // <= kMaxRun points per thread, as many lines per CTA as the 256 threads allow.
+// Runs are 4 points on short lines (C5's 8/9-point lines) and 8 otherwise;
+// the padded segment is long enough for whole runs (the fast kernel computes
+// full runs and discards outputs past the segment).
 PassCfg pass_cfg(int n) {
   PassCfg c;
   c.S = std::min(n, 64);
-  c.P = (c.S + 7) / 8;
-  if (c.P > kMaxRun) c.P = kMaxRun;
+  c.P = (n <= 16) ? 4 : 8;
   const int R = (c.S + c.P - 1) / c.P;
   c.W = kPassThreads / R;
-  c.pitch = c.S + 6;
+  c.pitch = R * c.P + 6;
   if (c.pitch % 2 == 0) c.pitch += 1;
   return c;
 }
@@ -209,7 +211,8 @@ namespace {
 int arith_of(const sgwg_family* f) { return f->ctx->arith; }
 
 cudaError_t do_launch_pass(const sgwg_family* f, const PassParams& p, int kdim) {
-  const size_t nsplit = (p.flux == kFluxBurgers) ? 2 : 1;
+  // split-flux arrays (+ a du array in the fast kernel) + coefficients + line bases
+  const size_t nsplit = ((p.flux == kFluxBurgers) ? 2 : 1) + 1;
   const size_t smem =
       (nsplit * (size_t)f->smem_doubles[kdim] + 2 * (size_t)f->maxW[kdim]) * sizeof(double);
   if (arith_of(f) == SGWG_ARITH_FAST) return fast::launch_pass(p, f->ntasks[kdim], smem, f->ctx->stream);
