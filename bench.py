@@ -40,6 +40,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = "C2"
+WORKLOADS = {
+    "C1": "C1: 2D advection [0,2]^2 periodic, root 16, N_L=3 (7 grids, 11264 pts/stage), "
+          "dt=0.5h^(5/3), T=1, WENO prolongation",
+    "C2": "C2: 2D Burgers [0,2]^2 periodic, root 32x32, N_L=5, 11 component grids "
+          "(278528 pts/stage), finest 1024^2, CFL 0.5, stops {0.1,0.5}, WENO5-JS+LF, SSP-RK3, "
+          "WENO prolongation",
+    "C3": "C3: 3D advection [0,2]^3 periodic, root 16, N_L=4 (31 grids, 1409024 pts/stage), "
+          "finest 256^3, dt=h^(5/3), T=0.5",
+    "C4": "C4: 1D1V Vlasov-Poisson Landau damping, root 32, N_L=5 (11 grids), CFL 0.5, T=40",
+    "C5": "C5: 2D2V Vlasov-Poisson Landau damping, root 8, N_L=5 (121 grids, 12057728 "
+          "pts/stage), CFL 0.5",
+}
 
 
 def parse():
@@ -51,6 +63,10 @@ def parse():
     ap.add_argument("--arith", default="fast", choices=["fast", "exact"])
     ap.add_argument("--config", default=WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tfinal", type=float, default=None,
+                    help="override T (prefix runs of the long configs, e.g. C5)")
+    ap.add_argument("--no-combine", action="store_true",
+                    help="skip the combination at the stops (C5's finest grid is 34.6 GB)")
     return ap.parse_args()
 
 
@@ -86,6 +102,15 @@ def _levels(cfg):
 
     rec(0, 0, [])
     return sorted(out)
+
+
+def kernel_name(cfg, arith):
+    phys = {0: "Advect", 1: "Burgers", 3: "VlasovPoisson"}.get(cfg["kind"], "?")
+    if cfg["d"] == 2:
+        k = "stage2d_fast_kernel" if arith == "fast" else "stage2d_kernel"
+        return f"{k}<{phys}> (both WENO5 sweeps + RK3 stage, all members, 1 launch)"
+    return (f"pass_kernel<{phys}> ({arith}; one WENO5 direction of all members per launch, "
+            "RK3 stage fused into the last direction)")
 
 
 def cpu_info():
@@ -218,6 +243,9 @@ def run_b200(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = configs.config(args.config)
+    if args.tfinal is not None:
+        cfg["tfinal"] = args.tfinal
+        cfg["stops"] = [s for s in cfg["stops"] if s < args.tfinal]
     levels = _levels(cfg)
     pts_all = shard.member_points(levels, cfg["root"], cfg["bc"])
     total_pts = sum(pts_all)
@@ -238,8 +266,12 @@ def run_b200(args):
     n_local = fam.total_points
     dev_init = torch.empty(n_local, dtype=torch.float64, device=f"cuda:{local}")
     fam.download_device(dev_init.data_ptr(), n_local)
-    combined = torch.empty(fam.finest_points, dtype=torch.float64, device=f"cuda:{local}")
-    pinned_out = torch.empty((2, fam.finest_points), dtype=torch.float64).pin_memory()
+    if args.no_combine:
+        combined = pinned_out = None
+        pinned_states = torch.empty(n_local, dtype=torch.float64).pin_memory()
+    else:
+        combined = torch.empty(fam.finest_points, dtype=torch.float64, device=f"cuda:{local}")
+        pinned_out = torch.empty(fam.finest_points, dtype=torch.float64).pin_memory()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
     stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
 
@@ -254,13 +286,16 @@ def run_b200(args):
             fam.upload_device(dev_init.data_ptr(), n_local)
 
         def on_stop(t):
-            if host_io:
-                outs.append(fam.combine(cfg["interp"], cfg["epsilon"]))  # D2H of the result
+            if host_io:  # D2H of the combined field into pinned host memory
+                outs.append(fam.combine(cfg["interp"], cfg["epsilon"], out=pinned_out.numpy()))
             else:
                 fam.combine(cfg["interp"], cfg["epsilon"], out_device_ptr=combined.data_ptr())
 
-        dts = fam.evolve_config(cfg, on_stop=on_stop)
+        dts = fam.evolve_config(cfg, on_stop=None if args.no_combine else on_stop)
         nsteps_box["n"] = len(dts)
+        nsteps_box["dts"] = dts
+        if host_io and args.no_combine:  # the result is the member states
+            fam.download_into(pinned_states.numpy())
         return outs
 
     def barrier():
@@ -313,7 +348,8 @@ def run_b200(args):
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall_e2e * 1e3))
     e2e_value = pu * args.steps / (e2e_ms * 1e-3)
     h2d = n_local * 8
-    d2h = 2 * fam.finest_points * 8
+    n_out = 1 + len(cfg["stops"])
+    d2h = n_local * 8 if args.no_combine else n_out * fam.finest_points * 8
 
     # ---- roofline of the dominant kernel: the fused WENO5 + RK3 stage kernel,
     # launched back to back between CUDA events on the library's stream ----
@@ -336,7 +372,7 @@ def run_b200(args):
     # ---- CPU baseline: the reference on this host, bounded sample (rank 0, N=1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
+        cpu = cpu_baseline(cfg, nsteps_box.get("dts"))
 
     if rank == 0:
         clocks = clk.summary()
@@ -345,11 +381,12 @@ def run_b200(args):
             "value": value, "unit": "pt-stage/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_total / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (analytic initial condition of BASELINE C2, no dataset)",
-            "config": {"workload": f"{args.config}: 2D Burgers [0,2]^2 periodic, root 32x32, N_L=5, "
-                                   "11 component grids (278528 pts/stage), finest 1024^2, CFL 0.5, "
-                                   "stops {0.1,0.5}, WENO5-JS+LF, SSP-RK3, WENO prolongation",
-                       "step": "one full simulation to T=0.5 incl. combine at both stops",
+            "data": f"synthetic (analytic initial condition of BASELINE {args.config}, no dataset)",
+            "config": {"workload": WORKLOADS.get(args.config, args.config),
+                       "members": len(levels), "pts_per_stage": total_pts,
+                       "step": f"one full simulation to T={cfg['tfinal']} "
+                               + ("(no combine)" if args.no_combine else
+                                  f"incl. combine at t={cfg['stops'] + [cfg['tfinal']]}"),
                        "rk_steps_per_sim": nsteps, "arith": args.arith,
                        "l2": "flushed (256 MB write) between timed steps",
                        "parallelism": f"members sharded over {world} GPU(s) (LPT)",
@@ -363,11 +400,11 @@ def run_b200(args):
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "traffic": traffic,
-                         "kernel": ("stage2d_fast_kernel<Burgers>" if args.arith == "fast"
-                                    else "stage2d_kernel<Burgers>") +
-                                   " (both WENO5 sweeps + RK3 stage, all 11 members, 1 launch)",
-                         "per_launch": "algorithmic flops = 278528 pts x (2 x 142 + 2) "
-                                       "(SURVEY 8(a)/(d) counting, RK stage 1)",
+                         "kernel": kernel_name(cfg, args.arith),
+                         "per_launch": f"algorithmic flops of RK stage 1 over all {len(levels)} "
+                                       f"members ({total_pts} pts; SURVEY 8(a)/(d) counting: "
+                                       "142/70 flops per point and direction, +2 RK) divided "
+                                       "by the stage's launches",
                          "avg_launch_us": avg_ms * 1e3,
                          "flops_per_launch": flops_per_launch,
                          "peak_source": "measured live: DFMA microbenchmark (sgwg_fp64_peak)",
@@ -387,7 +424,9 @@ def run_b200(args):
     return 0
 
 
-def cpu_baseline(cfg):
+def cpu_baseline(cfg, dts=None):
+    """The reference on this host, bounded sample: the first RK steps of the
+    same run (~10 s of single-thread work at ~1e7 pt-stage/s)."""
     from oracle import oracle as O
     ncores, model = cpu_info()
     dom = O.make_domain(cfg["d"], cfg["nl"], cfg["lower"], cfg["upper"], cfg["root"], cfg["bc"])
@@ -395,8 +434,16 @@ def cpu_baseline(cfg):
                      cfg["space_dim"], cfg["theta"], cfg["tau"])
     pol = O.make_policy(cfg["dt_mode"], cfg["cfl"], cfg["reference_spacing"], cfg["dt_scale"])
     pts = family_pts_stage(cfg)
-    t_sample = 0.02
-    if O.ref_available():
+    nsteps = max(1, int(1.0e8 / (3 * pts)))
+    if dts is not None and len(dts) > 0:
+        t_sample = float(sum(dts[:nsteps])) * (1 - 1e-9)
+    else:
+        t_sample = 0.02
+    vp = cfg["kind"] == 3
+    if vp:  # no Vlasov-Poisson in the reference: time the transport only
+        nsteps = 1
+        t_sample = float(dts[0]) if dts is not None and len(dts) else 1e-3
+    if O.ref_available() and not vp:
         ref = O.Reference()
         secs, n, _ = ref.time_prefix(dom, m, pol, cfg["ic"], t_sample, 1, cfg["interp"])
         kind, desc = "reference", "reference headers (oracle/_ref/libsgwref.so), threads=1"
@@ -408,8 +455,8 @@ def cpu_baseline(cfg):
         secs, n = time.perf_counter() - t0, len(dts)
         kind, desc = "port", "C restatement (oracle/liboracle.so), 1 thread"
     return {"value": pts * 3 * n / secs, "unit": "pt-stage/s", "cores": 1, "kind": kind,
-            "sample": f"{desc}: evolve_family of the C2 family to t={t_sample} ({n} RK steps, "
-                      f"{secs:.1f} s) on {model} ({ncores} host cores)"}
+            "sample": f"{desc}: evolve_family of the {cfg['name']} family to t={t_sample:.4g} "
+                      f"({n} RK steps, {secs:.1f} s) on {model} ({ncores} host cores)"}
 
 
 def main():

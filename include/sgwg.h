@@ -186,6 +186,14 @@ int sgwg_evolve(sgwg_family* fam, const sgwg_policy* policy, double tfinal, cons
  * so every rank receives the combined field. */
 int sgwg_combine(sgwg_family* fam, int interp_mode, double eps, double* out, size_t n,
                  int out_is_device);
+/* The same combination restricted to finest-grid rows [row_begin, row_end) of
+ * dimension 0 (d >= 2): out holds (row_end-row_begin) x (finest points per
+ * row).  Prolongation is dimension-sequential with dimension 0 first
+ * (interp.hpp:217-244), so rows are independent after the dimension-0 sweep;
+ * this is how sgwg_combine handles finest grids too large for one pass
+ * (BASELINE C5: 4.3e9 points) and how a sharded output is produced. */
+int sgwg_combine_rows(sgwg_family* fam, int interp_mode, double eps, long long row_begin,
+                      long long row_end, double* out, size_t n, int out_is_device);
 /* prolong (interp.hpp:197-250) of one local member onto the finest grid. */
 int sgwg_prolong(sgwg_family* fam, int mi, int interp_mode, double eps, double* out, size_t n,
                  int out_is_device);
@@ -198,6 +206,11 @@ int sgwg_rhs(sgwg_family* fam, double* out, size_t n, int out_is_device);
 int sgwg_rk3_step(sgwg_family* fam, double dt, sgwg_failure* fail);
 
 int sgwg_get_stats(const sgwg_family* fam, sgwg_stats* stats);
+
+/* Vlasov-Poisson (new physics): charge density rho = 1 - int f dv and
+ * field E (space_dim components) of the current member states, packed per
+ * member (rho: x-points of each member; E: component-major per member). */
+int sgwg_vp_field(sgwg_family* fam, double* rho, size_t nrho, double* E, size_t nE);
 
 /* ---- host-side initial data: initialize_family (models.hpp:855-871) ------- */
 /* Initial-condition presets of BASELINE C1-C5 and the paper examples,

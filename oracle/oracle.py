@@ -349,12 +349,15 @@ class Reference(_Lib):
             raise ValueError("combine failed")
         return out
 
-    def time_prefix(self, dom, model, policy, preset, tfinal, threads=1, interp_mode=WENO):
+    def time_prefix(self, dom, model, policy, preset, tfinal, threads=1, interp_mode=WENO,
+                    with_combine=False):
+        """(evolve seconds, steps, combine seconds or 0).  The reference's combine
+        materialises the whole finest grid on the host: off unless asked for."""
         secs, csecs = C.c_double(0), C.c_double(0)
         ns = C.c_long(0)
         st = self.lib.sgwref_time_prefix(C.byref(dom), C.byref(model), C.byref(policy), preset,
                                          tfinal, threads, C.byref(secs), C.byref(ns),
-                                         C.byref(csecs), interp_mode)
+                                         C.byref(csecs) if with_combine else None, interp_mode)
         if st:
             raise ValueError("time_prefix failed")
         return secs.value, ns.value, csecs.value

@@ -941,10 +941,10 @@ __global__ void __launch_bounds__(256) upsample_kernel(const UpsampleParams p) {
   for (long long q = start + threadIdx.x; q < end; q += blockDim.x) {
     const long long o = q / ((long long)n_dst * inner);
     const long long rem = q - o * (long long)n_dst * inner;
-    const int j = (int)(rem / inner);
-    const long long i = rem - (long long)j * inner;
+    const int jl = (int)(rem / inner);  // local row (slab of dimension 0: + jrow0)
+    const long long i = rem - (long long)jl * inner;
     const long long base = o * (long long)n_src * inner + i;
-    dst[q] = interp_point(src, base, inner, n_src, j, m, p.bc, p.mode, p.eps);
+    dst[q] = interp_point(src, base, inner, n_src, jl + p.jrow0, m, p.bc, p.mode, p.eps);
   }
 }
 
@@ -953,16 +953,17 @@ __global__ void __launch_bounds__(256) final_kernel(const FinalParams p) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long first = p.row0 * (long long)p.fine_last;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < p.nfine; q += stride) {
-    const long long idx = first + q;
-    const long long o = idx / p.fine_last;
-    const int j = (int)(idx - o * p.fine_last);
+    // sources are local to this launch's rows: q indexes them, first + q the grid
+    const long long o = q / p.fine_last;
+    const int j = (int)(q - o * p.fine_last);
+    (void)first;
     double acc = 0.0;
     for (int mi = 0; mi < p.nm; ++mi) {
       const int m = p.mrefine[mi];
       const double* src = p.src[mi];
       double v;
       if (m == 0) {
-        v = src[idx];
+        v = src[q];
       } else {
         const int n_src = p.msrc_ext[mi];
         v = interp_point(src, o * (long long)n_src, 1, n_src, j, m, p.bc_last, p.mode, p.eps);

@@ -147,6 +147,7 @@ struct ProlongPlan {
   int* fext = nullptr;
   int* fref = nullptr;
   int nm = 0;
+  long long row_a = 0, row_b = 0;  // dimension-0 fine rows covered
 };
 
 struct sgwg_family {
@@ -187,6 +188,10 @@ struct sgwg_family {
   // prolongation plans
   ProlongPlan* full_plan = nullptr;
   double* fine_buf = nullptr;
+  double* slab_arena = nullptr;  // row-slab combination intermediates
+  long long slab_arena_doubles = 0;
+  double* slab_out = nullptr;
+  long long slab_out_doubles = 0;
   // multi-GPU
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -724,11 +729,50 @@ int upload_vec(T** dptr, const std::vector<T>& v) {
 
 constexpr int kUpsampleChunk = 2048;
 
-int build_plan(sgwg_family* f, const std::vector<int>& mis, ProlongPlan** out) {
+// doubles of intermediate storage a plan for fine rows [a, b) of dimension 0 needs
+long long plan_doubles(const sgwg_family* f, const std::vector<int>& mis, long long a, long long b) {
+  const int d = f->d;
+  long long tot = 0;
+  for (int mi : mis) {
+    const MemberDesc& M = f->hmem[mi];
+    long long ext[4];
+    for (int q = 0; q < 4; ++q) ext[q] = (q < d) ? M.ext[q] : 1;
+    for (int k = 0; k + 1 < d; ++k) {
+      if (f->nl - M.level[k] == 0) {
+        if (k == 0) ext[0] = b - a;  // row view of the member
+        continue;
+      }
+      ext[k] = (k == 0) ? (b - a) : f->fine_ext[k];
+      long long n = 1;
+      for (int q = 0; q < d; ++q) n *= ext[q];
+      tot += n;
+    }
+  }
+  return tot;
+}
+
+// Prolongation plan of members `mis` restricted to fine rows [a, b) of
+// dimension 0 (the whole grid for a = 0, b = fine_ext[0]).  Prolongation is
+// dimension-sequential with dimension 0 first (interp.hpp:217-244), so after
+// the dimension-0 sweep every row of the finest grid is independent: a slab
+// of rows needs only its own rows of the intermediates.  Intermediates are
+// carved from `arena` (or one owned allocation when arena is null).
+int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long long b,
+               double* arena, ProlongPlan** out) {
   ProlongPlan* pl = new ProlongPlan();
   const int d = f->d;
   std::vector<long long> coefs(d);
   for (int j = 0; j < d; ++j) coefs[j] = (j % 2 == 0 ? 1 : -1) * binomial(d - 1, j);
+  if (arena == nullptr) {
+    const long long nd = plan_doubles(f, mis, a, b);
+    if (nd > 0) {
+      CK(cudaMalloc(&arena, sizeof(double) * nd));
+      pl->owned.push_back(arena);
+    }
+  }
+  long long carved = 0;
+  pl->row_a = a;
+  pl->row_b = b;
   // current array and extents per member
   std::vector<const double*> cur(mis.size());
   std::vector<std::array<int, 4>> ext(mis.size());
@@ -736,6 +780,10 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, ProlongPlan** out) {
     const MemberDesc& M = f->hmem[mis[s]];
     cur[s] = f->u + M.offset;
     for (int q = 0; q < 4; ++q) ext[s][q] = (q < d) ? M.ext[q] : 1;
+    if (d > 1 && f->nl - M.level[0] == 0) {  // dimension 0 already finest: row view
+      cur[s] += a * (M.npts / M.ext[0]);
+      ext[s][0] = (int)(b - a);
+    }
   }
   for (int k = 0; k + 1 < d; ++k) {
     std::vector<int2> tasks;
@@ -747,10 +795,10 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, ProlongPlan** out) {
       const MemberDesc& M = f->hmem[mis[s]];
       if (f->nl - M.level[k] == 0) continue;  // interp.hpp:219
       long long n = 1;
-      for (int q = 0; q < d; ++q) n *= (q == k) ? f->fine_ext[k] : ext[s][q];
-      double* buf = nullptr;
-      CK(cudaMalloc(&buf, sizeof(double) * n));
-      pl->owned.push_back(buf);
+      for (int q = 0; q < d; ++q)
+        n *= (q == k) ? (k == 0 ? (b - a) : f->fine_ext[k]) : ext[s][q];
+      double* buf = arena + carved;
+      carved += n;
       const int slot = (int)src.size();
       src.push_back(cur[s]);
       dst.push_back(buf);
@@ -759,7 +807,7 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, ProlongPlan** out) {
       sn.push_back(n);
       for (long long c = 0; c * kUpsampleChunk < n; ++c) tasks.push_back(make_int2(slot, (int)c));
       cur[s] = buf;
-      ext[s][k] = f->fine_ext[k];
+      ext[s][k] = (k == 0) ? (int)(b - a) : f->fine_ext[k];
     }
     auto& dm = pl->dims[k];
     dm.nslots = (int)src.size();
@@ -799,6 +847,7 @@ int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, 
     auto& dm = pl->dims[k];
     if (dm.ntasks == 0) continue;
     UpsampleParams p{};
+    p.jrow0 = (k == 0) ? (int)pl->row_a : 0;
     p.mem = f->dmem;
     p.tasks = dm.tasks;
     p.src = dm.src;
@@ -827,8 +876,12 @@ int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, 
   fp.d = d;
   fp.nl = f->nl;
   fp.fine_last = f->fine_ext[d - 1];
-  fp.nfine = f->finest;
-  fp.row0 = 0;
+  // rows of the finest grid flattened over dims 0..d-2; this plan covers
+  // dimension-0 rows [row_a, row_b)
+  long long per_row0 = 1;  // finest points per dimension-0 row
+  for (int q = 1; q < d; ++q) per_row0 *= f->fine_ext[q];
+  fp.nfine = (d == 1) ? f->finest : (pl->row_b - pl->row_a) * per_row0;
+  fp.row0 = (d == 1) ? 0 : pl->row_a * (per_row0 / f->fine_ext[d - 1]);
   fp.bc_last = f->dom.bc[d - 1];
   fp.mode = mode;
   fp.eps = eps;
@@ -848,6 +901,53 @@ int copy_out(sgwg_family* f, const double* dev, double* out, size_t n, int out_i
   }
   CK(cudaStreamSynchronize(f->ctx->stream));
   return SGWG_OK;
+}
+
+// device memory the combination may use for intermediates (SGWG_COMBINE_BUDGET_GB, default 24)
+long long combine_budget_doubles() {
+  const char* e = std::getenv("SGWG_COMBINE_BUDGET_GB");
+  const double gb = e ? std::atof(e) : 24.0;
+  return (long long)(gb * 1e9 / 8.0);
+}
+
+// combination of fine rows [a, b) of dimension 0 into out (host or device)
+int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, double eps,
+                      long long a, long long b, double* out, int out_is_device) {
+  const long long need = plan_doubles(f, mis, a, b);
+  if (f->slab_arena_doubles < need) {
+    cudaFree(f->slab_arena);
+    f->slab_arena = nullptr;
+    f->slab_arena_doubles = 0;
+    if (need > 0) CK(cudaMalloc(&f->slab_arena, sizeof(double) * need));
+    f->slab_arena_doubles = need;
+  }
+  const long long per_row = (long long)(f->finest / f->fine_ext[0]);
+  const long long nout = (b - a) * per_row;
+  if (f->slab_out_doubles < nout && !out_is_device) {
+    cudaFree(f->slab_out);
+    CK(cudaMalloc(&f->slab_out, sizeof(double) * nout));
+    f->slab_out_doubles = nout;
+  }
+  double* dst = out_is_device ? out : f->slab_out;
+  ProlongPlan* pl = nullptr;
+  TRY(build_plan(f, mis, a, b, f->slab_arena, &pl));
+  CK(cudaEventRecord(f->ev0, f->ctx->stream));
+  int st = run_plan(f, pl, mode, eps, 0, dst);
+  if (st == SGWG_OK && f->comm != nullptr && f->nranks > 1) {
+    ncclResult_t r = ncclAllReduce(dst, dst, (size_t)nout, ncclDouble, ncclSum, f->comm,
+                                   f->ctx->stream);
+    if (r != ncclSuccess) st = fail_with(SGWG_ENCCL, ncclGetErrorString(r));
+  }
+  if (st == SGWG_OK) {
+    CK(cudaEventRecord(f->ev1, f->ctx->stream));
+    CK(cudaEventSynchronize(f->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+    f->stats.combine_ms = ms;
+    st = copy_out(f, dst, out, (size_t)nout, out_is_device);
+  }
+  free_plan(pl);
+  return st;
 }
 
 int ensure_fine_buf(sgwg_family* f) {
@@ -962,6 +1062,8 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->E);
   cudaFree(f->emax);
   cudaFree(f->fine_buf);
+  cudaFree(f->slab_arena);
+  cudaFree(f->slab_out);
   cudaEventDestroy(f->ev0);
   cudaEventDestroy(f->ev1);
   delete f;
@@ -1285,6 +1387,25 @@ int sgwg_rk3_step(sgwg_family* f, double dt, sgwg_failure* fail) {
   return SGWG_OK;
 }
 
+int sgwg_vp_field(sgwg_family* f, double* rho, size_t nrho, double* E, size_t nE) {
+  if (f == nullptr || rho == nullptr || E == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  TRY(require_model(f));
+  if (f->model.kind != SGWG_VLASOV_POISSON)
+    return fail_with(SGWG_EINVAL, "vp_field: model is not Vlasov-Poisson");
+  const int dx = f->model.space_dim;
+  if (nrho != (size_t)f->nx_total || nE != (size_t)(f->nx_total * dx))
+    return fail_with(SGWG_EINVAL, "vp_field: sizes must be (sum of x-points) and space_dim x that");
+  CK(cudaSetDevice(f->ctx->device));
+  std::memset(f->hctl, 0, sizeof(StepCtl));
+  f->hctl->active = 1;
+  CK(cudaMemcpyAsync(f->ctl, f->hctl, sizeof(StepCtl), cudaMemcpyHostToDevice, f->ctx->stream));
+  TRY(launch_field_for(f, f->u, 0));
+  CK(cudaMemcpyAsync(rho, f->rho, sizeof(double) * nrho, cudaMemcpyDeviceToHost, f->ctx->stream));
+  CK(cudaMemcpyAsync(E, f->E, sizeof(double) * nE, cudaMemcpyDeviceToHost, f->ctx->stream));
+  CK(cudaStreamSynchronize(f->ctx->stream));
+  return SGWG_OK;
+}
+
 int sgwg_time_stage(sgwg_family* f, int reps, double* avg_ms, double* flops, double* bytes) {
   if (f == nullptr || reps < 1 || avg_ms == nullptr) return fail_with(SGWG_EINVAL, "bad argument");
   TRY(require_model(f));
@@ -1341,28 +1462,61 @@ int sgwg_combine(sgwg_family* f, int mode, double eps, double* out, size_t n, in
     return fail_with(SGWG_EINVAL, "weno_interp5: epsilon must be positive");
   if (f->nm == 0 && f->comm == nullptr) return fail_with(SGWG_EINVAL, "combine: empty family");
   CK(cudaSetDevice(f->ctx->device));
-  if (f->full_plan == nullptr) {
-    std::vector<int> mis(f->nm);
-    for (int i = 0; i < f->nm; ++i) mis[i] = i;
-    TRY(build_plan(f, mis, &f->full_plan));
-  }
-  double* dst = out_is_device ? out : nullptr;
-  if (dst == nullptr) {
-    TRY(ensure_fine_buf(f));
-    dst = f->fine_buf;
-  }
+  std::vector<int> mis(f->nm);
+  for (int i = 0; i < f->nm; ++i) mis[i] = i;
+  const long long rows = (f->d == 1) ? 1 : f->fine_ext[0];
+  const long long full_need = plan_doubles(f, mis, 0, rows);
   f->stats.combine_launches = 0;
-  CK(cudaEventRecord(f->ev0, f->ctx->stream));
-  TRY(run_plan(f, f->full_plan, mode, eps, 0, dst));
-  if (f->comm != nullptr && f->nranks > 1) {
-    CKN(ncclAllReduce(dst, dst, (size_t)f->finest, ncclDouble, ncclSum, f->comm, f->ctx->stream));
+  if (f->d == 1 || full_need <= combine_budget_doubles()) {
+    // whole finest grid in one plan (cached: pointers are stable for the family)
+    if (f->full_plan == nullptr) TRY(build_plan(f, mis, 0, rows, nullptr, &f->full_plan));
+    double* dst = out_is_device ? out : nullptr;
+    if (dst == nullptr) {
+      TRY(ensure_fine_buf(f));
+      dst = f->fine_buf;
+    }
+    CK(cudaEventRecord(f->ev0, f->ctx->stream));
+    TRY(run_plan(f, f->full_plan, mode, eps, 0, dst));
+    if (f->comm != nullptr && f->nranks > 1)
+      CKN(ncclAllReduce(dst, dst, (size_t)f->finest, ncclDouble, ncclSum, f->comm,
+                        f->ctx->stream));
+    CK(cudaEventRecord(f->ev1, f->ctx->stream));
+    CK(cudaEventSynchronize(f->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+    f->stats.combine_ms = ms;
+    return copy_out(f, dst, out, n, out_is_device);
   }
-  CK(cudaEventRecord(f->ev1, f->ctx->stream));
-  CK(cudaEventSynchronize(f->ev1));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
-  f->stats.combine_ms = ms;
-  return copy_out(f, dst, out, n, out_is_device);
+  // too large for one plan (BASELINE C5: finest grid 4.3e9 points): slabs of
+  // dimension-0 rows, each combined into its part of `out`
+  const long long per_row = (long long)(f->finest / f->fine_ext[0]);
+  long long slab = rows;
+  while (slab > 1 && plan_doubles(f, mis, 0, slab) > combine_budget_doubles()) slab = (slab + 1) / 2;
+  double ms_total = 0.0;
+  for (long long a = 0; a < rows; a += slab) {
+    const long long b = std::min(rows, a + slab);
+    TRY(combine_rows_impl(f, mis, mode, eps, a, b, out + a * per_row, out_is_device));
+    ms_total += f->stats.combine_ms;
+  }
+  f->stats.combine_ms = ms_total;
+  return SGWG_OK;
+}
+
+int sgwg_combine_rows(sgwg_family* f, int mode, double eps, long long row_begin,
+                      long long row_end, double* out, size_t n, int out_is_device) {
+  if (f == nullptr || out == nullptr || f->d < 2 || row_begin < 0 || row_end > f->fine_ext[0] ||
+      row_begin >= row_end)
+    return fail_with(SGWG_EINVAL, "combine_rows: bad row range (needs d >= 2)");
+  const long long per_row = (long long)(f->finest / f->fine_ext[0]);
+  if (n != (size_t)((row_end - row_begin) * per_row))
+    return fail_with(SGWG_EINVAL, "combine_rows: output size must equal rows x points per row");
+  if (mode != SGWG_INTERP_WENO && mode != SGWG_INTERP_LAGRANGE)
+    return fail_with(SGWG_EINVAL, "unknown interpolation mode");
+  CK(cudaSetDevice(f->ctx->device));
+  std::vector<int> mis(f->nm);
+  for (int i = 0; i < f->nm; ++i) mis[i] = i;
+  f->stats.combine_launches = 0;
+  return combine_rows_impl(f, mis, mode, eps, row_begin, row_end, out, out_is_device);
 }
 
 int sgwg_prolong(sgwg_family* f, int mi, int mode, double eps, double* out, size_t n,
@@ -1374,7 +1528,7 @@ int sgwg_prolong(sgwg_family* f, int mi, int mode, double eps, double* out, size
     return fail_with(SGWG_EINVAL, "unknown interpolation mode");
   CK(cudaSetDevice(f->ctx->device));
   ProlongPlan* pl = nullptr;
-  TRY(build_plan(f, std::vector<int>{mi}, &pl));
+  TRY(build_plan(f, std::vector<int>{mi}, 0, (f->d == 1) ? 1 : f->fine_ext[0], nullptr, &pl));
   double* dst = out_is_device ? out : nullptr;
   if (dst == nullptr) {
     int st = ensure_fine_buf(f);

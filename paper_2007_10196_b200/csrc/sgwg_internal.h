@@ -138,6 +138,7 @@ struct UpsampleParams {
   int mode;                // InterpMode
   double eps;
   int chunk;
+  int jrow0;               // dimension-0 slab: fine index of the first output row
 };
 
 struct FinalParams {

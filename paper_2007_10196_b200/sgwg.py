@@ -110,6 +110,9 @@ SIGNATURES = {
     "sgwg_family_init_fn": (C.c_int, [_VP, IC_CB, _VP, C.c_int]),
     "sgwg_fp64_peak": (C.c_int, [_VP, _DP]),
     "sgwg_time_stage": (C.c_int, [_VP, C.c_int, _DP, _DP, _DP]),
+    "sgwg_combine_rows": (C.c_int, [_VP, C.c_int, C.c_double, C.c_longlong, C.c_longlong, _VP,
+                                    C.c_size_t, C.c_int]),
+    "sgwg_vp_field": (C.c_int, [_VP, _DP, C.c_size_t, _DP, C.c_size_t]),
 }
 
 
@@ -267,6 +270,11 @@ class Family:
         _check(load().sgwg_family_download(self.h, out.ctypes.data_as(_DP), out.size))
         return out
 
+    def download_into(self, out: np.ndarray):
+        assert out.dtype == np.float64 and out.size == self.total_points and out.flags.c_contiguous
+        _check(load().sgwg_family_download(self.h, out.ctypes.data_as(_DP), out.size))
+        return out
+
     def upload_device(self, ptr: int, n: int):
         _check(load().sgwg_family_upload_device(self.h, _VP(ptr), n))
 
@@ -326,19 +334,56 @@ class Family:
         return out
 
     # -- combine / prolong -------------------------------------------------------
-    def combine(self, mode=1, eps=1e-6, out_device_ptr: Optional[int] = None) -> np.ndarray:
+    def combine(self, mode=1, eps=1e-6, out_device_ptr: Optional[int] = None,
+                out: Optional[np.ndarray] = None) -> np.ndarray:
         if out_device_ptr is not None:
             _check(load().sgwg_combine(self.h, mode, eps, _VP(out_device_ptr),
                                        self.finest_points, 1))
             return None
-        out = np.empty(self.finest_points)
+        if out is None:
+            out = np.empty(self.finest_points)
+        assert out.dtype == np.float64 and out.size == self.finest_points and out.flags.c_contiguous
         _check(load().sgwg_combine(self.h, mode, eps, out.ctypes.data, out.size, 0))
         return out
+
+    def combine_rows(self, row_begin, row_end, mode=1, eps=1e-6,
+                     out_device_ptr: Optional[int] = None) -> np.ndarray:
+        """combination restricted to dimension-0 rows [row_begin, row_end) of the finest grid"""
+        per_row = self.finest_points // self.fine_extent0
+        n = (row_end - row_begin) * per_row
+        if out_device_ptr is not None:
+            _check(load().sgwg_combine_rows(self.h, mode, eps, row_begin, row_end,
+                                            _VP(out_device_ptr), n, 1))
+            return None
+        out = np.empty(n)
+        _check(load().sgwg_combine_rows(self.h, mode, eps, row_begin, row_end, out.ctypes.data,
+                                        n, 0))
+        return out
+
+    @property
+    def fine_extent0(self) -> int:
+        return (self.dom.root_cells[0] << self.nl) + (1 if self.dom.bc[0] == 1 else 0)
 
     def prolong(self, mi, mode=1, eps=1e-6) -> np.ndarray:
         out = np.empty(self.finest_points)
         _check(load().sgwg_prolong(self.h, mi, mode, eps, out.ctypes.data, out.size, 0))
         return out
+
+    def vp_field(self):
+        """(rho, E) of the current states, per member: lists of arrays (E: [space_dim, nx])."""
+        dx = self.model.space_dim
+        nxs = [int(np.prod(p[:dx])) for p in self.points]
+        ntot = sum(nxs)
+        rho = np.empty(ntot)
+        E = np.empty(ntot * dx)
+        _check(load().sgwg_vp_field(self.h, rho.ctypes.data_as(_DP), rho.size,
+                                    E.ctypes.data_as(_DP), E.size))
+        out_r, out_e, o = [], [], 0
+        for nx in nxs:
+            out_r.append(rho[o:o + nx])
+            out_e.append(E[o * dx:(o + nx) * dx].reshape(dx, nx))
+            o += nx
+        return out_r, out_e
 
     def time_stage(self, reps=50):
         """(avg ms per stage-kernel launch, algorithmic flops, bytes per launch)."""

@@ -1,0 +1,54 @@
+"""Vlasov-Poisson physics check (BASELINE C4 has no reference: SURVEY F4).
+
+Linear Landau damping of the k = 0.5 mode: the electric-field energy
+log ||E||_2 decays at the rate gamma ~ -0.1533 (classical result for
+f0 = (1 + a cos(kx)) exp(-v^2/2)/sqrt(2 pi), k = 0.5).  The sparse-grid
+solution on the GPU (fast build, reduced level) is combined at output times,
+rho = 1 - int f dv, E from the periodic Poisson equation, and the decay rate
+of the envelope is fitted.
+"""
+import numpy as np
+import pytest
+
+from helpers import gpu_family
+from paper_2007_10196_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def field_norm(comb, cfg):
+    nx = cfg["root"][0] << cfg["nl"]
+    nv = (cfg["root"][1] << cfg["nl"]) + 1
+    f = comb.reshape(nx, nv)
+    hv = (cfg["upper"][1] - cfg["lower"][1]) / (nv - 1)
+    w = np.full(nv, hv)
+    w[0] *= 0.5
+    w[-1] *= 0.5
+    rho = 1.0 - f @ w
+    L = cfg["upper"][0] - cfg["lower"][0]
+    k = 2 * np.pi * np.fft.fftfreq(nx, d=L / nx)
+    rh = np.fft.fft(rho)
+    Eh = np.zeros_like(rh)
+    nz = k != 0
+    Eh[nz] = -1j * rh[nz] / k[nz]
+    E = np.real(np.fft.ifft(Eh))
+    return np.sqrt(L / nx * np.sum(E * E))
+
+
+def test_landau_damping_rate(ctx_fast):
+    cfg = configs.config("C4", nl=3)
+    fam = gpu_family(ctx_fast, cfg)
+    fam.initialize(cfg["ic"])
+    ts = np.arange(0.25, 20.0 + 1e-9, 0.25)
+    norms = []
+    fam.evolve(cfg["dt_mode"], 20.0, list(ts[:-1]), cfl=cfg["cfl"],
+               on_stop=lambda t: norms.append(field_norm(fam.combine(cfg["interp"], 1e-6), cfg)))
+    norms = np.array(norms)
+    assert len(norms) == len(ts)
+    logE = np.log(norms)
+    # envelope: local maxima of log|E|, fitted over the linear phase
+    peaks = [i for i in range(1, len(logE) - 1) if logE[i] >= logE[i - 1] and logE[i] >= logE[i + 1]]
+    peaks = [i for i in peaks if ts[i] <= 18.0]
+    assert len(peaks) >= 4
+    slope = np.polyfit(ts[peaks], logE[peaks], 1)[0]
+    assert -0.18 < slope < -0.13, slope

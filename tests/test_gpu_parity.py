@@ -99,6 +99,32 @@ def test_combine_bitwise(ctx, oracle, name, over, mode):
     assert bitwise_equal(got, want), maxabs(got, want)
 
 
+@pytest.mark.parametrize("name,over", [
+    ("C3", {"nl": 3, "root": [8, 8, 8]}),
+    ("C2", {"nl": 3, "root": [8, 8], "bc": [1, 0]}),
+    ("C3", {"d": 4, "nl": 3, "lower": [0.0] * 4, "upper": [2.0] * 4, "root": [6] * 4,
+            "bc": [0, 0, 1, 1], "speeds": [1.0] * 4}),
+])
+def test_combine_row_slabs_bitwise(ctx, oracle, monkeypatch, name, over):
+    """Row-slab combination (how C5's 4.3e9-point finest grid is produced):
+    forced by a tiny memory budget, and sgwg_combine_rows on a sub-range."""
+    cfg = configs.config(name, **over)
+    s = random_states(oracle, cfg, seed=29)
+    dom, _, _ = oracle_objs(cfg)
+    want = oracle.combine(dom, s, O.WENO, 1e-6)
+    fam = gpu_family(ctx, cfg)
+    fam.upload(s)
+    monkeypatch.setenv("SGWG_COMBINE_BUDGET_GB", "0.00002")  # 20 kB: many slabs
+    got = fam.combine(O.WENO, 1e-6)
+    assert bitwise_equal(got, want), maxabs(got, want)
+    monkeypatch.delenv("SGWG_COMBINE_BUDGET_GB")
+    rows = fam.fine_extent0
+    per_row = fam.finest_points // rows
+    a, b = rows // 3, rows // 3 + 5
+    part = fam.combine_rows(a, b, O.WENO, 1e-6)
+    assert bitwise_equal(part, want[a * per_row:b * per_row])
+
+
 def test_prolong_bitwise(ctx, oracle):
     cfg = configs.config("C3", nl=3, root=[8, 8, 8])
     s = random_states(oracle, cfg, seed=31)
@@ -171,6 +197,44 @@ def test_evolve_c3_short_bitwise(ctx, oracle):
     assert len(gd) == len(wd) == 4
     assert bitwise_equal(got, want), maxabs(got, want)
     assert bitwise_equal(gc[-1], wc[-1]), maxabs(gc[-1], wc[-1])
+
+
+def test_sharded_family_with_nccl_comm_bitwise(ctx, oracle):
+    """The multi-GPU step (local speeds -> NCCL all-reduce(max) -> dt, captured
+    in the step graph) and the combine all-reduce, on a one-rank communicator:
+    identical to the single-device path and to the oracle."""
+    from paper_2007_10196_b200 import sgwg
+    cfg = configs.config("C2", nl=3, root=[16, 16])
+    dom, model, pol = oracle_objs(cfg)
+    s0 = oracle.init_family(cfg["ic"], dom)
+    want, wd, st, _ = oracle.evolve(dom, model, pol, s0, 0.03)
+    fam = gpu_family(ctx, cfg, members=list(range(len(oracle.levels(2, 3)))))
+    fam.set_comm(sgwg.nccl_unique_id(), 1, 0)
+    fam.upload(s0)
+    gd = fam.evolve_config(cfg, tfinal=0.03, stops=[])
+    assert bitwise_equal(gd, wd)
+    assert bitwise_equal(fam.download(), want)
+    assert bitwise_equal(fam.combine(O.WENO, 1e-6), oracle.combine(dom, want, O.WENO, 1e-6))
+
+
+def test_shard_subset_matches_members(ctx, oracle):
+    """A shard holds only its members; its partial combination is the sum over them."""
+    cfg = configs.config("C2", nl=3, root=[16, 16])
+    dom, model, pol = oracle_objs(cfg)
+    s0 = oracle.init_family(cfg["ic"], dom)
+    lv = oracle.levels(2, 3)
+    pts = [int(np.prod(_points(cfg, l))) for l in lv]
+    offs = np.concatenate([[0], np.cumsum(pts)])
+    mine = [1, 4, 5]
+    fam = gpu_family(ctx, cfg, members=mine)
+    fam.upload(np.concatenate([s0[offs[m]:offs[m + 1]] for m in mine]))
+    fam.rk3_step(1e-3)
+    got = fam.download()
+    o = 0
+    for m in mine:
+        w, f = oracle.rk3_step(dom, lv[m], model, s0[offs[m]:offs[m + 1]], 1e-3)
+        assert bitwise_equal(got[o:o + pts[m]], w)
+        o += pts[m]
 
 
 def test_evolve_fast_within_tol(ctx_fast, oracle):
