@@ -66,6 +66,44 @@ __device__ void fft_lines(double* re, double* im, int n1, int n2, int axis, int 
   }
 }
 
+// rho(x) = 1 - sum_v w_v f(x, v) (moment_density models.hpp:294-306 with the
+// trapezoid block weights 240-257, 64-71): one warp per x point, lanes stride
+// the contiguous velocity block with 4 loads in flight; fixed reduction order.
+__global__ void __launch_bounds__(256) moment_kernel(const FieldParams p) {
+  if (p.ctl != nullptr && !p.ctl->active) return;
+  const int2 tk = p.mtasks[blockIdx.x];
+  const MemberDesc* M = p.mem + tk.x;
+  const int dx = p.space_dim;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int xi = tk.y + warp;
+  if (xi >= M->nx) return;
+  const int vn = M->vn;
+  const int ev0 = M->ext[dx], ev1 = (dx == 2) ? M->ext[dx + 1] : 1;
+  const double hv0 = M->h[dx], hv1 = (dx == 2) ? M->h[dx + 1] : 1.0;
+  const int zb0 = M->bc[dx], zb1 = (dx == 2) ? M->bc[dx + 1] : 0;
+  const double* block = p.f + M->offset + (long long)xi * vn;
+  const float inv_ev1 = 1.0f / (float)ev1;
+  auto weight = [&](int vi) {
+    const int i0 = (int)(((float)vi + 0.5f) * inv_ev1), i1 = vi - i0 * ev1;
+    double w0 = hv0, w1 = hv1;
+    if (zb0 == 1 && (i0 == 0 || i0 == ev0 - 1)) w0 *= 0.5;
+    if (dx == 2 && zb1 == 1 && (i1 == 0 || i1 == ev1 - 1)) w1 *= 0.5;
+    return (dx == 2) ? w0 * w1 : w0;
+  };
+  double acc = 0.0;
+  for (int vb = lane; vb < vn; vb += 4 * 32) {
+    double v[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) v[b] = (vb + 32 * b < vn) ? __ldg(block + vb + 32 * b) : 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (vb + 32 * b < vn) acc = fma(weight(vb + 32 * b), v[b], acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) p.rho[M->xoff + xi] = 1.0 - acc;
+}
+
 __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams p) {
   if (p.ctl != nullptr && !p.ctl->active) return;
   const MemberDesc* M = p.mem + blockIdx.x;
@@ -80,30 +118,11 @@ __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams 
   double* ei = sh + 3 * nx;
   __shared__ double red[kFieldThreads / 32][2];
 
-  // rho(x) = 1 - sum_v w_v f(x, v): one warp per x point
+  // rho(x) from the moment kernel
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int ev0 = M->ext[dx], ev1 = (dx == 2) ? M->ext[dx + 1] : 1;
-  const double hv0 = M->h[dx], hv1 = (dx == 2) ? M->h[dx + 1] : 1.0;
-  const int zb0 = M->bc[dx], zb1 = (dx == 2) ? M->bc[dx + 1] : 0;
-  const double* f = p.f + M->offset;
-  for (int xi = warp; xi < nx; xi += nwarps) {
-    const double* block = f + (long long)xi * vn;
-    double acc = 0.0;
-    for (int vi = lane; vi < vn; vi += 32) {
-      const int i0 = vi / ev1, i1 = vi - i0 * ev1;
-      double w0 = hv0, w1 = hv1;
-      if (zb0 == 1 && (i0 == 0 || i0 == ev0 - 1)) w0 *= 0.5;
-      if (dx == 2 && zb1 == 1 && (i1 == 0 || i1 == ev1 - 1)) w1 *= 0.5;
-      const double w = (dx == 2) ? w0 * w1 : w0;
-      acc = fma(w, block[vi], acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      rr[xi] = 1.0 - acc;
-      ri[xi] = 0.0;
-      p.rho[M->xoff + xi] = 1.0 - acc;
-    }
+  for (int xi = threadIdx.x; xi < nx; xi += blockDim.x) {
+    rr[xi] = p.rho[M->xoff + xi];
+    ri[xi] = 0.0;
   }
   __syncthreads();
   fft_lines(rr, ri, n1, n2, 1, -1);
@@ -160,6 +179,7 @@ cudaError_t configure_field() {
 
 cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s) {
   if (nmembers <= 0) return cudaSuccess;
+  moment_kernel<<<p.nmtasks, 256, 0, s>>>(p);
   const size_t smem = 4 * kFieldMaxX * sizeof(double);
   field_kernel<<<nmembers, kFieldThreads, smem, s>>>(p);
   return cudaGetLastError();

@@ -122,17 +122,23 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
   double* sfp = smem;
   double* sfm = smem + p.dyn_smem_doubles;
   double* scoef = smem + (BURGERS ? 2 : 1) * p.dyn_smem_doubles;
-  long long* sbase = reinterpret_cast<long long*>(scoef + W);
+  long long* sbase = reinterpret_cast<long long*>(scoef + W);  // member-local line bases
 
   if (p.amax_zero != nullptr && blockIdx.x == 0)
     for (int i = tid; i < p.nmembers; i += blockDim.x) p.amax_zero[i] = 0ull;
 
+  // fixed (line, run) coordinates of this thread: lane-consecutive lines
+  const int R = (S + P - 1) / P;
+  const int w = tid % W;
+  const int r = tid / W;
+  const int in32 = (int)inner;  // member-local offsets fit in 32 bits
+
   // line bases and per-line coefficients (advective_sweep coef_of_line)
-  for (int w = tid; w < Weff; w += blockDim.x) {
-    const long long L = L0 + w;
+  if (tid < Weff) {
+    const long long L = L0 + tid;
     const long long o = L / inner, i = L % inner;
     const long long base = o * (long long)n * inner + i;
-    sbase[w] = base;
+    sbase[tid] = base;
     double c = p.c_const;
     if (p.flux == kFluxKinX) {  // models.hpp:341-344: coefficient v_j
       const int q = p.space_dim + k;
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
       const long long xi = base / M->vn;
       c = -p.efield[M->xoff * p.space_dim + (long long)comp * M->nx + xi];
     }
-    scoef[w] = c;
+    scoef[tid] = c;
   }
   __syncthreads();
 
@@ -156,44 +162,69 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
   const double* u = p.uin + M->offset;
   const int len = Seff + 6;
   const double alpha = BURGERS ? __longlong_as_double((long long)p.amax_in[tk.x]) : 0.0;
-  for (int q = tid; q < Weff * len; q += blockDim.x) {
-    int w, jj;
-    if (inner > 1) {
-      w = q % Weff;
-      jj = q / Weff;
-    } else {
-      jj = q % len;
-      w = q / len;
+  auto load_in = [&](int ww, int jj) -> double {
+    int j = seg0 - 3 + jj;
+    if (bc == 0) {  // |excursion| <= 3 < n (periodic lines have n >= 6)
+      j = (j < 0) ? j + n : (j >= n ? j - n : j);
+      return __ldg(u + (int)sbase[ww] + j * in32);
     }
-    const int j = seg0 - 3 + jj;
-    double uj;
-    if (bc == 0) {
-      int jw = j % n;
-      if (jw < 0) jw += n;
-      uj = __ldg(u + sbase[w] + (long long)jw * inner);
-    } else {
-      uj = (j >= 0 && j < n) ? __ldg(u + sbase[w] + (long long)j * inner) : 0.0;
-    }
+    return (j >= 0 && j < n) ? __ldg(u + (int)sbase[ww] + j * in32) : 0.0;
+  };
+  auto stage_in = [&](int ww, int jj, double uj) {
     if (BURGERS) {
       const double f = 0.5 * uj * uj;           // models.hpp:194
       const double fpj = 0.5 * (f + alpha * uj);  // weno.hpp:138-140
-      sfp[w * pitch + jj] = fpj;
-      sfm[w * pitch + jj] = f - fpj;
+      sfp[ww * pitch + jj] = fpj;
+      sfm[ww * pitch + jj] = f - fpj;
     } else {
 #if SGWG_FAST
-      sfp[w * pitch + jj] = uj;  // sweep_run applies the line coefficient
+      sfp[ww * pitch + jj] = uj;  // sweep_run applies the line coefficient
 #else
-      sfp[w * pitch + jj] = scoef[w] * uj;  // weno.hpp:176
+      sfp[ww * pitch + jj] = scoef[ww] * uj;  // weno.hpp:176
 #endif
+    }
+  };
+  // loads are issued in batches of kBatch before any of them is used
+  constexpr int kBatch = 8;
+  if (inner > 1) {  // strided lines: lanes walk adjacent lines (coalesced), rows by run
+    if (w < Weff && r < R) {
+      for (int jb = r; jb < len; jb += kBatch * R) {
+        double v[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+          const int jj = jb + b * R;
+          v[b] = (jj < len) ? load_in(w, jj) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+          const int jj = jb + b * R;
+          if (jj < len) stage_in(w, jj, v[b]);
+        }
+      }
+    }
+  } else {  // contiguous lines: lanes walk along the line
+    const float inv_len = 1.0f / (float)len;
+    const int tot = Weff * len;
+    for (int qb = tid; qb < tot; qb += kBatch * blockDim.x) {
+      double v[kBatch];
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) {
+        const int q = qb + b * blockDim.x;
+        const int ww = (int)(((float)q + 0.5f) * inv_len);
+        v[b] = (q < tot) ? load_in(ww, q - ww * len) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) {
+        const int q = qb + b * blockDim.x;
+        const int ww = (int)(((float)q + 0.5f) * inv_len);
+        if (q < tot) stage_in(ww, q - ww * len, v[b]);
+      }
     }
   }
   __syncthreads();
 
   // interfaces and flux differences: thread (w, r) owns points [r*P, r*P+P)
   // of line w and recomputes the interface left of its run.
-  const int R = (S + P - 1) / P;
-  const int w = tid % W;
-  const int r = tid / W;
   const int j0 = r * P;
   const bool mine = (r < R) && (w < Weff) && (j0 < Seff);
   const double eps = p.eps;
@@ -277,21 +308,32 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
   // on the last pass, the SSP-RK3 stage update (timestep.hpp:93,98,103).
   double lmax = 0.0;
   const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
-  for (int q = tid; q < Weff * Seff; q += blockDim.x) {
-    int ww, jl;
-    if (inner > 1) {
-      ww = q % Weff;
-      jl = q / Weff;
-    } else {
-      jl = q % Seff;
-      ww = q / Seff;
+  double* kb = p.kbuf + M->offset;
+  const double* ub = p.uin + M->offset;
+  const double* nb = p.un + M->offset;
+  double* ob = p.out + M->offset;
+  // phase 1 of a batch: the global values this point needs (k accumulator,
+  // u_in, u^n); phase 2: accumulate / RK update / store
+  struct Pre {
+    double k, ui, un;
+  };
+  auto prefetch = [&](int ww, int jl) -> Pre {
+    const int gi = (int)sbase[ww] + (seg0 + jl) * in32;
+    Pre v{0.0, 0.0, 0.0};
+    if (!p.first) v.k = kb[gi];
+    if (p.last && p.stage > 0) {
+      v.ui = ub[gi];
+      if (p.stage > 1) v.un = nb[gi];
     }
-    const long long gi = M->offset + sbase[ww] + (long long)(seg0 + jl) * inner;
+    return v;
+  };
+  auto finish = [&](int ww, int jl, const Pre& v) {
+    const int gi = (int)sbase[ww] + (seg0 + jl) * in32;
     const double d = dub[ww * dpitch + jl];
-    const double kv = p.first ? (0.0 - d) : (p.kbuf[gi] - d);
+    const double kv = p.first ? (0.0 - d) : (v.k - d);
     if (!p.last) {
-      p.kbuf[gi] = kv;
-      continue;
+      kb[gi] = kv;
+      return;
     }
     double o;
     if (p.stage == 0) {
@@ -302,17 +344,49 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
             (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
         atomicMin(p.fail + tk.x, code);
       }
-      const double ui = p.uin[gi];
+      const double ui = v.ui;
       if (p.stage == 1) {
         o = ui + dt * kv;
       } else if (p.stage == 2) {
-        o = 0.75 * p.un[gi] + 0.25 * (ui + dt * kv);
+        o = 0.75 * v.un + 0.25 * (ui + dt * kv);
       } else {
-        o = (1.0 / 3.0) * p.un[gi] + (2.0 / 3.0) * (ui + dt * kv);
+        o = (1.0 / 3.0) * v.un + (2.0 / 3.0) * (ui + dt * kv);
       }
     }
-    p.out[gi] = o;
+    ob[gi] = o;
     lmax = fmax(lmax, fabs(o));
+  };
+  constexpr int kEpi = 4;
+  if (inner > 1) {
+    if (w < Weff && r < R) {
+      for (int jb = r; jb < Seff; jb += kEpi * R) {
+        Pre v[kEpi];
+#pragma unroll
+        for (int b = 0; b < kEpi; ++b)
+          if (jb + b * R < Seff) v[b] = prefetch(w, jb + b * R);
+#pragma unroll
+        for (int b = 0; b < kEpi; ++b)
+          if (jb + b * R < Seff) finish(w, jb + b * R, v[b]);
+      }
+    }
+  } else {
+    const float inv_s = 1.0f / (float)Seff;
+    const int tot = Weff * Seff;
+    for (int qb = tid; qb < tot; qb += kEpi * blockDim.x) {
+      Pre v[kEpi];
+#pragma unroll
+      for (int b = 0; b < kEpi; ++b) {
+        const int q = qb + b * blockDim.x;
+        const int ww = (int)(((float)q + 0.5f) * inv_s);
+        if (q < tot) v[b] = prefetch(ww, q - ww * Seff);
+      }
+#pragma unroll
+      for (int b = 0; b < kEpi; ++b) {
+        const int q = qb + b * blockDim.x;
+        const int ww = (int)(((float)q + 0.5f) * inv_s);
+        if (q < tot) finish(ww, q - ww * Seff, v[b]);
+      }
+    }
   }
   if (p.last && p.track_max) {
     lmax = warp_max(lmax);
@@ -554,10 +628,14 @@ __device__ __noinline__ void sweep_run(const double* __restrict__ P,
   // upwind side is selected per line.
   constexpr int NV = RUN + 6;
   const double sc = BURGERS ? 1.0 : c;
+  // advection: a downwind line (c < 0, weno.hpp:178-183) is the positive
+  // reconstruction of the reversed line, so only the addressing depends on
+  // the direction (no per-value selects)
+  const bool rev = !BURGERS && (c < 0.0);
   double fp[NV], fm[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    fp[q] = sc * P[(p0 + q) * st];
+    fp[q] = sc * P[(p0 + (rev ? NV - 1 - q : q)) * st];
     if (BURGERS) fm[q] = Mv[(p0 + q) * st];
   }
   auto Dof = [](const double* f, int q) { return fma(-2.0, f[q], f[q - 1] + f[q + 1]); };
@@ -577,24 +655,23 @@ __device__ __noinline__ void sweep_run(const double* __restrict__ P,
     dp[q] = fp[q] - fp[q - 1];
     if (BURGERS) dm[q] = fm[q] - fm[q - 1];
   }
-  const bool down = (c < 0.0);
   double fprev = 0.0;
 #pragma unroll
   for (int t = 0; t <= RUN; ++t) {
     const int i = t + 2, m = t + 3;
-    double F;
-    if (BURGERS) {
-      F = recon_roles<LINEAR>(fp[i], Dp[i - 1], Dp[i], Dp[i + 1], Kp[i - 1], Kp[i], Kp[i + 1],
-                              dp[i], dp[i + 1]) +
-          recon_roles<LINEAR>(fm[m], Dm[m + 1], Dm[m], Dm[m - 1], Km[m + 1], Km[m], Km[m - 1],
-                              -dm[m + 1], -dm[m]);
-    } else {  // downwind: the mirror window centred one point right (weno.hpp:178-183)
-      F = recon_roles<LINEAR>(
-          down ? fp[m] : fp[i], down ? Dp[m + 1] : Dp[i - 1], down ? Dp[m] : Dp[i],
-          down ? Dp[m - 1] : Dp[i + 1], down ? Kp[m + 1] : Kp[i - 1], down ? Kp[m] : Kp[i],
-          down ? Kp[m - 1] : Kp[i + 1], down ? -dp[m + 1] : dp[i], down ? -dp[m] : dp[i + 1]);
+    double F = recon_roles<LINEAR>(fp[i], Dp[i - 1], Dp[i], Dp[i + 1], Kp[i - 1], Kp[i],
+                                   Kp[i + 1], dp[i], dp[i + 1]);
+    if (BURGERS)
+      F += recon_roles<LINEAR>(fm[m], Dm[m + 1], Dm[m], Dm[m - 1], Km[m + 1], Km[m], Km[m - 1],
+                               -dm[m + 1], -dm[m]);
+    if (t > 0) {
+      // reversed: step t yields the flux left of padded point RUN+3-t, so
+      // du(local RUN-t) = (F_{t-1} - F_t) / h
+      if (rev)
+        out[(RUN - t) * ost] = (fprev - F) * inv_h;
+      else
+        out[(t - 1) * ost] = (F - fprev) * inv_h;
     }
-    if (t > 0) out[(t - 1) * ost] = (F - fprev) * inv_h;
     fprev = F;
   }
 }

@@ -182,6 +182,8 @@ struct sgwg_family {
   // Vlasov-Poisson
   double *rho = nullptr, *E = nullptr, *emax = nullptr;
   long long nx_total = 0;
+  int2* dmtasks = nullptr;  // moment kernel work list
+  int nmtasks = 0;
   // graphs: steps per chunk -> exec
   std::map<int, cudaGraphExec_t> graphs;
   long long graph_key_policy = -1;
@@ -269,8 +271,10 @@ int launch_field_for(sgwg_family* f, const double* state, int stage) {
   fp.L[0] = f->dom.upper[0] - f->dom.lower[0];
   fp.L[1] = (m.space_dim == 2) ? f->dom.upper[1] - f->dom.lower[1] : 1.0;
   fp.ctl = f->ctl;
+  fp.mtasks = f->dmtasks;
+  fp.nmtasks = f->nmtasks;
   CK(launch_field(fp, f->nm, f->ctx->stream));
-  f->stats.kernel_launches++;
+  f->stats.kernel_launches += 2;
   return SGWG_OK;
 }
 
@@ -602,6 +606,9 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   return SGWG_OK;
 }
 
+template <class T>
+int upload_vec(T** dptr, const std::vector<T>& v);
+
 int setup_vp(sgwg_family* f) {
   const int dx = f->model.space_dim;
   if (dx < 1 || dx > 2 || f->d != 2 * dx)
@@ -627,6 +634,13 @@ int setup_vp(sgwg_family* f) {
   }
   f->nx_total = xoff;
   CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
+  std::vector<int2> mt;  // moment kernel: 8 x points (one warp each) per CTA
+  for (int mi = 0; mi < f->nm; ++mi)
+    for (int x0 = 0; x0 < f->hmem[mi].nx; x0 += 8) mt.push_back(make_int2(mi, x0));
+  cudaFree(f->dmtasks);
+  f->dmtasks = nullptr;
+  f->nmtasks = (int)mt.size();
+  TRY(upload_vec(&f->dmtasks, mt));
   if (f->model.kind == SGWG_VLASOV_POISSON && f->rho == nullptr) {
     CK(cudaMalloc(&f->rho, sizeof(double) * std::max<long long>(1, xoff)));
     CK(cudaMalloc(&f->E, sizeof(double) * std::max<long long>(1, xoff * dx)));
@@ -670,7 +684,7 @@ int launches_per_step(const sgwg_family* f) {
   const int np = (f->d == 2 && f->ntiles2d > 0) ? 1 : (int)pass_order(f).size();
   int n = 3 * np;
   if (!dt_fusable(f)) n += 1;
-  if (f->model.kind == SGWG_VLASOV_POISSON) n += 3;
+  if (f->model.kind == SGWG_VLASOV_POISSON) n += 6;  // moment + FFT field per stage
   if (f->comm != nullptr) n += 1;
   return n;
 }
@@ -1061,6 +1075,7 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->rho);
   cudaFree(f->E);
   cudaFree(f->emax);
+  cudaFree(f->dmtasks);
   cudaFree(f->fine_buf);
   cudaFree(f->slab_arena);
   cudaFree(f->slab_out);

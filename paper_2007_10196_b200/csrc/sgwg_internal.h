@@ -170,6 +170,8 @@ struct FieldParams {
   int stage;
   double L[2];             // periodic x lengths
   const StepCtl* ctl;
+  const int2* mtasks;      // moment kernel work: (member, first x point), 8 x points each
+  int nmtasks;
 };
 
 // launchers: one set per arithmetic TU (k_exact.cu, k_fast.cu)

@@ -14,6 +14,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--arith", default="fast")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--nl", type=int, default=None)
+ap.add_argument("--no-combine", action="store_true")
 args = ap.parse_args()
 
 over = {} if args.nl is None else {"nl": args.nl}
@@ -25,7 +26,7 @@ h = cfg["reference_spacing"]
 dt = 0.5 * h if cfg["dt_mode"] == 0 else cfg["dt_scale"] * h ** (5.0 / 3.0)
 for _ in range(args.steps):
     fam.rk3_step(dt * 0.5)
-out = fam.combine(cfg["interp"], cfg["epsilon"])
+out = fam.download() if args.no_combine else fam.combine(cfg["interp"], cfg["epsilon"])
 st = fam.stats()
 print(f"{args.config} members={fam.num_members} pts={fam.total_points} finest={fam.finest_points} "
       f"sum={out.sum():.6e}")
