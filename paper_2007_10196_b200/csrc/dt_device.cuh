@@ -13,31 +13,48 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long* p)
   return *(volatile const unsigned long long*)p;
 }
 
+__device__ __forceinline__ double warp_allmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = (v < w) ? w : v;
+  }
+  return v;
+}
+
 // FamilyModel::family_wave_speeds (models.hpp:791-839) over the local members;
 // sp[kMaxD] carries the failure flag so one all-reduce(max) propagates it.
+// Warp-cooperative: all 32 lanes call, each loads a strided subset of the
+// per-member values (through L2) and the maxima are reduced across the warp
+// (max is exact and order-independent); every lane gets the result.
 __device__ inline void device_local_speeds(const DtParams& p, double* sp) {
+  const int lane = threadIdx.x & 31;
   for (int k = 0; k < kMaxD + 1; ++k) sp[k] = 0.0;
+  double failed = 0.0;
+  for (int m = lane; m < p.nmembers; m += 32)
+    if (__ldcg(p.fail + m) != ULLONG_MAX) failed = 1.0;
   if (p.kind == 1) {  // Burgers: family max|u^n| (models.hpp:798-802)
     double umax = 0.0;
-    for (int m = 0; m < p.nmembers; ++m) {
-      const double a = __longlong_as_double((long long)vload(p.amax + m));
+    for (int m = lane; m < p.nmembers; m += 32) {
+      const double a = __longlong_as_double((long long)__ldcg(p.amax + m));
       umax = (umax < a) ? a : umax;
     }
+    umax = warp_allmax(umax);
     for (int k = 0; k < p.d; ++k) sp[k] = umax;
   } else {
     for (int k = 0; k < p.d; ++k) sp[k] = p.const_speeds[k];
     if (p.kind == 3) {  // Vlasov-Poisson: v-directions from the family max|E_j|
-      for (int m = 0; m < p.nmembers; ++m)
-        for (int j = 0; j < p.space_dim; ++j) {
-          const double a = vload(p.emax + m * p.space_dim + j);
-          sp[p.space_dim + j] = (sp[p.space_dim + j] < a) ? a : sp[p.space_dim + j];
+      for (int j = 0; j < p.space_dim; ++j) {
+        double e = 0.0;
+        for (int m = lane; m < p.nmembers; m += 32) {
+          const double a = __ldcg(p.emax + m * p.space_dim + j);
+          e = (e < a) ? a : e;
         }
+        sp[p.space_dim + j] = warp_allmax(e);
+      }
     }
   }
-  double failed = 0.0;
-  for (int m = 0; m < p.nmembers; ++m)
-    if (vload(p.fail + m) != ULLONG_MAX) failed = 1.0;
-  sp[kMaxD] = failed;
+  sp[kMaxD] = warp_allmax(failed);
 }
 
 // one iteration of evolve_family's step loop (timestep.hpp:152-168):
@@ -50,22 +67,28 @@ __device__ inline void device_step_dt(const DtParams& p, bool use_reduced) {
   device_step_dt_on(p, p.ctl, use_reduced, true);
 }
 
+// Warp-cooperative: all 32 lanes of one warp call it; lane 0 writes c.
 __device__ inline void device_step_dt_on(const DtParams& p, StepCtl* c, bool use_reduced,
                                          bool write_dts) {
-  if (!c->active) return;
+  const bool lead = (threadIdx.x & 31) == 0;
+  const int active = c->active;
+  const double t = c->t, stop = c->stop, eps_t = c->eps_t;
+  const long long step = c->step;
+  __syncwarp();
+  if (!active) return;
   double sp[kMaxD + 1];
   if (use_reduced) {
     for (int k = 0; k < kMaxD + 1; ++k) sp[k] = vload(&c->speeds[k]);
   } else {
     device_local_speeds(p, sp);
   }
+  if (!lead) return;
   if (sp[kMaxD] > 0.0) {
     c->active = 0;
     c->failed = 1;
     return;
   }
-  const double t = c->t, stop = c->stop;
-  if (!(__dsub_rn(stop, t) > c->eps_t)) {
+  if (!(__dsub_rn(stop, t) > eps_t)) {
     c->active = 0;
     return;
   }
@@ -84,11 +107,11 @@ __device__ inline void device_step_dt_on(const DtParams& p, StepCtl* c, bool use
     dt = p.base_dt;
     dt = (remaining < dt) ? remaining : dt;
   }
-  if (__dsub_rn(stop, __dadd_rn(t, dt)) <= c->eps_t) dt = __dsub_rn(stop, t);
+  if (__dsub_rn(stop, __dadd_rn(t, dt)) <= eps_t) dt = __dsub_rn(stop, t);
   c->dt = dt;
-  c->cur_step = c->step;
-  if (write_dts && p.dts != nullptr && c->step < p.dts_cap) p.dts[c->step] = dt;
-  c->step = c->step + 1;
+  c->cur_step = step;
+  if (write_dts && p.dts != nullptr && step < p.dts_cap) p.dts[step] = dt;
+  c->step = step + 1;
   c->t = __dadd_rn(t, dt);
 }
 
@@ -104,9 +127,9 @@ __device__ inline void fused_step_dt(const DtParams* dtp, unsigned int* counter)
     s_last = (prev == gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
+  if (s_last && threadIdx.x < 32) {
     __threadfence();
-    *counter = 0u;
+    if (threadIdx.x == 0) *counter = 0u;
     device_step_dt(*dtp, false);
   }
 }

@@ -15,18 +15,21 @@ namespace sgwg {
 
 __global__ void local_speeds_kernel(const DtParams p) {
   if (!p.ctl->active) return;
-  device_local_speeds(p, p.ctl->speeds);
+  double sp[kMaxD + 1];
+  device_local_speeds(p, sp);  // warp-cooperative
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kMaxD + 1; ++k) p.ctl->speeds[k] = sp[k];
 }
 
 __global__ void dt_kernel(const DtParams p) { device_step_dt(p, p.use_reduced != 0); }
 
 cudaError_t launch_local_speeds(const DtParams& p, cudaStream_t s) {
-  local_speeds_kernel<<<1, 1, 0, s>>>(p);
+  local_speeds_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dt(const DtParams& p, cudaStream_t s) {
-  dt_kernel<<<1, 1, 0, s>>>(p);
+  dt_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,8 @@ __device__ __forceinline__ int bitrev(int x, int bits) { return (int)(__brev((un
 
 // radix-2 FFTs of all lines of an n1 x n2 complex array along `axis` (1 = x2,
 // contiguous).  sign -1: forward e^{-i...}; +1: inverse (unnormalised).
-__device__ void fft_lines(double* re, double* im, int n1, int n2, int axis, int sign) {
+__device__ void fft_lines(double* re, double* im, int n1, int n2, int axis, int sign,
+                          const double* twc, const double* tws, int H) {
   const int len = axis ? n2 : n1;
   if (len <= 1) return;
   const int nx = n1 * n2;
@@ -52,8 +53,9 @@ __device__ void fft_lines(double* re, double* im, int n1, int n2, int axis, int 
       const int base = axis ? line * n2 : line;
       const int i0 = base + (grp * 2 * half + pos) * stride;
       const int i1 = i0 + half * stride;
-      double s, c;
-      sincospi(sign * (double)pos / (double)half, &s, &c);
+      // e^{sign i pi pos/half} from the table e^{i pi k/H}, k = pos * H/half
+      const int ti = pos * (H / half);
+      const double c = twc[ti], s = sign * tws[ti];
       const double br = re[i1] * c - im[i1] * s;
       const double bi = re[i1] * s + im[i1] * c;
       const double ar = re[i0], ai = im[i0];
@@ -116,6 +118,10 @@ __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams 
   double* ri = sh + nx;
   double* er = sh + 2 * nx;
   double* ei = sh + 3 * nx;
+  // twiddles e^{i pi k/H}, k < H = max(n1, n2)/2, shared by every stage and transform
+  const int H = max(1, max(n1, n2) / 2);
+  double* twc = sh + 4 * nx;
+  double* tws = twc + H;
   __shared__ double red[kFieldThreads / 32][2];
 
   // rho(x) from the moment kernel
@@ -124,9 +130,10 @@ __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams 
     rr[xi] = p.rho[M->xoff + xi];
     ri[xi] = 0.0;
   }
+  for (int k = threadIdx.x; k < H; k += blockDim.x) sincospi((double)k / (double)H, &tws[k], &twc[k]);
   __syncthreads();
-  fft_lines(rr, ri, n1, n2, 1, -1);
-  fft_lines(rr, ri, n1, n2, 0, -1);
+  fft_lines(rr, ri, n1, n2, 1, -1, twc, tws, H);
+  fft_lines(rr, ri, n1, n2, 0, -1, twc, tws, H);
 
   const double two_pi = 6.283185307179586476925286766559;
   for (int comp = 0; comp < dx; ++comp) {
@@ -149,8 +156,8 @@ __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams 
       }
     }
     __syncthreads();
-    fft_lines(er, ei, n1, n2, 1, +1);
-    fft_lines(er, ei, n1, n2, 0, +1);
+    fft_lines(er, ei, n1, n2, 1, +1, twc, tws, H);
+    fft_lines(er, ei, n1, n2, 0, +1, twc, tws, H);
     double lmax = 0.0;
     const double inv_n = 1.0 / (double)nx;
     double* E = p.efield + M->xoff * dx + (long long)comp * nx;
@@ -174,13 +181,13 @@ __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams 
 
 cudaError_t configure_field() {
   return cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(4 * kFieldMaxX * sizeof(double)));
+                              (int)(5 * kFieldMaxX * sizeof(double)));
 }
 
 cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s) {
   if (nmembers <= 0) return cudaSuccess;
   moment_kernel<<<p.nmtasks, 256, 0, s>>>(p);
-  const size_t smem = 4 * kFieldMaxX * sizeof(double);
+  const size_t smem = 5 * kFieldMaxX * sizeof(double);
   field_kernel<<<nmembers, kFieldThreads, smem, s>>>(p);
   return cudaGetLastError();
 }

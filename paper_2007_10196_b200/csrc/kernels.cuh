@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(512, 1) evolve2d_persistent_kernel(const Persi
   __syncthreads();
   const int nm = pp.base.nmembers;
   for (int step = 0; step < pp.nsteps; ++step) {
-    if (threadIdx.x == 0) device_step_dt_on(sdt, &sctl, false, blockIdx.x == 0);
+    if (threadIdx.x < 32) device_step_dt_on(sdt, &sctl, false, blockIdx.x == 0);
     __syncthreads();
     if (!sctl.active) break;  // identical decision in every CTA
     for (int s = 1; s <= 3; ++s) {
