@@ -72,6 +72,17 @@ def config(name, **over):
                  kind=VLASOV_BOLTZMANN, speeds=[0.0] * 4, weno_mode=NONLINEAR, epsilon=1e-6,
                  dt_mode=DT_CFL, cfl=0.4, dt_scale=1.0, tfinal=3.0, stops=[0.5, 1.0],
                  interp=WENO, ic=IC_EX5B, space_dim=2, theta=1.0, tau=1.0)
+    elif name == "S2":    # large-problem stress case for the kernel roofline:
+        # C2's physics on root 2048, N_L = 1 (3 members, 20.97M points per stage)
+        c = dict(d=2, nl=1, lower=[0.0, 0.0], upper=[2.0, 2.0], root=[2048, 2048],
+                 bc=[PERIODIC] * 2, kind=BURGERS, speeds=[0.0, 0.0], weno_mode=NONLINEAR,
+                 epsilon=1e-6, dt_mode=DT_CFL, cfl=0.5, dt_scale=1.0, tfinal=0.002, stops=[],
+                 interp=WENO, ic=IC_C2, space_dim=0)
+    elif name == "S3":    # 3D advection stress case: root 128, N_L = 2 (10 members, 8.4M pts)
+        c = dict(d=3, nl=2, lower=[0.0] * 3, upper=[2.0] * 3, root=[128] * 3, bc=[PERIODIC] * 3,
+                 kind=ADVECTION, speeds=[1.0, 1.0, 1.0], weno_mode=NONLINEAR, epsilon=1e-6,
+                 dt_mode=DT_ACCURACY, cfl=0.4, dt_scale=1.0, tfinal=0.0002, stops=[],
+                 interp=WENO, ic=IC_C3, space_dim=0)
     else:
         raise KeyError(name)
     c.setdefault("theta", 1.0)

@@ -681,10 +681,19 @@ __device__ __forceinline__ double ldx(const double* p) {
   return PERSIST ? __ldcg(p) : __ldg(p);
 }
 
+// run length of the fast 2D sweeps: 8 points per thread -> 512 threads per
+// 2048-point tile.  (4 -> 1024 threads at <= 64 registers was measured slower:
+// spills plus 25% redundant interfaces outweigh the doubled warp count.)
+#ifndef SGWG_FAST_RUN
+#define SGWG_FAST_RUN 8
+#endif
+constexpr int kFastRun = SGWG_FAST_RUN;
+constexpr int kFastThreads = 2 * 2048 / kFastRun;
+
 template <bool BURGERS, bool PERSIST, int TX, int TY>
 __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const MemberDesc* M,
                                                   int mi, int i0, int j0, double* sm) {
-  constexpr int RUN = 8;
+  constexpr int RUN = kFastRun;
   constexpr int PY = ((TY + 6) % 2 == 0) ? TY + 7 : TY + 6;  // odd pitch
   constexpr int DP = TY + 1;                                  // du pitch (odd for TY even)
   constexpr int NS = TX * TY / RUN;  // threads per sweep; x and y sweeps run concurrently
@@ -841,7 +850,7 @@ __device__ __forceinline__ void tile_body(const Stage2DParams& p, const MemberDe
 }
 
 template <bool BURGERS>
-__global__ void __launch_bounds__(512, 1) stage2d_fast_kernel(const Stage2DParams p) {
+__global__ void __launch_bounds__(kFastThreads, 1) stage2d_fast_kernel(const Stage2DParams p) {
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const int4 tk = p.tiles[blockIdx.x];
@@ -860,7 +869,8 @@ __global__ void __launch_bounds__(512, 1) stage2d_fast_kernel(const Stage2DParam
 // step-control block, and CTA 0 publishes it.  Loads of data written by other
 // CTAs in this launch go through L2 (ld.global.cg).
 template <bool BURGERS>
-__global__ void __launch_bounds__(512, 1) evolve2d_persistent_kernel(const PersistParams pp) {
+__global__ void __launch_bounds__(kFastThreads, 1)
+    evolve2d_persistent_kernel(const PersistParams pp) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
@@ -913,9 +923,11 @@ __global__ void __launch_bounds__(512, 1) evolve2d_persistent_kernel(const Persi
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s) {
   void* args[] = {(void*)&p};
   if (p.base.burgers)
-    return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<true>, nblocks, 512,
+    return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<true>, nblocks,
+                                       kFastThreads,
                                        args, smem, s);
-  return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<false>, nblocks, 512, args,
+  return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<false>, nblocks,
+                                     kFastThreads, args,
                                      smem, s);
 }
 
@@ -924,7 +936,7 @@ int persist2d_max_blocks(int burgers, size_t smem) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &per_sm, burgers ? (const void*)evolve2d_persistent_kernel<true>
                        : (const void*)evolve2d_persistent_kernel<false>,
-      512, smem);
+      kFastThreads, smem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1080,9 +1092,9 @@ cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cud
   if (nblocks <= 0) return cudaSuccess;
 #if SGWG_FAST
   if (p.burgers)
-    stage2d_fast_kernel<true><<<nblocks, 512, smem, s>>>(p);
+    stage2d_fast_kernel<true><<<nblocks, kFastThreads, smem, s>>>(p);
   else
-    stage2d_fast_kernel<false><<<nblocks, 512, smem, s>>>(p);
+    stage2d_fast_kernel<false><<<nblocks, kFastThreads, smem, s>>>(p);
 #else
   if (p.burgers)
     stage2d_kernel<true><<<nblocks, 256, smem, s>>>(p);
