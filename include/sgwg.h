@@ -140,6 +140,10 @@ int sgwg_family_create(sgwg_ctx* ctx, const sgwg_domain* dom, sgwg_family** out)
  * sharded combine returns this shard's partial combination sum. */
 int sgwg_family_create_shard(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members,
                              int count, sgwg_family** out);
+/* Single-grid mode: one grid at level (N_L, ..., N_L) -- make_single_grid
+ * (runner.hpp:106-115), the reference's full-grid comparison run.  Its
+ * "combination" is the grid's own field (runner.hpp:323-324). */
+int sgwg_family_create_single(sgwg_ctx* ctx, const sgwg_domain* dom, sgwg_family** out);
 int sgwg_family_destroy(sgwg_family* fam);
 /* enumerate_combination_levels (grid.hpp:57-79), sorted: count, then levels[count*d] */
 int sgwg_enumerate_levels(int d, int nl, int* levels, int cap, int* count);
@@ -211,6 +215,12 @@ int sgwg_get_stats(const sgwg_family* fam, sgwg_stats* stats);
  * field E (space_dim components) of the current member states, packed per
  * member (rho: x-points of each member; E: component-major per member). */
 int sgwg_vp_field(sgwg_family* fam, double* rho, size_t nrho, double* E, size_t nE);
+/* Per-step field energy of the last sgwg_evolve (BASELINE C4 "log|E|_2 recorded
+ * per step"): out[s] = ||E_c||_2 at the start of step s, E_c = sum_m c_m I_m(E_m)
+ * on the finest x-grid (I_m: separable degree-4 Lagrange interpolation,
+ * interp.hpp:36-53), ||.||_2 with the finest x-spacings.  Local members only in
+ * a sharded family. */
+int sgwg_field_energy(sgwg_family* fam, double* out, size_t cap, size_t* n);
 
 /* ---- host-side initial data: initialize_family (models.hpp:855-871) ------- */
 /* Initial-condition presets of BASELINE C1-C5 and the paper examples,

@@ -179,6 +179,87 @@ __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams 
   }
 }
 
+// degree-4 Lagrange weights in the reference's cell form (interp.hpp:36-53
+// with OffsetTable::cell_weights, interp.hpp:119-122) for fine index j of a
+// periodic line refined by 2^m: 5 source indices i-2..i+2 and weights.
+__device__ __forceinline__ void lagrange5(int j, int m, int n_src, int* idx, double* w) {
+  const int f = 1 << m, r = j & (f - 1), i = j >> m;
+  const double t = (double)r / f;
+  if (r == 0) {
+    for (int q = 0; q < 5; ++q) {
+      idx[q] = ((i - 2 + q) % n_src + n_src) % n_src;
+      w[q] = (q == 2) ? 1.0 : 0.0;
+    }
+    return;
+  }
+  const double c0 = (t - 1.0) * (t - 2.0) / 12.0, c1 = (4.0 - t * t) / 6.0,
+               c2 = (t + 2.0) * (t + 1.0) / 12.0;
+  // sum_k c_k p_k(t) expanded into point weights (substencil_values, interp.hpp:45-53)
+  const double a0 = 0.5 * (t + 1.0) * t, a1 = -(t + 2.0) * t, a2 = 0.5 * (t + 2.0) * (t + 1.0);
+  const double b1 = 0.5 * t * (t - 1.0), b2 = -(t + 1.0) * (t - 1.0), b3 = 0.5 * (t + 1.0) * t;
+  const double e2 = 0.5 * (t - 1.0) * (t - 2.0), e3 = -t * (t - 2.0), e4 = 0.5 * t * (t - 1.0);
+  w[0] = c0 * a0;
+  w[1] = c0 * a1 + c1 * b1;
+  w[2] = c0 * a2 + c1 * b2 + c2 * e2;
+  w[3] = c1 * b3 + c2 * e3;
+  w[4] = c2 * e4;
+  for (int q = 0; q < 5; ++q) idx[q] = ((i - 2 + q) % n_src + n_src) % n_src;
+}
+
+// ||E||_2 of the combined field on the finest x-grid: E_c = sum_m c_m I_m(E_m),
+// I_m the separable degree-4 Lagrange interpolation from member m's x-grid;
+// h-weighted sum of |E_c|^2 accumulated into *out (diagnostic).
+__global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p,
+                                                           const double* coef, int fine0,
+                                                           int fine1, double hvol,
+                                                           double* out_base, long long cap) {
+  if (p.ctl != nullptr && !p.ctl->active) return;
+  const long long slot = (p.ctl != nullptr) ? p.ctl->step : 0;  // the step about to be taken
+  if (slot >= cap) return;
+  double* out = out_base + slot;
+  const int dx = p.space_dim;
+  const int nfine = fine0 * fine1;
+  double acc = 0.0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nfine; q += gridDim.x * blockDim.x) {
+    const int i = q / fine1, j = q - (q / fine1) * fine1;
+    double ec[2] = {0.0, 0.0};
+    for (int mi = 0; mi < p.nmembers; ++mi) {
+      const MemberDesc* M = p.mem + mi;
+      const int n0 = M->xext[0], n1 = M->xext[1];
+      int ia[5], ja[5];
+      double wa[5], wb[5];
+      lagrange5(i, __ffs(fine0 / n0) - 1, n0, ia, wa);
+      if (dx == 2) {
+        lagrange5(j, __ffs(fine1 / n1) - 1, n1, ja, wb);
+      } else {
+        for (int b = 0; b < 5; ++b) ja[b] = 0, wb[b] = (b == 2) ? 1.0 : 0.0;
+      }
+      for (int c = 0; c < dx; ++c) {
+        const double* E = p.efield + M->xoff * dx + (long long)c * M->nx;
+        double v = 0.0;
+        for (int a = 0; a < 5; ++a) {
+          double s = 0.0;
+          for (int b = 0; b < 5; ++b) s = fma(wb[b], E[ia[a] * n1 + ja[b]], s);
+          v = fma(wa[a], s, v);
+        }
+        ec[c] = fma(coef[mi], v, ec[c]);
+      }
+    }
+    for (int c = 0; c < dx; ++c) acc = fma(ec[c], ec[c], acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc * hvol);
+}
+
+cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
+                                double hvol, double* out_base, long long cap, cudaStream_t s) {
+  int blocks = (fine0 * fine1 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  field_energy_kernel<<<blocks, 256, 0, s>>>(p, coef, fine0, fine1, hvol, out_base, cap);
+  return cudaGetLastError();
+}
+
 cudaError_t configure_field() {
   return cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(5 * kFieldMaxX * sizeof(double)));

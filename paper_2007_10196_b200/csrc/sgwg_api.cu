@@ -184,6 +184,9 @@ struct sgwg_family {
   long long nx_total = 0;
   int2* dmtasks = nullptr;  // moment kernel work list
   int nmtasks = 0;
+  double* fe = nullptr;     // per-step sum of |E_combined|^2 h (Vlasov-Poisson diagnostic)
+  long long fe_cap = 0;
+  double* dcoef = nullptr;  // combination coefficient of each local member
   // graphs: steps per chunk -> exec
   std::map<int, cudaGraphExec_t> graphs;
   long long graph_key_policy = -1;
@@ -211,6 +214,7 @@ struct sgwg_family {
   int ntiles2d_fast = 0;
   int smem2d_fast = 0;
   bool no_fused2d = false;  // SGWG_NO_FUSED2D=1: use the per-dimension pass kernels
+  bool single = false;      // single-grid mode (runner.hpp:106-115): combine = the grid itself
 };
 
 namespace {
@@ -258,7 +262,7 @@ void account_timed(sgwg_family* f, int stage, int npass_dims, bool last, float m
   }
 }
 
-int launch_field_for(sgwg_family* f, const double* state, int stage) {
+int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_energy = false) {
   const sgwg_model& m = f->model;
   FieldParams fp{};
   fp.mem = f->dmem;
@@ -273,8 +277,17 @@ int launch_field_for(sgwg_family* f, const double* state, int stage) {
   fp.ctl = f->ctl;
   fp.mtasks = f->dmtasks;
   fp.nmtasks = f->nmtasks;
+  fp.nmembers = f->nm;
   CK(launch_field(fp, f->nm, f->ctx->stream));
   f->stats.kernel_launches += 2;
+  if (with_energy && f->fe != nullptr) {  // ||E||_2 of u^n, recorded per step
+    const int dx = m.space_dim;
+    const int fine1 = (dx == 2) ? f->fine_ext[1] : 1;
+    const double hvol = f->fine_h[0] * ((dx == 2) ? f->fine_h[1] : 1.0);
+    CK(launch_field_energy(fp, f->dcoef, f->fine_ext[0], fine1, hvol, f->fe, f->fe_cap,
+                           f->ctx->stream));
+    f->stats.kernel_launches++;
+  }
   return SGWG_OK;
 }
 
@@ -412,7 +425,7 @@ int launch_step(sgwg_family* f, bool timed) {
   const bool vp = f->model.kind == SGWG_VLASOV_POISSON;
   const bool fused = dt_fusable(f);
   if (!fused) {
-    if (vp) TRY(launch_field_for(f, f->u, 1));
+    if (vp) TRY(launch_field_for(f, f->u, 1, /*with_energy=*/true));
     TRY(launch_dt_step(f));
   }
   // stage 1: u -> A; stage 2: (A, u) -> B; stage 3: (B, u) -> u (timestep.hpp:91-103)
@@ -521,11 +534,23 @@ int check_domain(const sgwg_domain* dom) {
 }
 
 int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int count,
-                  sgwg_family** out) {
+                  sgwg_family** out, bool single = false) {
   if (ctx == nullptr || out == nullptr) return fail_with(SGWG_EINVAL, "null argument");
-  TRY(check_domain(dom));
+  if (single) {  // make_single_grid (runner.hpp:106-115): one grid at (N_L, ..., N_L)
+    if (dom == nullptr || dom->d < 1 || dom->d > 4 || dom->nl < 0)
+      return fail_with(SGWG_EINVAL, "single grid: bad domain");
+  } else {
+    TRY(check_domain(dom));
+  }
   CK(cudaSetDevice(ctx->device));
-  auto all = enumerate_levels(dom->d, dom->nl);
+  std::vector<std::array<int, 4>> all;
+  if (single) {
+    std::array<int, 4> lv{0, 0, 0, 0};
+    for (int k = 0; k < dom->d; ++k) lv[k] = dom->nl;
+    all.push_back(lv);
+  } else {
+    all = enumerate_levels(dom->d, dom->nl);
+  }
   std::vector<int> sel;
   if (members == nullptr) {
     for (int i = 0; i < (int)all.size(); ++i) sel.push_back(i);
@@ -543,6 +568,7 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   f->nl = dom->nl;
   f->nfull = (int)all.size();
   f->nm = (int)sel.size();
+  f->single = single;
   const int d = f->d;
   for (int k = 0; k < d; ++k) {  // finest_geometry (combine.hpp:85-91)
     const int cells = dom->root_cells[k] << dom->nl;
@@ -640,6 +666,19 @@ int setup_vp(sgwg_family* f) {
   cudaFree(f->dmtasks);
   f->dmtasks = nullptr;
   f->nmtasks = (int)mt.size();
+  {  // combination coefficients of the local members (combine.hpp:34-43, 116)
+    std::vector<double> cf;
+    const int d = f->d;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      int ls = 0;
+      for (int k = 0; k < d; ++k) ls += f->levels[mi][k];
+      const int j = f->nl - ls;
+      cf.push_back(f->single ? 1.0 : (double)((j % 2 == 0 ? 1 : -1) * binomial(d - 1, j)));
+    }
+    cudaFree(f->dcoef);
+    f->dcoef = nullptr;
+    TRY(upload_vec(&f->dcoef, cf));
+  }
   TRY(upload_vec(&f->dmtasks, mt));
   if (f->model.kind == SGWG_VLASOV_POISSON && f->rho == nullptr) {
     CK(cudaMalloc(&f->rho, sizeof(double) * std::max<long long>(1, xoff)));
@@ -1043,6 +1082,10 @@ int sgwg_family_create(sgwg_ctx* ctx, const sgwg_domain* dom, sgwg_family** out)
   return family_create(ctx, dom, nullptr, 0, out);
 }
 
+int sgwg_family_create_single(sgwg_ctx* ctx, const sgwg_domain* dom, sgwg_family** out) {
+  return family_create(ctx, dom, nullptr, 0, out, true);
+}
+
 int sgwg_family_create_shard(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members,
                              int count, sgwg_family** out) {
   if (members == nullptr || count < 0) return fail_with(SGWG_EINVAL, "bad shard member list");
@@ -1070,6 +1113,8 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->counter);
   cudaFree(f->dtiles2d);
   cudaFree(f->dtiles2d_fast);
+  cudaFree(f->fe);
+  cudaFree(f->dcoef);
   cudaFreeHost(f->hctl);
   cudaFree(f->dts);
   cudaFree(f->rho);
@@ -1243,6 +1288,15 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
     CK(cudaMalloc(&f->dts, sizeof(double) * want_cap));
     f->dts_cap = want_cap;
     clear_graphs(f);
+  }
+  if (f->model.kind == SGWG_VLASOV_POISSON) {  // per-step ||E||_2 record
+    if (f->fe_cap < f->dts_cap) {
+      cudaFree(f->fe);
+      CK(cudaMalloc(&f->fe, sizeof(double) * f->dts_cap));
+      f->fe_cap = f->dts_cap;
+      clear_graphs(f);
+    }
+    CK(cudaMemsetAsync(f->fe, 0, sizeof(double) * f->fe_cap, s));
   }
   dp.dts = f->dts;
   dp.dts_cap = f->dts_cap;
@@ -1421,6 +1475,18 @@ int sgwg_vp_field(sgwg_family* f, double* rho, size_t nrho, double* E, size_t nE
   return SGWG_OK;
 }
 
+int sgwg_field_energy(sgwg_family* f, double* out, size_t cap, size_t* n) {
+  if (f == nullptr || out == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  if (f->model.kind != SGWG_VLASOV_POISSON || f->fe == nullptr)
+    return fail_with(SGWG_EINVAL, "field_energy: no Vlasov-Poisson evolve recorded");
+  const size_t steps = (size_t)std::min<long long>(f->stats.steps, f->fe_cap);
+  const size_t m = std::min(cap, steps);
+  if (m > 0) CK(cudaMemcpy(out, f->fe, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < m; ++i) out[i] = std::sqrt(out[i]);
+  if (n) *n = m;
+  return SGWG_OK;
+}
+
 int sgwg_time_stage(sgwg_family* f, int reps, double* avg_ms, double* flops, double* bytes) {
   if (f == nullptr || reps < 1 || avg_ms == nullptr) return fail_with(SGWG_EINVAL, "bad argument");
   TRY(require_model(f));
@@ -1476,6 +1542,10 @@ int sgwg_combine(sgwg_family* f, int mode, double eps, double* out, size_t n, in
   if (mode == SGWG_INTERP_WENO && !(eps > 0.0))
     return fail_with(SGWG_EINVAL, "weno_interp5: epsilon must be positive");
   if (f->nm == 0 && f->comm == nullptr) return fail_with(SGWG_EINVAL, "combine: empty family");
+  if (f->single) {  // runner.hpp:323-324: the single grid's field is the result
+    f->stats.combine_ms = 0.0;
+    return copy_out(f, f->u, out, n, out_is_device);
+  }
   CK(cudaSetDevice(f->ctx->device));
   std::vector<int> mis(f->nm);
   for (int i = 0; i < f->nm; ++i) mis[i] = i;

@@ -172,6 +172,7 @@ struct FieldParams {
   const StepCtl* ctl;
   const int2* mtasks;      // moment kernel work: (member, first x point), 8 x points each
   int nmtasks;
+  int nmembers;
 };
 
 // launchers: one set per arithmetic TU (k_exact.cu, k_fast.cu)
@@ -215,6 +216,8 @@ cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* t
                               const double* u, unsigned long long* amax, cudaStream_t s);
 cudaError_t configure_field();
 cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s);
+cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
+                                double hvol, double* out_base, long long cap, cudaStream_t s);
 cudaError_t launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t s);
 
 }  // namespace sgwg

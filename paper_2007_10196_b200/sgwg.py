@@ -88,6 +88,7 @@ SIGNATURES = {
     "sgwg_family_create_shard": (C.c_int, [_VP, C.POINTER(Domain), _IP, C.c_int,
                                            C.POINTER(_VP)]),
     "sgwg_family_destroy": (C.c_int, [_VP]),
+    "sgwg_family_create_single": (C.c_int, [_VP, C.POINTER(Domain), C.POINTER(_VP)]),
     "sgwg_enumerate_levels": (C.c_int, [C.c_int, C.c_int, _IP, C.c_int, _IP]),
     "sgwg_family_num_members": (C.c_int, [_VP, _IP]),
     "sgwg_family_member": (C.c_int, [_VP, C.c_int, _IP, _IP, _IP]),
@@ -113,6 +114,7 @@ SIGNATURES = {
     "sgwg_combine_rows": (C.c_int, [_VP, C.c_int, C.c_double, C.c_longlong, C.c_longlong, _VP,
                                     C.c_size_t, C.c_int]),
     "sgwg_vp_field": (C.c_int, [_VP, _DP, C.c_size_t, _DP, C.c_size_t]),
+    "sgwg_field_energy": (C.c_int, [_VP, _DP, C.c_size_t, C.POINTER(C.c_size_t)]),
 }
 
 
@@ -205,20 +207,24 @@ class Family:
     """CombinationSet + FamilyModel on the device (make_family, combine.hpp:69-83)."""
 
     def __init__(self, ctx: Context, d, nl, lower, upper, root_cells, bc,
-                 members: Optional[Sequence[int]] = None):
+                 members: Optional[Sequence[int]] = None, single: bool = False):
         lib = load()
         self.ctx = ctx
         self.dom = make_domain(d, nl, lower, upper, root_cells, bc)
         self.d, self.nl = d, nl
+        self.single = single
         h = _VP()
-        if members is None:
+        if single:  # make_single_grid (runner.hpp:106-115)
+            _check(lib.sgwg_family_create_single(ctx.h, C.byref(self.dom), C.byref(h)))
+        elif members is None:
             _check(lib.sgwg_family_create(ctx.h, C.byref(self.dom), C.byref(h)))
         else:
             m = np.ascontiguousarray(members, dtype=np.int32)
             _check(lib.sgwg_family_create_shard(ctx.h, C.byref(self.dom),
                                                 m.ctypes.data_as(_IP), len(m), C.byref(h)))
         self.h = h
-        self.all_levels = enumerate_combination_levels(d, nl)
+        self.all_levels = (np.full((1, d), nl, dtype=np.int32) if single
+                           else enumerate_combination_levels(d, nl))
         n = C.c_int(0)
         _check(lib.sgwg_family_num_members(h, C.byref(n)))
         self.num_members = n.value
@@ -237,9 +243,9 @@ class Family:
         self._keep = []
 
     @classmethod
-    def from_config(cls, ctx: Context, cfg: dict, members=None) -> "Family":
+    def from_config(cls, ctx: Context, cfg: dict, members=None, single=False) -> "Family":
         f = cls(ctx, cfg["d"], cfg["nl"], cfg["lower"], cfg["upper"], cfg["root"], cfg["bc"],
-                members)
+                members, single)
         f.set_model(cfg["kind"], speeds=cfg["speeds"], epsilon=cfg["epsilon"],
                     weno_mode=cfg["weno_mode"], space_dim=cfg["space_dim"],
                     theta=cfg["theta"], tau=cfg["tau"])
@@ -384,6 +390,13 @@ class Family:
             out_e.append(E[o * dx:(o + nx) * dx].reshape(dx, nx))
             o += nx
         return out_r, out_e
+
+    def field_energy(self, cap=1 << 20) -> np.ndarray:
+        """||E||_2 of the combined field at the start of every step of the last evolve."""
+        out = np.empty(cap)
+        n = C.c_size_t(0)
+        _check(load().sgwg_field_energy(self.h, out.ctypes.data_as(_DP), cap, C.byref(n)))
+        return out[:n.value].copy()
 
     def time_stage(self, reps=50):
         """(avg ms per stage-kernel launch, algorithmic flops, bytes per launch)."""

@@ -35,6 +35,28 @@ def field_norm(comb, cfg):
     return np.sqrt(L / nx * np.sum(E * E))
 
 
+def test_field_energy_record(ctx_fast, oracle):
+    """sgwg_field_energy: per-step ||E_c||_2, E_c = sum_m c_m Lagrange(E_m) on the
+    finest x-grid, checked at step 0 against a host restatement."""
+    from oracle import oracle as O
+    cfg = configs.config("C4", nl=3)
+    fam = gpu_family(ctx_fast, cfg)
+    fam.initialize(cfg["ic"])
+    rho, E = fam.vp_field()  # field of u^0 (= what step 0 records)
+    nfx = cfg["root"][0] << cfg["nl"]
+    Ec = np.zeros(nfx)
+    for mi, lv in enumerate(fam.levels):
+        m = cfg["nl"] - lv[0]
+        c = [1, -1][cfg["nl"] - sum(lv)]
+        Ec += c * oracle.upsample_line(E[mi][0], nfx, m, O.PERIODIC, O.LAGRANGE) if m else c * E[mi][0]
+    want0 = np.sqrt(np.sum(Ec * Ec) * (cfg["upper"][0] - cfg["lower"][0]) / nfx)
+    dts = fam.evolve(cfg["dt_mode"], 1.0, cfl=cfg["cfl"])
+    fe = fam.field_energy()
+    assert len(fe) == len(dts) > 10
+    assert abs(fe[0] - want0) <= 1e-12 * want0
+    assert np.all(np.isfinite(fe)) and np.all(fe > 0)
+
+
 def test_landau_damping_rate(ctx_fast):
     cfg = configs.config("C4", nl=3)
     fam = gpu_family(ctx_fast, cfg)
