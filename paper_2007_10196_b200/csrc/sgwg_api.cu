@@ -213,6 +213,9 @@ struct sgwg_family {
   int4* dtiles2d_fast = nullptr;
   int ntiles2d_fast = 0;
   int smem2d_fast = 0;
+  int4* dtiles3d_fast = nullptr;  // fast 3D stage tiles (advection)
+  int ntiles3d_fast = 0;
+  int smem3d_fast = 0;
   bool no_fused2d = false;  // SGWG_NO_FUSED2D=1: use the per-dimension pass kernels
   bool single = false;      // single-grid mode (runner.hpp:106-115): combine = the grid itself
 };
@@ -305,6 +308,39 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
   unsigned long long* zero_slot =
       (burgers && stage > 0) ? f->amax + (size_t)((stage + 1) % 3) * f->nm : nullptr;
   const DtParams* dtp = (fuse_dt && stage == 3) ? f->d_dtp : nullptr;
+  if (f->d == 3 && f->ntiles3d_fast > 0 && arith_of(f) == SGWG_ARITH_FAST &&
+      m.kind == SGWG_ADVECTION) {  // fused 3D stage (all three sweeps + RK, one launch)
+    Stage2DParams p{};
+    p.mem = f->dmem;
+    p.tiles = f->dtiles3d_fast;
+    p.flux0 = p.flux1 = p.flux2 = kFluxAdvect;
+    p.c0 = m.speeds[0];
+    p.c1 = m.speeds[1];
+    p.c2 = m.speeds[2];
+    p.stage = stage;
+    p.linear = (m.weno_mode == SGWG_WENO_LINEAR);
+    p.eps = m.epsilon;
+    p.uin = b.uin;
+    p.un = b.un;
+    p.out = b.out;
+    p.ctl = f->ctl;
+    p.nmembers = f->nm;
+    p.fail = f->fail;
+    p.dtp = dtp;
+    p.counter = f->counter;
+    if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
+    CK(fast::launch_stage3d(p, f->ntiles3d_fast, (size_t)f->smem3d_fast * sizeof(double),
+                            f->ctx->stream));
+    if (timed) {
+      CK(cudaEventRecord(f->ev1, f->ctx->stream));
+      CK(cudaEventSynchronize(f->ev1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+      account_timed(f, stage, 3, true, ms);
+    }
+    f->stats.kernel_launches++;
+    return SGWG_OK;
+  }
   if (f->d == 2 && f->ntiles2d > 0) {
     Stage2DParams p{};
     const bool fastk = arith_of(f) == SGWG_ARITH_FAST;
@@ -506,6 +542,42 @@ int build_tasks(sgwg_family* f) {
     f->smem2d_fast = sfmax;
     CK(cudaMalloc(&f->dtiles2d_fast, sizeof(int4) * std::max<size_t>(1, tf.size())));
     CK(cudaMemcpy(f->dtiles2d_fast, tf.data(), sizeof(int4) * tf.size(), cudaMemcpyHostToDevice));
+  }
+  if (f->d == 3 && !f->no_fused2d) {  // fast 3D stage tiles: 2048 points, 3 shapes
+    static const int shp3[3][3] = {{8, 16, 16}, {16, 8, 16}, {16, 16, 8}};
+    std::vector<int4> t3;
+    int smax = 0;
+    bool ok = true;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      const MemberDesc& M = f->hmem[mi];
+      if (M.ext[0] >= 65536 || M.ext[1] >= 65536) ok = false;
+      int best = 0;
+      long long bw = -1;
+      for (int s = 0; s < 3; ++s) {
+        long long cov = 1;
+        for (int k = 0; k < 3; ++k)
+          cov *= (long long)((M.ext[k] + shp3[s][k] - 1) / shp3[s][k]) * shp3[s][k];
+        if (bw < 0 || cov < bw) {
+          bw = cov;
+          best = s;
+        }
+      }
+      const int TX = shp3[best][0], TY = shp3[best][1], TZ = shp3[best][2];
+      const int PZ = ((TZ + 6) % 2 == 0) ? TZ + 7 : TZ + 6;
+      const int sm = (TX + 6) * (TY + 6) * PZ + 3 * TX * TY * (TZ + 1) + TY * TZ + TX * TZ + TX * TY;
+      smax = std::max(smax, sm);
+      for (int i0 = 0; i0 < M.ext[0]; i0 += TX)
+        for (int j0 = 0; j0 < M.ext[1]; j0 += TY)
+          for (int l0 = 0; l0 < M.ext[2]; l0 += TZ)
+            t3.push_back(make_int4(mi, (i0 << 16) | j0, (l0 << 8) | best, 0));
+    }
+    if (ok) {
+      f->ntiles3d_fast = (int)t3.size();
+      f->smem3d_fast = smax;
+      CK(cudaMalloc(&f->dtiles3d_fast, sizeof(int4) * std::max<size_t>(1, t3.size())));
+      CK(cudaMemcpy(f->dtiles3d_fast, t3.data(), sizeof(int4) * t3.size(),
+                    cudaMemcpyHostToDevice));
+    }
   }
   std::vector<int2> mt;
   for (int mi = 0; mi < f->nm; ++mi)
@@ -720,7 +792,9 @@ int get_graph(sgwg_family* f, int nsteps, cudaGraphExec_t* exec) {
 }
 
 int launches_per_step(const sgwg_family* f) {
-  const int np = (f->d == 2 && f->ntiles2d > 0) ? 1 : (int)pass_order(f).size();
+  const bool fused3d = f->d == 3 && f->ntiles3d_fast > 0 && arith_of(f) == SGWG_ARITH_FAST &&
+                       f->model.kind == SGWG_ADVECTION;
+  const int np = ((f->d == 2 && f->ntiles2d > 0) || fused3d) ? 1 : (int)pass_order(f).size();
   int n = 3 * np;
   if (!dt_fusable(f)) n += 1;
   if (f->model.kind == SGWG_VLASOV_POISSON) n += 6;  // moment + FFT field per stage
@@ -1113,6 +1187,7 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->counter);
   cudaFree(f->dtiles2d);
   cudaFree(f->dtiles2d_fast);
+  cudaFree(f->dtiles3d_fast);
   cudaFree(f->fe);
   cudaFree(f->dcoef);
   cudaFreeHost(f->hctl);

@@ -91,6 +91,8 @@ struct Stage2DParams {
   int burgers;
   int flux0, flux1;        // FluxKind of the dimension-0 / dimension-1 sweep
   double c0, c1;           // advection speeds
+  int flux2;               // 3D stage kernel: dimension-2 sweep
+  double c2;
   int stage;               // 1..3, 0 = tendency only
   int linear;
   double eps;
@@ -187,6 +189,7 @@ struct FieldParams {
 SGWG_DECLARE_LAUNCHERS(exact)
 SGWG_DECLARE_LAUNCHERS(fast)
 namespace fast {
+cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s);
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s);
 int persist2d_max_blocks(int burgers, size_t smem);
 }  // namespace fast
