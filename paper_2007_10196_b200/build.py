@@ -31,7 +31,7 @@ UNITS = {
     "k_field.cu": ["--fmad=true"],
     "sgwg_api.cu": ["--fmad=false"],
 }
-HEADERS = ["kernels.cuh", "sgwg_internal.h"]
+HEADERS = ["kernels.cuh", "sgwg_internal.h", "dt_device.cuh", "field_device.cuh"]
 
 
 def _stale(obj, deps):

@@ -1,214 +1,31 @@
-// k_field.cu -- Vlasov-Poisson field of every member (BASELINE C4/C5).
+// k_field.cu -- Vlasov-Poisson field kernels of every member (BASELINE C4/C5);
+// the device code is in field_device.cuh (shared with the persistent kernel).
 //
-// NEW PHYSICS: the reference has no Poisson solver.  This
-// follows the kinetic template of vb_rhs_into (models.hpp:334-363): the
-// charge density uses the reference's trapezoid weights over the contiguous
-// velocity block (moment_density models.hpp:294-306, block_weights 240-257,
-// trapezoid_weights_1d 64-71), rho(x) = 1 - sum_v w_v f(x, v); the field solves
-// -lap(phi) = rho, E = -grad(phi) spectrally on the member's own periodic
-// x-grid (mean and Nyquist modes dropped), as the oracle restatement
-// oracle/sgw_oracle.c:spectral_poisson does with a direct DFT.
-//
-// One CTA per member: the x-grid has <= 2048 points (C4: 32*2^l; C5:
-// (8*2^l1)x(8*2^l2), l1+l2 <= 5), so the whole 2D FFT lives in shared memory.
-#include <math.h>
-
-#include "sgwg_internal.h"
+// moment_kernel: rho of every x point (one warp each, many CTAs).
+// field_kernel:  one CTA per member: the x-grid has <= 2048 points (C4: 32*2^l;
+//                C5: (8*2^l1)x(8*2^l2), l1+l2 <= 5), so the 2D FFT lives in
+//                shared memory.
+// field_energy_kernel: per-step ||E_c||_2 diagnostic.
+#include "field_device.cuh"
 
 namespace sgwg {
 
-constexpr int kFieldThreads = 512;
-constexpr int kFieldMaxX = 2048;
-
-__device__ __forceinline__ int bitrev(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }
-
-// radix-2 FFTs of all lines of an n1 x n2 complex array along `axis` (1 = x2,
-// contiguous).  sign -1: forward e^{-i...}; +1: inverse (unnormalised).
-__device__ void fft_lines(double* re, double* im, int n1, int n2, int axis, int sign,
-                          const double* twc, const double* tws, int H) {
-  const int len = axis ? n2 : n1;
-  if (len <= 1) return;
-  const int nx = n1 * n2;
-  const int stride = axis ? 1 : n2;
-  const int bits = __ffs(len) - 1;
-  for (int idx = threadIdx.x; idx < nx; idx += blockDim.x) {
-    const int line = idx / len, pos = idx - line * len;
-    const int rev = bitrev(pos, bits);
-    if (pos < rev) {
-      const int base = axis ? line * n2 : line;
-      const int a = base + pos * stride, b = base + rev * stride;
-      const double tr = re[a], ti = im[a];
-      re[a] = re[b];
-      im[a] = im[b];
-      re[b] = tr;
-      im[b] = ti;
-    }
-  }
-  __syncthreads();
-  for (int half = 1; half < len; half <<= 1) {
-    for (int bfly = threadIdx.x; bfly < nx / 2; bfly += blockDim.x) {
-      const int per = len / 2;
-      const int line = bfly / per, q = bfly - line * per;
-      const int grp = q / half, pos = q - grp * half;
-      const int base = axis ? line * n2 : line;
-      const int i0 = base + (grp * 2 * half + pos) * stride;
-      const int i1 = i0 + half * stride;
-      // e^{sign i pi pos/half} from the table e^{i pi k/H}, k = pos * H/half
-      const int ti = pos * (H / half);
-      const double c = twc[ti], s = sign * tws[ti];
-      const double br = re[i1] * c - im[i1] * s;
-      const double bi = re[i1] * s + im[i1] * c;
-      const double ar = re[i0], ai = im[i0];
-      re[i0] = ar + br;
-      im[i0] = ai + bi;
-      re[i1] = ar - br;
-      im[i1] = ai - bi;
-    }
-    __syncthreads();
-  }
-}
-
-// rho(x) = 1 - sum_v w_v f(x, v) (moment_density models.hpp:294-306 with the
-// trapezoid block weights 240-257, 64-71): one warp per x point, lanes stride
-// the contiguous velocity block with 4 loads in flight; fixed reduction order.
 __global__ void __launch_bounds__(256) moment_kernel(const FieldParams p) {
   if (p.ctl != nullptr && !p.ctl->active) return;
   const int2 tk = p.mtasks[blockIdx.x];
   const MemberDesc* M = p.mem + tk.x;
-  const int dx = p.space_dim;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int xi = tk.y + warp;
+  const int xi = tk.y + (threadIdx.x >> 5);
   if (xi >= M->nx) return;
-  const int vn = M->vn;
-  const int ev0 = M->ext[dx], ev1 = (dx == 2) ? M->ext[dx + 1] : 1;
-  const double hv0 = M->h[dx], hv1 = (dx == 2) ? M->h[dx + 1] : 1.0;
-  const int zb0 = M->bc[dx], zb1 = (dx == 2) ? M->bc[dx + 1] : 0;
-  const double* block = p.f + M->offset + (long long)xi * vn;
-  const float inv_ev1 = 1.0f / (float)ev1;
-  auto weight = [&](int vi) {
-    const int i0 = (int)(((float)vi + 0.5f) * inv_ev1), i1 = vi - i0 * ev1;
-    double w0 = hv0, w1 = hv1;
-    if (zb0 == 1 && (i0 == 0 || i0 == ev0 - 1)) w0 *= 0.5;
-    if (dx == 2 && zb1 == 1 && (i1 == 0 || i1 == ev1 - 1)) w1 *= 0.5;
-    return (dx == 2) ? w0 * w1 : w0;
-  };
-  double acc = 0.0;
-  for (int vb = lane; vb < vn; vb += 4 * 32) {
-    double v[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) v[b] = (vb + 32 * b < vn) ? __ldg(block + vb + 32 * b) : 0.0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (vb + 32 * b < vn) acc = fma(weight(vb + 32 * b), v[b], acc);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) p.rho[M->xoff + xi] = 1.0 - acc;
+  moment_point<false>(p, M, xi);
 }
 
 __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams p) {
   if (p.ctl != nullptr && !p.ctl->active) return;
-  const MemberDesc* M = p.mem + blockIdx.x;
-  const int dx = p.space_dim;
-  const int n1 = M->xext[0], n2 = M->xext[1];
-  const int nx = M->nx;
-  const int vn = M->vn;
   extern __shared__ double sh[];
-  double* rr = sh;
-  double* ri = sh + nx;
-  double* er = sh + 2 * nx;
-  double* ei = sh + 3 * nx;
-  // twiddles e^{i pi k/H}, k < H = max(n1, n2)/2, shared by every stage and transform
-  const int H = max(1, max(n1, n2) / 2);
-  double* twc = sh + 4 * nx;
-  double* tws = twc + H;
-  __shared__ double red[kFieldThreads / 32][2];
-
-  // rho(x) from the moment kernel
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int xi = threadIdx.x; xi < nx; xi += blockDim.x) {
-    rr[xi] = p.rho[M->xoff + xi];
-    ri[xi] = 0.0;
-  }
-  for (int k = threadIdx.x; k < H; k += blockDim.x) sincospi((double)k / (double)H, &tws[k], &twc[k]);
-  __syncthreads();
-  fft_lines(rr, ri, n1, n2, 1, -1, twc, tws, H);
-  fft_lines(rr, ri, n1, n2, 0, -1, twc, tws, H);
-
-  const double two_pi = 6.283185307179586476925286766559;
-  for (int comp = 0; comp < dx; ++comp) {
-    for (int id = threadIdx.x; id < nx; id += blockDim.x) {
-      const int k1 = id / n2, k2 = id - k1 * n2;
-      const int s1 = (k1 <= n1 / 2) ? k1 : k1 - n1;
-      const int s2 = (k2 <= n2 / 2) ? k2 : k2 - n2;
-      const bool nyq = ((n1 % 2 == 0) && k1 == n1 / 2 && n1 > 1) ||
-                       ((n2 % 2 == 0) && k2 == n2 / 2 && n2 > 1);
-      const double kap1 = two_pi * (double)s1 / p.L[0];
-      const double kap2 = (dx == 2) ? two_pi * (double)s2 / p.L[1] : 0.0;
-      const double k2s = kap1 * kap1 + kap2 * kap2;
-      if ((s1 == 0 && s2 == 0) || nyq) {
-        er[id] = 0.0;
-        ei[id] = 0.0;
-      } else {
-        const double kc = (comp == 0) ? kap1 : kap2;
-        er[id] = kc * ri[id] / k2s;  // -i kc rhat / |k|^2
-        ei[id] = -kc * rr[id] / k2s;
-      }
-    }
-    __syncthreads();
-    fft_lines(er, ei, n1, n2, 1, +1, twc, tws, H);
-    fft_lines(er, ei, n1, n2, 0, +1, twc, tws, H);
-    double lmax = 0.0;
-    const double inv_n = 1.0 / (double)nx;
-    double* E = p.efield + M->xoff * dx + (long long)comp * nx;
-    for (int id = threadIdx.x; id < nx; id += blockDim.x) {
-      const double e = er[id] * inv_n;
-      E[id] = e;
-      lmax = fmax(lmax, fabs(e));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    if (lane == 0) red[warp][0] = lmax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double m = 0.0;
-      for (int q = 0; q < nwarps; ++q) m = fmax(m, red[q][0]);
-      p.emax[blockIdx.x * dx + comp] = m;
-    }
-    __syncthreads();
-  }
+  __shared__ double red[kFieldThreads / 32];
+  field_member<false>(p, blockIdx.x, sh, red);
 }
 
-// degree-4 Lagrange weights in the reference's cell form (interp.hpp:36-53
-// with OffsetTable::cell_weights, interp.hpp:119-122) for fine index j of a
-// periodic line refined by 2^m: 5 source indices i-2..i+2 and weights.
-__device__ __forceinline__ void lagrange5(int j, int m, int n_src, int* idx, double* w) {
-  const int f = 1 << m, r = j & (f - 1), i = j >> m;
-  const double t = (double)r / f;
-  if (r == 0) {
-    for (int q = 0; q < 5; ++q) {
-      idx[q] = ((i - 2 + q) % n_src + n_src) % n_src;
-      w[q] = (q == 2) ? 1.0 : 0.0;
-    }
-    return;
-  }
-  const double c0 = (t - 1.0) * (t - 2.0) / 12.0, c1 = (4.0 - t * t) / 6.0,
-               c2 = (t + 2.0) * (t + 1.0) / 12.0;
-  // sum_k c_k p_k(t) expanded into point weights (substencil_values, interp.hpp:45-53)
-  const double a0 = 0.5 * (t + 1.0) * t, a1 = -(t + 2.0) * t, a2 = 0.5 * (t + 2.0) * (t + 1.0);
-  const double b1 = 0.5 * t * (t - 1.0), b2 = -(t + 1.0) * (t - 1.0), b3 = 0.5 * (t + 1.0) * t;
-  const double e2 = 0.5 * (t - 1.0) * (t - 2.0), e3 = -t * (t - 2.0), e4 = 0.5 * t * (t - 1.0);
-  w[0] = c0 * a0;
-  w[1] = c0 * a1 + c1 * b1;
-  w[2] = c0 * a2 + c1 * b2 + c2 * e2;
-  w[3] = c1 * b3 + c2 * e3;
-  w[4] = c2 * e4;
-  for (int q = 0; q < 5; ++q) idx[q] = ((i - 2 + q) % n_src + n_src) % n_src;
-}
-
-// ||E||_2 of the combined field on the finest x-grid: E_c = sum_m c_m I_m(E_m),
-// I_m the separable degree-4 Lagrange interpolation from member m's x-grid;
-// h-weighted sum of |E_c|^2 accumulated into *out (diagnostic).
 __global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p,
                                                            const double* coef, int fine0,
                                                            int fine1, double hvol,
@@ -216,40 +33,13 @@ __global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p,
   if (p.ctl != nullptr && !p.ctl->active) return;
   const long long slot = (p.ctl != nullptr) ? p.ctl->step : 0;  // the step about to be taken
   if (slot >= cap) return;
-  double* out = out_base + slot;
-  const int dx = p.space_dim;
-  const int nfine = fine0 * fine1;
   double acc = 0.0;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nfine; q += gridDim.x * blockDim.x) {
-    const int i = q / fine1, j = q - (q / fine1) * fine1;
-    double ec[2] = {0.0, 0.0};
-    for (int mi = 0; mi < p.nmembers; ++mi) {
-      const MemberDesc* M = p.mem + mi;
-      const int n0 = M->xext[0], n1 = M->xext[1];
-      int ia[5], ja[5];
-      double wa[5], wb[5];
-      lagrange5(i, __ffs(fine0 / n0) - 1, n0, ia, wa);
-      if (dx == 2) {
-        lagrange5(j, __ffs(fine1 / n1) - 1, n1, ja, wb);
-      } else {
-        for (int b = 0; b < 5; ++b) ja[b] = 0, wb[b] = (b == 2) ? 1.0 : 0.0;
-      }
-      for (int c = 0; c < dx; ++c) {
-        const double* E = p.efield + M->xoff * dx + (long long)c * M->nx;
-        double v = 0.0;
-        for (int a = 0; a < 5; ++a) {
-          double s = 0.0;
-          for (int b = 0; b < 5; ++b) s = fma(wb[b], E[ia[a] * n1 + ja[b]], s);
-          v = fma(wa[a], s, v);
-        }
-        ec[c] = fma(coef[mi], v, ec[c]);
-      }
-    }
-    for (int c = 0; c < dx; ++c) acc = fma(ec[c], ec[c], acc);
-  }
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < fine0 * fine1;
+       q += gridDim.x * blockDim.x)
+    acc += energy_point<false>(p, coef, q, fine0, fine1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc * hvol);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out_base + slot, acc * hvol);
 }
 
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
@@ -262,14 +52,13 @@ cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fi
 
 cudaError_t configure_field() {
   return cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(5 * kFieldMaxX * sizeof(double)));
+                              (int)(kFieldSmemDoubles * sizeof(double)));
 }
 
 cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s) {
   if (nmembers <= 0) return cudaSuccess;
   moment_kernel<<<p.nmtasks, 256, 0, s>>>(p);
-  const size_t smem = 5 * kFieldMaxX * sizeof(double);
-  field_kernel<<<nmembers, kFieldThreads, smem, s>>>(p);
+  field_kernel<<<nmembers, kFieldThreads, kFieldSmemDoubles * sizeof(double), s>>>(p);
   return cudaGetLastError();
 }
 
