@@ -748,12 +748,28 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   constexpr int NHL = (NH + NT - 1) / NT;
   double vin[NE], pre_n[NE], vh[NHL];
   int ih[NHL];
+  // resident tile (persistent launch, one tile per CTA): the tile's own stage
+  // input and u^n stay in shared memory between stages; only halos and
+  // out-of-member padding come from L2
+  double* UC = cy + TX;
+  double* UN = UC + TX * TY;
+  const bool resident = PERSIST && p.resident;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const int q = tid + e * NT;
-    const int g = gindex(q / TY + 3, q % TY + 3);
-    vin[e] = (g >= 0) ? ldx<PERSIST>(u + g) : 0.0;
-    pre_n[e] = (p.stage > 1 && g >= 0) ? ldx<PERSIST>(p.un + M->offset + g) : 0.0;
+    const bool inside = (i0 + q / TY < n0) && (j0 + q % TY < n1);
+    if (resident && !p.resident_load && inside) {
+      vin[e] = UC[q];
+      pre_n[e] = UN[q];
+    } else {
+      const int g = gindex(q / TY + 3, q % TY + 3);
+      vin[e] = (g >= 0) ? ldx<PERSIST>(u + g) : 0.0;
+      pre_n[e] = (p.stage > 1 && g >= 0) ? ldx<PERSIST>(p.un + M->offset + g) : 0.0;
+      if (resident && inside) {
+        UC[q] = vin[e];
+        UN[q] = (p.stage == 1) ? vin[e] : pre_n[e];
+      }
+    }
   }
 #pragma unroll
   for (int e = 0; e < NHL; ++e) {
@@ -830,6 +846,10 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
         o = fma(1.0 / 3.0, pre_n[e], (2.0 / 3.0) * fma(dt, kv, ui));
     }
     p.out[gi] = o;
+    if (resident) {  // next stage's input (and u^{n+1} after stage 3) stay on chip
+      UC[q] = o;
+      if (p.stage == 3) UN[q] = o;
+    }
     lmax = fmax(lmax, fabs(o));
   }
   if (p.track_max) {
@@ -1097,6 +1117,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
       p.amax_out = pp.base.amax_zero + (size_t)(s % 3) * nm;
       p.dt_value = sctl.dt;
       p.cur_step = (unsigned long long)sctl.cur_step;
+      p.resident = pp.base.resident && (pp.base.ntiles <= (int)gridDim.x);
+      p.resident_load = (step == 0 && s == 1);
       if (BURGERS && blockIdx.x == 0)  // stage s clears the slot stage s+1 writes
         for (int i = threadIdx.x; i < nm; i += blockDim.x)
           pp.base.amax_zero[(size_t)((s + 1) % 3) * nm + i] = 0ull;

@@ -1405,7 +1405,8 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   // small 2D families (fast build, single rank): persistent cooperative kernel
   PersistParams pp{};
   int persist_blocks = 0;
-  const size_t persist_smem = (size_t)f->smem2d_fast * sizeof(double);
+  // + the resident tile (stage input and u^n, 2 x 2048 doubles)
+  const size_t persist_smem = ((size_t)f->smem2d_fast + 2 * 2048) * sizeof(double);
   if (arith_of(f) == SGWG_ARITH_FAST && f->d == 2 && f->ntiles2d_fast > 0 && dt_fusable(f) &&
       !f->ctx->profile && std::getenv("SGWG_NO_PERSIST") == nullptr) {
     const int maxb = fast::persist2d_max_blocks(f->model.kind == SGWG_BURGERS, persist_smem);
@@ -1431,6 +1432,8 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
     p.track_max = p.burgers;
     p.fail = f->fail;
     p.dtp = f->d_dtp;
+    p.resident = (f->ntiles2d_fast <= persist_blocks &&
+                  std::getenv("SGWG_NO_RESIDENT") == nullptr) ? 1 : 0;
     pp.u = f->u;
     pp.A = f->A;
     pp.B = f->B;

@@ -115,6 +115,8 @@ struct Stage2DParams {
   double dt_value;
   unsigned long long cur_step;
   int ntiles;
+  int resident;       // one tile per CTA: stage input / u^n kept in shared memory
+  int resident_load;  // first stage of the launch: fill the resident copy from HBM
 };
 
 struct PersistParams {

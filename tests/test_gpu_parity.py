@@ -245,6 +245,22 @@ def test_evolve_fast_within_tol(ctx_fast, oracle):
     assert maxabs(gc[-1], wc[-1]) < TOL
 
 
+@pytest.mark.parametrize("T,stops", [
+    (0.0, []),                                   # tfinal == 0: one stop at 0, no steps
+    (0.02, [-1.0, 0.0, 0.01, 0.01 + 1e-14, 0.5]),  # out-of-range and duplicate stops
+    (0.02, [0.02, 0.005]),                         # unsorted, stop == T
+])
+def test_evolve_stop_list_semantics(ctx, oracle, T, stops):
+    """timestep.hpp:133-172 stop handling, bitwise (dts, stop count, combined fields)."""
+    cfg = configs.config("C2", nl=3, root=[16, 16])
+    got, want, gd, wd, gc, wc = _evolve_both(ctx, oracle, cfg, T, stops=stops)
+    assert len(gc) == len(wc)
+    assert bitwise_equal(gd, wd), (gd, wd)
+    assert bitwise_equal(got, want)
+    for a, b in zip(gc, wc):
+        assert bitwise_equal(a, b)
+
+
 def test_failure_injection(ctx, oracle):
     """test_timestep.cpp:145-155: state x 1e150 -> FamilyIntegratorFailure."""
     from paper_2007_10196_b200 import sgwg
