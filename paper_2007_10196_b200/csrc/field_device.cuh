@@ -78,9 +78,9 @@ __device__ inline void fft_lines(double* re, double* im, int n1, int n2, int axi
   }
 }
 
-// rho(x_i) = 1 - sum_v w_v f(x_i, v) for one x point, computed by one warp
+// sum_v w_v f(x_i, v) for one x point (rho = 1 - that), computed by one warp
 // (lanes stride the contiguous velocity block, 4 loads in flight, fixed
-// reduction order).
+// reduction order), stored as partial 0 of the point (the others zeroed).
 template <bool COH>
 __device__ inline void moment_point(const FieldParams& p, const MemberDesc* M, int xi) {
   const int dx = p.space_dim;
@@ -109,7 +109,8 @@ __device__ inline void moment_point(const FieldParams& p, const MemberDesc* M, i
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) p.rho[M->xoff + xi] = 1.0 - acc;
+  if (lane < M->rparts)  // partial-sum form: the whole sum in part 0
+    p.rho_parts[(M->xoff + xi) * kRhoParts + lane] = (lane == 0) ? acc : 0.0;
 }
 
 // E of member mi from its rho (whole block; sh >= kFieldSmemDoubles doubles;
@@ -129,7 +130,12 @@ __device__ inline void field_member(const FieldParams& p, int mi, double* sh, do
   double* tws = twc + H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int xi = threadIdx.x; xi < nx; xi += blockDim.x) {
-    rr[xi] = fld_ld<COH>(p.rho + M->xoff + xi);
+    const double* pt = p.rho_parts + (M->xoff + xi) * kRhoParts;
+    double acc = fld_ld<COH>(pt);
+    for (int t = 1; t < M->rparts; ++t) acc += fld_ld<COH>(pt + t);
+    const double r = 1.0 - acc;
+    p.rho[M->xoff + xi] = r;
+    rr[xi] = r;
     ri[xi] = 0.0;
   }
   for (int k = threadIdx.x; k < H; k += blockDim.x)

@@ -55,9 +55,9 @@ cudaError_t configure_field() {
                               (int)(kFieldSmemDoubles * sizeof(double)));
 }
 
-cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s) {
+cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, cudaStream_t s) {
   if (nmembers <= 0) return cudaSuccess;
-  moment_kernel<<<p.nmtasks, 256, 0, s>>>(p);
+  if (with_moment) moment_kernel<<<p.nmtasks, 256, 0, s>>>(p);
   field_kernel<<<nmembers, kFieldThreads, kFieldSmemDoubles * sizeof(double), s>>>(p);
   return cudaGetLastError();
 }

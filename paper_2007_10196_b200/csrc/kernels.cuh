@@ -1081,6 +1081,326 @@ __global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_fast_kernel(const 
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
 }
 
+// ---------------------------------------------------------------------------
+// fast 4D stage (kinetic transport / advection) as two plane launches
+// ---------------------------------------------------------------------------
+// A 4D member splits into planes of the dimension pairs (0,1) and (2,3): for
+// the kinetic models the x-lines of a fixed velocity point carry the constant
+// coefficients (v_1, v_2) (models.hpp:341-344) and the v-lines of a fixed x
+// point the constants (-E_1(x), -E_2(x)), so each plane is a 2D constant-speed
+// advection problem.  Launch pr = 0 sweeps dims 0 and 1 of every plane and
+// stores K = (0 - du_0) - du_1; launch pr = 1 sweeps dims 2 and 3, forms
+// k = (K - du_2) - du_3 and applies the RK stage (and, for Vlasov-Poisson, the
+// charge-density partial sums of the stage output).  A tile is nv consecutive
+// planes restricted to a window, staged with 3-point halos (periodic wrap or
+// zero ghosts, weno.hpp:131-141); the two sweeps run concurrently in two
+// 128-thread halves over runs of 8 points (a line of 8m+1 points: m runs and a
+// 1-point tail).  Compulsory traffic 16 B (pr 0) + 24..32 B (pr 1) per point.
+constexpr int kPlaneThreads = 256;
+constexpr int kPlaneMaxE = 8;  // tile points <= kPlaneThreads * kPlaneMaxE
+
+// q / n for 0 <= q < 2^21, 0 < n < 2^12 via a float reciprocal (exact: the quotient
+// (q + 1/2) / n is >= 1/(2n) away from an integer; float error < q 2^-23 / n)
+__device__ __forceinline__ int qdiv(int q, float inv_n) {
+  return (int)(((float)q + 0.5f) * inv_n);
+}
+
+struct PlaneGeom {
+  int TX, TY, V;
+  int RA, RB, tailA, tailB, TXr, TYr, PA, PB, DPB;
+  __host__ __device__ PlaneGeom(int nv, int tx, int ty) : TX(tx), TY(ty), V(nv) {
+    tailA = (TX & 7) == 1;
+    tailB = (TY & 7) == 1;
+    RA = tailA ? TX >> 3 : (TX + 7) >> 3;
+    RB = tailB ? TY >> 3 : (TY + 7) >> 3;
+    TXr = tailA ? TX : RA * 8;
+    TYr = tailB ? TY : RB * 8;
+    PA = TXr + 6;
+    PB = (TYr + 6) | 1;  // odd pitches
+    DPB = TYr | 1;
+  }
+  __host__ __device__ int smem_doubles() const {
+    return V * PA * PB + 2 * V * TXr * DPB + 2 * kPlaneMaxV;
+  }
+};
+
+template <bool LINEAR>
+__device__ __forceinline__ void plane_sweeps(const PlaneGeom& G, const double* FP, double* DX,
+                                             double* DY, const double* sca, const double* scb,
+                                             double eps4, double inv_ha, double inv_hb) {
+  constexpr int NSW = kPlaneThreads / 2;
+  const int tid = threadIdx.x;
+  const int plane = G.PA * G.PB;
+  const float iTX = 1.0f / (float)G.TX, iTY = 1.0f / (float)G.TY, iV = 1.0f / (float)G.V;
+  if (tid < NSW) {  // a-sweep: lines (v, j), runs along a; lanes walk j
+    const int nit = G.V * G.TY * G.RA;
+#pragma unroll 1
+    for (int w = tid; w < nit; w += NSW) {
+      const int r2 = qdiv(w, iTY), j = w - r2 * G.TY, r = qdiv(r2, iV), v = r2 - r * G.V;
+      const double* P = FP + v * plane + j + 3;
+      sweep_run<false, 8, LINEAR>(P, P, G.PB, r * 8, sca[v], eps4, inv_ha,
+                                  DX + (v * G.TXr + r * 8) * G.DPB + j, G.DPB);
+    }
+    if (G.tailA)
+#pragma unroll 1
+      for (int w = tid; w < G.V * G.TY; w += NSW) {
+        const int v = qdiv(w, iTY), j = w - v * G.TY;
+        const double* P = FP + v * plane + j + 3;
+        sweep_run<false, 1, LINEAR>(P, P, G.PB, G.TX - 1, sca[v], eps4, inv_ha,
+                                    DX + (v * G.TXr + G.TX - 1) * G.DPB + j, G.DPB);
+      }
+  } else {  // b-sweep: lines (v, i), runs along b; lanes walk i (odd pitch)
+    const int t = tid - NSW;
+    const int nit = G.V * G.TX * G.RB;
+#pragma unroll 1
+    for (int w = t; w < nit; w += NSW) {
+      const int r2 = qdiv(w, iTX), i = w - r2 * G.TX, r = qdiv(r2, iV), v = r2 - r * G.V;
+      const double* P = FP + v * plane + (i + 3) * G.PB;
+      sweep_run<false, 8, LINEAR>(P, P, 1, r * 8, scb[v], eps4, inv_hb,
+                                  DY + (v * G.TXr + i) * G.DPB + r * 8, 1);
+    }
+    if (G.tailB)
+#pragma unroll 1
+      for (int w = t; w < G.V * G.TX; w += NSW) {
+        const int v = qdiv(w, iTX), i = w - v * G.TX;
+        const double* P = FP + v * plane + (i + 3) * G.PB;
+        sweep_run<false, 1, LINEAR>(P, P, 1, G.TY - 1, scb[v], eps4, inv_hb,
+                                    DY + (v * G.TXr + i) * G.DPB + G.TY - 1, 1);
+      }
+  }
+}
+
+__global__ void __launch_bounds__(kPlaneThreads, 3) plane_fast_kernel(const PlaneParams p) {
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  const PlaneTile tl = p.tiles[blockIdx.x];
+  const MemberDesc* M = p.mem + tl.mi;
+  const int a = 2 * p.pr, b = a + 1;
+  const PlaneGeom G(tl.nv, tl.tx, tl.ty);
+  const int na = M->ext[a], nb = M->ext[b];
+  const int sa = (int)M->stride[a], sb = (int)M->stride[b];
+  const int ps = (p.pr == 0) ? 1 : M->ext[2] * M->ext[3];  // plane -> memory offset
+  const bool vfast = (p.pr == 0);  // consecutive planes are adjacent in memory
+  const int bca = M->bc[a], bcb = M->bc[b];
+  const int TX = G.TX, TY = G.TY, V = G.V;
+  const int NP = V * TX * TY;
+  const int plane = G.PA * G.PB;
+  extern __shared__ double sm[];
+  double* FP = sm;
+  double* DX = FP + V * plane;
+  double* DY = DX + V * G.TXr * G.DPB;
+  double* sca = DY + V * G.TXr * G.DPB;
+  double* scb = sca + kPlaneMaxV;
+  const int tid = threadIdx.x;
+  if (tid < V) {  // per-plane line coefficients (line_coef)
+    const int pl = tl.plane0 + tid;
+    if (p.pr == 0) {  // x_j lines at velocity point pl: v_j (models.hpp:341-344)
+      const int n3 = M->ext[3];
+      sca[tid] = line_coef(p.flux_a, M, 0, p.space_dim, pl / n3, p.c_a, p.efield);
+      scb[tid] = line_coef(p.flux_b, M, 1, p.space_dim, pl % n3, p.c_b, p.efield);
+    } else {  // v_j lines at x point pl: -E_j(x)
+      sca[tid] = line_coef(p.flux_a, M, 2, p.space_dim, pl, p.c_a, p.efield);
+      scb[tid] = line_coef(p.flux_b, M, 3, p.space_dim, pl, p.c_b, p.efield);
+    }
+  }
+  const double* u = p.uin + M->offset;
+  // tile point q -> (v, i, j): planes fastest when adjacent in memory, else j
+  const float iTX = 1.0f / (float)TX, iTY = 1.0f / (float)TY, iV = 1.0f / (float)V;
+  auto decode = [&](int q, int& v, int& i, int& j) {
+    if (vfast) {
+      const int r = qdiv(q, iV);
+      v = q - r * V;
+      i = qdiv(r, iTY);
+      j = r - i * TY;
+    } else {
+      const int r = qdiv(q, iTY);
+      j = q - r * TY;
+      v = qdiv(r, iTX);
+      i = r - v * TX;
+    }
+  };
+  // interior: one load per point (all in flight before any use)
+  const bool wholeA = (TX == na), wholeB = (TY == nb);
+  double vin[kPlaneMaxE];
+  int sidx[kPlaneMaxE], ij[kPlaneMaxE];
+#pragma unroll
+  for (int e = 0; e < kPlaneMaxE; ++e) {
+    const int q = tid + e * kPlaneThreads;
+    vin[e] = 0.0;
+    sidx[e] = -1;
+    ij[e] = 0;
+    if (q < NP) {
+      int v, i, j;
+      decode(q, v, i, j);
+      vin[e] = __ldg(u + (tl.plane0 + v) * ps + (tl.i0 + i) * sa + (tl.j0 + j) * sb);
+      sidx[e] = v * plane + (i + 3) * G.PB + j + 3;
+      ij[e] = (i << 16) | j;
+    }
+  }
+  // halos along a window-split dimension: 3 rows above/below (a), 3 columns
+  // left/right (b) of every plane, from L2/HBM (periodic wrap or zero ghosts)
+  const int HA = wholeA ? 0 : 6 * TY, HB = wholeB ? 0 : 6 * TX;
+  const int HP = HA + HB;
+  const int NH = V * HP;
+  if (NH > 0) {
+    const float iHP = 1.0f / (float)HP;
+#pragma unroll 1
+    for (int h0 = tid; h0 < NH; h0 += 4 * kPlaneThreads) {
+      double hv[4];
+      int hs[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int h = h0 + e * kPlaneThreads;
+        hv[e] = 0.0;
+        hs[e] = -1;
+        if (h < NH) {
+          int v, hh;
+          if (vfast) {
+            hh = qdiv(h, iV);
+            v = h - hh * V;
+          } else {
+            v = qdiv(h, iHP);
+            hh = h - v * HP;
+          }
+          int ia, jb;  // padded tile coordinates
+          if (hh < HA) {
+            const int r6 = qdiv(hh, iTY);
+            ia = (r6 < 3) ? r6 : TX + r6;
+            jb = hh - r6 * TY + 3;
+          } else {
+            const int h2 = hh - HA, r6 = qdiv(h2, 1.0f / 6.0f), c6 = h2 - r6 * 6;
+            ia = r6 + 3;
+            jb = (c6 < 3) ? c6 : TY + c6;
+          }
+          hs[e] = v * plane + ia * G.PB + jb;
+          int gi = tl.i0 - 3 + ia, gj = tl.j0 - 3 + jb;
+          bool zero = false;
+          if (gi < 0 || gi >= na) {
+            if (bca != 0) zero = true;
+            gi = (gi < 0) ? gi + na : gi - na;  // |excursion| <= 3 < n
+          }
+          if (gj < 0 || gj >= nb) {
+            if (bcb != 0) zero = true;
+            gj = (gj < 0) ? gj + nb : gj - nb;
+          }
+          if (!zero) hv[e] = __ldg(u + (tl.plane0 + v) * ps + gi * sa + gj * sb);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (hs[e] >= 0) FP[hs[e]] = hv[e];
+    }
+  }
+  // interior stores; along a whole dimension a point near an edge also fills
+  // its halo copy: the periodic image (weno.hpp:131-136) or a zero ghost
+  const int upA = ((bca != 0) ? -3 : TX) * G.PB, dnA = ((bca != 0) ? 3 : -TX) * G.PB;
+  const int upB = (bcb != 0) ? -3 : TY, dnB = (bcb != 0) ? 3 : -TY;
+#pragma unroll
+  for (int e = 0; e < kPlaneMaxE; ++e) {
+    if (sidx[e] < 0) continue;
+    const double val = vin[e];
+    const int si = sidx[e], i = ij[e] >> 16, j = ij[e] & 0xffff;
+    FP[si] = val;
+    if (wholeA) {
+      const double g = (bca != 0) ? 0.0 : val;
+      if (i < 3) FP[si + upA] = g;
+      if (i >= TX - 3) FP[si + dnA] = g;
+    }
+    if (wholeB) {
+      const double g = (bcb != 0) ? 0.0 : val;
+      if (j < 3) FP[si + upB] = g;
+      if (j >= TY - 3) FP[si + dnB] = g;
+    }
+  }
+  __syncthreads();
+  const double eps4 = 4.0 * p.eps;
+  if (p.linear)
+    plane_sweeps<true>(G, FP, DX, DY, sca, scb, eps4, M->inv_h[a], M->inv_h[b]);
+  else
+    plane_sweeps<false>(G, FP, DX, DY, sca, scb, eps4, M->inv_h[a], M->inv_h[b]);
+  __syncthreads();
+  // epilogue: coalesced in the staging order; loads of a batch before use
+  double* kb = p.kbuf + M->offset;
+  const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
+  const bool moment = (p.pr == 1) && (p.rho_parts != nullptr) && (p.stage > 0);
+  const double ha = M->h[a], hb = M->h[b];
+#pragma unroll
+  for (int e0 = 0; e0 < kPlaneMaxE; e0 += 4) {
+    double kin[4], unv[4];
+    int gq[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int q = tid + (e0 + e) * kPlaneThreads;
+      kin[e] = 0.0;
+      unv[e] = 0.0;
+      gq[e] = -1;
+      if (q < NP) {
+        int v, i, j;
+        decode(q, v, i, j);
+        gq[e] = (tl.plane0 + v) * ps + (tl.i0 + i) * sa + (tl.j0 + j) * sb;
+        if (p.pr == 1) {
+          kin[e] = __ldg(kb + gq[e]);
+          if (p.stage > 1) unv[e] = __ldg(p.un + M->offset + gq[e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int q = tid + (e0 + e) * kPlaneThreads;
+      if (q >= NP) continue;
+      int v, i, j;
+      decode(q, v, i, j);
+      const int dq = (v * G.TXr + i) * G.DPB + j;
+      const double dx = DX[dq], dy = DY[dq];
+      if (p.pr == 0) {
+        kb[gq[e]] = (0.0 - dx) - dy;
+        continue;
+      }
+      const double kv = (kin[e] - dx) - dy;
+      double o;
+      if (p.stage == 0) {
+        o = kv;
+      } else {
+        if (!isfinite(kv)) {
+          const unsigned long long code =
+              (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
+          atomicMin(p.fail + tl.mi, code);
+        }
+        const double ui = FP[v * plane + (i + 3) * G.PB + j + 3];
+        if (p.stage == 1)
+          o = fma(dt, kv, ui);
+        else if (p.stage == 2)
+          o = fma(0.75, unv[e], 0.25 * fma(dt, kv, ui));
+        else
+          o = fma(1.0 / 3.0, unv[e], (2.0 / 3.0) * fma(dt, kv, ui));
+      }
+      p.out[M->offset + gq[e]] = o;
+      if (moment) {  // trapezoid weights of the velocity block (models.hpp:64-71,240-257)
+        const int ia = tl.i0 + i, jb = tl.j0 + j;
+        const double wa = (bca == 1 && (ia == 0 || ia == na - 1)) ? 0.5 * ha : ha;
+        const double wb = (bcb == 1 && (jb == 0 || jb == nb - 1)) ? 0.5 * hb : hb;
+        DX[dq] = (wa * wb) * o;
+      }
+    }
+  }
+  if (moment) {  // per-plane sums in a fixed order: one warp per plane
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5;
+    const int pp = TX * TY;
+    for (int v = warp; v < V; v += kPlaneThreads / 32) {
+      double acc = 0.0;
+      for (int q = lane; q < pp; q += 32) {
+        const int i = qdiv(q, iTY), j = q - i * TY;
+        acc += DX[(v * G.TXr + i) * G.DPB + j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) p.rho_parts[(M->xoff + tl.plane0 + v) * kRhoParts + tl.part] = acc;
+    }
+  }
+  if (p.pr == 1 && p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+
 // Persistent cooperative variant for small families (C1/C2/C4-sized): one
 // launch runs up to `nsteps` RK steps.  Stages are separated by grid-wide
 // barriers; every CTA computes the step's dt redundantly from the same
@@ -1146,6 +1466,14 @@ cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cud
   stage3d_fast_kernel<<<nblocks, kStage3DThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
+
+cudaError_t launch_plane(const PlaneParams& p, int nblocks, size_t smem, cudaStream_t s) {
+  if (nblocks <= 0) return cudaSuccess;
+  plane_fast_kernel<<<nblocks, kPlaneThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+int plane_smem_doubles(int nv, int tx, int ty) { return PlaneGeom(nv, tx, ty).smem_doubles(); }
 
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s) {
   void* args[] = {(void*)&p};
@@ -1302,6 +1630,9 @@ cudaError_t configure() {
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(stage3d_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            200 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(plane_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             200 * 1024);
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true>,

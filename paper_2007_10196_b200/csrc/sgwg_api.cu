@@ -216,6 +216,11 @@ struct sgwg_family {
   int4* dtiles3d_fast = nullptr;  // fast 3D stage tiles (advection)
   int ntiles3d_fast = 0;
   int smem3d_fast = 0;
+  PlaneTile* dptiles[2] = {nullptr, nullptr};  // fast 4D plane tiles (pairs (0,1), (2,3))
+  int nptiles[2] = {0, 0};
+  int psmem = 0;
+  double* rho_parts = nullptr;      // Vlasov-Poisson charge-density partial sums
+  const double* parts_of = nullptr; // the state rho_parts currently describes (or null)
   bool no_fused2d = false;  // SGWG_NO_FUSED2D=1: use the per-dimension pass kernels
   bool single = false;      // single-grid mode (runner.hpp:106-115): combine = the grid itself
 };
@@ -265,6 +270,14 @@ void account_timed(sgwg_family* f, int stage, int npass_dims, bool last, float m
   }
 }
 
+// fast 4D plane path (kernels.cuh plane_fast_kernel)
+bool plane_path(const sgwg_family* f) {
+  return f->d == 4 && f->nptiles[0] > 0 && f->nptiles[1] > 0 && arith_of(f) == SGWG_ARITH_FAST;
+}
+
+// Vlasov-Poisson field of `state`.  The charge density comes from the
+// partial sums the plane kernel left for its stage output when they describe
+// `state`; otherwise the moment kernel recomputes them.
 int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_energy = false) {
   const sgwg_model& m = f->model;
   FieldParams fp{};
@@ -281,8 +294,11 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
   fp.mtasks = f->dmtasks;
   fp.nmtasks = f->nmtasks;
   fp.nmembers = f->nm;
-  CK(launch_field(fp, f->nm, f->ctx->stream));
-  f->stats.kernel_launches += 2;
+  fp.rho_parts = f->rho_parts;
+  const bool with_moment = (f->parts_of != state);
+  CK(launch_field(fp, f->nm, with_moment, f->ctx->stream));
+  f->parts_of = state;
+  f->stats.kernel_launches += with_moment ? 2 : 1;
   if (with_energy && f->fe != nullptr) {  // ||E||_2 of u^n, recorded per step
     const int dx = m.space_dim;
     const int fine1 = (dx == 2) ? f->fine_ext[1] : 1;
@@ -308,6 +324,51 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
   unsigned long long* zero_slot =
       (burgers && stage > 0) ? f->amax + (size_t)((stage + 1) % 3) * f->nm : nullptr;
   const DtParams* dtp = (fuse_dt && stage == 3) ? f->d_dtp : nullptr;
+  // every path below but the plane path writes a state without its rho partials
+  if (stage > 0 && !plane_path(f)) f->parts_of = nullptr;
+  if (plane_path(f)) {  // fast 4D: dims (0,1) -> K, dims (2,3) + RK stage
+    const bool vp = (m.kind == SGWG_VLASOV_POISSON);
+    PlaneParams p{};
+    p.mem = f->dmem;
+    p.stage = stage;
+    p.linear = (m.weno_mode == SGWG_WENO_LINEAR);
+    p.eps = m.epsilon;
+    p.space_dim = m.space_dim;
+    p.uin = b.uin;
+    p.un = b.un;
+    p.out = b.out;
+    p.kbuf = f->K;
+    p.efield = f->E;
+    p.ctl = f->ctl;
+    p.fail = f->fail;
+    p.counter = f->counter;
+    for (int pr = 0; pr < 2; ++pr) {
+      p.pr = pr;
+      p.tiles = f->dptiles[pr];
+      if (vp) {
+        p.flux_a = p.flux_b = (pr == 0) ? kFluxKinX : kFluxKinVP;
+      } else {
+        p.flux_a = p.flux_b = kFluxAdvect;
+        p.c_a = m.speeds[2 * pr];
+        p.c_b = m.speeds[2 * pr + 1];
+      }
+      p.rho_parts = (pr == 1 && vp) ? f->rho_parts : nullptr;
+      p.dtp = (pr == 1) ? dtp : nullptr;
+      if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
+      CK(fast::launch_plane(p, f->nptiles[pr], (size_t)f->psmem * sizeof(double),
+                            f->ctx->stream));
+      if (timed) {
+        CK(cudaEventRecord(f->ev1, f->ctx->stream));
+        CK(cudaEventSynchronize(f->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+        account_timed(f, stage, 2, pr == 1, ms);
+      }
+      f->stats.kernel_launches++;
+    }
+    if (stage > 0) f->parts_of = vp ? b.out : nullptr;
+    return SGWG_OK;
+  }
   if (f->d == 3 && f->ntiles3d_fast > 0 && arith_of(f) == SGWG_ARITH_FAST &&
       m.kind == SGWG_ADVECTION) {  // fused 3D stage (all three sweeps + RK, one launch)
     Stage2DParams p{};
@@ -719,6 +780,7 @@ int setup_vp(sgwg_family* f) {
     M.xext[0] = M.ext[0];
     M.xext[1] = (dx == 2) ? M.ext[1] : 1;
     M.xoff = xoff;
+    M.rparts = 1;
     xoff += M.nx;
     if (f->model.kind == SGWG_VLASOV_POISSON) {
       for (int k = 0; k < dx; ++k)
@@ -756,7 +818,85 @@ int setup_vp(sgwg_family* f) {
     CK(cudaMalloc(&f->rho, sizeof(double) * std::max<long long>(1, xoff)));
     CK(cudaMalloc(&f->E, sizeof(double) * std::max<long long>(1, xoff * dx)));
     CK(cudaMalloc(&f->emax, sizeof(double) * std::max(1, f->nm * dx)));
+    CK(cudaMalloc(&f->rho_parts, sizeof(double) * std::max<long long>(1, xoff) * kRhoParts));
   }
+  f->parts_of = nullptr;
+  return SGWG_OK;
+}
+
+// Fast 4D plane tiles (kernels.cuh plane_fast_kernel).  Pair pr covers the
+// planes of dims (2pr, 2pr+1); a tile holds nv consecutive planes (>= 4 for
+// pr = 0, whose planes interleave in memory, so loads use whole sectors), split
+// into windows of multiples of 8 (+1) points when a plane exceeds the point
+// cap.  Caps: <= 2048 points (8 per thread) and <= 9000 doubles of shared
+// memory (3 CTAs per SM).  For Vlasov-Poisson the number of windows of a
+// velocity plane is the member's count of charge-density partials.
+int build_plane_tiles(sgwg_family* f) {
+  for (int pr = 0; pr < 2; ++pr) {
+    cudaFree(f->dptiles[pr]);
+    f->dptiles[pr] = nullptr;
+    f->nptiles[pr] = 0;
+  }
+  f->psmem = 0;
+  const sgwg_model& m = f->model;
+  if (f->d != 4 || f->no_fused2d || f->nm == 0) return SGWG_OK;
+  if (m.kind != SGWG_ADVECTION && m.kind != SGWG_VLASOV_POISSON) return SGWG_OK;
+  if (m.kind == SGWG_VLASOV_POISSON && m.space_dim != 2) return SGWG_OK;
+  int cap = 2048;
+  if (const char* e = std::getenv("SGWG_PLANE_CAP")) cap = std::max(256, std::min(2048, std::atoi(e)));
+  const int smem_cap = 9000;
+  auto piece = [](int n, int k) { return std::min(n, ((n + k - 1) / k + 7) / 8 * 8); };
+  std::vector<PlaneTile> t[2];
+  std::vector<int> rparts(f->nm, 1);
+  int smax = 0;
+  for (int mi = 0; mi < f->nm; ++mi) {
+    const MemberDesc& M = f->hmem[mi];
+    if (M.npts >= (1LL << 31)) return SGWG_OK;  // 32-bit member-local offsets
+    for (int pr = 0; pr < 2; ++pr) {
+      const int na = M.ext[2 * pr], nb = M.ext[2 * pr + 1];
+      const int nplanes = (pr == 0) ? M.ext[2] * M.ext[3] : M.ext[0] * M.ext[1];
+      const int vmin = (pr == 0) ? std::min(4, nplanes) : 1;
+      auto fits = [&](int V, int pa, int pb) {
+        return V * pa * pb <= cap && fast::plane_smem_doubles(V, pa, pb) <= smem_cap;
+      };
+      int ka = 1, kb = 1;
+      while (!fits(vmin, piece(na, ka), piece(nb, kb))) {
+        const int pa = piece(na, ka), pb = piece(nb, kb);
+        if (pa >= pb && pa > 8)
+          ++ka;
+        else if (pb > 8)
+          ++kb;
+        else
+          return fail_with(SGWG_EINVAL, "plane tiling: no window fits");
+      }
+      const int pa = piece(na, ka), pb = piece(nb, kb);
+      int V = vmin;
+      if (pa == na && pb == nb)
+        while (V < kPlaneMaxV && V < nplanes && fits(V + 1, na, nb)) ++V;
+      int part = 0;
+      for (int i0 = 0; i0 < na; i0 += pa)
+        for (int j0 = 0; j0 < nb; j0 += pb, ++part) {
+          const int tx = std::min(pa, na - i0), ty = std::min(pb, nb - j0);
+          for (int p0 = 0; p0 < nplanes; p0 += V) {
+            const int nv = std::min(V, nplanes - p0);
+            t[pr].push_back(PlaneTile{mi, p0, nv, part, i0, j0, tx, ty});
+            smax = std::max(smax, fast::plane_smem_doubles(nv, tx, ty));
+          }
+        }
+      if (pr == 1) {
+        if (part > kRhoParts) return SGWG_OK;  // (no such member in the BASELINE families)
+        rparts[mi] = part;
+      }
+    }
+  }
+  for (int mi = 0; mi < f->nm; ++mi) f->hmem[mi].rparts = rparts[mi];
+  CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
+  for (int pr = 0; pr < 2; ++pr) {
+    f->nptiles[pr] = (int)t[pr].size();
+    TRY(upload_vec(&f->dptiles[pr], t[pr]));
+  }
+  f->psmem = smax;
+  f->parts_of = nullptr;
   return SGWG_OK;
 }
 
@@ -794,10 +934,12 @@ int get_graph(sgwg_family* f, int nsteps, cudaGraphExec_t* exec) {
 int launches_per_step(const sgwg_family* f) {
   const bool fused3d = f->d == 3 && f->ntiles3d_fast > 0 && arith_of(f) == SGWG_ARITH_FAST &&
                        f->model.kind == SGWG_ADVECTION;
-  const int np = ((f->d == 2 && f->ntiles2d > 0) || fused3d) ? 1 : (int)pass_order(f).size();
+  const int np = ((f->d == 2 && f->ntiles2d > 0) || fused3d) ? 1
+                 : plane_path(f)                             ? 2
+                                                             : (int)pass_order(f).size();
   int n = 3 * np;
   if (!dt_fusable(f)) n += 1;
-  if (f->model.kind == SGWG_VLASOV_POISSON) n += 6;  // moment + FFT field per stage
+  if (f->model.kind == SGWG_VLASOV_POISSON) n += plane_path(f) ? 3 : 6;  // (moment +) field
   if (f->comm != nullptr) n += 1;
   return n;
 }
@@ -1188,6 +1330,9 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dtiles2d);
   cudaFree(f->dtiles2d_fast);
   cudaFree(f->dtiles3d_fast);
+  cudaFree(f->dptiles[0]);
+  cudaFree(f->dptiles[1]);
+  cudaFree(f->rho_parts);
   cudaFree(f->fe);
   cudaFree(f->dcoef);
   cudaFreeHost(f->hctl);
@@ -1232,6 +1377,7 @@ int sgwg_family_upload(sgwg_family* f, const double* host, size_t n) {
   if (f == nullptr || host == nullptr || n != (size_t)f->total)
     return fail_with(SGWG_EINVAL, "upload: size must equal the packed member points");
   CK(cudaSetDevice(f->ctx->device));
+  f->parts_of = nullptr;
   CK(cudaMemcpyAsync(f->u, host, sizeof(double) * n, cudaMemcpyHostToDevice, f->ctx->stream));
   CK(cudaStreamSynchronize(f->ctx->stream));
   return SGWG_OK;
@@ -1249,6 +1395,7 @@ int sgwg_family_download(sgwg_family* f, double* host, size_t n) {
 int sgwg_family_upload_device(sgwg_family* f, const double* dev, size_t n) {
   if (f == nullptr || dev == nullptr || n != (size_t)f->total)
     return fail_with(SGWG_EINVAL, "upload: size must equal the packed member points");
+  f->parts_of = nullptr;
   CK(cudaMemcpyAsync(f->u, dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, f->ctx->stream));
   CK(cudaStreamSynchronize(f->ctx->stream));
   return SGWG_OK;
@@ -1278,6 +1425,7 @@ int sgwg_set_model(sgwg_family* f, const sgwg_model* m) {
   f->model = *m;
   f->has_model = true;
   if (m->kind == SGWG_VLASOV_POISSON) TRY(setup_vp(f));
+  TRY(build_plane_tiles(f));
   clear_graphs(f);
   return SGWG_OK;
 }
@@ -1467,6 +1615,9 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
         while (left > 0) {
           int chunk = 1;
           while (chunk * 2 <= left && chunk < 64) chunk *= 2;
+          // captured steps take the rho partials of u^n as given
+          if (f->model.kind == SGWG_VLASOV_POISSON && plane_path(f) && f->parts_of != f->u)
+            TRY(launch_field_for(f, f->u, 0));
           cudaGraphExec_t ge;
           TRY(get_graph(f, chunk, &ge));
           CK(cudaGraphLaunch(ge, s));

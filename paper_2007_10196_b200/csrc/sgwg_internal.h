@@ -42,7 +42,13 @@ struct MemberDesc {
   int vn;                  // points of the velocity block (contiguous)
   int xext[2];             // x extents (dx=1: {n0, 1})
   int tx, ty;              // 2D fused-stage tile (d == 2)
+  int rparts;              // Vlasov-Poisson: charge-density partial sums per x point
 };
+
+// Vlasov-Poisson charge density in partial-sum form: rho(x) = 1 - sum_t parts[x][t],
+// t < MemberDesc::rparts (one partial per velocity-plane tile, fixed order)
+constexpr int kRhoParts = 8;
+constexpr int kPlaneMaxV = 32;  // planes per fast 4D plane tile
 
 // Step control block (timestep.hpp:126-174 loop state), device resident.
 struct StepCtl {
@@ -127,6 +133,36 @@ struct PersistParams {
   int nsteps;              // steps of this launch (early exit when the stop is reached)
 };
 
+// fast 4D stage as two plane launches (kernels.cuh plane_fast_kernel): a tile
+// is nv consecutive planes of the pair of dimensions (a, a+1), a = 2*pr, each
+// restricted to the window [i0, i0+tx) x [j0, j0+ty).
+struct PlaneTile {
+  int mi, plane0, nv, part;
+  int i0, j0, tx, ty;
+};
+
+struct PlaneParams {
+  const MemberDesc* mem;
+  const PlaneTile* tiles;
+  int pr;                  // 0: dims (0,1) -> tendency K; 1: dims (2,3) + RK stage
+  int flux_a, flux_b;      // FluxKind of the two sweeps
+  double c_a, c_b;         // advection speeds
+  int stage;               // 1..3, 0 = tendency only
+  int linear;
+  double eps;
+  int space_dim;
+  const double* uin;
+  const double* un;
+  double* out;
+  double* kbuf;
+  const double* efield;
+  const StepCtl* ctl;
+  unsigned long long* fail;
+  double* rho_parts;       // pr = 1, Vlasov-Poisson: sum_v w_v out per (x point, part)
+  const struct DtParams* dtp;
+  unsigned int* counter;
+};
+
 struct UpsampleParams {
   const MemberDesc* mem;
   const int2* tasks;       // (member-slot, first output index of the chunk)
@@ -177,6 +213,7 @@ struct FieldParams {
   const int2* mtasks;      // moment kernel work: (member, first x point), 8 x points each
   int nmtasks;
   int nmembers;
+  double* rho_parts;       // kRhoParts partial sums per x point (see MemberDesc::rparts)
 };
 
 // launchers: one set per arithmetic TU (k_exact.cu, k_fast.cu)
@@ -192,6 +229,8 @@ SGWG_DECLARE_LAUNCHERS(exact)
 SGWG_DECLARE_LAUNCHERS(fast)
 namespace fast {
 cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s);
+cudaError_t launch_plane(const PlaneParams& p, int nblocks, size_t smem, cudaStream_t s);
+int plane_smem_doubles(int nv, int tx, int ty);
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s);
 int persist2d_max_blocks(int burgers, size_t smem);
 }  // namespace fast
@@ -220,7 +259,7 @@ cudaError_t launch_dt(const DtParams& p, cudaStream_t s);
 cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* tasks, int ntasks,
                               const double* u, unsigned long long* amax, cudaStream_t s);
 cudaError_t configure_field();
-cudaError_t launch_field(const FieldParams& p, int nmembers, cudaStream_t s);
+cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, cudaStream_t s);
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
                                 double hvol, double* out_base, long long cap, cudaStream_t s);
 cudaError_t launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t s);

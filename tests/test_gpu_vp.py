@@ -40,3 +40,65 @@ def test_vp_c5_small_evolve(ctx, oracle):
     assert maxabs(gd, wd) < 1e-14
     assert maxabs(got, want) < 1e-10
     assert maxabs(gc[-1], wc[-1]) < 1e-10
+
+
+@pytest.mark.parametrize("cap", [None, "256"])
+def test_vp_c5_small_evolve_fast(ctx_fast, oracle, monkeypatch, cap):
+    """Fast build, 2D2V: the two plane launches per stage (dims (x1,x2) ->
+    tendency, dims (v1,v2) + RK stage + charge-density partials); cap 256
+    splits velocity planes into several windows (several partials per x)."""
+    if cap is not None:
+        monkeypatch.setenv("SGWG_PLANE_CAP", cap)
+    cfg = configs.config("C5", **C5_SMALL)
+    got, want, gd, wd, gc, wc = _evolve_both(ctx_fast, oracle, cfg, 0.02)
+    assert len(gd) == len(wd) > 0
+    assert maxabs(gd, wd) < 1e-14
+    assert maxabs(got, want) < 1e-10
+    assert maxabs(gc[-1], wc[-1]) < 1e-10
+
+
+def test_vp_c5_partials_track_state(ctx_fast, oracle, monkeypatch):
+    """The charge density the field solve uses after an evolve comes from the
+    plane kernel's partial sums; after an upload it must be recomputed."""
+    monkeypatch.setenv("SGWG_PLANE_CAP", "512")
+    cfg = configs.config("C5", **C5_SMALL)
+    dom, model, pol = oracle_objs(cfg)
+    fam = gpu_family(ctx_fast, cfg)
+    fam.initialize(cfg["ic"])
+    fam.evolve_config(cfg, tfinal=0.01)
+    s = fam.download()
+    dxs = cfg["space_dim"]
+
+    def check(fam, s):
+        rho_g, E_g = fam.vp_field()
+        off = 0
+        for mi, lv in enumerate(oracle.levels(cfg["d"], cfg["nl"])):
+            n = int(np.prod(fam.points[mi]))
+            nx = int(np.prod(fam.points[mi][:dxs]))
+            rho_o, E_o = oracle.vp_field(dom, lv, dxs, s[off:off + n], nx)
+            assert maxabs(rho_g[mi], rho_o) < 1e-13, mi
+            assert maxabs(E_g[mi], E_o) < 1e-12 * (1 + np.max(np.abs(E_o))), mi
+            off += n
+
+    check(fam, s)                      # partials left by the last stage-3 launch
+    s2 = s * (1.0 + 0.01 * np.random.default_rng(5).standard_normal(s.size))
+    fam.upload(s2)                     # invalidates them
+    check(fam, s2)
+    # evolve again from the uploaded state: graphs captured earlier assume fresh
+    # partials at entry, which the runtime must re-establish
+    fam.evolve_config(cfg, tfinal=0.01)
+    fam2 = gpu_family(ctx_fast, cfg)
+    fam2.upload(s2)
+    fam2.evolve_config(cfg, tfinal=0.01)
+    assert maxabs(fam.download(), fam2.download()) == 0.0
+
+
+def test_advection_4d_evolve_fast(ctx_fast, oracle):
+    """4D constant-speed advection through the plane launches (fused dt)."""
+    cfg = configs.config("C3", d=4, nl=3, lower=[0.0] * 4, upper=[2.0] * 4, root=[8] * 4,
+                         bc=[0, 0, 1, 1], speeds=[1.0, -1.0, 0.5, -0.25])
+    T = 4 * cfg["reference_spacing"] ** (5.0 / 3.0)
+    got, want, gd, wd, gc, wc = _evolve_both(ctx_fast, oracle, cfg, T)
+    assert len(gd) == len(wd) == 4
+    assert maxabs(got, want) < 1e-10
+    assert maxabs(gc[-1], wc[-1]) < 1e-10
