@@ -21,7 +21,7 @@ namespace sgwg {
 
 constexpr int kFieldThreads = 512;
 constexpr int kFieldMaxX = 2048;
-constexpr int kFieldSmemDoubles = 5 * kFieldMaxX;
+constexpr int kFieldSmemDoubles = 6 * kFieldMaxX + kFieldMaxX / 2 * 2;
 
 template <bool COH>
 __device__ __forceinline__ double fld_ld(const double* p) {
@@ -32,47 +32,59 @@ __device__ __forceinline__ int bitrev(int x, int bits) {
   return (int)(__brev((unsigned)x) >> (32 - bits));
 }
 
-// radix-2 FFTs of all lines of an n1 x n2 complex array along `axis` (1 = x2,
-// contiguous).  sign -1: forward e^{-i...}; +1: inverse (unnormalised).
-// Twiddles from the table e^{i pi k/H}, k < H.
-__device__ inline void fft_lines(double* re, double* im, int n1, int n2, int axis, int sign,
-                                 const double* twc, const double* tws, int H) {
-  const int len = axis ? n2 : n1;
-  if (len <= 1) return;
-  const int nx = n1 * n2;
-  const int stride = axis ? 1 : n2;
-  const int bits = __ffs(len) - 1;
+// radix-2 FFTs of all lines along `axis` (1 = x2, contiguous) of na complex
+// n1 x n2 arrays (re[k], im[k]) at once (one barrier per butterfly stage for
+// all of them); n1 = 2^b1, n2 = 2^b2.  sign -1: forward e^{-i...}; +1: inverse
+// (unnormalised).  Twiddles from the table e^{i pi k/H}, k < H.
+template <int NA>
+__device__ inline void fft_lines(double* const* re, double* const* im, int b1, int b2, int axis,
+                                 int sign, const double* twc, const double* tws, int H) {
+  const int bits = axis ? b2 : b1;
+  if (bits == 0) return;
+  const int len = 1 << bits;
+  const int nx = 1 << (b1 + b2);
+  const int stride = axis ? 1 : (1 << b2);
+  auto base_of = [&](int line) { return axis ? (line << b2) : line; };
+  // lanes walk positions along contiguous lines (axis 1) and walk lines when
+  // the lines are strided (axis 0), so shared-memory accesses stay conflict-free
+  const int lbits = b1 + b2 - bits;  // log2(number of lines)
   for (int idx = threadIdx.x; idx < nx; idx += blockDim.x) {
-    const int line = idx / len, pos = idx - line * len;
+    const int line = axis ? idx >> bits : idx & ((1 << lbits) - 1);
+    const int pos = axis ? idx & (len - 1) : idx >> lbits;
     const int rev = bitrev(pos, bits);
     if (pos < rev) {
-      const int base = axis ? line * n2 : line;
-      const int a = base + pos * stride, b = base + rev * stride;
-      const double tr = re[a], ti = im[a];
-      re[a] = re[b];
-      im[a] = im[b];
-      re[b] = tr;
-      im[b] = ti;
+      const int a = base_of(line) + pos * stride, b = base_of(line) + rev * stride;
+#pragma unroll
+      for (int k = 0; k < NA; ++k) {
+        const double tr = re[k][a], ti = im[k][a];
+        re[k][a] = re[k][b];
+        im[k][a] = im[k][b];
+        re[k][b] = tr;
+        im[k][b] = ti;
+      }
     }
   }
   __syncthreads();
-  for (int half = 1; half < len; half <<= 1) {
-    for (int bfly = threadIdx.x; bfly < nx / 2; bfly += blockDim.x) {
-      const int per = len / 2;
-      const int line = bfly / per, q = bfly - line * per;
-      const int grp = q / half, pos = q - grp * half;
-      const int base = axis ? line * n2 : line;
-      const int i0 = base + (grp * 2 * half + pos) * stride;
+  for (int lh = 0; lh < bits; ++lh) {
+    const int half = 1 << lh;
+    for (int bf = threadIdx.x; bf < nx / 2; bf += blockDim.x) {
+      const int line = axis ? bf >> (bits - 1) : bf & ((1 << lbits) - 1);
+      const int q = axis ? bf & ((len >> 1) - 1) : bf >> lbits;
+      const int grp = q >> lh, pos = q & (half - 1);
+      const int i0 = base_of(line) + ((grp << (lh + 1)) + pos) * stride;
       const int i1 = i0 + half * stride;
-      const int ti = pos * (H / half);  // e^{sign i pi pos/half}
+      const int ti = pos * (H >> lh);  // e^{sign i pi pos/half}
       const double c = twc[ti], s = sign * tws[ti];
-      const double br = re[i1] * c - im[i1] * s;
-      const double bi = re[i1] * s + im[i1] * c;
-      const double ar = re[i0], ai = im[i0];
-      re[i0] = ar + br;
-      im[i0] = ai + bi;
-      re[i1] = ar - br;
-      im[i1] = ai - bi;
+#pragma unroll
+      for (int k = 0; k < NA; ++k) {
+        const double br = re[k][i1] * c - im[k][i1] * s;
+        const double bi = re[k][i1] * s + im[k][i1] * c;
+        const double ar = re[k][i0], ai = im[k][i0];
+        re[k][i0] = ar + br;
+        im[k][i0] = ai + bi;
+        re[k][i1] = ar - br;
+        im[k][i1] = ai - bi;
+      }
     }
     __syncthreads();
   }
@@ -113,20 +125,23 @@ __device__ inline void moment_point(const FieldParams& p, const MemberDesc* M, i
     p.rho_parts[(M->xoff + xi) * kRhoParts + lane] = (lane == 0) ? acc : 0.0;
 }
 
-// E of member mi from its rho (whole block; sh >= kFieldSmemDoubles doubles;
-// red >= blockDim/32 doubles); also p.emax[mi*dx + comp] = max|E_comp|.
+// E of member mi from its rho partials (whole block; sh >= kFieldSmemDoubles
+// doubles; red >= 2 * blockDim/32 doubles); also p.rho and
+// p.emax[mi*dx + comp] = max|E_comp|.  Both field components are transformed
+// back together.
 template <bool COH>
 __device__ inline void field_member(const FieldParams& p, int mi, double* sh, double* red) {
   const MemberDesc* M = p.mem + mi;
   const int dx = p.space_dim;
   const int n1 = M->xext[0], n2 = M->xext[1];
+  const int b1 = __ffs(n1) - 1, b2 = __ffs(n2) - 1;
   const int nx = M->nx;
   double* rr = sh;
   double* ri = sh + nx;
-  double* er = sh + 2 * nx;
-  double* ei = sh + 3 * nx;
+  double* er[2] = {sh + 2 * nx, sh + 4 * nx};
+  double* ei[2] = {sh + 3 * nx, sh + 5 * nx};
   const int H = max(1, max(n1, n2) / 2);
-  double* twc = sh + 4 * nx;
+  double* twc = sh + 6 * nx;
   double* tws = twc + H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int xi = threadIdx.x; xi < nx; xi += blockDim.x) {
@@ -141,49 +156,59 @@ __device__ inline void field_member(const FieldParams& p, int mi, double* sh, do
   for (int k = threadIdx.x; k < H; k += blockDim.x)
     sincospi((double)k / (double)H, &tws[k], &twc[k]);
   __syncthreads();
-  fft_lines(rr, ri, n1, n2, 1, -1, twc, tws, H);
-  fft_lines(rr, ri, n1, n2, 0, -1, twc, tws, H);
+  {
+    double* R[1] = {rr};
+    double* I[1] = {ri};
+    fft_lines<1>(R, I, b1, b2, 1, -1, twc, tws, H);
+    fft_lines<1>(R, I, b1, b2, 0, -1, twc, tws, H);
+  }
   const double two_pi = 6.283185307179586476925286766559;
-  for (int comp = 0; comp < dx; ++comp) {
-    for (int id = threadIdx.x; id < nx; id += blockDim.x) {
-      const int k1 = id / n2, k2 = id - k1 * n2;
-      const int s1 = (k1 <= n1 / 2) ? k1 : k1 - n1;
-      const int s2 = (k2 <= n2 / 2) ? k2 : k2 - n2;
-      const bool nyq = ((n1 % 2 == 0) && k1 == n1 / 2 && n1 > 1) ||
-                       ((n2 % 2 == 0) && k2 == n2 / 2 && n2 > 1);
-      const double kap1 = two_pi * (double)s1 / p.L[0];
-      const double kap2 = (dx == 2) ? two_pi * (double)s2 / p.L[1] : 0.0;
-      const double k2s = kap1 * kap1 + kap2 * kap2;
-      if ((s1 == 0 && s2 == 0) || nyq) {
-        er[id] = 0.0;
-        ei[id] = 0.0;
-      } else {
-        const double kc = (comp == 0) ? kap1 : kap2;
-        er[id] = kc * ri[id] / k2s;  // -i kc rhat / |k|^2
-        ei[id] = -kc * rr[id] / k2s;
-      }
+  for (int id = threadIdx.x; id < nx; id += blockDim.x) {
+    const int k1 = id >> b2, k2 = id & (n2 - 1);
+    const int s1 = (k1 <= n1 / 2) ? k1 : k1 - n1;
+    const int s2 = (k2 <= n2 / 2) ? k2 : k2 - n2;
+    const bool nyq = ((n1 % 2 == 0) && k1 == n1 / 2 && n1 > 1) ||
+                     ((n2 % 2 == 0) && k2 == n2 / 2 && n2 > 1);
+    const double kap1 = two_pi * (double)s1 / p.L[0];
+    const double kap2 = (dx == 2) ? two_pi * (double)s2 / p.L[1] : 0.0;
+    const bool drop = (s1 == 0 && s2 == 0) || nyq;
+    const double inv = drop ? 0.0 : 1.0 / (kap1 * kap1 + kap2 * kap2);
+    for (int comp = 0; comp < dx; ++comp) {
+      const double kc = (comp == 0) ? kap1 : kap2;
+      er[comp][id] = drop ? 0.0 : kc * ri[id] * inv;  // -i kc rhat / |k|^2
+      ei[comp][id] = drop ? 0.0 : -kc * rr[id] * inv;
     }
-    __syncthreads();
-    fft_lines(er, ei, n1, n2, 1, +1, twc, tws, H);
-    fft_lines(er, ei, n1, n2, 0, +1, twc, tws, H);
-    double lmax = 0.0;
-    const double inv_n = 1.0 / (double)nx;
+  }
+  __syncthreads();
+  if (dx == 2) {
+    fft_lines<2>(er, ei, b1, b2, 1, +1, twc, tws, H);
+    fft_lines<2>(er, ei, b1, b2, 0, +1, twc, tws, H);
+  } else {
+    fft_lines<1>(er, ei, b1, b2, 1, +1, twc, tws, H);
+    fft_lines<1>(er, ei, b1, b2, 0, +1, twc, tws, H);
+  }
+  double lmax[2] = {0.0, 0.0};
+  const double inv_n = 1.0 / (double)nx;
+  for (int comp = 0; comp < dx; ++comp) {
     double* E = p.efield + M->xoff * dx + (long long)comp * nx;
     for (int id = threadIdx.x; id < nx; id += blockDim.x) {
-      const double e = er[id] * inv_n;
+      const double e = er[comp][id] * inv_n;
       E[id] = e;
-      lmax = fmax(lmax, fabs(e));
+      lmax[comp] = fmax(lmax[comp], fabs(e));
     }
+  }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    if (lane == 0) red[warp] = lmax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double m = 0.0;
-      for (int q = 0; q < nwarps; ++q) m = fmax(m, red[q]);
-      p.emax[mi * dx + comp] = m;
-    }
-    __syncthreads();
+  for (int comp = 0; comp < 2; ++comp) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      lmax[comp] = fmax(lmax[comp], __shfl_xor_sync(0xffffffffu, lmax[comp], o));
+    if (lane == 0) red[comp * nwarps + warp] = lmax[comp];
+  }
+  __syncthreads();
+  if (threadIdx.x < dx) {
+    double m = 0.0;
+    for (int q = 0; q < nwarps; ++q) m = fmax(m, red[threadIdx.x * nwarps + q]);
+    p.emax[mi * dx + threadIdx.x] = m;
   }
 }
 
@@ -211,17 +236,42 @@ __device__ __forceinline__ void lagrange5(int j, int m, int n_src, int* idx, dou
   w[4] = c2 * e4;
 }
 
-// h-weighted |E_c|^2 contribution of finest x point q: E_c = sum_m c_m I_m(E_m),
-// I_m separable degree-4 Lagrange interpolation from member m's x-grid.
+// Members that share an x-grid are combined on that grid before interpolating
+// (interpolation is linear): per group g, Eg_c = sum_{m in g} c_m E_m,c in
+// member order (one thread per group x point).
 template <bool COH>
-__device__ inline double energy_point(const FieldParams& p, const double* coef, int q, int fine0,
-                                      int fine1) {
+__device__ inline void group_point(const FieldParams& p, const double* coef, int X) {
+  int g = 0;
+  while (g + 1 < p.negrp && p.egrp[g + 1].w <= X) ++g;
+  const int4 G = p.egrp[g];
+  const int nxg = G.x * G.y, xi = X - G.w;
+  const int dx = p.space_dim;
+  const int2 mr = p.egrp_m[g];
+  for (int c = 0; c < dx; ++c) {
+    double acc = 0.0;
+    for (int k = 0; k < mr.y; ++k) {
+      const int mi = p.egrp_mem[mr.x + k];
+      const MemberDesc* M = p.mem + mi;
+      acc = fma(coef[mi], fld_ld<COH>(p.efield + M->xoff * dx + (long long)c * M->nx + xi), acc);
+    }
+    p.egrid[G.z + c * nxg + xi] = acc;
+  }
+}
+
+// h-weighted |E_c|^2 contribution of finest x point q: E_c = sum_g I_g(Eg),
+// I_g separable degree-4 Lagrange interpolation from group g's x-grid (or,
+// without groups, E_c = sum_m c_m I_m(E_m) member by member).
+template <bool COH>
+__device__ inline double energy_point(const FieldParams& p, int q, int fine0, int fine1) {
   const int dx = p.space_dim;
   const int i = q / fine1, j = q - (q / fine1) * fine1;
   double ec[2] = {0.0, 0.0};
-  for (int mi = 0; mi < p.nmembers; ++mi) {
-    const MemberDesc* M = p.mem + mi;
-    const int n0 = M->xext[0], n1 = M->xext[1];
+  const bool direct = (p.negrp == 0);  // small families: every member, no group pass
+  const int ng = direct ? p.nmembers : p.negrp;
+  for (int g = 0; g < ng; ++g) {
+    const MemberDesc* M = p.mem + g;
+    const int4 G = direct ? make_int4(M->xext[0], M->xext[1], 0, 0) : p.egrp[g];
+    const int n0 = G.x, n1 = G.y;
     int ia[5], ja[5];
     double wa[5], wb[5];
     lagrange5(i, __ffs(fine0 / n0) - 1, n0, ia, wa);
@@ -231,14 +281,18 @@ __device__ inline double energy_point(const FieldParams& p, const double* coef, 
       for (int b = 0; b < 5; ++b) ja[b] = 0, wb[b] = (b == 2) ? 1.0 : 0.0;
     }
     for (int c = 0; c < dx; ++c) {
-      const double* E = p.efield + M->xoff * dx + (long long)c * M->nx;
+      const double* E = direct ? p.efield + M->xoff * dx + (long long)c * M->nx
+                               : p.egrid + G.z + c * n0 * n1;
       double v = 0.0;
       for (int a = 0; a < 5; ++a) {
         double s = 0.0;
         for (int b = 0; b < 5; ++b) s = fma(wb[b], fld_ld<COH>(E + ia[a] * n1 + ja[b]), s);
         v = fma(wa[a], s, v);
       }
-      ec[c] = fma(coef[mi], v, ec[c]);
+      if (direct)
+        ec[c] = fma(p.ecoef[g], v, ec[c]);
+      else
+        ec[c] += v;
     }
   }
   double acc = 0.0;

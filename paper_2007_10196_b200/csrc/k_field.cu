@@ -22,12 +22,17 @@ __global__ void __launch_bounds__(256) moment_kernel(const FieldParams p) {
 __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams p) {
   if (p.ctl != nullptr && !p.ctl->active) return;
   extern __shared__ double sh[];
-  __shared__ double red[kFieldThreads / 32];
+  __shared__ double red[2 * kFieldThreads / 32];
   field_member<false>(p, blockIdx.x, sh, red);
 }
 
-__global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p,
-                                                           const double* coef, int fine0,
+__global__ void __launch_bounds__(256) group_field_kernel(const FieldParams p, const double* coef) {
+  if (p.ctl != nullptr && !p.ctl->active) return;
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  if (X < p.ngx) group_point<false>(p, coef, X);
+}
+
+__global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p, int fine0,
                                                            int fine1, double hvol,
                                                            double* out_base, long long cap) {
   if (p.ctl != nullptr && !p.ctl->active) return;
@@ -36,7 +41,7 @@ __global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p,
   double acc = 0.0;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < fine0 * fine1;
        q += gridDim.x * blockDim.x)
-    acc += energy_point<false>(p, coef, q, fine0, fine1);
+    acc += energy_point<false>(p, q, fine0, fine1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(out_base + slot, acc * hvol);
@@ -44,9 +49,12 @@ __global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p,
 
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
                                 double hvol, double* out_base, long long cap, cudaStream_t s) {
+  FieldParams q = p;
+  q.ecoef = coef;
+  if (q.negrp > 0) group_field_kernel<<<(q.ngx + 255) / 256, 256, 0, s>>>(q, coef);
   int blocks = (fine0 * fine1 + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  field_energy_kernel<<<blocks, 256, 0, s>>>(p, coef, fine0, fine1, hvol, out_base, cap);
+  field_energy_kernel<<<blocks, 256, 0, s>>>(q, fine0, fine1, hvol, out_base, cap);
   return cudaGetLastError();
 }
 

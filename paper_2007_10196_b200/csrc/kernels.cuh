@@ -1096,6 +1096,9 @@ __global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_fast_kernel(const 
 // zero ghosts, weno.hpp:131-141); the two sweeps run concurrently in two
 // 128-thread halves over runs of 8 points (a line of 8m+1 points: m runs and a
 // 1-point tail).  Compulsory traffic 16 B (pr 0) + 24..32 B (pr 1) per point.
+#ifndef SGWG_PLANE_MINB
+#define SGWG_PLANE_MINB 3
+#endif
 constexpr int kPlaneThreads = 256;
 constexpr int kPlaneMaxE = 8;  // tile points <= kPlaneThreads * kPlaneMaxE
 
@@ -1170,7 +1173,7 @@ __device__ __forceinline__ void plane_sweeps(const PlaneGeom& G, const double* F
   }
 }
 
-__global__ void __launch_bounds__(kPlaneThreads, 3) plane_fast_kernel(const PlaneParams p) {
+__global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_kernel(const PlaneParams p) {
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const PlaneTile tl = p.tiles[blockIdx.x];

@@ -187,6 +187,11 @@ struct sgwg_family {
   double* fe = nullptr;     // per-step sum of |E_combined|^2 h (Vlasov-Poisson diagnostic)
   long long fe_cap = 0;
   double* dcoef = nullptr;  // combination coefficient of each local member
+  int4* degrp = nullptr;     // field-energy groups (members sharing an x-grid)
+  int2* degrp_m = nullptr;
+  int* degrp_mem = nullptr;
+  int negrp = 0, ngx = 0;
+  double* egrid = nullptr;
   // graphs: steps per chunk -> exec
   std::map<int, cudaGraphExec_t> graphs;
   long long graph_key_policy = -1;
@@ -295,6 +300,16 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
   fp.nmtasks = f->nmtasks;
   fp.nmembers = f->nm;
   fp.rho_parts = f->rho_parts;
+  fp.egrp = f->degrp;
+  fp.egrp_m = f->degrp_m;
+  fp.egrp_mem = f->degrp_mem;
+  // members grouped by x-grid when the per-point member loop would be large
+  const long long fine_x = (long long)f->fine_ext[0] * ((m.space_dim == 2) ? f->fine_ext[1] : 1);
+  bool groups = fine_x * f->nm > (1LL << 20);
+  if (const char* e = std::getenv("SGWG_ENERGY_GROUPS")) groups = (e[0] == '1');
+  fp.negrp = groups ? f->negrp : 0;
+  fp.ngx = f->ngx;
+  fp.egrid = f->egrid;
   const bool with_moment = (f->parts_of != state);
   CK(launch_field(fp, f->nm, with_moment, f->ctx->stream));
   f->parts_of = state;
@@ -305,7 +320,7 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
     const double hvol = f->fine_h[0] * ((dx == 2) ? f->fine_h[1] : 1.0);
     CK(launch_field_energy(fp, f->dcoef, f->fine_ext[0], fine1, hvol, f->fe, f->fe_cap,
                            f->ctx->stream));
-    f->stats.kernel_launches++;
+    f->stats.kernel_launches += (fp.negrp > 0) ? 2 : 1;
   }
   return SGWG_OK;
 }
@@ -814,6 +829,46 @@ int setup_vp(sgwg_family* f) {
     TRY(upload_vec(&f->dcoef, cf));
   }
   TRY(upload_vec(&f->dmtasks, mt));
+  {  // field-energy groups: members sharing an x-grid, in member order
+    std::vector<std::pair<int, int>> keys;
+    std::vector<std::vector<int>> mem;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      const std::pair<int, int> k(f->hmem[mi].xext[0], f->hmem[mi].xext[1]);
+      size_t g = 0;
+      while (g < keys.size() && keys[g] != k) ++g;
+      if (g == keys.size()) {
+        keys.push_back(k);
+        mem.emplace_back();
+      }
+      mem[g].push_back(mi);
+    }
+    std::vector<int4> gd;
+    std::vector<int2> gm;
+    std::vector<int> gmem;
+    int off = 0, gx = 0;
+    for (size_t g = 0; g < keys.size(); ++g) {
+      const int nxg = keys[g].first * keys[g].second;
+      gd.push_back(make_int4(keys[g].first, keys[g].second, off, gx));
+      gm.push_back(make_int2((int)gmem.size(), (int)mem[g].size()));
+      gmem.insert(gmem.end(), mem[g].begin(), mem[g].end());
+      off += nxg * dx;
+      gx += nxg;
+    }
+    cudaFree(f->degrp);
+    cudaFree(f->degrp_m);
+    cudaFree(f->degrp_mem);
+    cudaFree(f->egrid);
+    f->degrp = nullptr;
+    f->degrp_m = nullptr;
+    f->degrp_mem = nullptr;
+    f->egrid = nullptr;
+    TRY(upload_vec(&f->degrp, gd));
+    TRY(upload_vec(&f->degrp_m, gm));
+    TRY(upload_vec(&f->degrp_mem, gmem));
+    CK(cudaMalloc(&f->egrid, sizeof(double) * std::max(1, off)));
+    f->negrp = (int)keys.size();
+    f->ngx = gx;
+  }
   if (f->model.kind == SGWG_VLASOV_POISSON && f->rho == nullptr) {
     CK(cudaMalloc(&f->rho, sizeof(double) * std::max<long long>(1, xoff)));
     CK(cudaMalloc(&f->E, sizeof(double) * std::max<long long>(1, xoff * dx)));
@@ -844,7 +899,8 @@ int build_plane_tiles(sgwg_family* f) {
   if (m.kind == SGWG_VLASOV_POISSON && m.space_dim != 2) return SGWG_OK;
   int cap = 2048;
   if (const char* e = std::getenv("SGWG_PLANE_CAP")) cap = std::max(256, std::min(2048, std::atoi(e)));
-  const int smem_cap = 9000;
+  int smem_cap = 9000;
+  if (const char* e = std::getenv("SGWG_PLANE_SMEM")) smem_cap = std::max(2000, std::atoi(e));
   auto piece = [](int n, int k) { return std::min(n, ((n + k - 1) / k + 7) / 8 * 8); };
   std::vector<PlaneTile> t[2];
   std::vector<int> rparts(f->nm, 1);
@@ -939,7 +995,11 @@ int launches_per_step(const sgwg_family* f) {
                                                              : (int)pass_order(f).size();
   int n = 3 * np;
   if (!dt_fusable(f)) n += 1;
-  if (f->model.kind == SGWG_VLASOV_POISSON) n += plane_path(f) ? 3 : 6;  // (moment +) field
+  if (f->model.kind == SGWG_VLASOV_POISSON) {  // (moment +) field per stage, energy per step
+    const long long fine_x = (long long)f->fine_ext[0] *
+                             ((f->model.space_dim == 2) ? f->fine_ext[1] : 1);
+    n += (plane_path(f) ? 3 : 6) + ((fine_x * f->nm > (1LL << 20)) ? 2 : 1);
+  }
   if (f->comm != nullptr) n += 1;
   return n;
 }
@@ -1333,6 +1393,10 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dptiles[0]);
   cudaFree(f->dptiles[1]);
   cudaFree(f->rho_parts);
+  cudaFree(f->degrp);
+  cudaFree(f->degrp_m);
+  cudaFree(f->degrp_mem);
+  cudaFree(f->egrid);
   cudaFree(f->fe);
   cudaFree(f->dcoef);
   cudaFreeHost(f->hctl);

@@ -214,6 +214,14 @@ struct FieldParams {
   int nmtasks;
   int nmembers;
   double* rho_parts;       // kRhoParts partial sums per x point (see MemberDesc::rparts)
+  // field-energy diagnostic: members grouped by x-grid
+  const int4* egrp;        // (n0, n1, offset in egrid, first group x point)
+  const int2* egrp_m;      // (first, count) into egrp_mem
+  const int* egrp_mem;     // member indices, sorted order within a group
+  int negrp;
+  int ngx;                 // total group x points
+  double* egrid;           // per group: sum_m c_m E_m on the group's x-grid
+  const double* ecoef;     // combination coefficient per member (negrp == 0: no groups)
 };
 
 // launchers: one set per arithmetic TU (k_exact.cu, k_fast.cu)

@@ -22,7 +22,7 @@ import numpy as np
 from . import configs as _cfg
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsgwg.so")
+LIB_PATH = os.environ.get("SGWG_LIB") or os.path.join(HERE, "libsgwg.so")
 
 OK, EINVAL, ENONFINITE, ECUDA, ENCCL, EUNSUPPORTED = range(6)
 ARITH_EXACT, ARITH_FAST = 0, 1

@@ -74,3 +74,37 @@ def test_landau_damping_rate(ctx_fast):
     assert len(peaks) >= 4
     slope = np.polyfit(ts[peaks], logE[peaks], 1)[0]
     assert -0.18 < slope < -0.13, slope
+
+
+@pytest.mark.parametrize("groups", ["0", "1"])
+def test_field_energy_record_2d2v(ctx_fast, oracle, monkeypatch, groups):
+    """Same record for 2D2V (member by member, or members grouped by x-grid
+    on the device): step 0 against separable Lagrange upsampling of every
+    member's (E_1, E_2)."""
+    from oracle import oracle as O
+    monkeypatch.setenv("SGWG_ENERGY_GROUPS", groups)
+    cfg = configs.config("C5", nl=3)
+    fam = gpu_family(ctx_fast, cfg)
+    fam.initialize(cfg["ic"])
+    rho, E = fam.vp_field()
+    nf = [cfg["root"][k] << cfg["nl"] for k in range(2)]
+    Ec = np.zeros((2, nf[0], nf[1]))
+    for mi, lv in enumerate(fam.levels):
+        c = [1, -3, 3, -1][cfg["nl"] - sum(lv)]
+        n0, n1 = fam.points[mi][0], fam.points[mi][1]
+        for comp in range(2):
+            g = np.asarray(E[mi][comp]).reshape(n0, n1)
+            m1 = cfg["nl"] - lv[1]
+            rows = np.array([oracle.upsample_line(g[i], nf[1], m1, O.PERIODIC, O.LAGRANGE)
+                             if m1 else g[i] for i in range(n0)])
+            m0 = cfg["nl"] - lv[0]
+            full = np.array([oracle.upsample_line(rows[:, j], nf[0], m0, O.PERIODIC, O.LAGRANGE)
+                             if m0 else rows[:, j] for j in range(nf[1])]).T
+            Ec[comp] += c * full
+    hvol = (cfg["upper"][0] - cfg["lower"][0]) / nf[0] * (cfg["upper"][1] - cfg["lower"][1]) / nf[1]
+    want0 = np.sqrt(np.sum(Ec * Ec) * hvol)
+    fam.evolve(cfg["dt_mode"], 0.05, cfl=cfg["cfl"])
+    fe = fam.field_energy()
+    assert len(fe) > 3
+    assert abs(fe[0] - want0) <= 1e-12 * want0
+    assert np.all(np.isfinite(fe)) and np.all(fe > 0)
