@@ -91,8 +91,11 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 #if SGWG_FAST
+#ifndef SGWG_SWEEP_ATTR
+#define SGWG_SWEEP_ATTR __noinline__
+#endif
 template <bool BURGERS, int RUN, bool LINEAR>
-__device__ __noinline__ void sweep_run(const double* __restrict__ P,
+__device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
                                        const double* __restrict__ Mv, int st, int p0, double c,
                                        double eps4, double inv_h, double* __restrict__ out,
                                        int ost);
@@ -618,10 +621,10 @@ __device__ __forceinline__ double recon_roles(double fc, double A, double B, dou
 // x and y sweeps of every tile shape, keeping the hot code in the i-cache.
 // du[t] is written to out[t * ost] (shared memory).
 template <bool BURGERS, int RUN, bool LINEAR>
-__device__ __noinline__ void sweep_run(const double* __restrict__ P,
-                                       const double* __restrict__ Mv, int st, int p0, double c,
-                                       double eps4, double inv_h, double* __restrict__ out,
-                                       int ost) {
+__device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
+                                          const double* __restrict__ Mv, int st, int p0,
+                                          double c, double eps4, double inv_h,
+                                          double* __restrict__ out, int ost) {
   // Fully unrolled sliding window: interface t has left point q = t + 2
   // (q = padded index relative to p0); D, d, K of a point are computed once and
   // reused by the three interfaces that see it.  For advection Mv == P and the
@@ -1330,16 +1333,18 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
 #pragma unroll
   for (int e0 = 0; e0 < kPlaneMaxE; e0 += 4) {
     double kin[4], unv[4];
-    int gq[4];
+    int gq[4], pk[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int q = tid + (e0 + e) * kPlaneThreads;
       kin[e] = 0.0;
       unv[e] = 0.0;
       gq[e] = -1;
+      pk[e] = 0;
       if (q < NP) {
         int v, i, j;
         decode(q, v, i, j);
+        pk[e] = (v << 22) | (i << 11) | j;  // v < 32, i, j < 2048
         gq[e] = (tl.plane0 + v) * ps + (tl.i0 + i) * sa + (tl.j0 + j) * sb;
         if (p.pr == 1) {
           kin[e] = __ldg(kb + gq[e]);
@@ -1349,10 +1354,8 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int q = tid + (e0 + e) * kPlaneThreads;
-      if (q >= NP) continue;
-      int v, i, j;
-      decode(q, v, i, j);
+      if (gq[e] < 0) continue;
+      const int v = pk[e] >> 22, i = (pk[e] >> 11) & 2047, j = pk[e] & 2047;
       const int dq = (v * G.TXr + i) * G.DPB + j;
       const double dx = DX[dq], dy = DY[dq];
       if (p.pr == 0) {
