@@ -1126,7 +1126,7 @@ struct PlaneGeom {
     DPB = TYr | 1;
   }
   __host__ __device__ int smem_doubles() const {
-    return V * PA * PB + 2 * V * TXr * DPB + 2 * kPlaneMaxV;
+    return V * PA * PB + 2 * V * TXr * DPB + 2 * kPlaneMaxV + TXr + TYr;
   }
 };
 
@@ -1197,6 +1197,8 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
   double* DY = DX + V * G.TXr * G.DPB;
   double* sca = DY + V * G.TXr * G.DPB;
   double* scb = sca + kPlaneMaxV;
+  double* WA = scb + kPlaneMaxV;  // pr = 1: trapezoid weights of the window rows / columns
+  double* WB = WA + G.TXr;
   const int tid = threadIdx.x;
   if (tid < V) {  // per-plane line coefficients (line_coef)
     const int pl = tl.plane0 + tid;
@@ -1207,6 +1209,16 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
     } else {  // v_j lines at x point pl: -E_j(x)
       sca[tid] = line_coef(p.flux_a, M, 2, p.space_dim, pl, p.c_a, p.efield);
       scb[tid] = line_coef(p.flux_b, M, 3, p.space_dim, pl, p.c_b, p.efield);
+    }
+  }
+  if (p.pr == 1 && p.rho_parts != nullptr) {  // models.hpp:64-71,240-257
+    for (int i = tid; i < TX; i += kPlaneThreads) {
+      const int ia = tl.i0 + i;
+      WA[i] = (bca == 1 && (ia == 0 || ia == na - 1)) ? 0.5 * M->h[a] : M->h[a];
+    }
+    for (int j = tid; j < TY; j += kPlaneThreads) {
+      const int jb = tl.j0 + j;
+      WB[j] = (bcb == 1 && (jb == 0 || jb == nb - 1)) ? 0.5 * M->h[b] : M->h[b];
     }
   }
   const double* u = p.uin + M->offset;
@@ -1329,7 +1341,6 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
   double* kb = p.kbuf + M->offset;
   const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
   const bool moment = (p.pr == 1) && (p.rho_parts != nullptr) && (p.stage > 0);
-  const double ha = M->h[a], hb = M->h[b];
 #pragma unroll
   for (int e0 = 0; e0 < kPlaneMaxE; e0 += 4) {
     double kin[4], unv[4];
@@ -1381,23 +1392,25 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
           o = fma(1.0 / 3.0, unv[e], (2.0 / 3.0) * fma(dt, kv, ui));
       }
       p.out[M->offset + gq[e]] = o;
-      if (moment) {  // trapezoid weights of the velocity block (models.hpp:64-71,240-257)
-        const int ia = tl.i0 + i, jb = tl.j0 + j;
-        const double wa = (bca == 1 && (ia == 0 || ia == na - 1)) ? 0.5 * ha : ha;
-        const double wb = (bcb == 1 && (jb == 0 || jb == nb - 1)) ? 0.5 * hb : hb;
-        DX[dq] = (wa * wb) * o;
-      }
+      if (moment) DX[dq] = (WA[i] * WB[j]) * o;  // trapezoid weights of the velocity block
     }
   }
   if (moment) {  // per-plane sums in a fixed order: one warp per plane
     __syncthreads();
     const int lane = tid & 31, warp = tid >> 5;
-    const int pp = TX * TY;
+    const int di = qdiv(32, iTY), dj = 32 - di * TY;  // lane stride 32 in (i, j)
+    const int i0 = qdiv(lane, iTY), j0 = lane - i0 * TY;
     for (int v = warp; v < V; v += kPlaneThreads / 32) {
       double acc = 0.0;
-      for (int q = lane; q < pp; q += 32) {
-        const int i = qdiv(q, iTY), j = q - i * TY;
-        acc += DX[(v * G.TXr + i) * G.DPB + j];
+      const double* D = DX + v * G.TXr * G.DPB;
+      for (int i = i0, j = j0; i < TX;) {
+        acc += D[i * G.DPB + j];
+        i += di;
+        j += dj;
+        if (j >= TY) {
+          j -= TY;
+          ++i;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
