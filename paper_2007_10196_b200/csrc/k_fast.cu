@@ -3,3 +3,10 @@
 #define SGWG_NS fast
 #define SGWG_FAST 1
 #include "kernels.cuh"
+
+#ifdef SGWG_TRACE
+// experiment builds only: copy the phase trace of the persistent kernel out
+extern "C" int sgwg_trace_dump(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, sgwg::fast::sgwg_trace, sizeof(sgwg::fast::sgwg_trace));
+}
+#endif

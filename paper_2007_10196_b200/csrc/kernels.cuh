@@ -693,6 +693,21 @@ __device__ __forceinline__ double ldx(const double* p) {
 constexpr int kFastRun = SGWG_FAST_RUN;
 constexpr int kFastThreads = 2 * 2048 / kFastRun;
 
+#ifdef SGWG_TRACE
+// phase timestamps of the persistent kernel (experiment builds only)
+__device__ long long sgwg_trace[4][600][5];
+__device__ __forceinline__ void trace_mark(int slot, int step_stage, int ph) {
+  const int b = blockIdx.x;
+  const int w = (b == 0) ? 0 : (b == 40) ? 1 : (b == 80) ? 2 : (b == 120) ? 3 : -1;
+  if (w >= 0 && threadIdx.x == 0 && step_stage >= 0 && step_stage < 600)
+    sgwg_trace[w][step_stage][ph] = clock64();
+  (void)slot;
+}
+#define SGWG_MARK(ss, ph) trace_mark(0, ss, ph)
+#else
+#define SGWG_MARK(ss, ph)
+#endif
+
 template <bool BURGERS, bool PERSIST, int TX, int TY>
 __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const MemberDesc* M,
                                                   int mi, int i0, int j0, double* sm) {
@@ -800,6 +815,7 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   for (int e = 0; e < NHL; ++e)
     if (ih[e] >= 0) split_store(ih[e] >> 10, ih[e] & 1023, vh[e]);
   __syncthreads();
+  if (PERSIST) SGWG_MARK(p.trace_ss, 1);
   const double eps4 = 4.0 * p.eps;
   if (tid < NS) {  // x-sweep warps: thread = (column j, run of RUN rows)
     const int j = tid % TY, r = tid / TY;
@@ -821,6 +837,7 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
                                      r * RUN, c, eps4, M->inv_h[1], DY + i * DP + r * RUN, 1);
   }
   __syncthreads();
+  if (PERSIST) SGWG_MARK(p.trace_ss, 2);
   // epilogue: k = (0 - du_x) - du_y, RK stage, coalesced along j
   double lmax = 0.0;
   const StepCtl* ctl = p.ctl;
@@ -1458,6 +1475,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
       p.cur_step = (unsigned long long)sctl.cur_step;
       p.resident = pp.base.resident && (pp.base.ntiles <= (int)gridDim.x);
       p.resident_load = (step == 0 && s == 1);
+      p.trace_ss = step * 3 + (s - 1);
+      SGWG_MARK(p.trace_ss, 0);
       if (BURGERS && blockIdx.x == 0)  // stage s clears the slot stage s+1 writes
         for (int i = threadIdx.x; i < nm; i += blockDim.x)
           pp.base.amax_zero[(size_t)((s + 1) % 3) * nm + i] = 0ull;
@@ -1466,7 +1485,9 @@ __global__ void __launch_bounds__(kFastThreads, 1)
         tile_body<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
         __syncthreads();
       }
+      SGWG_MARK(p.trace_ss, 3);
       grid.sync();
+      SGWG_MARK(p.trace_ss, 4);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
