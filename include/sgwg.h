@@ -202,6 +202,32 @@ int sgwg_combine_rows(sgwg_family* fam, int interp_mode, double eps, long long r
 int sgwg_prolong(sgwg_family* fam, int mi, int interp_mode, double eps, double* out, size_t n,
                  int out_is_device);
 
+/* ---- combined-field diagnostics and output (runner.hpp) ----- */
+/* Diagnostics of the combined finest-grid field (combine(set, mode, eps)),
+ * reduced on the device slab by slab (the field is never downloaded):
+ *   mass      quadrature_mass (models.hpp:75-94)
+ *   min, max  field_min / field_max (runner.hpp:202-211)
+ *   l1, linf  error_norms (diag.hpp:30-43) against the exact solution of linear
+ *             advection of a periodic preset, u0(x - a t): exact_preset one of
+ *             SGWG_IC_C1, _C3, _EX1, _EX2 for an SGWG_ADVECTION model, or -1
+ *             (then l1 = linf = NaN). */
+typedef struct sgwg_field_stats {
+  double mass;
+  double min, max;
+  double l1, linf;
+  double points;  /* finest-grid points reduced */
+} sgwg_field_stats;
+int sgwg_combined_stats(sgwg_family* fam, int interp_mode, double eps, int exact_preset,
+                        double t, sgwg_field_stats* out);
+/* Combined field at npoints finest-grid multi-indices idx[p*d + k] (cut planes,
+ * probes; write_cuts runner.hpp:159-200): each point equals the same point of
+ * sgwg_combine (bitwise in the exact build) without forming the finest grid. */
+int sgwg_eval_points(sgwg_family* fam, int interp_mode, double eps, const int* idx,
+                     size_t npoints, double* out);
+/* SGW5 snapshot of the combined field (write_field_dump, io.hpp:17-54): 64-byte
+ * header + row-major float64 payload, streamed slab by slab from the device. */
+int sgwg_write_snapshot(sgwg_family* fam, int interp_mode, double eps, const char* path);
+
 /* ---- single-stage entry points (unit-level parity) ------------ */
 /* FamilyModel::rhs (models.hpp:772-788) of every local member: tendency of the
  * current states into out (packed like the states). */

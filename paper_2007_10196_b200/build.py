@@ -6,6 +6,7 @@ object travels with the repository snapshot to the GPU box:
 * ``k_exact.cu``  -- reference-order arithmetic, ``--fmad=false`` (bitwise parity)
 * ``k_fast.cu``   -- FMA-contracted, divide-reduced arithmetic
 * ``k_field.cu``  -- Vlasov-Poisson moment + spectral Poisson
+* ``k_diag.cu``   -- diagnostics of the combined field (mass, min/max, error norms)
 * ``sgwg_api.cu`` -- host runtime behind the C ABI (include/sgwg.h), links NCCL
 """
 from __future__ import annotations
@@ -29,6 +30,7 @@ UNITS = {
     "k_exact.cu": ["--fmad=false", "-Xptxas", "-v"],
     "k_fast.cu": ["--fmad=true", "-Xptxas", "-v"],
     "k_field.cu": ["--fmad=true"],
+    "k_diag.cu": ["--fmad=true"],
     "sgwg_api.cu": ["--fmad=false"],
 }
 HEADERS = ["kernels.cuh", "sgwg_internal.h", "dt_device.cuh", "field_device.cuh"]

@@ -1,0 +1,106 @@
+// k_diag.cu -- device-side diagnostics of the combined finest-grid field
+// (SURVEY 8(f) row 2), reduced slab by slab so the 34.6 GB BASELINE C5 grid is
+// never materialised:
+//   mass      quadrature_mass (models.hpp:75-94): trapezoid weights, h per point
+//             (periodic), h/2 at zero-boundary ends (trapezoid_weights_1d, 64-71)
+//   min, max  field_min / field_max (runner.hpp:202-211); with an admissible
+//             interval they give oscillation_metrics (diag.hpp:92-101)
+//   l1, linf  error_norms against the exact solution (diag.hpp:30-43): the
+//             grid-point average of |u - u_exact| and its maximum; exact
+//             solutions exist for linear advection of the periodic presets,
+//             u(x, t) = u0(x - a t)
+// Deterministic: a fixed grid of CTAs writes per-CTA partials that one CTA sums
+// in a fixed order.
+#include <math.h>
+
+#include "sgwg_internal.h"
+
+namespace sgwg {
+
+constexpr int kStatsBlocks = 592;  // 4 x 148 SMs
+constexpr int kStatsThreads = 256;
+
+__device__ double preset_value(int preset, const double* x, int d) {
+  const double pi = 3.14159265358979323846;
+  switch (preset) {
+    case 0: return sin(pi * (x[0] + x[1]));                    // SGWG_IC_C1
+    case 2: return sin(pi * (x[0] + x[1] + x[2]));             // SGWG_IC_C3
+    case 5: return 0.3 + 0.7 * sin(0.5 * pi * (x[0] + x[1]));  // SGWG_IC_EX1
+    case 9: return 1.0 + 0.5 * sin(x[0] + x[1] + x[2]);        // SGWG_IC_EX2
+  }
+  (void)d;
+  return 0.0;
+}
+
+__device__ __forceinline__ void stats_merge(double* a, const double* b) {
+  a[0] += b[0];
+  a[1] = fmin(a[1], b[1]);
+  a[2] = fmax(a[2], b[2]);
+  a[3] += b[3];
+  a[4] = fmax(a[4], b[4]);
+}
+
+__device__ void block_stats(double* acc, double* out) {
+  __shared__ double red[kStatsThreads / 32][5];
+  for (int o = 16; o > 0; o >>= 1) {
+    double b[5];
+    for (int k = 0; k < 5; ++k) b[k] = __shfl_xor_sync(0xffffffffu, acc[k], o);
+    stats_merge(acc, b);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 5; ++k) red[w][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[5] = {red[0][0], red[0][1], red[0][2], red[0][3], red[0][4]};
+    for (int q = 1; q < kStatsThreads / 32; ++q) stats_merge(r, red[q]);
+    for (int k = 0; k < 5; ++k) out[k] = r[k];
+  }
+}
+
+__global__ void __launch_bounds__(kStatsThreads) stats_kernel(const StatsParams p) {
+  double acc[5] = {0.0, INFINITY, -INFINITY, 0.0, 0.0};
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < p.n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const double v = p.field[q];
+    long long lin = p.first + q;
+    int idx[kMaxD];
+    for (int k = p.d - 1; k >= 0; --k) {
+      idx[k] = (int)(lin % p.ext[k]);
+      lin /= p.ext[k];
+    }
+    double w = 1.0;
+    for (int k = 0; k < p.d; ++k) {
+      const bool end = p.bc[k] != 0 && (idx[k] == 0 || idx[k] == p.ext[k] - 1);
+      w *= end ? 0.5 * p.h[k] : p.h[k];
+    }
+    acc[0] = fma(w, v, acc[0]);
+    acc[1] = fmin(acc[1], v);
+    acc[2] = fmax(acc[2], v);
+    if (p.exact >= 0) {
+      double x[kMaxD];
+      for (int k = 0; k < p.d; ++k) x[k] = p.lower[k] + idx[k] * p.h[k] - p.a[k] * p.t;
+      const double e = fabs(v - preset_value(p.exact, x, p.d));
+      acc[3] += e;
+      acc[4] = fmax(acc[4], e);
+    }
+  }
+  block_stats(acc, p.partial + 5 * blockIdx.x);
+}
+
+__global__ void __launch_bounds__(kStatsThreads) stats_final_kernel(const double* partial, int nb,
+                                                                    double* out) {
+  double acc[5] = {0.0, INFINITY, -INFINITY, 0.0, 0.0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) stats_merge(acc, partial + 5 * b);
+  block_stats(acc, out);
+}
+
+int stats_partial_doubles() { return 5 * kStatsBlocks + 5; }
+
+cudaError_t launch_stats(const StatsParams& p, double* out5, cudaStream_t s) {
+  stats_kernel<<<kStatsBlocks, kStatsThreads, 0, s>>>(p);
+  stats_final_kernel<<<1, kStatsThreads, 0, s>>>(p.partial, kStatsBlocks, out5);
+  return cudaGetLastError();
+}
+
+}  // namespace sgwg

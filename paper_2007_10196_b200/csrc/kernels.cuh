@@ -1546,12 +1546,17 @@ int persist2d_max_blocks(int burgers, size_t smem) {
 // One point of upsample_line (interp.hpp:151-189) with OffsetTable::make
 // (interp.hpp:124-146): fine index j of a line of n_src source values at
 // src[base + i*stride], refinement 2^m.
-__device__ __forceinline__ double interp_point(const double* __restrict__ src, long long base,
-                                               long long stride, int n_src, int j, int m, int bc,
-                                               int mode, double eps) {
+// Interpolation weights of fine index j on a line refined by 2^m (r = j mod 2^m
+// != 0): stencil centre i, offset t and linear weights c (OffsetTable::make,
+// interp.hpp:124-146; linear_interp_weights interp.hpp:36-40).
+struct InterpAt {
+  int i;
+  double t, c0, c1, c2;
+};
+
+__device__ __forceinline__ InterpAt interp_at(int j, int m, int mode) {
   const int f = 1 << m;
   const int r = j & (f - 1);
-  if (r == 0) return src[base + (long long)((j >> m) % n_src) * stride];
   int di;
   double t;
   if (mode == 1) {  // InterpMode::weno
@@ -1561,23 +1566,20 @@ __device__ __forceinline__ double interp_point(const double* __restrict__ src, l
     di = 0;
     t = (double)r / f;
   }
-  const double c0 = (t - 1.0) * (t - 2.0) / 12.0;  // interp.hpp:39 / 120-121
-  const double c1 = (4.0 - t * t) / 6.0;
-  const double c2 = (t + 2.0) * (t + 1.0) / 12.0;
-  const int i = (j >> m) + di;
-  double s[5];
-#pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    const int ii = i - 2 + q;
-    if (bc == 0) {
-      int iw = ii % n_src;
-      if (iw < 0) iw += n_src;
-      s[q] = src[base + (long long)iw * stride];
-    } else {
-      s[q] = (ii >= 0 && ii < n_src) ? src[base + (long long)ii * stride] : 0.0;
-    }
-  }
-  // substencil_values (interp.hpp:45-53)
+  InterpAt a;
+  a.c0 = (t - 1.0) * (t - 2.0) / 12.0;  // interp.hpp:39 / 120-121
+  a.c1 = (4.0 - t * t) / 6.0;
+  a.c2 = (t + 2.0) * (t + 1.0) / 12.0;
+  a.i = (j >> m) + di;
+  a.t = t;
+  return a;
+}
+
+// the value from the 5 stencil values s[0..4] around a.i (upsample_line,
+// interp.hpp:179-187 with substencil_values interp.hpp:45-53)
+__device__ __forceinline__ double interp_vals(const double* s, const InterpAt& a, int mode,
+                                              double eps) {
+  const double t = a.t, c0 = a.c0, c1 = a.c1, c2 = a.c2;
   const double p0 = s[0] * 0.5 * (t + 1.0) * t - s[1] * (t + 2.0) * t +
                     s[2] * 0.5 * (t + 2.0) * (t + 1.0);
   const double p1 = s[1] * 0.5 * t * (t - 1.0) - s[2] * (t + 1.0) * (t - 1.0) +
@@ -1601,6 +1603,114 @@ __device__ __forceinline__ double interp_point(const double* __restrict__ src, l
   const double a1 = c1 / sq(eps + b1);
   const double a2 = c2 / sq(eps + b2);
   return (a0 * p0 + a1 * p1 + a2 * p2) / (a0 + a1 + a2);
+}
+
+__device__ __forceinline__ double interp_point(const double* __restrict__ src, long long base,
+                                               long long stride, int n_src, int j, int m, int bc,
+                                               int mode, double eps) {
+  const int f = 1 << m;
+  const int r = j & (f - 1);
+  if (r == 0) return src[base + (long long)((j >> m) % n_src) * stride];
+  const InterpAt a = interp_at(j, m, mode);
+  double s[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int ii = a.i - 2 + q;
+    if (bc == 0) {
+      int iw = ii % n_src;
+      if (iw < 0) iw += n_src;
+      s[q] = src[base + (long long)iw * stride];
+    } else {
+      s[q] = (ii >= 0 && ii < n_src) ? src[base + (long long)ii * stride] : 0.0;
+    }
+  }
+  return interp_vals(s, a, mode, eps);
+}
+
+// Combined value at single finest-grid points (cut planes, probes): for each
+// member, prolong restricted to the point -- the dimension-by-dimension
+// interpolation (interp.hpp:217-244) evaluated recursively on the 5^k source
+// values it depends on, with the same arithmetic as upsample_kernel /
+// final_kernel, so a point equals the same point of the full combination --
+// then acc = acc + c*P(u) in member order (combine.hpp:113-120).
+struct EvalDim {
+  int copy;  // 1: the point's source index along this dimension is i (no interpolation)
+  int i, n, bc;
+  long long stride;
+  InterpAt a;
+};
+
+template <int K>
+struct EvalRec {
+  static __device__ double go(const double* u, const EvalDim* D, long long off, int mode,
+                              double eps) {
+    const EvalDim& e = D[K];
+    if (e.copy) return EvalRec<K - 1>::go(u, D, off + (long long)e.i * e.stride, mode, eps);
+    double s[5];
+    for (int q = 0; q < 5; ++q) {
+      int ii = e.a.i - 2 + q;
+      if (e.bc == 0) {
+        ii %= e.n;
+        if (ii < 0) ii += e.n;
+      } else if (ii < 0 || ii >= e.n) {
+        s[q] = 0.0;
+        continue;
+      }
+      s[q] = EvalRec<K - 1>::go(u, D, off + (long long)ii * e.stride, mode, eps);
+    }
+    return interp_vals(s, e.a, mode, eps);
+  }
+};
+template <>
+struct EvalRec<-1> {
+  static __device__ double go(const double* u, const EvalDim*, long long off, int, double) {
+    return u[off];
+  }
+};
+
+__global__ void __launch_bounds__(128) eval_points_kernel(const EvalParams p) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= p.npts) return;
+  const int d = p.d;
+  int j[kMaxD];
+  for (int k = 0; k < d; ++k) j[k] = p.idx[q * d + k];
+  double acc = 0.0;
+  for (int mi = 0; mi < p.nm; ++mi) {
+    const MemberDesc* M = p.mem + mi;
+    EvalDim D[kMaxD];
+    for (int k = 0; k < d; ++k) {
+      const int m = p.nl - M->level[k];
+      EvalDim& e = D[k];
+      e.n = M->ext[k];
+      e.bc = M->bc[k];
+      e.stride = M->stride[k];
+      e.copy = 1;
+      if (m == 0) {
+        e.i = j[k];
+      } else if ((j[k] & ((1 << m) - 1)) == 0) {
+        e.i = (j[k] >> m) % e.n;
+      } else {
+        e.copy = 0;
+        e.a = interp_at(j[k], m, p.mode);
+      }
+    }
+    const double* u = p.u + M->offset;
+    double v;
+    switch (d) {
+      case 1: v = EvalRec<0>::go(u, D, 0, p.mode, p.eps); break;
+      case 2: v = EvalRec<1>::go(u, D, 0, p.mode, p.eps); break;
+      case 3: v = EvalRec<2>::go(u, D, 0, p.mode, p.eps); break;
+      default: v = EvalRec<3>::go(u, D, 0, p.mode, p.eps); break;
+    }
+    acc = acc + p.coef[mi] * v;  // combine.hpp:119
+  }
+  p.out[q] = acc;
+}
+
+cudaError_t launch_eval_points(const EvalParams& p, cudaStream_t s) {
+  if (p.npts <= 0) return cudaSuccess;
+  eval_points_kernel<<<(unsigned)((p.npts + 127) / 128), 128, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 // dimension k of prolong for a batch of members: dst has finest extent along

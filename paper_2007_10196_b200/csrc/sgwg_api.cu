@@ -198,6 +198,9 @@ struct sgwg_family {
   // prolongation plans
   ProlongPlan* full_plan = nullptr;
   double* fine_buf = nullptr;
+  double* diag_slab = nullptr;     // combined-field slab for diagnostics / snapshots
+  long long diag_slab_doubles = 0;
+  double* diag_scratch = nullptr;  // stats partials + result
   double* slab_arena = nullptr;  // row-slab combination intermediates
   long long slab_arena_doubles = 0;
   double* slab_out = nullptr;
@@ -1406,6 +1409,8 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->emax);
   cudaFree(f->dmtasks);
   cudaFree(f->fine_buf);
+  cudaFree(f->diag_slab);
+  cudaFree(f->diag_scratch);
   cudaFree(f->slab_arena);
   cudaFree(f->slab_out);
   cudaEventDestroy(f->ev0);
@@ -1825,6 +1830,223 @@ int sgwg_rhs(sgwg_family* f, double* out, size_t n, int out_is_device) {
   StageBufs b{f->u, f->u, f->A};
   TRY(launch_stage(f, 0, b, false));
   return copy_out(f, f->A, out, n, out_is_device);
+}
+
+}  // extern "C"
+
+namespace {
+
+// combination coefficient of each local member (combine.hpp:34-43, 116)
+std::vector<double> member_coefs(const sgwg_family* f) {
+  std::vector<double> cf;
+  for (int mi = 0; mi < f->nm; ++mi) {
+    int ls = 0;
+    for (int k = 0; k < f->d; ++k) ls += f->levels[mi][k];
+    const int j = f->nl - ls;
+    cf.push_back(f->single ? 1.0 : (double)((j % 2 == 0 ? 1 : -1) * binomial(f->d - 1, j)));
+  }
+  return cf;
+}
+
+int check_interp(int mode, double eps) {
+  if (mode != SGWG_INTERP_WENO && mode != SGWG_INTERP_LAGRANGE)
+    return fail_with(SGWG_EINVAL, "unknown interpolation mode");
+  if (mode == SGWG_INTERP_WENO && !(eps > 0.0))
+    return fail_with(SGWG_EINVAL, "weno_interp5: epsilon must be positive");
+  return SGWG_OK;
+}
+
+// Visit the combined finest-grid field in dimension-0 row slabs on the device:
+// fn(dev, first_linear_index, points).  One slab when the whole grid fits the
+// combination budget (or the family is a single grid).
+template <class Fn>
+int for_each_combined_slab(sgwg_family* f, int mode, double eps, Fn&& fn) {
+  CK(cudaSetDevice(f->ctx->device));
+  if (f->single) return fn((const double*)f->u, 0LL, f->finest);
+  if (f->nm == 0 && f->comm == nullptr) return fail_with(SGWG_EINVAL, "combine: empty family");
+  std::vector<int> mis(f->nm);
+  for (int i = 0; i < f->nm; ++i) mis[i] = i;
+  const long long rows = (f->d == 1) ? 1 : f->fine_ext[0];
+  if (f->d == 1 || plan_doubles(f, mis, 0, rows) <= combine_budget_doubles()) {
+    if (f->full_plan == nullptr) TRY(build_plan(f, mis, 0, rows, nullptr, &f->full_plan));
+    TRY(ensure_fine_buf(f));
+    TRY(run_plan(f, f->full_plan, mode, eps, 0, f->fine_buf));
+    if (f->comm != nullptr && f->nranks > 1)
+      CKN(ncclAllReduce(f->fine_buf, f->fine_buf, (size_t)f->finest, ncclDouble, ncclSum,
+                        f->comm, f->ctx->stream));
+    return fn((const double*)f->fine_buf, 0LL, f->finest);
+  }
+  const long long per_row = (long long)(f->finest / f->fine_ext[0]);
+  long long slab = rows;
+  while (slab > 1 && plan_doubles(f, mis, 0, slab) > combine_budget_doubles()) slab = (slab + 1) / 2;
+  if (f->diag_slab_doubles < slab * per_row) {
+    cudaFree(f->diag_slab);
+    f->diag_slab = nullptr;
+    CK(cudaMalloc(&f->diag_slab, sizeof(double) * slab * per_row));
+    f->diag_slab_doubles = slab * per_row;
+  }
+  for (long long a = 0; a < rows; a += slab) {
+    const long long b = std::min(rows, a + slab);
+    TRY(combine_rows_impl(f, mis, mode, eps, a, b, f->diag_slab, 1));
+    TRY(fn((const double*)f->diag_slab, a * per_row, (b - a) * per_row));
+  }
+  return SGWG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, double t,
+                        sgwg_field_stats* out) {
+  if (f == nullptr || out == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  TRY(check_interp(mode, eps));
+  if (exact_preset >= 0) {
+    if (!f->has_model || f->model.kind != SGWG_ADVECTION)
+      return fail_with(SGWG_EINVAL, "combined_stats: exact solutions need a linear advection model");
+    if (exact_preset != SGWG_IC_C1 && exact_preset != SGWG_IC_C3 && exact_preset != SGWG_IC_EX1 &&
+        exact_preset != SGWG_IC_EX2)
+      return fail_with(SGWG_EINVAL, "combined_stats: no exact solution for this preset");
+  }
+  CK(cudaSetDevice(f->ctx->device));
+  if (f->diag_scratch == nullptr)
+    CK(cudaMalloc(&f->diag_scratch, sizeof(double) * stats_partial_doubles()));
+  StatsParams sp{};
+  sp.d = f->d;
+  for (int k = 0; k < f->d; ++k) {
+    sp.ext[k] = f->fine_ext[k];
+    sp.bc[k] = (f->dom.bc[k] == SGWG_PERIODIC) ? 0 : 1;
+    sp.h[k] = f->fine_h[k];
+    sp.lower[k] = f->dom.lower[k];
+    sp.a[k] = (exact_preset >= 0) ? f->model.speeds[k] : 0.0;
+  }
+  sp.exact = exact_preset;
+  sp.t = t;
+  sp.partial = f->diag_scratch;
+  double mass = 0.0, mn = INFINITY, mx = -INFINITY, l1 = 0.0, linf = 0.0;
+  TRY(for_each_combined_slab(f, mode, eps, [&](const double* dev, long long first, long long n) -> int {
+    StatsParams q = sp;
+    q.field = dev;
+    q.first = first;
+    q.n = n;
+    double h5[5];
+    CK(launch_stats(q, f->diag_scratch + stats_partial_doubles() - 5, f->ctx->stream));
+    CK(cudaMemcpyAsync(h5, f->diag_scratch + stats_partial_doubles() - 5, sizeof(h5),
+                       cudaMemcpyDeviceToHost, f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    mass += h5[0];
+    mn = std::min(mn, h5[1]);
+    mx = std::max(mx, h5[2]);
+    l1 += h5[3];
+    linf = std::max(linf, h5[4]);
+    return SGWG_OK;
+  }));
+  out->mass = mass;
+  out->min = mn;
+  out->max = mx;
+  out->points = (double)f->finest;
+  out->l1 = (exact_preset >= 0) ? l1 / (double)f->finest : NAN;
+  out->linf = (exact_preset >= 0) ? linf : NAN;
+  return SGWG_OK;
+}
+
+int sgwg_eval_points(sgwg_family* f, int mode, double eps, const int* idx, size_t npoints,
+                     double* out) {
+  if (f == nullptr || (npoints > 0 && (idx == nullptr || out == nullptr)))
+    return fail_with(SGWG_EINVAL, "null argument");
+  TRY(check_interp(mode, eps));
+  for (size_t q = 0; q < npoints; ++q)
+    for (int k = 0; k < f->d; ++k)
+      if (idx[q * f->d + k] < 0 || idx[q * f->d + k] >= f->fine_ext[k])
+        return fail_with(SGWG_EINVAL, "eval_points: index outside the finest grid");
+  if (npoints == 0) return SGWG_OK;
+  CK(cudaSetDevice(f->ctx->device));
+  int* didx = nullptr;
+  double *dcoef = nullptr, *dout = nullptr;
+  const std::vector<double> cf = member_coefs(f);
+  int st = SGWG_OK;
+  auto fail_cuda = [&](cudaError_t e) {
+    return (e == cudaSuccess) ? SGWG_OK : fail_with(SGWG_ECUDA, cudaGetErrorString(e));
+  };
+  st = fail_cuda(cudaMalloc(&didx, sizeof(int) * npoints * f->d));
+  if (st == SGWG_OK) st = fail_cuda(cudaMalloc(&dcoef, sizeof(double) * std::max(1, f->nm)));
+  if (st == SGWG_OK) st = fail_cuda(cudaMalloc(&dout, sizeof(double) * npoints));
+  if (st == SGWG_OK)
+    st = fail_cuda(cudaMemcpyAsync(didx, idx, sizeof(int) * npoints * f->d,
+                                   cudaMemcpyHostToDevice, f->ctx->stream));
+  if (st == SGWG_OK && f->nm > 0)
+    st = fail_cuda(cudaMemcpyAsync(dcoef, cf.data(), sizeof(double) * f->nm,
+                                   cudaMemcpyHostToDevice, f->ctx->stream));
+  if (st == SGWG_OK) {
+    EvalParams p{};
+    p.mem = f->dmem;
+    p.u = f->u;
+    p.coef = dcoef;
+    p.idx = didx;
+    p.npts = (long long)npoints;
+    p.nm = f->nm;
+    p.d = f->d;
+    p.nl = f->single ? f->levels[0][0] : f->nl;
+    p.mode = mode;
+    p.eps = eps;
+    p.out = dout;
+    st = fail_cuda(arith_of(f) == SGWG_ARITH_FAST ? fast::launch_eval_points(p, f->ctx->stream)
+                                                   : exact::launch_eval_points(p, f->ctx->stream));
+  }
+  if (st == SGWG_OK && f->comm != nullptr && f->nranks > 1) {
+    const ncclResult_t r = ncclAllReduce(dout, dout, npoints, ncclDouble, ncclSum, f->comm,
+                                         f->ctx->stream);
+    if (r != ncclSuccess) st = fail_with(SGWG_ENCCL, ncclGetErrorString(r));
+  }
+  if (st == SGWG_OK)
+    st = fail_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * npoints, cudaMemcpyDeviceToHost,
+                                   f->ctx->stream));
+  if (st == SGWG_OK) st = fail_cuda(cudaStreamSynchronize(f->ctx->stream));
+  cudaFree(didx);
+  cudaFree(dcoef);
+  cudaFree(dout);
+  return st;
+}
+
+int sgwg_write_snapshot(sgwg_family* f, int mode, double eps, const char* path) {
+  if (f == nullptr || path == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  TRY(check_interp(mode, eps));
+  // FieldDumpHeader (io.hpp:17-26): magic, version, rank, extents, pad, spacings
+  unsigned char hdr[64];
+  std::memset(hdr, 0, sizeof(hdr));
+  std::memcpy(hdr, "SGW5", 4);
+  const uint32_t version = 1, dim = (uint32_t)f->d;
+  std::memcpy(hdr + 4, &version, 4);
+  std::memcpy(hdr + 8, &dim, 4);
+  for (int k = 0; k < f->d; ++k) {
+    const uint32_t e = (uint32_t)f->fine_ext[k];
+    std::memcpy(hdr + 12 + 4 * k, &e, 4);
+    std::memcpy(hdr + 32 + 8 * k, &f->fine_h[k], 8);
+  }
+  FILE* fp = std::fopen(path, "wb");
+  if (fp == nullptr) return fail_with(SGWG_EINVAL, std::string("write_snapshot: cannot open ") + path);
+  int st = (std::fwrite(hdr, 1, sizeof(hdr), fp) == sizeof(hdr))
+               ? SGWG_OK
+               : fail_with(SGWG_EINVAL, "write_snapshot: write failed");
+  double* host = nullptr;
+  long long host_n = 0;
+  if (st == SGWG_OK)
+    st = for_each_combined_slab(f, mode, eps, [&](const double* dev, long long, long long n) -> int {
+      if (host_n < n) {
+        cudaFreeHost(host);
+        host = nullptr;
+        CK(cudaMallocHost(&host, sizeof(double) * n));
+        host_n = n;
+      }
+      CK(cudaMemcpyAsync(host, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, f->ctx->stream));
+      CK(cudaStreamSynchronize(f->ctx->stream));
+      if (std::fwrite(host, sizeof(double), (size_t)n, fp) != (size_t)n)
+        return fail_with(SGWG_EINVAL, "write_snapshot: write failed");
+      return SGWG_OK;
+    });
+  cudaFreeHost(host);
+  if (std::fclose(fp) != 0 && st == SGWG_OK) st = fail_with(SGWG_EINVAL, "write_snapshot: close failed");
+  return st;
 }
 
 int sgwg_combine(sgwg_family* f, int mode, double eps, double* out, size_t n, int out_is_device) {

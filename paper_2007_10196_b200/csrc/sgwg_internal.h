@@ -201,6 +201,32 @@ struct FinalParams {
   double* out;
 };
 
+struct EvalParams {        // combined field at single finest-grid points
+  const MemberDesc* mem;
+  const double* u;         // packed member states
+  const double* coef;      // combination coefficient per member
+  const int* idx;          // npts x d finest multi-indices
+  long long npts;
+  int nm, d, nl, mode;
+  double eps;
+  double* out;
+};
+
+struct StatsParams {       // k_diag.cu: diagnostics of a slab of the combined field
+  const double* field;
+  long long n;             // points of the slab
+  long long first;         // finest-grid linear index of field[0]
+  int d;
+  int ext[kMaxD];
+  int bc[kMaxD];
+  double h[kMaxD];
+  double lower[kMaxD];
+  int exact;               // preset of the exact solution (linear advection) or -1
+  double t;
+  double a[kMaxD];         // advection speeds
+  double* partial;         // stats_partial_doubles() scratch
+};
+
 struct FieldParams {
   const MemberDesc* mem;
   const double* f;         // stage input (packed)
@@ -233,6 +259,7 @@ struct FieldParams {
   cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s); \
   cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s);      \
   cudaError_t launch_final(const FinalParams& p, cudaStream_t s);                         \
+  cudaError_t launch_eval_points(const EvalParams& p, cudaStream_t s);                    \
   }
 SGWG_DECLARE_LAUNCHERS(exact)
 SGWG_DECLARE_LAUNCHERS(fast)
@@ -272,5 +299,7 @@ cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, c
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
                                 double hvol, double* out_base, long long cap, cudaStream_t s);
 cudaError_t launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t s);
+int stats_partial_doubles();
+cudaError_t launch_stats(const StatsParams& p, double* out5, cudaStream_t s);
 
 }  // namespace sgwg

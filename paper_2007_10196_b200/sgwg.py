@@ -62,6 +62,11 @@ class Failure(C.Structure):
     _fields_ = [("member", C.c_int), ("step", C.c_longlong), ("stage", C.c_int)]
 
 
+class FieldStats(C.Structure):
+    _fields_ = [("mass", C.c_double), ("min", C.c_double), ("max", C.c_double),
+                ("l1", C.c_double), ("linf", C.c_double), ("points", C.c_double)]
+
+
 class Stats(C.Structure):
     _fields_ = [("evolve_ms", C.c_double), ("combine_ms", C.c_double), ("steps", C.c_longlong),
                 ("kernel_launches", C.c_longlong), ("combine_launches", C.c_longlong),
@@ -115,6 +120,11 @@ SIGNATURES = {
                                     C.c_size_t, C.c_int]),
     "sgwg_vp_field": (C.c_int, [_VP, _DP, C.c_size_t, _DP, C.c_size_t]),
     "sgwg_field_energy": (C.c_int, [_VP, _DP, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "sgwg_combined_stats": (C.c_int, [_VP, C.c_int, C.c_double, C.c_int, C.c_double,
+                                      C.POINTER(FieldStats)]),
+    "sgwg_eval_points": (C.c_int, [_VP, C.c_int, C.c_double, C.POINTER(C.c_int), C.c_size_t,
+                                   _DP]),
+    "sgwg_write_snapshot": (C.c_int, [_VP, C.c_int, C.c_double, C.c_char_p]),
 }
 
 
@@ -370,6 +380,12 @@ class Family:
     def fine_extent0(self) -> int:
         return (self.dom.root_cells[0] << self.nl) + (1 if self.dom.bc[0] == 1 else 0)
 
+    @property
+    def fine_extents(self) -> tuple:
+        """finest-grid points per dimension (GridGeometry::make at level nl)"""
+        return tuple((self.dom.root_cells[k] << self.nl) + (1 if self.dom.bc[k] == 1 else 0)
+                     for k in range(self.d))
+
     def prolong(self, mi, mode=1, eps=1e-6) -> np.ndarray:
         out = np.empty(self.finest_points)
         _check(load().sgwg_prolong(self.h, mi, mode, eps, out.ctypes.data, out.size, 0))
@@ -390,6 +406,37 @@ class Family:
             out_e.append(E[o * dx:(o + nx) * dx].reshape(dx, nx))
             o += nx
         return out_r, out_e
+
+    # -- combined-field diagnostics and output ----------------------
+    def combined_stats(self, mode=1, eps=1e-6, exact_preset=-1, t=0.0) -> dict:
+        """mass / min / max of the combined field and, for linear advection of a
+        periodic preset, error_norms (l1 average, linf) against u0(x - a t)."""
+        st = FieldStats()
+        _check(load().sgwg_combined_stats(self.h, mode, eps, exact_preset, t, C.byref(st)))
+        return {n: getattr(st, n) for n, _ in FieldStats._fields_}
+
+    def eval_points(self, idx, mode=1, eps=1e-6) -> np.ndarray:
+        """combined field at finest-grid multi-indices idx (npoints x d)"""
+        idx = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1, self.d)
+        out = np.empty(idx.shape[0])
+        _check(load().sgwg_eval_points(self.h, mode, eps,
+                                       idx.ctypes.data_as(C.POINTER(C.c_int)), idx.shape[0],
+                                       out.ctypes.data_as(_DP)))
+        return out
+
+    def cut_plane(self, dim_a, dim_b, fixed, mode=1, eps=1e-6) -> np.ndarray:
+        """combined field on the plane (dim_a, dim_b) through the finest-grid
+        indices `fixed` of the other dimensions (write_plane_csv, runner.hpp:126-141)"""
+        na, nb = self.fine_extents[dim_a], self.fine_extents[dim_b]
+        ia, ib = np.meshgrid(np.arange(na), np.arange(nb), indexing="ij")
+        idx = np.tile(np.asarray(fixed, dtype=np.int32), (na * nb, 1))
+        idx[:, dim_a] = ia.ravel()
+        idx[:, dim_b] = ib.ravel()
+        return self.eval_points(idx, mode, eps).reshape(na, nb)
+
+    def write_snapshot(self, path, mode=1, eps=1e-6):
+        """SGW5 dump of the combined field (write_field_dump, io.hpp:17-54)"""
+        _check(load().sgwg_write_snapshot(self.h, mode, eps, os.fsencode(path)))
 
     def field_energy(self, cap=1 << 20) -> np.ndarray:
         """||E||_2 of the combined field at the start of every step of the last evolve."""
@@ -428,3 +475,20 @@ def nccl_unique_id() -> bytes:
 
 
 config = _cfg.config
+
+
+def read_snapshot(path):
+    """read_field_dump (io.hpp:56-75): (extents, spacings, values)."""
+    with open(path, "rb") as fh:
+        hdr = fh.read(64)
+        if len(hdr) != 64 or hdr[:4] != b"SGW5":
+            raise ValueError(f"read_snapshot: bad header in {path}")
+        version, dim = np.frombuffer(hdr[4:12], dtype="<u4")
+        if version != 1 or not 1 <= dim <= 4:
+            raise ValueError(f"read_snapshot: bad header in {path}")
+        ext = [int(e) for e in np.frombuffer(hdr[12:28], dtype="<u4")[:dim]]
+        h = [float(x) for x in np.frombuffer(hdr[32:64], dtype="<f8")[:dim]]
+        vals = np.frombuffer(fh.read(), dtype="<f8")
+    if vals.size != int(np.prod(ext)):
+        raise ValueError(f"read_snapshot: truncated payload in {path}")
+    return ext, h, vals
