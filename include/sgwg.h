@@ -207,10 +207,11 @@ int sgwg_prolong(sgwg_family* fam, int mi, int interp_mode, double eps, double* 
  * reduced on the device slab by slab (the field is never downloaded):
  *   mass      quadrature_mass (models.hpp:75-94)
  *   min, max  field_min / field_max (runner.hpp:202-211)
- *   l1, linf  error_norms (diag.hpp:30-43) against the exact solution of linear
- *             advection of a periodic preset, u0(x - a t): exact_preset one of
- *             SGWG_IC_C1, _C3, _EX1, _EX2 for an SGWG_ADVECTION model, or -1
- *             (then l1 = linf = NaN). */
+ *   l1, linf  error_norms (diag.hpp:30-43) against the exact solution: linear
+ *             advection of a periodic preset, u0(x - a t) (exact_preset one of
+ *             SGWG_IC_C1, _C3, _EX1, _EX2, SGWG_ADVECTION model), or the Burgers
+ *             sine waves before the shock (SGWG_IC_C2 in 2D, SGWG_IC_EX3;
+ *             burgers_sine_exact models.hpp:533-560); -1: none (l1 = linf = NaN). */
 typedef struct sgwg_field_stats {
   double mass;
   double min, max;

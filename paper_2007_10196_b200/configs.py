@@ -57,6 +57,16 @@ def config(name, **over):
                  kind=ADVECTION, speeds=[1.0, 1.0], weno_mode=LINEAR, epsilon=1e-6,
                  dt_mode=DT_ACCURACY, cfl=0.4, dt_scale=1.0, tfinal=0.5, stops=[],
                  interp=LAGRANGE, ic=IC_EX1, space_dim=0)
+    elif name == "ex2":   # models.hpp:619-638 (Table 2): 3D linear advection
+        c = dict(d=3, nl=3, lower=[0.0] * 3, upper=[2 * pi] * 3, root=[10] * 3,
+                 bc=[PERIODIC] * 3, kind=ADVECTION, speeds=[1.0, 1.0, 1.0], weno_mode=LINEAR,
+                 epsilon=1e-6, dt_mode=DT_ACCURACY, cfl=0.4, dt_scale=1.0, tfinal=0.5, stops=[],
+                 interp=LAGRANGE, ic=IC_EX2, space_dim=0)
+    elif name == "ex3b":  # models.hpp:639-664 (3D Burgers), T = 0.1
+        c = dict(d=3, nl=3, lower=[0.0] * 3, upper=[2 * pi] * 3, root=[10] * 3,
+                 bc=[PERIODIC] * 3, kind=BURGERS, speeds=[0.0] * 3, weno_mode=NONLINEAR,
+                 epsilon=1e-6, dt_mode=DT_ACCURACY, cfl=0.4, dt_scale=1.0, tfinal=0.1, stops=[],
+                 interp=WENO, ic=IC_EX3, space_dim=0)
     elif name == "ex3a":  # models.hpp:639-664 (Table 4), paper epsilon 1e-3
         c = dict(d=2, nl=3, lower=[0.0, 0.0], upper=[2 * pi, 2 * pi], root=[10, 10],
                  bc=[PERIODIC] * 2, kind=BURGERS, speeds=[0.0, 0.0], weno_mode=NONLINEAR,

@@ -8,7 +8,8 @@
 //   l1, linf  error_norms against the exact solution (diag.hpp:30-43): the
 //             grid-point average of |u - u_exact| and its maximum; exact
 //             solutions exist for linear advection of the periodic presets,
-//             u(x, t) = u0(x - a t)
+//             u(x, t) = u0(x - a t), and for the Burgers sine waves before the
+//             shock (burgers_sine_exact, models.hpp:533-560)
 // Deterministic: a fixed grid of CTAs writes per-CTA partials that one CTA sums
 // in a fixed order.
 #include <math.h>
@@ -19,6 +20,51 @@ namespace sgwg {
 
 constexpr int kStatsBlocks = 592;  // 4 x 148 SMs
 constexpr int kStatsThreads = 256;
+
+// burgers_sine_exact (models.hpp:533-560): u = mean + amp sin(xi - rate u),
+// Newton from the linearised start with a bisection fallback on [mean-|amp|,
+// mean+|amp|] (rate = d t for the d-dimensional Burgers sine waves).
+__device__ double burgers_sine_exact(double mean, double amp, double xi, double rate) {
+  const double tol = 1e-14;
+  auto g = [&](double u) { return u - mean - amp * sin(xi - rate * u); };
+  auto gp = [&](double u) { return 1.0 + amp * rate * cos(xi - rate * u); };
+  const double lo = mean - fabs(amp), hi = mean + fabs(amp);
+  double u = mean + amp * sin(xi - rate * mean);
+  for (int it = 0; it < 100; ++it) {
+    const double r = g(u);
+    if (fabs(r) <= tol) return u;
+    const double dp = gp(u);
+    double next = (dp != 0.0) ? u - r / dp : lo - 1.0;
+    if (!(next >= lo && next <= hi)) {
+      if (g(lo) > 0.0 || g(hi) < 0.0) return u;
+      double a = lo, b = hi;
+      for (int k = 0; k < 200; ++k) {
+        const double m = 0.5 * (a + b);
+        if (g(m) <= 0.0)
+          a = m;
+        else
+          b = m;
+      }
+      next = 0.5 * (a + b);
+    }
+    u = next;
+  }
+  return u;
+}
+
+// exact solutions at (x, t): linear advection of a periodic preset (the host
+// shifts x by a t), or the Burgers sine waves before shock formation
+__device__ double exact_value(int preset, const double* x, int d, double t) {
+  const double pi = 3.14159265358979323846;
+  if (preset == 1)  // SGWG_IC_C2 under Burgers: 0.5 + sin(pi(x + y - 2 t u))
+    return burgers_sine_exact(0.5, 1.0, pi * (x[0] + x[1]), 2.0 * pi * t);
+  if (preset == 6) {  // SGWG_IC_EX3 (ex3a/ex3b, models.hpp:652-656)
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s += x[k];
+    return burgers_sine_exact(1.0, 0.5, s, d * t);
+  }
+  return 0.0;
+}
 
 __device__ double preset_value(int preset, const double* x, int d) {
   const double pi = 3.14159265358979323846;
@@ -80,7 +126,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const StatsParams 
     if (p.exact >= 0) {
       double x[kMaxD];
       for (int k = 0; k < p.d; ++k) x[k] = p.lower[k] + idx[k] * p.h[k] - p.a[k] * p.t;
-      const double e = fabs(v - preset_value(p.exact, x, p.d));
+      const double ex = p.burgers ? exact_value(p.exact, x, p.d, p.t)
+                                  : preset_value(p.exact, x, p.d);
+      const double e = fabs(v - ex);
       acc[3] += e;
       acc[4] = fmax(acc[4], e);
     }

@@ -1901,12 +1901,15 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
                         sgwg_field_stats* out) {
   if (f == nullptr || out == nullptr) return fail_with(SGWG_EINVAL, "null argument");
   TRY(check_interp(mode, eps));
+  const bool burgers = f->has_model && f->model.kind == SGWG_BURGERS;
   if (exact_preset >= 0) {
-    if (!f->has_model || f->model.kind != SGWG_ADVECTION)
-      return fail_with(SGWG_EINVAL, "combined_stats: exact solutions need a linear advection model");
-    if (exact_preset != SGWG_IC_C1 && exact_preset != SGWG_IC_C3 && exact_preset != SGWG_IC_EX1 &&
-        exact_preset != SGWG_IC_EX2)
-      return fail_with(SGWG_EINVAL, "combined_stats: no exact solution for this preset");
+    const bool adv_ok = f->has_model && f->model.kind == SGWG_ADVECTION &&
+                        (exact_preset == SGWG_IC_C1 || exact_preset == SGWG_IC_C3 ||
+                         exact_preset == SGWG_IC_EX1 || exact_preset == SGWG_IC_EX2);
+    const bool bur_ok = burgers && ((exact_preset == SGWG_IC_C2 && f->d == 2) ||
+                                    exact_preset == SGWG_IC_EX3);
+    if (!adv_ok && !bur_ok)
+      return fail_with(SGWG_EINVAL, "combined_stats: no exact solution for this model and preset");
   }
   CK(cudaSetDevice(f->ctx->device));
   if (f->diag_scratch == nullptr)
@@ -1918,9 +1921,10 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
     sp.bc[k] = (f->dom.bc[k] == SGWG_PERIODIC) ? 0 : 1;
     sp.h[k] = f->fine_h[k];
     sp.lower[k] = f->dom.lower[k];
-    sp.a[k] = (exact_preset >= 0) ? f->model.speeds[k] : 0.0;
+    sp.a[k] = (exact_preset >= 0 && !burgers) ? f->model.speeds[k] : 0.0;
   }
   sp.exact = exact_preset;
+  sp.burgers = burgers ? 1 : 0;
   sp.t = t;
   sp.partial = f->diag_scratch;
   double mass = 0.0, mn = INFINITY, mx = -INFINITY, l1 = 0.0, linf = 0.0;

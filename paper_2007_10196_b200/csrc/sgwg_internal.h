@@ -221,7 +221,8 @@ struct StatsParams {       // k_diag.cu: diagnostics of a slab of the combined f
   int bc[kMaxD];
   double h[kMaxD];
   double lower[kMaxD];
-  int exact;               // preset of the exact solution (linear advection) or -1
+  int exact;               // preset of the exact solution or -1
+  int burgers;             // exact solution of the Burgers sine waves (else advection)
   double t;
   double a[kMaxD];         // advection speeds
   double* partial;         // stats_partial_doubles() scratch

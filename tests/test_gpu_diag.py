@@ -72,10 +72,13 @@ def test_error_norms_linear_advection(ctx, ctx_fast):
         assert st["l1"] < 1e-3
 
 
-def test_stats_exact_requires_advection(ctx):
-    cfg, fam = _evolved(ctx, "C2", 0.0, nl=3, root=[16, 16])
+def test_stats_exact_requires_a_known_solution(ctx):
+    cfg, fam = _evolved(ctx, "C2", 0.0, nl=3, root=[16, 16])  # Burgers
     with pytest.raises(ValueError):
-        fam.combined_stats(exact_preset=1)
+        fam.combined_stats(exact_preset=0)  # the advection preset
+    cfg, fam = _evolved(ctx, "C4", 0.0, nl=3, root=[16, 16])  # Vlasov-Poisson
+    with pytest.raises(ValueError):
+        fam.combined_stats(exact_preset=3)
 
 
 def test_stats_slabs_match_single_plan(ctx, monkeypatch):
