@@ -1626,8 +1626,10 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   const size_t persist_smem = ((size_t)f->smem2d_fast + 2 * 2048) * sizeof(double);
   if (arith_of(f) == SGWG_ARITH_FAST && f->d == 2 && f->ntiles2d_fast > 0 && dt_fusable(f) &&
       !f->ctx->profile && std::getenv("SGWG_NO_PERSIST") == nullptr) {
+    // one tile per CTA (tiles resident in shared memory across stages); larger
+    // families run faster as graph-captured stage launches (measured: S2)
     const int maxb = fast::persist2d_max_blocks(f->model.kind == SGWG_BURGERS, persist_smem);
-    persist_blocks = std::min(f->ntiles2d_fast, maxb);
+    persist_blocks = (f->ntiles2d_fast <= maxb) ? f->ntiles2d_fast : 0;
     const auto order = pass_order(f);
     Stage2DParams& p = pp.base;
     p.mem = f->dmem;
