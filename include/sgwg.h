@@ -43,8 +43,17 @@ enum {
 
 /* grid.hpp:14 BoundaryKind */
 enum { SGWG_PERIODIC = 0, SGWG_ZERO = 1 };
-/* models.hpp:19 ModelKind (+ the Vlasov-Poisson model of BASELINE C4/C5) */
-enum { SGWG_ADVECTION = 0, SGWG_BURGERS = 1, SGWG_VLASOV_BOLTZMANN = 2, SGWG_VLASOV_POISSON = 3 };
+/* models.hpp:19 ModelKind (+ the Vlasov-Poisson model of BASELINE C4/C5).
+ * SGWG_VLASOV_MAXWELL: the reduced (x2, xi1, xi2) system of models.hpp:376-527;
+ * a member's state is its distribution followed by the field lines E1, E2, B3
+ * over its x2 points (initialize_family, models.hpp:855-871). */
+enum {
+  SGWG_ADVECTION = 0,
+  SGWG_BURGERS = 1,
+  SGWG_VLASOV_BOLTZMANN = 2,
+  SGWG_VLASOV_POISSON = 3,
+  SGWG_VLASOV_MAXWELL = 4
+};
 /* weno.hpp:17 WenoMode */
 enum { SGWG_WENO_NONLINEAR = 0, SGWG_WENO_LINEAR = 1 };
 /* interp.hpp:16 InterpMode */
@@ -264,7 +273,8 @@ enum {
   SGWG_IC_EX3 = 6,  /* 1 + 0.5 sin(sum x)             models.hpp:647  */
   SGWG_IC_EX5A = 7, /* models.hpp:690-694, mass-normalised            */
   SGWG_IC_EX5B = 8, /* models.hpp:709-714, mass-normalised            */
-  SGWG_IC_EX2 = 9   /* 1 + 0.5 sin(x+y+z)             models.hpp:625  */
+  SGWG_IC_EX2 = 9,  /* 1 + 0.5 sin(x+y+z)             models.hpp:625  */
+  SGWG_IC_EX6 = 10  /* Vlasov-Maxwell two-stream + B3 = b sin(k0 x2), models.hpp:722-742 */
 };
 int sgwg_family_init_preset(sgwg_family* fam, int preset);
 /* General initial data: ic(x, d, user) evaluated on the host at every grid

@@ -26,7 +26,7 @@ ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libsgwref.so")
 
 PERIODIC, ZERO = 0, 1
-ADVECTION, BURGERS, VLASOV_BOLTZMANN, VLASOV_POISSON = 0, 1, 2, 3
+ADVECTION, BURGERS, VLASOV_BOLTZMANN, VLASOV_POISSON, VLASOV_MAXWELL = 0, 1, 2, 3, 4
 NONLINEAR, LINEAR = 0, 1
 LAGRANGE, WENO = 0, 1
 DT_CFL, DT_ACCURACY = 0, 1
@@ -297,6 +297,8 @@ class Reference(_Lib):
         L.sgwref_evolve_replay.restype = C.c_int
         L.sgwref_combine.argtypes = [C.POINTER(Domain), _DP, C.c_int, C.c_double, _DP, C.c_int]
         L.sgwref_combine.restype = C.c_int
+        L.sgwref_rhs.argtypes = [C.POINTER(Domain), _IP, C.POINTER(Model), _DP, _DP]
+        L.sgwref_rhs.restype = C.c_int
         L.sgwref_init_family.argtypes = [C.c_int, C.POINTER(Domain), C.POINTER(Model), _DP]
         L.sgwref_init_family.restype = C.c_int
         L.sgwref_time_prefix.argtypes = [C.POINTER(Domain), C.POINTER(Model), C.POINTER(Policy),
@@ -305,8 +307,10 @@ class Reference(_Lib):
         L.sgwref_time_prefix.restype = C.c_int
         self._o = Oracle()
 
-    def init_family(self, preset, dom, model):
-        s = np.zeros(self._o.total_points(dom))
+    def init_family(self, preset, dom, model, state_points=None):
+        """state_points: member-state doubles when they exceed the grid points
+        (Vlasov-Maxwell: + 3 field lines per member)."""
+        s = np.zeros(state_points or self._o.total_points(dom))
         if self.lib.sgwref_init_family(preset, C.byref(dom), C.byref(model), _dp(s)):
             raise ValueError("init_family failed")
         return s
@@ -341,6 +345,15 @@ class Reference(_Lib):
                                       tfinal, _dp(stops) if len(stops) else None, len(stops),
                                       _dp(dts), cap, C.byref(ns))
         return states, dts[:ns.value].copy()
+
+    def rhs(self, dom, level, model, state):
+        """FamilyModel::rhs of one member (state incl. any field lines)"""
+        level = np.ascontiguousarray(level, dtype=np.int32)
+        state = np.ascontiguousarray(state, dtype=np.float64)
+        out = np.zeros_like(state)
+        if self.lib.sgwref_rhs(C.byref(dom), _ip(level), C.byref(model), _dp(state), _dp(out)):
+            raise ValueError("rhs failed")
+        return out
 
     def combine(self, dom, states, mode=WENO, eps=1e-6, threads=1):
         states = np.ascontiguousarray(states, dtype=np.float64)

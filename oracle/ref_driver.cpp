@@ -75,6 +75,11 @@ ProblemSpec make_spec(const sgwo_domain* d, const sgwo_model* m, int preset) {
       p.kind = ModelKind::burgers;
       p.law = {ModelKind::burgers, {}};
       break;
+    case SGWO_VLASOV_MAXWELL:
+      p.kind = ModelKind::vlasov_maxwell;
+      p.vm = VlasovMaxwellSpec{};
+      p.init_b3 = make_example(ExampleId::ex6).problem.init_b3;
+      break;
     default:
       p.kind = ModelKind::vlasov_boltzmann;
       p.vb = VlasovBoltzmannSpec{m->space_dim, m->theta, m->tau};
@@ -93,6 +98,7 @@ ProblemSpec make_spec(const sgwo_domain* d, const sgwo_model* m, int preset) {
       p.initial = make_example(ExampleId::ex5b).problem.initial;
       p.normalize_initial_mass = true;
       break;
+    case SGWO_IC_EX6: p.initial = make_example(ExampleId::ex6).problem.initial; break;
     default: p.initial = [preset](std::span<const double> x) { return preset_value(preset, x); };
   }
   return p;
@@ -108,6 +114,14 @@ InterpMode interp_of(int mode) {
 
 CombinationSet family_of(const sgwo_domain* d) {
   return make_family(box_of(d), root_of(d), bc_of(d), d->nl);
+}
+// member states sized for the model (Vlasov-Maxwell: f + E1, E2, B3 lines)
+CombinationSet family_of(const sgwo_domain* d, const sgwo_model* m) {
+  CombinationSet set = family_of(d);
+  if (m->kind == SGWO_VLASOV_MAXWELL)
+    for (auto& mm : set.members)
+      mm.state.assign(mm.geom.total_points() + 3 * static_cast<std::size_t>(mm.geom.points[0]), 0.0);
+  return set;
 }
 
 void load_states(CombinationSet& set, const double* states) {
@@ -232,6 +246,11 @@ int sgwref_rhs(const sgwo_domain* dom, const int* level, const sgwo_model* m, co
       VlasovBoltzmannSpec vb{m->space_dim, m->theta, m->tau};
       auto ws = VbWorkspace::make(g, vb);
       vb_rhs_into(g, ws, s, vb, weno_of(m), 1, o);
+    } else if (m->kind == SGWO_VLASOV_MAXWELL) {
+      VlasovMaxwellSpec vm{};
+      auto ws = VmWorkspace::make(g, vm);
+      vm_rhs_into(g, ws, std::span<const double>(state, ws.state_size()), vm, weno_of(m), 1,
+                  std::span<double>(out, ws.state_size()));
     } else {
       return SGWO_EINVAL;  // Vlasov-Poisson has no reference implementation
     }
@@ -304,7 +323,7 @@ int sgwref_evolve(const sgwo_domain* dom, const sgwo_model* m, const sgwo_policy
                   sgwref_stop_cb cb, void* user, int threads, double* dts, long cap, long* nsteps,
                   int* fail_member, long* fail_step, int* fail_stage, double* seconds) {
   try {
-    CombinationSet set = family_of(dom);
+    CombinationSet set = family_of(dom, m);
     load_states(set, states);
     ProblemSpec spec = make_spec(dom, m, -1);
     FamilyModel model(spec, set, weno_of(m), threads);
@@ -355,7 +374,7 @@ int sgwref_evolve_replay(const sgwo_domain* dom, const sgwo_model* m, const sgwo
                          double* states, double tfinal, const double* stops, int nstops,
                          double* dts, long cap, long* nsteps) {
   try {
-    CombinationSet set = family_of(dom);
+    CombinationSet set = family_of(dom, m);
     load_states(set, states);
     ProblemSpec spec = make_spec(dom, m, -1);
     FamilyModel model(spec, set, weno_of(m), 1);

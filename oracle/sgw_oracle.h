@@ -31,7 +31,13 @@ extern "C" {
 #define SGWO_MAXD 4
 
 enum { SGWO_PERIODIC = 0, SGWO_ZERO = 1 };
-enum { SGWO_ADVECTION = 0, SGWO_BURGERS = 1, SGWO_VLASOV_BOLTZMANN = 2, SGWO_VLASOV_POISSON = 3 };
+enum {
+  SGWO_ADVECTION = 0,
+  SGWO_BURGERS = 1,
+  SGWO_VLASOV_BOLTZMANN = 2,
+  SGWO_VLASOV_POISSON = 3,
+  SGWO_VLASOV_MAXWELL = 4 /* reference only (oracle/ref_driver.cpp); no C restatement */
+};
 enum { SGWO_WENO_NONLINEAR = 0, SGWO_WENO_LINEAR = 1 };
 enum { SGWO_INTERP_LAGRANGE = 0, SGWO_INTERP_WENO = 1 };
 enum { SGWO_DT_CFL = 0, SGWO_DT_ACCURACY = 1 };
@@ -133,7 +139,8 @@ enum {
   SGWO_IC_EX3 = 6,    /* 1 + 0.5 sin(sum x) */
   SGWO_IC_EX5A = 7,   /* sin^2(x^2/2) exp(-(x^2+v^2)/2), normalized */
   SGWO_IC_EX5B = 8,   /* 4D VB, normalized */
-  SGWO_IC_EX2 = 9     /* 1 + 0.5 sin(x+y+z) */
+  SGWO_IC_EX2 = 9,    /* 1 + 0.5 sin(x+y+z) */
+  SGWO_IC_EX6 = 10    /* Vlasov-Maxwell ex6 (reference only) */
 };
 int sgwo_restrict_preset(int preset, const sgwo_domain* dom, const int* level, double* out);
 int sgwo_init_family(int preset, const sgwo_domain* dom, double* states);

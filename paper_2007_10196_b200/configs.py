@@ -9,14 +9,14 @@ SURVEY.md Appendix A.
 import math
 
 PERIODIC, ZERO = 0, 1
-ADVECTION, BURGERS, VLASOV_BOLTZMANN, VLASOV_POISSON = 0, 1, 2, 3
+ADVECTION, BURGERS, VLASOV_BOLTZMANN, VLASOV_POISSON, VLASOV_MAXWELL = 0, 1, 2, 3, 4
 NONLINEAR, LINEAR = 0, 1
 LAGRANGE, WENO = 0, 1
 DT_CFL, DT_ACCURACY = 0, 1
 
 # initial-condition presets (mirror oracle/sgw_oracle.h SGWO_IC_*; the same
 # ids are understood by the C-ABI's host-side sgwg_family_init_preset)
-IC_C1, IC_C2, IC_C3, IC_C4, IC_C5, IC_EX1, IC_EX3, IC_EX5A, IC_EX5B, IC_EX2 = range(10)
+IC_C1, IC_C2, IC_C3, IC_C4, IC_C5, IC_EX1, IC_EX3, IC_EX5A, IC_EX5B, IC_EX2, IC_EX6 = range(11)
 
 
 def _finest_h(cfg):
@@ -82,6 +82,11 @@ def config(name, **over):
                  kind=VLASOV_BOLTZMANN, speeds=[0.0] * 4, weno_mode=NONLINEAR, epsilon=1e-6,
                  dt_mode=DT_CFL, cfl=0.4, dt_scale=1.0, tfinal=3.0, stops=[0.5, 1.0],
                  interp=WENO, ic=IC_EX5B, space_dim=2, theta=1.0, tau=1.0)
+    elif name == "ex6":   # models.hpp:722-742: reduced Vlasov-Maxwell (x2, xi1, xi2), k0 = 0.2
+        c = dict(d=3, nl=3, lower=[0.0, -1.2, -1.2], upper=[2 * pi / 0.2, 1.2, 1.2],
+                 root=[10] * 3, bc=[PERIODIC, ZERO, ZERO], kind=VLASOV_MAXWELL, speeds=[0.0] * 3,
+                 weno_mode=NONLINEAR, epsilon=1e-6, dt_mode=DT_CFL, cfl=0.4, dt_scale=1.0,
+                 tfinal=10.0, stops=[10.0], interp=WENO, ic=IC_EX6, space_dim=1)
     elif name == "S2":    # large-problem stress case for the kernel roofline:
         # C2's physics on root 2048, N_L = 1 (3 members, 20.97M points per stage)
         c = dict(d=2, nl=1, lower=[0.0, 0.0], upper=[2.0, 2.0], root=[2048, 2048],

@@ -43,6 +43,16 @@ __device__ inline void device_local_speeds(const DtParams& p, double* sp) {
     for (int k = 0; k < p.d; ++k) sp[k] = umax;
   } else {
     for (int k = 0; k < p.d; ++k) sp[k] = p.const_speeds[k];
+    if (p.kind == 4) {  // Vlasov-Maxwell (models.hpp:816-836): s0 constant, s1, s2 per member
+      for (int j = 1; j <= 2; ++j) {
+        double e = 0.0;
+        for (int m = lane; m < p.nmembers; m += 32) {
+          const double a = __ldcg(p.vmspd + 2 * m + (j - 1));
+          e = (e < a) ? a : e;
+        }
+        sp[j] = warp_allmax(e);
+      }
+    }
     if (p.kind == 3) {  // Vlasov-Poisson: v-directions from the family max|E_j|
       for (int j = 0; j < p.space_dim; ++j) {
         double e = 0.0;

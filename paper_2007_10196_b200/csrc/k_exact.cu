@@ -55,6 +55,48 @@ cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* t
   return cudaGetLastError();
 }
 
+// family_wave_speeds, Vlasov-Maxwell branch (models.hpp:816-836), per member:
+// s1 = max |E1(x2) + xi2 B3(x2)|, s2 = max |E2(x2) - xi1 B3(x2)| over the
+// member's x2 points and velocity coordinates (max is exact in any order)
+__global__ void __launch_bounds__(256) vm_speeds_kernel(const VmParams p) {
+  if (p.ctl != nullptr && !p.ctl->active) return;
+  const MemberDesc* M = p.mem + blockIdx.x;
+  const int nx = M->nx, n1 = M->ext[1], n2 = M->ext[2];
+  const double* F = p.fin + M->xoff * 3;
+  double s1 = 0.0, s2 = 0.0;
+  for (int q = threadIdx.x; q < nx * n2; q += blockDim.x) {
+    const int ix = q / n2, i2 = q % n2;
+    const double xi2 = __dadd_rn(M->lower[2], __dmul_rn((double)i2, M->h[2]));
+    const double v = fabs(__dadd_rn(F[ix], __dmul_rn(xi2, F[2 * nx + ix])));
+    s1 = (s1 < v) ? v : s1;
+  }
+  for (int q = threadIdx.x; q < nx * n1; q += blockDim.x) {
+    const int ix = q / n1, i1 = q % n1;
+    const double xi1 = __dadd_rn(M->lower[1], __dmul_rn((double)i1, M->h[1]));
+    const double v = fabs(__dsub_rn(F[nx + ix], __dmul_rn(xi1, F[2 * nx + ix])));
+    s2 = (s2 < v) ? v : s2;
+  }
+  s1 = warp_allmax(s1);
+  s2 = warp_allmax(s2);
+  __shared__ double r[2][8];
+  if ((threadIdx.x & 31) == 0) {
+    r[0][threadIdx.x >> 5] = s1;
+    r[1][threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = (m < r[threadIdx.x][w]) ? r[threadIdx.x][w] : m;
+    p.speeds[2 * blockIdx.x + threadIdx.x] = m;
+  }
+}
+
+cudaError_t launch_vm_speeds(const VmParams& p, int nmembers, cudaStream_t s) {
+  if (nmembers <= 0) return cudaSuccess;
+  vm_speeds_kernel<<<nmembers, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 // DFMA throughput probe: 8 independent FMA chains per thread.
 __global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters) {
   double a[8];

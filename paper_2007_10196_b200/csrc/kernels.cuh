@@ -155,6 +155,18 @@ __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) 
       const int comp = k - p.space_dim;
       const long long xi = base / M->vn;
       c = -p.efield[M->xoff * p.space_dim + (long long)comp * M->nx + xi];
+    } else if (p.flux >= kFluxVM0) {  // Vlasov-Maxwell (models.hpp:456-480)
+      const int ix = (int)(base / M->stride[0]);
+      const int i1 = (int)((base / M->stride[1]) % M->ext[1]);
+      const int i2 = (int)(base % M->ext[2]);
+      const double* F = p.efield + M->xoff * 3;  // E1, E2, B3 of the stage input
+      const double xi1 = M->lower[1] + i1 * M->h[1], xi2 = M->lower[2] + i2 * M->h[2];
+      if (p.flux == kFluxVM0)
+        c = xi2;
+      else if (p.flux == kFluxVM1)
+        c = F[ix] + xi2 * F[2 * M->nx + ix];
+      else
+        c = F[M->nx + ix] - xi1 * F[2 * M->nx + ix];
     }
     scoef[tid] = c;
   }
@@ -1769,6 +1781,113 @@ __global__ void __launch_bounds__(256) final_kernel(const FinalParams p) {
     }
     p.out[q] = acc;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Vlasov-Maxwell field lines (vm_rhs_into, models.hpp:437-505 + SspRk3::step)
+// ---------------------------------------------------------------------------
+// One CTA per member.  Currents j1, j2 = sum_q w_j1/2[q] f(x2, q) over the
+// velocity block in the reference's order (vm_currents, models.hpp:420-433;
+// block_weights 238-257), the characteristic variables w+- = E1 +- B3 and their
+// upwind WENO derivatives along the periodic x2 line (advect_derivative_line,
+// weno.hpp:160-192) with speeds -1 / +1, the tendencies
+//   E1' = (tp + tm)/2, B3' = (tp - tm)/2, E2' = -j2, tp/m = -dw+-/dx2 - j1,
+// and the RK stage update of the three lines (timestep.hpp:93,98,103).
+// Dynamic smem: 4 * nx doubles.
+__device__ __forceinline__ double vm_fhat(const double* w, int n, int k, double c, double eps,
+                                          int linear) {
+  // fhat[k] of advect_derivative_line on the periodic line c*w (padded fp[j+3] = c*w[j mod n])
+  auto fp = [&](int j) {
+    int q = j % n;
+    if (q < 0) q += n;
+    return c * w[q];
+  };
+  if (c < 0.0)  // flux_neg5(&fp[k+2]): positive reconstruction of fp[k+6..k+2]
+    return recon(fp(k + 3), fp(k + 2), fp(k + 1), fp(k), fp(k - 1), eps, linear);
+  return recon(fp(k - 2), fp(k - 1), fp(k), fp(k + 1), fp(k + 2), eps, linear);
+}
+
+__global__ void __launch_bounds__(256) vm_fields_kernel(const VmParams p) {
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  const int mi = blockIdx.x;
+  const MemberDesc* M = p.mem + mi;
+  const int nx = M->nx, n1 = M->ext[1], n2 = M->ext[2], vn = M->vn;
+  extern __shared__ double vsm[];
+  double* wp = vsm;
+  double* wm = wp + nx;
+  double* j1 = wm + nx;
+  double* j2 = j1 + nx;
+  const double* F = p.fin + M->xoff * 3;
+  for (int ix = threadIdx.x; ix < nx; ix += blockDim.x) {
+    const double* block = p.f + M->offset + (long long)ix * vn;
+    double a = 0.0, b = 0.0;
+    for (int i1 = 0; i1 < n1; ++i1) {
+      const double xi1 = M->lower[1] + i1 * M->h[1];
+      double w1 = M->h[1];
+      if (M->bc[1] != 0 && (i1 == 0 || i1 == n1 - 1)) w1 *= 0.5;  // trapezoid_weights_1d
+      for (int i2 = 0; i2 < n2; ++i2) {
+        const double xi2 = M->lower[2] + i2 * M->h[2];
+        double w2 = M->h[2];
+        if (M->bc[2] != 0 && (i2 == 0 || i2 == n2 - 1)) w2 *= 0.5;
+        double wq = 1.0;  // block_weights: p = 1; p *= w_1; p *= w_2
+        wq *= w1;
+        wq *= w2;
+        const double v = block[i1 * n2 + i2];
+        a += (wq * xi1) * v;
+        b += (wq * xi2) * v;
+      }
+    }
+    j1[ix] = a;
+    j2[ix] = b;
+    wp[ix] = F[ix] + F[2 * nx + ix];
+    wm[ix] = F[ix] - F[2 * nx + ix];
+  }
+  __syncthreads();
+  const double hx = M->h[0];
+  const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
+  const double* U = p.fun + M->xoff * 3;
+  double* O = p.fout + M->xoff * 3;
+  for (int ix = threadIdx.x; ix < nx; ix += blockDim.x) {
+    const int im = (ix + nx - 1) % nx;
+    const double dwp = (vm_fhat(wp, nx, ix, -1.0, p.eps, p.linear) -
+                        vm_fhat(wp, nx, im, -1.0, p.eps, p.linear)) / hx;
+    const double dwm = (vm_fhat(wm, nx, ix, +1.0, p.eps, p.linear) -
+                        vm_fhat(wm, nx, im, +1.0, p.eps, p.linear)) / hx;
+    const double tp = -dwp - j1[ix];
+    const double tm = -dwm - j1[ix];
+    double k3[3];
+    k3[0] = 0.5 * (tp + tm);  // E1
+    k3[1] = -j2[ix];          // E2
+    k3[2] = 0.5 * (tp - tm);  // B3
+    for (int c = 0; c < 3; ++c) {
+      const double kv = k3[c];
+      double o;
+      if (p.stage == 0) {
+        o = kv;
+      } else {
+        if (!isfinite(kv)) {
+          const unsigned long long code =
+              (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
+          atomicMin(p.fail + mi, code);
+        }
+        const double ui = F[c * nx + ix];
+        if (p.stage == 1)
+          o = ui + dt * kv;
+        else if (p.stage == 2)
+          o = 0.75 * U[c * nx + ix] + 0.25 * (ui + dt * kv);
+        else
+          o = (1.0 / 3.0) * U[c * nx + ix] + (2.0 / 3.0) * (ui + dt * kv);
+      }
+      O[c * nx + ix] = o;
+    }
+  }
+}
+
+cudaError_t launch_vm_fields(const VmParams& p, int nmembers, int smem, cudaStream_t s) {
+  if (nmembers <= 0) return cudaSuccess;
+  vm_fields_kernel<<<nmembers, 256, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t configure() {

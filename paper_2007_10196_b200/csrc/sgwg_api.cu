@@ -160,7 +160,8 @@ struct sgwg_family {
   std::vector<std::array<int, 4>> levels;
   std::vector<MemberDesc> hmem;
   MemberDesc* dmem = nullptr;
-  long long total = 0;
+  long long total = 0;        // distribution points of the local members
+  long long state_total = 0;  // member state doubles (Vlasov-Maxwell: + 3 field lines each)
   long long finest = 0;
   int fine_ext[kMaxD] = {1, 1, 1, 1};
   double fine_h[kMaxD] = {0, 0, 0, 0};
@@ -181,6 +182,8 @@ struct sgwg_family {
   bool has_model = false;
   // Vlasov-Poisson
   double *rho = nullptr, *E = nullptr, *emax = nullptr;
+  // Vlasov-Maxwell field lines (E1, E2, B3 per member) of u^n / stage A / stage B
+  double *Fu = nullptr, *FA = nullptr, *FB = nullptr, *vmspd = nullptr;
   long long nx_total = 0;
   int2* dmtasks = nullptr;  // moment kernel work list
   int nmtasks = 0;
@@ -253,6 +256,10 @@ std::vector<PassDesc> pass_order(const sgwg_family* f) {
     for (int k = 0; k < f->d; ++k)
       v.push_back({k, m.kind == SGWG_BURGERS ? (int)kFluxBurgers : (int)kFluxAdvect,
                    m.kind == SGWG_ADVECTION ? m.speeds[k] : 0.0});
+  } else if (m.kind == SGWG_VLASOV_MAXWELL) {  // vm_rhs_into: x2, xi1, xi2 (models.hpp:455-480)
+    v.push_back({0, (int)kFluxVM0, 0.0});
+    v.push_back({1, (int)kFluxVM1, 0.0});
+    v.push_back({2, (int)kFluxVM2, 0.0});
   } else {  // vb_rhs_into order: x_0, v_0, x_1, v_1 (models.hpp:339-350)
     const int dx = m.space_dim;
     for (int j = 0; j < dx; ++j) {
@@ -328,6 +335,13 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
   return SGWG_OK;
 }
 
+// Vlasov-Maxwell field lines belonging to a distribution buffer
+double* fields_of(const sgwg_family* f, const double* state) {
+  if (state == f->A) return f->FA;
+  if (state == f->B) return f->FB;
+  return f->Fu;
+}
+
 // One RK stage (stage 1..3) or a bare tendency evaluation (stage 0).
 // fuse_dt: the stage-3 kernel also computes the next step's dt (last CTA).
 int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool with_field = true,
@@ -342,6 +356,26 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
   unsigned long long* zero_slot =
       (burgers && stage > 0) ? f->amax + (size_t)((stage + 1) % 3) * f->nm : nullptr;
   const DtParams* dtp = (fuse_dt && stage == 3) ? f->d_dtp : nullptr;
+  const bool vm = (m.kind == SGWG_VLASOV_MAXWELL);
+  if (vm) {  // field lines: currents, characteristic WENO derivatives, RK stage
+    VmParams vp{};
+    vp.mem = f->dmem;
+    vp.f = b.uin;
+    vp.fin = fields_of(f, b.uin);
+    vp.fun = f->Fu;
+    vp.fout = fields_of(f, b.out);
+    vp.stage = stage;
+    vp.linear = (m.weno_mode == SGWG_WENO_LINEAR);
+    vp.eps = m.epsilon;
+    vp.ctl = f->ctl;
+    vp.fail = f->fail;
+    int nxmax = 1;
+    for (const auto& M : f->hmem) nxmax = std::max(nxmax, M.nx);
+    const int smem = 4 * nxmax * (int)sizeof(double);
+    CK(arith_of(f) == SGWG_ARITH_FAST ? fast::launch_vm_fields(vp, f->nm, smem, f->ctx->stream)
+                                       : exact::launch_vm_fields(vp, f->nm, smem, f->ctx->stream));
+    f->stats.kernel_launches++;
+  }
   // every path below but the plane path writes a state without its rho partials
   if (stage > 0 && !plane_path(f)) f->parts_of = nullptr;
   if (plane_path(f)) {  // fast 4D: dims (0,1) -> K, dims (2,3) + RK stage
@@ -480,7 +514,7 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     p.un = b.un;
     p.out = b.out;
     p.kbuf = f->K;
-    p.efield = f->E;
+    p.efield = vm ? fields_of(f, b.uin) : f->E;
     p.ctl = f->ctl;
     p.amax_in = f->amax + (size_t)in_slot * f->nm;
     p.amax_out = f->amax + (size_t)out_slot * f->nm;
@@ -515,7 +549,8 @@ int launch_member_max_slot0(sgwg_family* f) {
 // dt of the next step can be fused into the stage-3 kernel when nothing has to
 // happen between the end of a step and the dt (no field solve, no all-reduce)
 bool dt_fusable(const sgwg_family* f) {
-  return f->comm == nullptr && f->model.kind != SGWG_VLASOV_POISSON;
+  return f->comm == nullptr && f->model.kind != SGWG_VLASOV_POISSON &&
+         f->model.kind != SGWG_VLASOV_MAXWELL;
 }
 
 // the (unfused) dt of a step: speeds (+ NCCL all-reduce(max)), dt kernel
@@ -541,6 +576,15 @@ int launch_step(sgwg_family* f, bool timed) {
   const bool fused = dt_fusable(f);
   if (!fused) {
     if (vp) TRY(launch_field_for(f, f->u, 1, /*with_energy=*/true));
+    if (f->model.kind == SGWG_VLASOV_MAXWELL) {  // family_wave_speeds of u^n
+      VmParams sp{};
+      sp.mem = f->dmem;
+      sp.fin = f->Fu;
+      sp.ctl = f->ctl;
+      sp.speeds = f->vmspd;
+      CK(launch_vm_speeds(sp, f->nm, f->ctx->stream));
+      f->stats.kernel_launches++;
+    }
     TRY(launch_dt_step(f));
   }
   // stage 1: u -> A; stage 2: (A, u) -> B; stage 3: (B, u) -> u (timestep.hpp:91-103)
@@ -758,6 +802,7 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
     off += M.npts;
   }
   f->total = off;
+  f->state_total = off;
   f->no_fused2d = std::getenv("SGWG_NO_FUSED2D") != nullptr;
   CK(cudaEventCreate(&f->ev0));
   CK(cudaEventCreate(&f->ev1));
@@ -882,6 +927,34 @@ int setup_vp(sgwg_family* f) {
   return SGWG_OK;
 }
 
+// Vlasov-Maxwell: per member nx = x2 points, the (xi1, xi2) block, the packed
+// offset of its field lines; the member state is f followed by E1, E2, B3
+// (initialize_family, models.hpp:855-871).
+int setup_vm(sgwg_family* f) {
+  long long xoff = 0;
+  for (auto& M : f->hmem) {
+    M.nx = M.ext[0];
+    M.vn = M.ext[1] * M.ext[2];
+    M.xext[0] = M.ext[0];
+    M.xext[1] = 1;
+    M.xoff = xoff;
+    M.rparts = 1;
+    xoff += M.nx;
+  }
+  CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
+  for (double** b : {&f->Fu, &f->FA, &f->FB}) {
+    cudaFree(*b);
+    *b = nullptr;
+    CK(cudaMalloc(b, sizeof(double) * std::max<long long>(1, 3 * xoff)));
+    CK(cudaMemset(*b, 0, sizeof(double) * std::max<long long>(1, 3 * xoff)));
+  }
+  cudaFree(f->vmspd);
+  f->vmspd = nullptr;
+  CK(cudaMalloc(&f->vmspd, sizeof(double) * 2 * std::max(1, f->nm)));
+  f->state_total = f->total + 3 * xoff;
+  return SGWG_OK;
+}
+
 // Fast 4D plane tiles (kernels.cuh plane_fast_kernel).  Pair pr covers the
 // planes of dims (2pr, 2pr+1); a tile holds nv consecutive planes (>= 4 for
 // pr = 0, whose planes interleave in memory, so loads use whole sectors), split
@@ -998,6 +1071,7 @@ int launches_per_step(const sgwg_family* f) {
                                                              : (int)pass_order(f).size();
   int n = 3 * np;
   if (!dt_fusable(f)) n += 1;
+  if (f->model.kind == SGWG_VLASOV_MAXWELL) n += 3 + 1;  // field lines per stage, speeds
   if (f->model.kind == SGWG_VLASOV_POISSON) {  // (moment +) field per stage, energy per step
     const long long fine_x = (long long)f->fine_ext[0] *
                              ((f->model.space_dim == 2) ? f->fine_ext[1] : 1);
@@ -1396,6 +1470,10 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dptiles[0]);
   cudaFree(f->dptiles[1]);
   cudaFree(f->rho_parts);
+  cudaFree(f->Fu);
+  cudaFree(f->FA);
+  cudaFree(f->FB);
+  cudaFree(f->vmspd);
   cudaFree(f->degrp);
   cudaFree(f->degrp_m);
   cudaFree(f->degrp_mem);
@@ -1437,51 +1515,86 @@ int sgwg_family_member(const sgwg_family* f, int mi, int* global_index, int* lev
 
 int sgwg_family_sizes(const sgwg_family* f, size_t* member_points, size_t* finest_points) {
   if (f == nullptr) return fail_with(SGWG_EINVAL, "null family");
-  if (member_points) *member_points = (size_t)f->total;
+  if (member_points) *member_points = (size_t)f->state_total;
   if (finest_points) *finest_points = (size_t)f->finest;
   return SGWG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// member states <-> device buffers: one copy, or (Vlasov-Maxwell) the
+// distribution and the field lines of every member separately
+int copy_states(sgwg_family* f, double* host_or_dev, bool to_device, cudaMemcpyKind kind,
+                double* dist = nullptr, double* fields = nullptr) {
+  cudaStream_t s = f->ctx->stream;
+  if (dist == nullptr) dist = f->u;
+  if (fields == nullptr) fields = f->Fu;
+  if (f->state_total == f->total) {
+    if (to_device)
+      CK(cudaMemcpyAsync(dist, host_or_dev, sizeof(double) * f->total, kind, s));
+    else
+      CK(cudaMemcpyAsync(host_or_dev, dist, sizeof(double) * f->total, kind, s));
+  } else {
+    long long so = 0;
+    for (const auto& M : f->hmem) {
+      double* a = host_or_dev + so;
+      double* b = host_or_dev + so + M.npts;
+      if (to_device) {
+        CK(cudaMemcpyAsync(dist + M.offset, a, sizeof(double) * M.npts, kind, s));
+        CK(cudaMemcpyAsync(fields + 3 * M.xoff, b, sizeof(double) * 3 * M.nx, kind, s));
+      } else {
+        CK(cudaMemcpyAsync(a, dist + M.offset, sizeof(double) * M.npts, kind, s));
+        CK(cudaMemcpyAsync(b, fields + 3 * M.xoff, sizeof(double) * 3 * M.nx, kind, s));
+      }
+      so += M.npts + 3 * M.nx;
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  return SGWG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int sgwg_family_upload(sgwg_family* f, const double* host, size_t n) {
-  if (f == nullptr || host == nullptr || n != (size_t)f->total)
-    return fail_with(SGWG_EINVAL, "upload: size must equal the packed member points");
+  if (f == nullptr || host == nullptr || n != (size_t)f->state_total)
+    return fail_with(SGWG_EINVAL, "upload: size must equal the packed member states");
   CK(cudaSetDevice(f->ctx->device));
   f->parts_of = nullptr;
-  CK(cudaMemcpyAsync(f->u, host, sizeof(double) * n, cudaMemcpyHostToDevice, f->ctx->stream));
-  CK(cudaStreamSynchronize(f->ctx->stream));
-  return SGWG_OK;
+  return copy_states(f, const_cast<double*>(host), true, cudaMemcpyHostToDevice);
 }
 
 int sgwg_family_download(sgwg_family* f, double* host, size_t n) {
-  if (f == nullptr || host == nullptr || n != (size_t)f->total)
-    return fail_with(SGWG_EINVAL, "download: size must equal the packed member points");
+  if (f == nullptr || host == nullptr || n != (size_t)f->state_total)
+    return fail_with(SGWG_EINVAL, "download: size must equal the packed member states");
   CK(cudaSetDevice(f->ctx->device));
-  CK(cudaMemcpyAsync(host, f->u, sizeof(double) * n, cudaMemcpyDeviceToHost, f->ctx->stream));
-  CK(cudaStreamSynchronize(f->ctx->stream));
-  return SGWG_OK;
+  return copy_states(f, host, false, cudaMemcpyDeviceToHost);
 }
 
 int sgwg_family_upload_device(sgwg_family* f, const double* dev, size_t n) {
-  if (f == nullptr || dev == nullptr || n != (size_t)f->total)
-    return fail_with(SGWG_EINVAL, "upload: size must equal the packed member points");
+  if (f == nullptr || dev == nullptr || n != (size_t)f->state_total)
+    return fail_with(SGWG_EINVAL, "upload: size must equal the packed member states");
   f->parts_of = nullptr;
-  CK(cudaMemcpyAsync(f->u, dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, f->ctx->stream));
-  CK(cudaStreamSynchronize(f->ctx->stream));
-  return SGWG_OK;
+  return copy_states(f, const_cast<double*>(dev), true, cudaMemcpyDeviceToDevice);
 }
 
 int sgwg_family_download_device(sgwg_family* f, double* dev, size_t n) {
-  if (f == nullptr || dev == nullptr || n != (size_t)f->total)
-    return fail_with(SGWG_EINVAL, "download: size must equal the packed member points");
-  CK(cudaMemcpyAsync(dev, f->u, sizeof(double) * n, cudaMemcpyDeviceToDevice, f->ctx->stream));
-  CK(cudaStreamSynchronize(f->ctx->stream));
-  return SGWG_OK;
+  if (f == nullptr || dev == nullptr || n != (size_t)f->state_total)
+    return fail_with(SGWG_EINVAL, "download: size must equal the packed member states");
+  return copy_states(f, dev, false, cudaMemcpyDeviceToDevice);
 }
 
 int sgwg_set_model(sgwg_family* f, const sgwg_model* m) {
   if (f == nullptr || m == nullptr) return fail_with(SGWG_EINVAL, "null argument");
-  if (m->kind < SGWG_ADVECTION || m->kind > SGWG_VLASOV_POISSON)
+  if (m->kind < SGWG_ADVECTION || m->kind > SGWG_VLASOV_MAXWELL)
     return fail_with(SGWG_EINVAL, "unknown model kind");
+  if (m->kind == SGWG_VLASOV_MAXWELL &&
+      (f->d != 3 || f->dom.bc[0] != SGWG_PERIODIC || f->dom.bc[1] != SGWG_ZERO ||
+       f->dom.bc[2] != SGWG_ZERO))  // VmWorkspace::make (models.hpp:389-393)
+    return fail_with(SGWG_EINVAL, "VmWorkspace: need rank 3, periodic x2 and zero xi boundaries");
   if (m->kind == SGWG_VLASOV_BOLTZMANN)
     return fail_with(SGWG_EUNSUPPORTED,
                      "Vlasov-Boltzmann relaxation is outside the B200 hot path (SURVEY 2.1)");
@@ -1494,6 +1607,7 @@ int sgwg_set_model(sgwg_family* f, const sgwg_model* m) {
   f->model = *m;
   f->has_model = true;
   if (m->kind == SGWG_VLASOV_POISSON) TRY(setup_vp(f));
+  if (m->kind == SGWG_VLASOV_MAXWELL) TRY(setup_vm(f));
   TRY(build_plane_tiles(f));
   clear_graphs(f);
   return SGWG_OK;
@@ -1561,6 +1675,15 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   for (int k = 0; k < f->d; ++k) dp.fine_h[k] = f->fine_h[k];
   if (f->model.kind == SGWG_ADVECTION) {
     for (int k = 0; k < f->d; ++k) dp.const_speeds[k] = std::abs(f->model.speeds[k]);
+  } else if (f->model.kind == SGWG_VLASOV_MAXWELL) {
+    // s0 = max(1, max|xi2|) over the members (models.hpp:825-826)
+    double s0 = 0.0;
+    for (const auto& M : f->hmem) {
+      double m0 = 1.0;
+      for (int i = 0; i < M.ext[2]; ++i) m0 = std::max(m0, std::abs(M.lower[2] + i * M.h[2]));
+      s0 = std::max(s0, m0);
+    }
+    dp.const_speeds[0] = s0;
   } else if (f->model.kind == SGWG_VLASOV_POISSON) {
     const int dx = f->model.space_dim;
     for (int j = 0; j < dx; ++j)
@@ -1571,6 +1694,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   dp.space_dim = f->model.space_dim;
   dp.amax = f->amax;
   dp.emax = f->emax;
+  dp.vmspd = f->vmspd;
   dp.nmembers = f->nm;
   dp.fail = f->fail;
   // dt record buffer
@@ -1820,8 +1944,8 @@ int sgwg_time_stage(sgwg_family* f, int reps, double* avg_ms, double* flops, dou
 }
 
 int sgwg_rhs(sgwg_family* f, double* out, size_t n, int out_is_device) {
-  if (f == nullptr || out == nullptr || n != (size_t)f->total)
-    return fail_with(SGWG_EINVAL, "rhs: size must equal the packed member points");
+  if (f == nullptr || out == nullptr || n != (size_t)f->state_total)
+    return fail_with(SGWG_EINVAL, "rhs: size must equal the packed member states");
   TRY(require_model(f));
   CK(cudaSetDevice(f->ctx->device));
   cudaStream_t s = f->ctx->stream;
@@ -1831,6 +1955,9 @@ int sgwg_rhs(sgwg_family* f, double* out, size_t n, int out_is_device) {
   if (f->model.kind == SGWG_BURGERS) TRY(launch_member_max_slot0(f));
   StageBufs b{f->u, f->u, f->A};
   TRY(launch_stage(f, 0, b, false));
+  if (f->state_total != f->total)  // Vlasov-Maxwell: tendency of f and of the field lines
+    return copy_states(f, out, false, out_is_device ? cudaMemcpyDeviceToDevice
+                                                    : cudaMemcpyDeviceToHost, f->A, f->FA);
   return copy_out(f, f->A, out, n, out_is_device);
 }
 
@@ -2187,17 +2314,39 @@ static double preset_value(int preset, const double* x, int d) {
 struct PresetIc {
   int preset;
 };
+// ex6 (models.hpp:722-742), VlasovMaxwellSpec defaults (models.hpp:43-50)
+static int g_ex6_marker = 0;
+static double ex6_f(const double* x, int, void*) {
+  const double pi = 3.14159265358979323846;  // std::numbers::pi
+  const double beta = 0.01, delta = 0.5, v01 = 0.3, v02 = 0.3;
+  const double xi1 = x[1], xi2 = x[2];
+  const double g1 = delta * std::exp(-(xi1 - v01) * (xi1 - v01) / beta);
+  const double g2 = (1.0 - delta) * std::exp(-(xi1 + v02) * (xi1 + v02) / beta);
+  return std::exp(-xi2 * xi2 / beta) * (g1 + g2) / (pi * beta);
+}
+static double ex6_b3(double x2) { return 0.001 * std::sin(0.2 * x2); }
 static double preset_cb(const double* x, int d, void* user) {
   return preset_value(static_cast<PresetIc*>(user)->preset, x, d);
 }
 
 int sgwg_family_init_fn(sgwg_family* f, sgwg_ic_fn ic, void* user, int normalize_mass) {
   if (f == nullptr || ic == nullptr) return fail_with(SGWG_EINVAL, "null argument");
-  std::vector<double> host((size_t)std::max<long long>(1, f->total));
+  std::vector<double> host((size_t)std::max<long long>(1, f->state_total));
   const int d = f->d;
+  const bool vm = f->state_total != f->total;
+  long long so = 0;
   for (int mi = 0; mi < f->nm; ++mi) {
     const MemberDesc& M = f->hmem[mi];
-    double* out = host.data() + M.offset;
+    double* out = host.data() + (vm ? so : M.offset);
+    if (vm) {  // field lines: E1 = E2 = 0, B3 = init_b3(x2) (initialize_family, models.hpp:861-867)
+      so += M.npts + 3 * M.nx;
+      for (int i = 0; i < M.nx; ++i) {
+        out[M.npts + i] = 0.0;
+        out[M.npts + M.nx + i] = 0.0;
+        const double x2 = M.lower[0] + i * M.h[0];
+        out[M.npts + 2 * M.nx + i] = (user == &g_ex6_marker) ? ex6_b3(x2) : 0.0;
+      }
+    }
     int idx[kMaxD] = {0, 0, 0, 0};
     double x[kMaxD];
     for (int k = 0; k < d; ++k) x[k] = M.lower[k];
@@ -2235,11 +2384,16 @@ int sgwg_family_init_fn(sgwg_family* f, sgwg_ic_fn ic, void* user, int normalize
       for (long long lin = 0; lin < M.npts; ++lin) out[lin] /= sum;
     }
   }
-  return sgwg_family_upload(f, host.data(), (size_t)f->total);
+  return sgwg_family_upload(f, host.data(), (size_t)f->state_total);
 }
 
 int sgwg_family_init_preset(sgwg_family* f, int preset) {
-  if (preset < SGWG_IC_C1 || preset > SGWG_IC_EX2) return fail_with(SGWG_EINVAL, "unknown preset");
+  if (preset < SGWG_IC_C1 || preset > SGWG_IC_EX6) return fail_with(SGWG_EINVAL, "unknown preset");
+  if (preset == SGWG_IC_EX6) {
+    if (f == nullptr || !f->has_model || f->model.kind != SGWG_VLASOV_MAXWELL)
+      return fail_with(SGWG_EINVAL, "init_preset: ex6 needs a Vlasov-Maxwell model");
+    return sgwg_family_init_fn(f, ex6_f, &g_ex6_marker, 0);
+  }
   PresetIc p{preset};
   const int norm = (preset == SGWG_IC_EX5A || preset == SGWG_IC_EX5B) ? 1 : 0;
   return sgwg_family_init_fn(f, preset_cb, &p, norm);

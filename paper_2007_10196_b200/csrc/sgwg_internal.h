@@ -20,7 +20,10 @@ enum FluxKind : int {
   kFluxBurgers = 1,  // 0.5 u^2 with Lax-Friedrichs split, alpha = max|u| of the member
   kFluxKinX = 2,     // kinetic x_j line: c = v_j coordinate      (models.hpp:341-344)
   kFluxKinVB = 3,    // kinetic v_j line: c = -x_j coordinate     (models.hpp:346-349)
-  kFluxKinVP = 4     // kinetic v_j line: c = -E_j(x) (Vlasov-Poisson, new physics)
+  kFluxKinVP = 4,    // kinetic v_j line: c = -E_j(x) (Vlasov-Poisson, new physics)
+  kFluxVM0 = 5,      // Vlasov-Maxwell x2 line: c = xi2               (models.hpp:456-460)
+  kFluxVM1 = 6,      // Vlasov-Maxwell xi1 line: c = E1(x2) + xi2 B3(x2) (models.hpp:461-470)
+  kFluxVM2 = 7       // Vlasov-Maxwell xi2 line: c = E2(x2) - xi1 B3(x2) (models.hpp:471-480)
 };
 
 // One component grid on the device (GridGeometry, grid.hpp:85-136).
@@ -164,6 +167,22 @@ struct PlaneParams {
   unsigned int* counter;
 };
 
+// Vlasov-Maxwell field lines (vm_rhs_into, models.hpp:437-505): per member the
+// packed fields F[3*xoff ...] = (E1[nx], E2[nx], B3[nx]) over its x2 points.
+struct VmParams {
+  const MemberDesc* mem;
+  const double* f;         // stage input distribution (packed)
+  const double* fin;       // stage input fields
+  const double* fun;       // u^n fields (stages 2, 3)
+  double* fout;            // stage output fields (stage 0: field tendencies)
+  int stage;
+  int linear;
+  double eps;
+  const StepCtl* ctl;
+  unsigned long long* fail;
+  double* speeds;          // vm_speeds: per member (s1, s2) of family_wave_speeds
+};
+
 struct UpsampleParams {
   const MemberDesc* mem;
   const int2* tasks;       // (member-slot, first output index of the chunk)
@@ -261,6 +280,7 @@ struct FieldParams {
   cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s);      \
   cudaError_t launch_final(const FinalParams& p, cudaStream_t s);                         \
   cudaError_t launch_eval_points(const EvalParams& p, cudaStream_t s);                    \
+  cudaError_t launch_vm_fields(const VmParams& p, int nmembers, int smem, cudaStream_t s);    \
   }
 SGWG_DECLARE_LAUNCHERS(exact)
 SGWG_DECLARE_LAUNCHERS(fast)
@@ -285,6 +305,7 @@ struct DtParams {
   int space_dim;
   const unsigned long long* amax;  // Burgers: per member max|u^n| (slot 0)
   const double* emax;              // VP: per member max|E_j|
+  const double* vmspd;             // Vlasov-Maxwell: per member (s1, s2)
   int nmembers;
   const unsigned long long* fail;
   double* dts;
@@ -300,6 +321,7 @@ cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, c
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
                                 double hvol, double* out_base, long long cap, cudaStream_t s);
 cudaError_t launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t s);
+cudaError_t launch_vm_speeds(const VmParams& p, int nmembers, cudaStream_t s);
 int stats_partial_doubles();
 cudaError_t launch_stats(const StatsParams& p, double* out5, cudaStream_t s);
 

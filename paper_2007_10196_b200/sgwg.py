@@ -307,6 +307,10 @@ class Family:
         m.space_dim, m.theta, m.tau = space_dim, theta, tau
         _check(load().sgwg_set_model(self.h, C.byref(m)))
         self.model = m
+        # member states may carry model state (Vlasov-Maxwell field lines)
+        mp, fp = C.c_size_t(0), C.c_size_t(0)
+        _check(load().sgwg_family_sizes(self.h, C.byref(mp), C.byref(fp)))
+        self.total_points = mp.value
 
     def set_comm(self, unique_id: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(bytes(unique_id), 128)
