@@ -24,6 +24,7 @@ for w in range(4):
     t = t[ok]
     d = np.diff(t, axis=1)
     per = t[1:, 0] - t[:-1, 0]
+    wait = t[1:, 0] - t[:-1, 4]
     print(f"cta{w}: stage {np.median(per):8.0f} cyc | staging {np.median(d[:,0]):6.0f} "
           f"sweep {np.median(d[:,1]):6.0f} epilogue {np.median(d[:,2]):6.0f} "
-          f"barrier {np.median(d[:,3]):6.0f} | n={len(t)}")
+          f"barrier {np.median(d[:,3]):6.0f} wait-next {np.median(wait):6.0f} | n={len(t)}")
