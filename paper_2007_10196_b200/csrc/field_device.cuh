@@ -90,14 +90,18 @@ __device__ inline void fft_lines(double* const* re, double* const* im, int b1, i
   }
 }
 
-// sum_v w_v f(x_i, v) for one x point (rho = 1 - that), computed by one warp
-// (lanes stride the contiguous velocity block, 4 loads in flight, fixed
-// reduction order), stored as partial 0 of the point (the others zeroed).
+// Partial charge-density sum of one x point over velocity chunk `part` of
+// M->rparts equal chunks: sum_v w_v f(x_i, v) (rho = 1 - sum of the partials),
+// computed by one warp (lanes stride the contiguous chunk, 4 loads in flight,
+// fixed reduction order).  Trapezoid weights of the velocity block
+// (moment_density models.hpp:294-306, block_weights 240-257).
 template <bool COH>
-__device__ inline void moment_point(const FieldParams& p, const MemberDesc* M, int xi) {
+__device__ inline void moment_part(const FieldParams& p, const MemberDesc* M, int xi, int part) {
   const int dx = p.space_dim;
   const int lane = threadIdx.x & 31;
   const int vn = M->vn;
+  const int chunk = (vn + M->rparts - 1) / M->rparts;
+  const int v0 = part * chunk, v1 = min(vn, v0 + chunk);
   const int ev0 = M->ext[dx], ev1 = (dx == 2) ? M->ext[dx + 1] : 1;
   const double hv0 = M->h[dx], hv1 = (dx == 2) ? M->h[dx + 1] : 1.0;
   const int zb0 = M->bc[dx], zb1 = (dx == 2) ? M->bc[dx + 1] : 0;
@@ -111,18 +115,17 @@ __device__ inline void moment_point(const FieldParams& p, const MemberDesc* M, i
     return (dx == 2) ? w0 * w1 : w0;
   };
   double acc = 0.0;
-  for (int vb = lane; vb < vn; vb += 4 * 32) {
+  for (int vb = v0 + lane; vb < v1; vb += 4 * 32) {
     double v[4];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) v[b] = (vb + 32 * b < vn) ? fld_ld<COH>(block + vb + 32 * b) : 0.0;
+    for (int b = 0; b < 4; ++b) v[b] = (vb + 32 * b < v1) ? fld_ld<COH>(block + vb + 32 * b) : 0.0;
 #pragma unroll
     for (int b = 0; b < 4; ++b)
-      if (vb + 32 * b < vn) acc = fma(weight(vb + 32 * b), v[b], acc);
+      if (vb + 32 * b < v1) acc = fma(weight(vb + 32 * b), v[b], acc);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane < M->rparts)  // partial-sum form: the whole sum in part 0
-    p.rho_parts[(M->xoff + xi) * kRhoParts + lane] = (lane == 0) ? acc : 0.0;
+  if (lane == 0) p.rho_parts[(M->xoff + xi) * kRhoParts + part] = acc;
 }
 
 // E of member mi from its rho partials (whole block; sh >= kFieldSmemDoubles
@@ -258,17 +261,23 @@ __device__ inline void group_point(const FieldParams& p, const double* coef, int
   }
 }
 
-// h-weighted |E_c|^2 contribution of finest x point q: E_c = sum_g I_g(Eg),
-// I_g separable degree-4 Lagrange interpolation from group g's x-grid (or,
-// without groups, E_c = sum_m c_m I_m(E_m) member by member).
-template <bool COH>
+// h-weighted |E_c|^2 contribution of finest x point q, computed by one thread
+// (WARP = false: consecutive threads take consecutive points, so the loads of
+// one group coalesce) or by one warp (WARP: lanes over the members, warp-reduced
+// in a fixed order, every lane returns the value; small families):
+// E_c = sum_g I_g(Eg), I_g separable degree-4 Lagrange
+// interpolation from group g's x-grid (or, without groups, E_c =
+// sum_m c_m I_m(E_m) member by member).
+template <bool COH, bool WARP>
 __device__ inline double energy_point(const FieldParams& p, int q, int fine0, int fine1) {
   const int dx = p.space_dim;
+  const int lane = WARP ? (threadIdx.x & 31) : 0;
+  const int lstep = WARP ? 32 : 1;
   const int i = q / fine1, j = q - (q / fine1) * fine1;
   double ec[2] = {0.0, 0.0};
   const bool direct = (p.negrp == 0);  // small families: every member, no group pass
   const int ng = direct ? p.nmembers : p.negrp;
-  for (int g = 0; g < ng; ++g) {
+  for (int g = lane; g < ng; g += lstep) {
     const MemberDesc* M = p.mem + g;
     const int4 G = direct ? make_int4(M->xext[0], M->xext[1], 0, 0) : p.egrp[g];
     const int n0 = G.x, n1 = G.y;
@@ -293,6 +302,13 @@ __device__ inline double energy_point(const FieldParams& p, int q, int fine0, in
         ec[c] = fma(p.ecoef[g], v, ec[c]);
       else
         ec[c] += v;
+    }
+  }
+  if (WARP) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ec[0] += __shfl_xor_sync(0xffffffffu, ec[0], o);
+      ec[1] += __shfl_xor_sync(0xffffffffu, ec[1], o);
     }
   }
   double acc = 0.0;

@@ -14,9 +14,9 @@ __global__ void __launch_bounds__(256) moment_kernel(const FieldParams p) {
   if (p.ctl != nullptr && !p.ctl->active) return;
   const int2 tk = p.mtasks[blockIdx.x];
   const MemberDesc* M = p.mem + tk.x;
-  const int xi = tk.y + (threadIdx.x >> 5);
-  if (xi >= M->nx) return;
-  moment_point<false>(p, M, xi);
+  const int item = tk.y + (threadIdx.x >> 5);  // (x point, velocity chunk)
+  if (item >= M->nx * M->rparts) return;
+  moment_part<false>(p, M, item / M->rparts, item % M->rparts);
 }
 
 __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams p) {
@@ -39,11 +39,18 @@ __global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p, 
   const long long slot = (p.ctl != nullptr) ? p.ctl->step : 0;  // the step about to be taken
   if (slot >= cap) return;
   double acc = 0.0;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < fine0 * fine1;
-       q += gridDim.x * blockDim.x)
-    acc += energy_point<false>(p, q, fine0, fine1);
+  if (p.negrp > 0) {  // groups (large fine grids): one thread per finest x point
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < fine0 * fine1;
+         q += gridDim.x * blockDim.x)
+      acc += energy_point<false, false>(p, q, fine0, fine1);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  } else {  // members directly (small families): one warp per finest x point
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < fine0 * fine1;
+         q += warps)
+      acc += energy_point<false, true>(p, q, fine0, fine1);
+  }
   if ((threadIdx.x & 31) == 0) atomicAdd(out_base + slot, acc * hvol);
 }
 
@@ -52,8 +59,9 @@ cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fi
   FieldParams q = p;
   q.ecoef = coef;
   if (q.negrp > 0) group_field_kernel<<<(q.ngx + 255) / 256, 256, 0, s>>>(q, coef);
-  int blocks = (fine0 * fine1 + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  int blocks = (q.negrp > 0) ? (fine0 * fine1 + 255) / 256  // a thread per point
+                             : (fine0 * fine1 + 7) / 8;     // a warp per point
+  if (blocks > 148 * 16) blocks = 148 * 16;
   field_energy_kernel<<<blocks, 256, 0, s>>>(q, fine0, fine1, hvol, out_base, cap);
   return cudaGetLastError();
 }

@@ -843,7 +843,9 @@ int setup_vp(sgwg_family* f) {
     M.xext[0] = M.ext[0];
     M.xext[1] = (dx == 2) ? M.ext[1] : 1;
     M.xoff = xoff;
-    M.rparts = 1;
+    // the charge density in partial sums over up to kRhoParts chunks of the
+    // velocity block, so long blocks are integrated by several warps
+    M.rparts = std::max(1, std::min(kRhoParts, (M.vn + 127) / 128));
     xoff += M.nx;
     if (f->model.kind == SGWG_VLASOV_POISSON) {
       for (int k = 0; k < dx; ++k)
@@ -857,12 +859,6 @@ int setup_vp(sgwg_family* f) {
   }
   f->nx_total = xoff;
   CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
-  std::vector<int2> mt;  // moment kernel: 8 x points (one warp each) per CTA
-  for (int mi = 0; mi < f->nm; ++mi)
-    for (int x0 = 0; x0 < f->hmem[mi].nx; x0 += 8) mt.push_back(make_int2(mi, x0));
-  cudaFree(f->dmtasks);
-  f->dmtasks = nullptr;
-  f->nmtasks = (int)mt.size();
   {  // combination coefficients of the local members (combine.hpp:34-43, 116)
     std::vector<double> cf;
     const int d = f->d;
@@ -876,7 +872,6 @@ int setup_vp(sgwg_family* f) {
     f->dcoef = nullptr;
     TRY(upload_vec(&f->dcoef, cf));
   }
-  TRY(upload_vec(&f->dmtasks, mt));
   {  // field-energy groups: members sharing an x-grid, in member order
     std::vector<std::pair<int, int>> keys;
     std::vector<std::vector<int>> mem;
@@ -924,6 +919,21 @@ int setup_vp(sgwg_family* f) {
     CK(cudaMalloc(&f->rho_parts, sizeof(double) * std::max<long long>(1, xoff) * kRhoParts));
   }
   f->parts_of = nullptr;
+  return SGWG_OK;
+}
+
+// moment kernel work: 8 (x point, velocity chunk) items -- one warp each -- per
+// CTA; rebuilt whenever the members' partial counts change (plane tiling)
+int build_moment_tasks(sgwg_family* f) {
+  std::vector<int2> mt;
+  for (int mi = 0; mi < f->nm; ++mi) {
+    const MemberDesc& M = f->hmem[mi];
+    for (int q0 = 0; q0 < M.nx * M.rparts; q0 += 8) mt.push_back(make_int2(mi, q0));
+  }
+  cudaFree(f->dmtasks);
+  f->dmtasks = nullptr;
+  f->nmtasks = (int)mt.size();
+  TRY(upload_vec(&f->dmtasks, mt));
   return SGWG_OK;
 }
 
@@ -1609,6 +1619,7 @@ int sgwg_set_model(sgwg_family* f, const sgwg_model* m) {
   if (m->kind == SGWG_VLASOV_POISSON) TRY(setup_vp(f));
   if (m->kind == SGWG_VLASOV_MAXWELL) TRY(setup_vm(f));
   TRY(build_plane_tiles(f));
+  if (m->kind == SGWG_VLASOV_POISSON) TRY(build_moment_tasks(f));
   clear_graphs(f);
   return SGWG_OK;
 }

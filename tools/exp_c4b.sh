@@ -1,5 +1,5 @@
 x() { tail -1 gpurun_out/$1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', round(d['ms_per_step'],2), d.get('gpu_launches'))" 2>&1 | tail -1; }
-B="python bench.py --config C4 --steps 2 --warmup 3 --no-cpu-baseline"
-timeout 300 $B > gpurun_out/c4_tail.log 2>&1; x c4_tail.log
-SGWG_VP_FIELD_TAIL=0 timeout 300 $B > gpurun_out/c4_notail.log 2>&1; x c4_notail.log
-SGWG_VP_FUSE_MOMENT=1 timeout 300 $B > gpurun_out/c4_fm.log 2>&1; x c4_fm.log
+timeout 900 python -m pytest tests/test_gpu_vp.py tests/test_gpu_landau.py tests/test_gpu_diag.py -q -x > gpurun_out/pytest_c4b.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_c4b.log
+timeout 300 python bench.py --config C4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/c4c.log 2>&1; x c4c.log
+timeout 300 python bench.py --config C5 --tfinal 0.05 --no-combine --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/c5c.log 2>&1; x c5c.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4b.csv python bench.py --config C4 --tfinal 0.05 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_c4.log 2>&1
