@@ -884,9 +884,16 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
     }
     lmax = fmax(lmax, fabs(o));
   }
-  if (p.track_max) {
+  if (p.track_max) {  // one atomic per CTA (max is exact in any order)
+    __shared__ double wmax[kFastThreads / 32];
     lmax = warp_max(lmax);
-    if ((tid & 31) == 0) atomicMax(p.amax_out + mi, (unsigned long long)__double_as_longlong(lmax));
+    if ((tid & 31) == 0) wmax[tid >> 5] = lmax;
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0.0;
+      for (int w = 0; w < NT / 32; ++w) m = fmax(m, wmax[w]);
+      atomicMax(p.amax_out + mi, (unsigned long long)__double_as_longlong(m));
+    }
   }
 }
 
