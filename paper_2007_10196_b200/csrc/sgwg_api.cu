@@ -2167,15 +2167,19 @@ int sgwg_write_snapshot(sgwg_family* f, int mode, double eps, const char* path) 
     std::memcpy(hdr + 12 + 4 * k, &e, 4);
     std::memcpy(hdr + 32 + 8 * k, &f->fine_h[k], 8);
   }
-  FILE* fp = std::fopen(path, "wb");
-  if (fp == nullptr) return fail_with(SGWG_EINVAL, std::string("write_snapshot: cannot open ") + path);
-  int st = (std::fwrite(hdr, 1, sizeof(hdr), fp) == sizeof(hdr))
+  // sharded family: every rank takes part in the combination's all-reduce, rank 0 writes
+  const bool writer = (f->comm == nullptr || f->rank == 0);
+  FILE* fp = writer ? std::fopen(path, "wb") : nullptr;
+  if (writer && fp == nullptr)
+    return fail_with(SGWG_EINVAL, std::string("write_snapshot: cannot open ") + path);
+  int st = (!writer || std::fwrite(hdr, 1, sizeof(hdr), fp) == sizeof(hdr))
                ? SGWG_OK
                : fail_with(SGWG_EINVAL, "write_snapshot: write failed");
   double* host = nullptr;
   long long host_n = 0;
   if (st == SGWG_OK)
     st = for_each_combined_slab(f, mode, eps, [&](const double* dev, long long, long long n) -> int {
+      if (!writer) return SGWG_OK;
       if (host_n < n) {
         cudaFreeHost(host);
         host = nullptr;
@@ -2189,7 +2193,8 @@ int sgwg_write_snapshot(sgwg_family* f, int mode, double eps, const char* path) 
       return SGWG_OK;
     });
   cudaFreeHost(host);
-  if (std::fclose(fp) != 0 && st == SGWG_OK) st = fail_with(SGWG_EINVAL, "write_snapshot: close failed");
+  if (fp != nullptr && std::fclose(fp) != 0 && st == SGWG_OK)
+    st = fail_with(SGWG_EINVAL, "write_snapshot: close failed");
   return st;
 }
 
