@@ -1120,6 +1120,202 @@ __global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_fast_kernel(const 
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
 }
 
+// Persistent, software-pipelined variant (advection): each CTA walks its
+// tiles in order and stages tile k+1 with asynchronous 8-byte copies
+// (cp.async, zero-filled ghosts) into the second of two padded boxes while
+// the sweeps of tile k run, so the halo/interior load latency overlaps the
+// fp64 work instead of preceding it.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int TX, int TY, int TZ>
+struct Box3 {
+  static constexpr int PZ = ((TZ + 6) % 2 == 0) ? TZ + 7 : TZ + 6;
+  static constexpr int PY = TY + 6;
+  static constexpr int BOX = (TX + 6) * PY * PZ;
+  static constexpr int NPTS = TX * TY * TZ;
+  static constexpr int NS = NPTS / 8;
+  static constexpr int NT = 3 * NS;
+  static constexpr int DZP = TZ + 1;
+  static constexpr int DN = TX * TY * DZP;
+};
+constexpr int kPipe3DBox = 7260;   // max Box3::BOX of the three tile shapes
+constexpr int kPipe3DDn = 2304;    // max Box3::DN
+
+// gindex of the padded box position (a, b, c) (weno.hpp:131-141 boundary rule)
+__device__ __forceinline__ int gidx3(const MemberDesc* M, int i0, int j0, int l0, int a, int b,
+                                     int c) {
+  const int n0 = M->ext[0], n1 = M->ext[1], n2 = M->ext[2];
+  int gi = i0 - 3 + a, gj = j0 - 3 + b, gl = l0 - 3 + c;
+  if (gi < 0 || gi >= n0) {
+    if (M->bc[0] != 0) return -1;
+    gi = (gi < 0) ? gi + n0 : gi - n0;  // |excursion| <= 3 < n (periodic n >= 6)
+  }
+  if (gj < 0 || gj >= n1) {
+    if (M->bc[1] != 0) return -1;
+    gj = (gj < 0) ? gj + n1 : gj - n1;
+  }
+  if (gl < 0 || gl >= n2) {
+    if (M->bc[2] != 0) return -1;
+    gl = (gl < 0) ? gl + n2 : gl - n2;
+  }
+  return (gi * n1 + gj) * n2 + gl;
+}
+
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ void stage3d_issue(const Stage2DParams& p, const MemberDesc* M, int i0,
+                                              int j0, int l0, double* U) {
+  using G = Box3<TX, TY, TZ>;
+  const double* u = p.uin + M->offset;
+  const int tid = threadIdx.x;
+  for (int q = tid; q < G::NPTS; q += G::NT) {
+    const int a = q / (TY * TZ), b = (q / TZ) % TY, c = q % TZ;
+    const int g = gidx3(M, i0, j0, l0, a + 3, b + 3, c + 3);
+    cp_async8(U + ((a + 3) * G::PY + (b + 3)) * G::PZ + (c + 3), u + max(g, 0), g >= 0);
+  }
+  constexpr int FX = 6 * TY * TZ, FY = 6 * TX * TZ, FZ = 6 * TX * TY;
+  for (int h = tid; h < FX + FY + FZ; h += G::NT) {
+    int a, b, c;
+    if (h < FX) {
+      const int r6 = h / (TY * TZ), rem = h % (TY * TZ);
+      a = (r6 < 3) ? r6 : TX + r6;
+      b = rem / TZ + 3;
+      c = rem % TZ + 3;
+    } else if (h < FX + FY) {
+      const int h2 = h - FX, r6 = h2 / (TX * TZ), rem = h2 % (TX * TZ);
+      b = (r6 < 3) ? r6 : TY + r6;
+      a = rem / TZ + 3;
+      c = rem % TZ + 3;
+    } else {
+      const int h3 = h - FX - FY, r6 = h3 / (TX * TY), rem = h3 % (TX * TY);
+      c = (r6 < 3) ? r6 : TZ + r6;
+      a = rem / TY + 3;
+      b = rem % TY + 3;
+    }
+    const int g = gidx3(M, i0, j0, l0, a, b, c);
+    cp_async8(U + (a * G::PY + b) * G::PZ + c, u + max(g, 0), g >= 0);
+  }
+}
+
+template <int TX, int TY, int TZ>
+__device__ __forceinline__ void stage3d_compute(const Stage2DParams& p, const MemberDesc* M,
+                                                int mi, int i0, int j0, int l0, const double* U,
+                                                double* D) {
+  using G = Box3<TX, TY, TZ>;
+  constexpr int RUN = 8, PY = G::PY, PZ = G::PZ, NS = G::NS, DZP = G::DZP, DN = G::DN;
+  double* DX = D;
+  double* DY = DX + DN;
+  double* DZ = DY + DN;
+  const int tid = threadIdx.x;
+  const double eps4 = 4.0 * p.eps;
+  if (tid < NS) {  // x-sweep: lines (j, l), runs along i
+    const int l = tid % TZ, j = (tid / TZ) % TY, r = tid / (TY * TZ);
+    const double* base = U + ((j + 3) * PZ) + (l + 3);
+    double* out = DX + ((r * RUN) * TY + j) * DZP + l;
+    if (p.linear)
+      sweep_run<false, RUN, true>(base, base, PY * PZ, r * RUN, p.c0, eps4, M->inv_h[0], out,
+                                  TY * DZP);
+    else
+      sweep_run<false, RUN, false>(base, base, PY * PZ, r * RUN, p.c0, eps4, M->inv_h[0], out,
+                                   TY * DZP);
+  } else if (tid < 2 * NS) {  // y-sweep: lines (i, l), runs along j
+    const int t2 = tid - NS;
+    const int l = t2 % TZ, i = (t2 / TZ) % TX, r = t2 / (TX * TZ);
+    const double* base = U + ((i + 3) * PY) * PZ + (l + 3);
+    double* out = DY + (i * TY + r * RUN) * DZP + l;
+    if (p.linear)
+      sweep_run<false, RUN, true>(base, base, PZ, r * RUN, p.c1, eps4, M->inv_h[1], out, DZP);
+    else
+      sweep_run<false, RUN, false>(base, base, PZ, r * RUN, p.c1, eps4, M->inv_h[1], out, DZP);
+  } else {  // z-sweep: lines (i, j), runs along l; lanes walk j (odd z pitch)
+    const int t3 = tid - 2 * NS;
+    const int j = t3 % TY, i = (t3 / TY) % TX, r = t3 / (TX * TY);
+    const double* base = U + ((i + 3) * PY + (j + 3)) * PZ;
+    double* out = DZ + (i * TY + j) * DZP + r * RUN;
+    if (p.linear)
+      sweep_run<false, RUN, true>(base, base, 1, r * RUN, p.c2, eps4, M->inv_h[2], out, 1);
+    else
+      sweep_run<false, RUN, false>(base, base, 1, r * RUN, p.c2, eps4, M->inv_h[2], out, 1);
+  }
+  __syncthreads();
+  const StepCtl* ctl = p.ctl;
+  const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
+  const int n0 = M->ext[0], n1 = M->ext[1], n2 = M->ext[2];
+  for (int q = tid; q < G::NPTS; q += G::NT) {
+    const int a = q / (TY * TZ), b = (q / TZ) % TY, c = q % TZ;
+    if (i0 + a >= n0 || j0 + b >= n1 || l0 + c >= n2) continue;
+    const int dq = (a * TY + b) * DZP + c;
+    const double kv = ((0.0 - DX[dq]) - DY[dq]) - DZ[dq];
+    const long long gi = M->offset + ((long long)(i0 + a) * n1 + (j0 + b)) * n2 + (l0 + c);
+    double o;
+    if (p.stage == 0) {
+      o = kv;
+    } else {
+      if (!isfinite(kv)) {
+        const unsigned long long code =
+            (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
+        atomicMin(p.fail + mi, code);
+      }
+      const double ui = U[((a + 3) * PY + (b + 3)) * PZ + (c + 3)];
+      if (p.stage == 1)
+        o = fma(dt, kv, ui);
+      else if (p.stage == 2)
+        o = fma(0.75, __ldg(p.un + gi), 0.25 * fma(dt, kv, ui));
+      else
+        o = fma(1.0 / 3.0, __ldg(p.un + gi), (2.0 / 3.0) * fma(dt, kv, ui));
+    }
+    p.out[gi] = o;
+  }
+}
+
+__device__ __forceinline__ void stage3d_issue_any(const Stage2DParams& p, int4 tk, double* U) {
+  const MemberDesc* M = p.mem + tk.x;
+  const int i0 = tk.y >> 16, j0 = tk.y & 0xffff, l0 = tk.z >> 8;
+  switch (tk.z & 0xff) {
+    case 0: stage3d_issue<8, 16, 16>(p, M, i0, j0, l0, U); break;
+    case 1: stage3d_issue<16, 8, 16>(p, M, i0, j0, l0, U); break;
+    default: stage3d_issue<16, 16, 8>(p, M, i0, j0, l0, U); break;
+  }
+}
+
+__global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_pipe_kernel(const Stage2DParams p) {
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  extern __shared__ double sm[];
+  double* Ub[2] = {sm, sm + kPipe3DBox};
+  double* D = sm + 2 * kPipe3DBox;
+  int t = blockIdx.x;
+  if (t < p.ntiles) stage3d_issue_any(p, p.tiles[t], Ub[0]);
+  cp_async_commit();
+  for (int k = 0; t < p.ntiles; t += gridDim.x, ++k) {
+    const int tn = t + gridDim.x;
+    if (tn < p.ntiles) stage3d_issue_any(p, p.tiles[tn], Ub[(k + 1) & 1]);
+    cp_async_commit();
+    cp_async_wait<1>();  // tile t's copies have landed (the newest group may be in flight)
+    __syncthreads();
+    const int4 tk = p.tiles[t];
+    const MemberDesc* M = p.mem + tk.x;
+    const int i0 = tk.y >> 16, j0 = tk.y & 0xffff, l0 = tk.z >> 8;
+    switch (tk.z & 0xff) {
+      case 0: stage3d_compute<8, 16, 16>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+      case 1: stage3d_compute<16, 8, 16>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+      default: stage3d_compute<16, 16, 8>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+    }
+    __syncthreads();  // box k&1 and D are reused by the next tiles
+  }
+  cp_async_wait<0>();
+  if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+
 // ---------------------------------------------------------------------------
 // fast 4D stage (kinetic transport / advection) as two plane launches
 // ---------------------------------------------------------------------------
@@ -1522,6 +1718,17 @@ __global__ void __launch_bounds__(kFastThreads, 1)
 
 cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
+  const char* e = getenv("SGWG_3D_PIPE");
+  if (!(e && e[0] == '0')) {  // persistent, pipelined: one CTA per SM
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    Stage2DParams q = p;
+    q.ntiles = nblocks;
+    stage3d_pipe_kernel<<<min(nblocks, sms), kStage3DThreads,
+                          (2 * kPipe3DBox + 3 * kPipe3DDn) * sizeof(double), s>>>(q);
+    return cudaGetLastError();
+  }
   stage3d_fast_kernel<<<nblocks, kStage3DThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
@@ -1910,6 +2117,9 @@ cudaError_t configure() {
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(plane_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             200 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage3d_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (2 * kPipe3DBox + 3 * kPipe3DDn) * (int)sizeof(double));
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
