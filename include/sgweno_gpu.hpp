@@ -97,12 +97,15 @@ inline sgwg_model model_of(const ProblemSpec& spec, const WenoParams& p) {
       m.theta = spec.vb.theta;
       m.tau = spec.vb.tau;
       break;
+    case ModelKind::vlasov_maxwell: m.kind = SGWG_VLASOV_MAXWELL; break;
     default: throw std::invalid_argument("model not on the B200 path");
   }
   return m;
 }
 
 // RAII device family mirroring a host CombinationSet
+// (member states are the reference's: the grid field followed by any model
+// state -- the Vlasov-Maxwell field lines -- once the model is set)
 class Family {
  public:
   Family(sgwg_ctx* ctx, const CombinationSet& set) {
@@ -111,20 +114,40 @@ class Family {
     check(sgwg_family_sizes(fam_, &npts_, &nfine_));
   }
   ~Family() { sgwg_family_destroy(fam_); }
+  void set_model(const sgwg_model& m) {
+    check(sgwg_set_model(fam_, &m));
+    check(sgwg_family_sizes(fam_, &npts_, &nfine_));
+  }
+  // whole member states when the device family carries the model state, the
+  // grid fields only otherwise (e.g. a combination of Vlasov-Maxwell states)
+  bool whole(const CombinationSet& set) const {
+    size_t field = 0, state = 0;
+    for (const auto& m : set.members) {
+      field += m.field_size();
+      state += m.state.size();
+    }
+    if (npts_ == state) return true;
+    if (npts_ == field) return false;
+    throw std::invalid_argument("member states do not match the device family");
+  }
   void upload(const CombinationSet& set) {
+    const bool all = whole(set);
     std::vector<double> buf;
     buf.reserve(npts_);
     for (const auto& m : set.members)
-      buf.insert(buf.end(), m.state.begin(), m.state.begin() + m.field_size());
+      buf.insert(buf.end(), m.state.begin(),
+                 all ? m.state.end() : m.state.begin() + m.field_size());
     check(sgwg_family_upload(fam_, buf.data(), buf.size()));
   }
   void download(CombinationSet& set) const {
+    const bool all = whole(set);
     std::vector<double> buf(npts_);
     check(sgwg_family_download(fam_, buf.data(), buf.size()));
     size_t off = 0;
     for (auto& m : set.members) {
-      std::memcpy(m.state.data(), buf.data() + off, sizeof(double) * m.field_size());
-      off += m.field_size();
+      const size_t n = all ? m.state.size() : m.field_size();
+      std::memcpy(m.state.data(), buf.data() + off, sizeof(double) * n);
+      off += n;
     }
   }
   sgwg_family* get() const { return fam_; }
@@ -144,9 +167,8 @@ inline std::vector<double> evolve_family(CombinationSet& set, const ProblemSpec&
                                          const std::function<void(double)>& on_stop = nullptr,
                                          Device& dev = default_device(), double dt_scale = 1.0) {
   detail::Family fam(dev.get(), set);
+  fam.set_model(detail::model_of(spec, params));
   fam.upload(set);
-  const sgwg_model m = detail::model_of(spec, params);
-  check(sgwg_set_model(fam.get(), &m));
   sgwg_policy pol{};
   pol.mode = (policy.mode == DtMode::cfl) ? SGWG_DT_CFL : SGWG_DT_ACCURACY;
   pol.cfl = policy.cfl_number;
@@ -193,6 +215,31 @@ inline GridField combine(const CombinationSet& set, InterpMode mode, double epsi
   check(sgwg_combine(fam.get(), mode == InterpMode::weno ? SGWG_INTERP_WENO : SGWG_INTERP_LAGRANGE,
                      epsilon, out.values.data(), out.values.size(), 0));
   return out;
+}
+
+// Runner-level outputs from the device (runner.hpp:330-366): diagnostics of
+// the combination without downloading it, and the SGW5 dump streamed in slabs.
+inline sgwg_field_stats combined_stats(const CombinationSet& set, InterpMode mode, double epsilon,
+                                       int exact_preset = -1, double t = 0.0,
+                                       const ProblemSpec* spec = nullptr,
+                                       Device& dev = default_device()) {
+  detail::Family fam(dev.get(), set);
+  if (spec != nullptr) fam.set_model(detail::model_of(*spec, WenoParams{epsilon, WenoMode::nonlinear}));
+  fam.upload(set);
+  sgwg_field_stats st{};
+  check(sgwg_combined_stats(fam.get(), mode == InterpMode::weno ? SGWG_INTERP_WENO
+                                                                 : SGWG_INTERP_LAGRANGE,
+                            epsilon, exact_preset, t, &st));
+  return st;
+}
+
+inline void write_field_dump(const std::string& path, const CombinationSet& set, InterpMode mode,
+                             double epsilon, Device& dev = default_device()) {
+  detail::Family fam(dev.get(), set);
+  fam.upload(set);
+  check(sgwg_write_snapshot(fam.get(), mode == InterpMode::weno ? SGWG_INTERP_WENO
+                                                                 : SGWG_INTERP_LAGRANGE,
+                            epsilon, path.c_str()));
 }
 
 }  // namespace sgweno::gpu

@@ -9,6 +9,8 @@
 #include <cstring>
 #include <numbers>
 
+#include "sgweno/io.hpp"
+#include "sgweno/runner.hpp"
 #include "sgweno_gpu.hpp"
 
 using namespace sgweno;
@@ -76,6 +78,47 @@ int main() {
                     gpu::combine(dev, InterpMode::weno, 1e-6).values);
     std::printf("3D advection (N_L=3) via shim: %zu steps, bitwise %s\n", dts_dev.size(),
                 ok ? "EQUAL" : "DIFFERENT");
+    bad += !ok;
+  }
+  // reduced Vlasov-Maxwell (paper ex6 at reduced size): states carry E1, E2, B3
+  {
+    ExampleDefaults ex = make_example(ExampleId::ex6);
+    const ProblemSpec& spec = ex.problem;
+    CombinationSet ref = make_family(spec.box, {8, 8, 8}, spec.boundary, 2);
+    initialize_family(ref, spec);
+    CombinationSet dev = ref;
+    StepPolicy pol;
+    pol.mode = DtMode::cfl;
+    pol.cfl_number = 0.4;
+    const WenoParams wp{1e-6, WenoMode::nonlinear};
+    FamilyModel model(spec, ref, wp, 1);
+    auto dts_ref = evolve_family(ref, model, pol, 0.5, {0.2});
+    auto dts_dev = gpu::evolve_family(dev, spec, wp, pol, 0.5, {0.2});
+    bool ok = same(dts_ref, dts_dev) && !dts_dev.empty();
+    for (size_t m = 0; ok && m < ref.members.size(); ++m)
+      ok = same(ref.members[m].state, dev.members[m].state);
+    ok = ok && same(combine(ref, InterpMode::weno, 1e-6).values,
+                    gpu::combine(dev, InterpMode::weno, 1e-6).values);
+    std::printf("Vlasov-Maxwell (ex6, N_L=2) via shim: %zu steps, bitwise %s\n", dts_dev.size(),
+                ok ? "EQUAL" : "DIFFERENT");
+    bad += !ok;
+  }
+  // runner outputs from the device: quadrature_mass / field_min / field_max of
+  // the combination, and the SGW5 dump read back with read_field_dump
+  {
+    ExampleDefaults ex = make_example(ExampleId::ex1);
+    CombinationSet set = make_family(ex.problem.box, {10, 10}, ex.problem.boundary, 3);
+    initialize_family(set, ex.problem);
+    GridField f = combine(set, InterpMode::lagrange, 1e-6);
+    const sgwg_field_stats st = gpu::combined_stats(set, InterpMode::lagrange, 1e-6);
+    const double mass = quadrature_mass(f);
+    bool ok = st.min == detail::field_min(f) && st.max == detail::field_max(f) &&
+              std::abs(st.mass - mass) <= 1e-13 * std::abs(mass);
+    const std::string path = "/tmp/sgwg_shim_snapshot.sgw5";
+    gpu::write_field_dump(path, set, InterpMode::lagrange, 1e-6);
+    const FieldDump d = read_field_dump(path);
+    ok = ok && same(d.values, f.values) && d.extents[0] == f.geom.points[0];
+    std::printf("runner outputs via shim (stats, SGW5 dump): %s\n", ok ? "EQUAL" : "DIFFERENT");
     bad += !ok;
   }
   // failure propagation: FamilyIntegratorFailure{level, step, stage}

@@ -17,4 +17,4 @@ def test_cpp_shim_bitwise_vs_reference():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("EQUAL") == 3
+    assert r.stdout.count("EQUAL") == 5
