@@ -21,7 +21,7 @@ namespace sgwg {
 
 constexpr int kFieldThreads = 512;
 constexpr int kFieldMaxX = 2048;
-constexpr int kFieldSmemDoubles = 6 * kFieldMaxX + kFieldMaxX / 2 * 2;
+constexpr int kFieldSmemDoubles = 6 * kFieldMaxX + 2 * kFieldMaxX;  // + 2 x 2H twiddles
 
 template <bool COH>
 __device__ __forceinline__ double fld_ld(const double* p) {
@@ -32,40 +32,29 @@ __device__ __forceinline__ int bitrev(int x, int bits) {
   return (int)(__brev((unsigned)x) >> (32 - bits));
 }
 
-// radix-2 FFTs of all lines along `axis` (1 = x2, contiguous) of na complex
+// radix-2 FFTs of all lines along `axis` (1 = x2, contiguous) of NA complex
 // n1 x n2 arrays (re[k], im[k]) at once (one barrier per butterfly stage for
-// all of them); n1 = 2^b1, n2 = 2^b2.  sign -1: forward e^{-i...}; +1: inverse
-// (unnormalised).  Twiddles from the table e^{i pi k/H}, k < H.
-template <int NA>
+// all of them); n1 = 2^b1, n2 = 2^b2.  DIF (forward, sign -1): natural order in,
+// bit-reversed order out; DIT (inverse, sign +1, unnormalised): bit-reversed in,
+// natural out -- so no bit-reversal pass is needed, and the spectral step works
+// in bit-reversed order.  Twiddles from the stage-major table
+// T[half + pos] = e^{i pi pos/half} (consecutive lanes read consecutive entries:
+// no shared-memory bank conflicts).
+template <int NA, bool DIF>
 __device__ inline void fft_lines(double* const* re, double* const* im, int b1, int b2, int axis,
-                                 int sign, const double* twc, const double* tws, int H) {
+                                 const double* tc, const double* ts) {
   const int bits = axis ? b2 : b1;
   if (bits == 0) return;
   const int len = 1 << bits;
   const int nx = 1 << (b1 + b2);
   const int stride = axis ? 1 : (1 << b2);
+  const double sign = DIF ? -1.0 : 1.0;
   auto base_of = [&](int line) { return axis ? (line << b2) : line; };
   // lanes walk positions along contiguous lines (axis 1) and walk lines when
   // the lines are strided (axis 0), so shared-memory accesses stay conflict-free
   const int lbits = b1 + b2 - bits;  // log2(number of lines)
-  for (int idx = threadIdx.x; idx < nx; idx += blockDim.x) {
-    const int line = axis ? idx >> bits : idx & ((1 << lbits) - 1);
-    const int pos = axis ? idx & (len - 1) : idx >> lbits;
-    const int rev = bitrev(pos, bits);
-    if (pos < rev) {
-      const int a = base_of(line) + pos * stride, b = base_of(line) + rev * stride;
-#pragma unroll
-      for (int k = 0; k < NA; ++k) {
-        const double tr = re[k][a], ti = im[k][a];
-        re[k][a] = re[k][b];
-        im[k][a] = im[k][b];
-        re[k][b] = tr;
-        im[k][b] = ti;
-      }
-    }
-  }
-  __syncthreads();
-  for (int lh = 0; lh < bits; ++lh) {
+  for (int st = 0; st < bits; ++st) {
+    const int lh = DIF ? bits - 1 - st : st;
     const int half = 1 << lh;
     for (int bf = threadIdx.x; bf < nx / 2; bf += blockDim.x) {
       const int line = axis ? bf >> (bits - 1) : bf & ((1 << lbits) - 1);
@@ -73,17 +62,24 @@ __device__ inline void fft_lines(double* const* re, double* const* im, int b1, i
       const int grp = q >> lh, pos = q & (half - 1);
       const int i0 = base_of(line) + ((grp << (lh + 1)) + pos) * stride;
       const int i1 = i0 + half * stride;
-      const int ti = pos * (H >> lh);  // e^{sign i pi pos/half}
-      const double c = twc[ti], s = sign * tws[ti];
+      const double c = tc[half + pos], s = sign * ts[half + pos];  // e^{sign i pi pos/half}
 #pragma unroll
       for (int k = 0; k < NA; ++k) {
-        const double br = re[k][i1] * c - im[k][i1] * s;
-        const double bi = re[k][i1] * s + im[k][i1] * c;
         const double ar = re[k][i0], ai = im[k][i0];
-        re[k][i0] = ar + br;
-        im[k][i0] = ai + bi;
-        re[k][i1] = ar - br;
-        im[k][i1] = ai - bi;
+        const double xr = re[k][i1], xi = im[k][i1];
+        if (DIF) {  // (a, b) -> (a + b, (a - b) w)
+          const double dr = ar - xr, di = ai - xi;
+          re[k][i0] = ar + xr;
+          im[k][i0] = ai + xi;
+          re[k][i1] = dr * c - di * s;
+          im[k][i1] = dr * s + di * c;
+        } else {    // (a, b) -> (a + b w, a - b w)
+          const double br = xr * c - xi * s, bi = xr * s + xi * c;
+          re[k][i0] = ar + br;
+          im[k][i0] = ai + bi;
+          re[k][i1] = ar - br;
+          im[k][i1] = ai - bi;
+        }
       }
     }
     __syncthreads();
@@ -132,8 +128,17 @@ __device__ inline void moment_part(const FieldParams& p, const MemberDesc* M, in
 // doubles; red >= 2 * blockDim/32 doubles); also p.rho and
 // p.emax[mi*dx + comp] = max|E_comp|.  Both field components are transformed
 // back together.
+#ifdef SGWG_TRACE
+__device__ long long sgwg_ftrace[128][8];  // per member: phase clocks of the last field launch
+#define SGWG_FMARK(mi, ph) \
+  if (threadIdx.x == 0 && (mi) < 128) sgwg_ftrace[mi][ph] = clock64()
+#else
+#define SGWG_FMARK(mi, ph)
+#endif
+
 template <bool COH>
 __device__ inline void field_member(const FieldParams& p, int mi, double* sh, double* red) {
+  SGWG_FMARK(mi, 0);
   const MemberDesc* M = p.mem + mi;
   const int dx = p.space_dim;
   const int n1 = M->xext[0], n2 = M->xext[1];
@@ -144,30 +149,45 @@ __device__ inline void field_member(const FieldParams& p, int mi, double* sh, do
   double* er[2] = {sh + 2 * nx, sh + 4 * nx};
   double* ei[2] = {sh + 3 * nx, sh + 5 * nx};
   const int H = max(1, max(n1, n2) / 2);
-  double* twc = sh + 6 * nx;
-  double* tws = twc + H;
+  double* twc = sh + 6 * nx;  // stage-major twiddles, 2H each
+  double* tws = twc + 2 * H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int xi = threadIdx.x; xi < nx; xi += blockDim.x) {
     const double* pt = p.rho_parts + (M->xoff + xi) * kRhoParts;
-    double acc = fld_ld<COH>(pt);
-    for (int t = 1; t < M->rparts; ++t) acc += fld_ld<COH>(pt + t);
+    double v[kRhoParts];  // all partial loads in flight, then summed in part order
+#pragma unroll
+    for (int t = 0; t < kRhoParts; ++t) v[t] = (t < M->rparts) ? fld_ld<COH>(pt + t) : 0.0;
+    double acc = v[0];
+#pragma unroll
+    for (int t = 1; t < kRhoParts; ++t)
+      if (t < M->rparts) acc += v[t];
     const double r = 1.0 - acc;
     p.rho[M->xoff + xi] = r;
     rr[xi] = r;
     ri[xi] = 0.0;
   }
-  for (int k = threadIdx.x; k < H; k += blockDim.x)
-    sincospi((double)k / (double)H, &tws[k], &twc[k]);
+  // twiddles: T[half + pos] = e^{i pi pos/half} = family table entry
+  // e^{i pi q/hmax}, q = pos hmax/half (half = 1 .. H)
+  for (int e = threadIdx.x; e < 2 * H; e += blockDim.x) {
+    if (e == 0) continue;
+    const int half = 1 << (31 - __clz(e)), pos = e - half;
+    const int q = pos * (p.hmax / half);
+    twc[e] = fld_ld<COH>(p.twid + q);
+    tws[e] = fld_ld<COH>(p.twid + p.hmax + q);
+  }
   __syncthreads();
-  {
+  SGWG_FMARK(mi, 1);
+  {  // forward, output in bit-reversed order along both axes
     double* R[1] = {rr};
     double* I[1] = {ri};
-    fft_lines<1>(R, I, b1, b2, 1, -1, twc, tws, H);
-    fft_lines<1>(R, I, b1, b2, 0, -1, twc, tws, H);
+    fft_lines<1, true>(R, I, b1, b2, 1, twc, tws);
+    fft_lines<1, true>(R, I, b1, b2, 0, twc, tws);
   }
+  SGWG_FMARK(mi, 2);
   const double two_pi = 6.283185307179586476925286766559;
-  for (int id = threadIdx.x; id < nx; id += blockDim.x) {
-    const int k1 = id >> b2, k2 = id & (n2 - 1);
+  for (int id = threadIdx.x; id < nx; id += blockDim.x) {  // bit-reversed storage order
+    const int k1 = (b1 > 0) ? bitrev(id >> b2, b1) : 0;
+    const int k2 = (b2 > 0) ? bitrev(id & (n2 - 1), b2) : 0;
     const int s1 = (k1 <= n1 / 2) ? k1 : k1 - n1;
     const int s2 = (k2 <= n2 / 2) ? k2 : k2 - n2;
     const bool nyq = ((n1 % 2 == 0) && k1 == n1 / 2 && n1 > 1) ||
@@ -183,13 +203,15 @@ __device__ inline void field_member(const FieldParams& p, int mi, double* sh, do
     }
   }
   __syncthreads();
-  if (dx == 2) {
-    fft_lines<2>(er, ei, b1, b2, 1, +1, twc, tws, H);
-    fft_lines<2>(er, ei, b1, b2, 0, +1, twc, tws, H);
+  SGWG_FMARK(mi, 3);
+  if (dx == 2) {  // inverse, bit-reversed in, natural out
+    fft_lines<2, false>(er, ei, b1, b2, 0, twc, tws);
+    fft_lines<2, false>(er, ei, b1, b2, 1, twc, tws);
   } else {
-    fft_lines<1>(er, ei, b1, b2, 1, +1, twc, tws, H);
-    fft_lines<1>(er, ei, b1, b2, 0, +1, twc, tws, H);
+    fft_lines<1, false>(er, ei, b1, b2, 0, twc, tws);
+    fft_lines<1, false>(er, ei, b1, b2, 1, twc, tws);
   }
+  SGWG_FMARK(mi, 4);
   double lmax[2] = {0.0, 0.0};
   const double inv_n = 1.0 / (double)nx;
   for (int comp = 0; comp < dx; ++comp) {
@@ -213,6 +235,7 @@ __device__ inline void field_member(const FieldParams& p, int mi, double* sh, do
     for (int q = 0; q < nwarps; ++q) m = fmax(m, red[threadIdx.x * nwarps + q]);
     p.emax[mi * dx + threadIdx.x] = m;
   }
+  SGWG_FMARK(mi, 5);
 }
 
 // degree-4 Lagrange weights in the reference's cell form (interp.hpp:36-53

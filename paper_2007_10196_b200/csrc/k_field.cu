@@ -66,6 +66,16 @@ cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fi
   return cudaGetLastError();
 }
 
+__global__ void twiddle_kernel(double* tw, int hmax) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < hmax) sincospi((double)k / (double)hmax, &tw[hmax + k], &tw[k]);
+}
+
+cudaError_t launch_twiddles(double* tw, int hmax, cudaStream_t s) {
+  twiddle_kernel<<<(hmax + 255) / 256, 256, 0, s>>>(tw, hmax);
+  return cudaGetLastError();
+}
+
 cudaError_t configure_field() {
   return cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(kFieldSmemDoubles * sizeof(double)));
@@ -79,3 +89,9 @@ cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, c
 }
 
 }  // namespace sgwg
+
+#ifdef SGWG_TRACE
+extern "C" int sgwg_ftrace_dump(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, sgwg::sgwg_ftrace, sizeof(sgwg::sgwg_ftrace));
+}
+#endif

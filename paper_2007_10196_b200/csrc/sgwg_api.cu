@@ -231,6 +231,8 @@ struct sgwg_family {
   int nptiles[2] = {0, 0};
   int psmem = 0;
   double* rho_parts = nullptr;      // Vlasov-Poisson charge-density partial sums
+  double* twid = nullptr;           // FFT twiddle table (2 x hmax)
+  int hmax = 1;
   const double* parts_of = nullptr; // the state rho_parts currently describes (or null)
   bool no_fused2d = false;  // SGWG_NO_FUSED2D=1: use the per-dimension pass kernels
   bool single = false;      // single-grid mode (runner.hpp:106-115): combine = the grid itself
@@ -310,6 +312,8 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
   fp.nmtasks = f->nmtasks;
   fp.nmembers = f->nm;
   fp.rho_parts = f->rho_parts;
+  fp.twid = f->twid;
+  fp.hmax = f->hmax;
   fp.egrp = f->degrp;
   fp.egrp_m = f->degrp_m;
   fp.egrp_mem = f->degrp_mem;
@@ -918,6 +922,16 @@ int setup_vp(sgwg_family* f) {
     CK(cudaMalloc(&f->emax, sizeof(double) * std::max(1, f->nm * dx)));
     CK(cudaMalloc(&f->rho_parts, sizeof(double) * std::max<long long>(1, xoff) * kRhoParts));
   }
+  {  // FFT twiddles for the largest x-grid line of the family
+    int hmax = 1;
+    for (const auto& M : f->hmem) hmax = std::max(hmax, std::max(M.xext[0], M.xext[1]) / 2);
+    cudaFree(f->twid);
+    f->twid = nullptr;
+    CK(cudaMalloc(&f->twid, sizeof(double) * 2 * hmax));
+    CK(launch_twiddles(f->twid, hmax, f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    f->hmax = hmax;
+  }
   f->parts_of = nullptr;
   return SGWG_OK;
 }
@@ -1480,6 +1494,7 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dptiles[0]);
   cudaFree(f->dptiles[1]);
   cudaFree(f->rho_parts);
+  cudaFree(f->twid);
   cudaFree(f->Fu);
   cudaFree(f->FA);
   cudaFree(f->FB);

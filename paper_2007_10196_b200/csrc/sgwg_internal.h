@@ -261,6 +261,8 @@ struct FieldParams {
   int nmtasks;
   int nmembers;
   double* rho_parts;       // kRhoParts partial sums per x point (see MemberDesc::rparts)
+  const double* twid;      // FFT twiddles: cos(pi q/hmax), then sin(pi q/hmax), q < hmax
+  int hmax;
   // field-energy diagnostic: members grouped by x-grid
   const int4* egrp;        // (n0, n1, offset in egrid, first group x point)
   const int2* egrp_m;      // (first, count) into egrp_mem
@@ -318,6 +320,7 @@ cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* t
                               const double* u, unsigned long long* amax, cudaStream_t s);
 cudaError_t configure_field();
 cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, cudaStream_t s);
+cudaError_t launch_twiddles(double* tw, int hmax, cudaStream_t s);
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
                                 double hvol, double* out_base, long long cap, cudaStream_t s);
 cudaError_t launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t s);

@@ -56,7 +56,8 @@ def test_c5_full_family_mass_and_charge_density(ctx, ctx_fast):
     assert np.all(np.isfinite(s1))
     ref = gpu_family(ctx, cfg)  # exact build, same start
     ref.upload(s0)
-    assert np.array_equal(ref.evolve_config(cfg, tfinal=0.006, stops=[]), dts)
+    # the dt comes from max|E|, whose last bits depend on the build's f
+    np.testing.assert_allclose(ref.evolve_config(cfg, tfinal=0.006, stops=[]), dts, rtol=1e-13)
     m0, m1, me = _member_sums(fam, s0), _member_sums(fam, s1), _member_sums(fam, ref.download())
     assert np.all(np.abs(m1 - m0) <= 1e-6 * np.abs(m0))
     assert np.all(np.abs(m1 - me) <= 1e-12 * np.abs(m0)), np.max(np.abs(m1 - me) / np.abs(m0))

@@ -12,9 +12,15 @@ from paper_2007_10196_b200 import build as B  # noqa: E402
 
 out, defs = sys.argv[1], sys.argv[2:]
 B.build()
-obj = os.path.join(B.OBJ, "k_fast_variant.o")
-cmd = [B.NVCC, "-c", os.path.join(B.CSRC, "k_fast.cu"), "-o", obj] + B.COMMON + B.UNITS["k_fast.cu"] + defs
-subprocess.run(cmd, check=True, capture_output=True)
-objs = [os.path.join(B.OBJ, u.replace(".cu", ".o")) for u in B.UNITS if u != "k_fast.cu"] + [obj]
+variant = ["k_fast.cu", "k_field.cu"]  # the TUs that take experiment -D flags
+objs = []
+for u in B.UNITS:
+    if u in variant:
+        obj = os.path.join(B.OBJ, u.replace(".cu", "_variant.o"))
+        cmd = [B.NVCC, "-c", os.path.join(B.CSRC, u), "-o", obj] + B.COMMON + B.UNITS[u] + defs
+        subprocess.run(cmd, check=True, capture_output=True)
+        objs.append(obj)
+    else:
+        objs.append(os.path.join(B.OBJ, u.replace(".cu", ".o")))
 subprocess.run([B.NVCC, "-shared", "-o", out] + objs + B.ARCH + ["-lnccl", "-lcudart"], check=True)
 print(out)

@@ -1,0 +1,5 @@
+x() { tail -1 gpurun_out/$1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', round(d['ms_per_step'],2))" 2>&1 | tail -1; }
+timeout 900 python -m pytest tests/test_gpu_vp.py tests/test_gpu_landau.py tests/test_gpu_fullsize.py -q -x > gpurun_out/pytest_c4c.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_c4c.log
+timeout 300 python bench.py --config C4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/c4d.log 2>&1; x c4d.log
+timeout 300 python bench.py --config C5 --tfinal 0.05 --no-combine --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/c5d.log 2>&1; x c5d.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4c.csv python bench.py --config C4 --tfinal 0.05 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_c4.log 2>&1
