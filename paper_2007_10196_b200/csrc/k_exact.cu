@@ -10,10 +10,12 @@
 #include <limits.h>
 
 #include "dt_device.cuh"
+#include "pdl.cuh"
 
 namespace sgwg {
 
 __global__ void local_speeds_kernel(const DtParams p) {
+  pdl_wait();
   if (!p.ctl->active) return;
   double sp[kMaxD + 1];
   device_local_speeds(p, sp);  // warp-cooperative
@@ -21,16 +23,17 @@ __global__ void local_speeds_kernel(const DtParams p) {
     for (int k = 0; k < kMaxD + 1; ++k) p.ctl->speeds[k] = sp[k];
 }
 
-__global__ void dt_kernel(const DtParams p) { device_step_dt(p, p.use_reduced != 0); }
+__global__ void dt_kernel(const DtParams p) {
+  pdl_wait();
+  device_step_dt(p, p.use_reduced != 0);
+}
 
 cudaError_t launch_local_speeds(const DtParams& p, cudaStream_t s) {
-  local_speeds_kernel<<<1, 32, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(local_speeds_kernel, dim3(1), dim3(32), 0, s, p);
 }
 
 cudaError_t launch_dt(const DtParams& p, cudaStream_t s) {
-  dt_kernel<<<1, 32, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(dt_kernel, dim3(1), dim3(32), 0, s, p);
 }
 
 // detail::max_abs (models.hpp:110-114) of every member, as u64 bit patterns
@@ -59,6 +62,7 @@ cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* t
 // s1 = max |E1(x2) + xi2 B3(x2)|, s2 = max |E2(x2) - xi1 B3(x2)| over the
 // member's x2 points and velocity coordinates (max is exact in any order)
 __global__ void __launch_bounds__(256) vm_speeds_kernel(const VmParams p) {
+  pdl_wait();
   if (p.ctl != nullptr && !p.ctl->active) return;
   const MemberDesc* M = p.mem + blockIdx.x;
   const int nx = M->nx, n1 = M->ext[1], n2 = M->ext[2];
@@ -93,8 +97,7 @@ __global__ void __launch_bounds__(256) vm_speeds_kernel(const VmParams p) {
 
 cudaError_t launch_vm_speeds(const VmParams& p, int nmembers, cudaStream_t s) {
   if (nmembers <= 0) return cudaSuccess;
-  vm_speeds_kernel<<<nmembers, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(vm_speeds_kernel, dim3(nmembers), dim3(256), 0, s, p);
 }
 
 // DFMA throughput probe: 8 independent FMA chains per thread.

@@ -7,10 +7,12 @@
 //                shared memory.
 // field_energy_kernel: per-step ||E_c||_2 diagnostic.
 #include "field_device.cuh"
+#include "pdl.cuh"
 
 namespace sgwg {
 
 __global__ void __launch_bounds__(256) moment_kernel(const FieldParams p) {
+  pdl_wait();
   if (p.ctl != nullptr && !p.ctl->active) return;
   const int2 tk = p.mtasks[blockIdx.x];
   const MemberDesc* M = p.mem + tk.x;
@@ -20,6 +22,7 @@ __global__ void __launch_bounds__(256) moment_kernel(const FieldParams p) {
 }
 
 __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams p) {
+  pdl_wait();
   if (p.ctl != nullptr && !p.ctl->active) return;
   extern __shared__ double sh[];
   __shared__ double red[2 * kFieldThreads / 32];
@@ -27,6 +30,7 @@ __global__ void __launch_bounds__(kFieldThreads) field_kernel(const FieldParams 
 }
 
 __global__ void __launch_bounds__(256) group_field_kernel(const FieldParams p, const double* coef) {
+  pdl_wait();
   if (p.ctl != nullptr && !p.ctl->active) return;
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   if (X < p.ngx) group_point<false>(p, coef, X);
@@ -35,6 +39,7 @@ __global__ void __launch_bounds__(256) group_field_kernel(const FieldParams p, c
 __global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p, int fine0,
                                                            int fine1, double hvol,
                                                            double* out_base, long long cap) {
+  pdl_wait();
   if (p.ctl != nullptr && !p.ctl->active) return;
   const long long slot = (p.ctl != nullptr) ? p.ctl->step : 0;  // the step about to be taken
   if (slot >= cap) return;
@@ -58,12 +63,15 @@ cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fi
                                 double hvol, double* out_base, long long cap, cudaStream_t s) {
   FieldParams q = p;
   q.ecoef = coef;
-  if (q.negrp > 0) group_field_kernel<<<(q.ngx + 255) / 256, 256, 0, s>>>(q, coef);
+  if (q.negrp > 0) {
+    cudaError_t e = launch_k(group_field_kernel, dim3((q.ngx + 255) / 256), dim3(256), 0, s, q, coef);
+    if (e != cudaSuccess) return e;
+  }
   int blocks = (q.negrp > 0) ? (fine0 * fine1 + 255) / 256  // a thread per point
                              : (fine0 * fine1 + 7) / 8;     // a warp per point
   if (blocks > 148 * 16) blocks = 148 * 16;
-  field_energy_kernel<<<blocks, 256, 0, s>>>(q, fine0, fine1, hvol, out_base, cap);
-  return cudaGetLastError();
+  return launch_k(field_energy_kernel, dim3(blocks), dim3(256), 0, s, q, fine0, fine1, hvol,
+                  out_base, cap);
 }
 
 __global__ void twiddle_kernel(double* tw, int hmax) {
@@ -83,9 +91,12 @@ cudaError_t configure_field() {
 
 cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, cudaStream_t s) {
   if (nmembers <= 0) return cudaSuccess;
-  if (with_moment) moment_kernel<<<p.nmtasks, 256, 0, s>>>(p);
-  field_kernel<<<nmembers, kFieldThreads, kFieldSmemDoubles * sizeof(double), s>>>(p);
-  return cudaGetLastError();
+  if (with_moment) {
+    cudaError_t e = launch_k(moment_kernel, dim3(p.nmtasks), dim3(256), 0, s, p);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_k(field_kernel, dim3(nmembers), dim3(kFieldThreads),
+                  kFieldSmemDoubles * sizeof(double), s, p);
 }
 
 }  // namespace sgwg

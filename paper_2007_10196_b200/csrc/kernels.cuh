@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include "dt_device.cuh"
+#include "pdl.cuh"
 #include "sgwg_internal.h"
 
 #ifndef SGWG_FAST
@@ -105,6 +106,7 @@ __device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
 // o*n*inner + i, element j at base + j*inner (grid.hpp:202-217, line_at order).
 template <bool BURGERS>
 __global__ void __launch_bounds__(kPassThreads) pass_kernel(const PassParams p) {
+  pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const int4 tk = p.tasks[blockIdx.x];
@@ -434,6 +436,7 @@ __device__ __forceinline__ double line_coef(int flux, const MemberDesc* M, int k
 
 template <bool BURGERS>
 __global__ void __launch_bounds__(256) stage2d_kernel(const Stage2DParams p) {
+  pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const int4 tk = p.tiles[blockIdx.x];
@@ -910,6 +913,7 @@ __device__ __forceinline__ void tile_body(const Stage2DParams& p, const MemberDe
 
 template <bool BURGERS>
 __global__ void __launch_bounds__(kFastThreads, 1) stage2d_fast_kernel(const Stage2DParams p) {
+  pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const int4 tk = p.tiles[blockIdx.x];
@@ -1106,6 +1110,7 @@ __device__ __forceinline__ void stage3d_fast_body(const Stage2DParams& p, const 
 constexpr int kStage3DThreads = 768;
 
 __global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_fast_kernel(const Stage2DParams p) {
+  pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const int4 tk = p.tiles[blockIdx.x];
@@ -1288,6 +1293,7 @@ __device__ __forceinline__ void stage3d_issue_any(const Stage2DParams& p, int4 t
 }
 
 __global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_pipe_kernel(const Stage2DParams p) {
+  pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   extern __shared__ double sm[];
@@ -1409,6 +1415,7 @@ __device__ __forceinline__ void plane_sweeps(const PlaneGeom& G, const double* F
 }
 
 __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_kernel(const PlaneParams p) {
+  pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const PlaneTile tl = p.tiles[blockIdx.x];
@@ -1725,18 +1732,15 @@ cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cud
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     Stage2DParams q = p;
     q.ntiles = nblocks;
-    stage3d_pipe_kernel<<<min(nblocks, sms), kStage3DThreads,
-                          (2 * kPipe3DBox + 3 * kPipe3DDn) * sizeof(double), s>>>(q);
-    return cudaGetLastError();
+    return launch_k(stage3d_pipe_kernel, dim3(min(nblocks, sms)), dim3(kStage3DThreads),
+                    (2 * kPipe3DBox + 3 * kPipe3DDn) * sizeof(double), s, q);
   }
-  stage3d_fast_kernel<<<nblocks, kStage3DThreads, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(stage3d_fast_kernel, dim3(nblocks), dim3(kStage3DThreads), smem, s, p);
 }
 
 cudaError_t launch_plane(const PlaneParams& p, int nblocks, size_t smem, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
-  plane_fast_kernel<<<nblocks, kPlaneThreads, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(plane_fast_kernel, dim3(nblocks), dim3(kPlaneThreads), smem, s, p);
 }
 
 int plane_smem_doubles(int nv, int tx, int ty) { return PlaneGeom(nv, tx, ty).smem_doubles(); }
@@ -1942,6 +1946,7 @@ cudaError_t launch_eval_points(const EvalParams& p, cudaStream_t s) {
 // dimension k of prolong for a batch of members: dst has finest extent along
 // k, src the member's current extents (finest for dims < k).
 __global__ void __launch_bounds__(256) upsample_kernel(const UpsampleParams p) {
+  pdl_wait();
   const int2 tk = p.tasks[blockIdx.x];
   const int slot = tk.x;
   const int mi = p.slot_member[slot];
@@ -1970,6 +1975,7 @@ __global__ void __launch_bounds__(256) upsample_kernel(const UpsampleParams p) {
 
 // last dimension of prolong fused with acc += c*p over members in sorted order.
 __global__ void __launch_bounds__(256) final_kernel(const FinalParams p) {
+  pdl_wait();
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long first = p.row0 * (long long)p.fine_last;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < p.nfine; q += stride) {
@@ -2022,6 +2028,7 @@ __device__ __forceinline__ double vm_fhat(const double* w, int n, int k, double 
 }
 
 __global__ void __launch_bounds__(256) vm_fields_kernel(const VmParams p) {
+  pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   const int mi = blockIdx.x;
@@ -2100,8 +2107,7 @@ __global__ void __launch_bounds__(256) vm_fields_kernel(const VmParams p) {
 
 cudaError_t launch_vm_fields(const VmParams& p, int nmembers, int smem, cudaStream_t s) {
   if (nmembers <= 0) return cudaSuccess;
-  vm_fields_kernel<<<nmembers, 256, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(vm_fields_kernel, dim3(nmembers), dim3(256), (size_t)smem, s, p);
 }
 
 cudaError_t configure() {
@@ -2139,14 +2145,14 @@ cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cud
   if (nblocks <= 0) return cudaSuccess;
 #if SGWG_FAST
   if (p.burgers)
-    stage2d_fast_kernel<true><<<nblocks, kFastThreads, smem, s>>>(p);
+    return launch_k(stage2d_fast_kernel<true>, dim3(nblocks), dim3(kFastThreads), smem, s, p);
   else
-    stage2d_fast_kernel<false><<<nblocks, kFastThreads, smem, s>>>(p);
+    return launch_k(stage2d_fast_kernel<false>, dim3(nblocks), dim3(kFastThreads), smem, s, p);
 #else
   if (p.burgers)
-    stage2d_kernel<true><<<nblocks, 256, smem, s>>>(p);
+    return launch_k(stage2d_kernel<true>, dim3(nblocks), dim3(256), smem, s, p);
   else
-    stage2d_kernel<false><<<nblocks, 256, smem, s>>>(p);
+    return launch_k(stage2d_kernel<false>, dim3(nblocks), dim3(256), smem, s, p);
 #endif
   return cudaGetLastError();
 }
@@ -2154,24 +2160,22 @@ cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cud
 cudaError_t launch_pass(const PassParams& p, int nblocks, size_t smem, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
   if (p.flux == kFluxBurgers)
-    pass_kernel<true><<<nblocks, kPassThreads, smem, s>>>(p);
+    return launch_k(pass_kernel<true>, dim3(nblocks), dim3(kPassThreads), smem, s, p);
   else
-    pass_kernel<false><<<nblocks, kPassThreads, smem, s>>>(p);
+    return launch_k(pass_kernel<false>, dim3(nblocks), dim3(kPassThreads), smem, s, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
-  upsample_kernel<<<nblocks, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(upsample_kernel, dim3(nblocks), dim3(256), 0, s, p);
 }
 
 cudaError_t launch_final(const FinalParams& p, cudaStream_t s) {
   if (p.nfine <= 0) return cudaSuccess;
   long long blocks = (p.nfine + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  final_kernel<<<(int)blocks, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(final_kernel, dim3((int)blocks), dim3(256), 0, s, p);
 }
 
 }  // namespace SGWG_NS
