@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(256) field_energy_kernel(const FieldParams p, 
                                                            double* out_base, long long cap) {
   pdl_wait();
   if (p.ctl != nullptr && !p.ctl->active) return;
-  const long long slot = (p.ctl != nullptr) ? p.ctl->step : 0;  // the step about to be taken
+  // launched after the step's dt kernel: the step being taken is step - 1
+  const long long slot = (p.ctl != nullptr) ? p.ctl->step - 1 : 0;
   if (slot >= cap) return;
   double acc = 0.0;
   if (p.negrp > 0) {  // groups (large fine grids): one thread per finest x point

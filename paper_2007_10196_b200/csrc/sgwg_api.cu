@@ -190,6 +190,7 @@ struct sgwg_family {
   double* fe = nullptr;     // per-step sum of |E_combined|^2 h (Vlasov-Poisson diagnostic)
   long long fe_cap = 0;
   double* dcoef = nullptr;  // combination coefficient of each local member
+  FieldParams energy_fp{};  // the stage-1 field parameters of the current step
   int4* degrp = nullptr;     // field-energy groups (members sharing an x-grid)
   int2* degrp_m = nullptr;
   int* degrp_mem = nullptr;
@@ -213,6 +214,8 @@ struct sgwg_family {
   int nranks = 1, rank = 0;
   sgwg_stats stats{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t side = nullptr;                 // off-critical-path work (energy record)
+  cudaEvent_t evfork = nullptr, evjoin = nullptr;
   // current policy for graph building
   DtParams dtp{};
   DtParams* d_dtp = nullptr;       // device copy (fused dt)
@@ -328,14 +331,24 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
   CK(launch_field(fp, f->nm, with_moment, f->ctx->stream));
   f->parts_of = state;
   f->stats.kernel_launches += with_moment ? 2 : 1;
-  if (with_energy && f->fe != nullptr) {  // ||E||_2 of u^n, recorded per step
-    const int dx = m.space_dim;
-    const int fine1 = (dx == 2) ? f->fine_ext[1] : 1;
-    const double hvol = f->fine_h[0] * ((dx == 2) ? f->fine_h[1] : 1.0);
-    CK(launch_field_energy(fp, f->dcoef, f->fine_ext[0], fine1, hvol, f->fe, f->fe_cap,
-                           f->ctx->stream));
-    f->stats.kernel_launches += (fp.negrp > 0) ? 2 : 1;
-  }
+  if (with_energy) f->energy_fp = fp;  // recorded after the dt (launch_step)
+  return SGWG_OK;
+}
+
+// ||E||_2 of u^n for the step record, on the side stream: forked after the
+// step's dt kernel, joined before stage 2's field solve overwrites E, so it
+// runs concurrently with stage 1
+int launch_energy_side(sgwg_family* f) {
+  if (f->fe == nullptr) return SGWG_OK;
+  const FieldParams& fp = f->energy_fp;
+  const int dx = f->model.space_dim;
+  const int fine1 = (dx == 2) ? f->fine_ext[1] : 1;
+  const double hvol = f->fine_h[0] * ((dx == 2) ? f->fine_h[1] : 1.0);
+  CK(cudaEventRecord(f->evfork, f->ctx->stream));
+  CK(cudaStreamWaitEvent(f->side, f->evfork, 0));
+  CK(launch_field_energy(fp, f->dcoef, f->fine_ext[0], fine1, hvol, f->fe, f->fe_cap, f->side));
+  CK(cudaEventRecord(f->evjoin, f->side));
+  f->stats.kernel_launches += (fp.negrp > 0) ? 2 : 1;
   return SGWG_OK;
 }
 
@@ -590,11 +603,13 @@ int launch_step(sgwg_family* f, bool timed) {
       f->stats.kernel_launches++;
     }
     TRY(launch_dt_step(f));
+    if (vp) TRY(launch_energy_side(f));
   }
   // stage 1: u -> A; stage 2: (A, u) -> B; stage 3: (B, u) -> u (timestep.hpp:91-103)
   StageBufs s1{f->u, f->u, f->A}, s2{f->A, f->u, f->B}, s3{f->B, f->u, f->u};
   // VP: the stage-1 field was computed above (it feeds dt); stages 2, 3 recompute it
   TRY(launch_stage(f, 1, s1, timed, /*with_field=*/!vp));
+  if (vp && !fused && f->fe != nullptr) CK(cudaStreamWaitEvent(f->ctx->stream, f->evjoin, 0));
   TRY(launch_stage(f, 2, s2, timed));
   TRY(launch_stage(f, 3, s3, timed, true, fused));
   return SGWG_OK;
@@ -810,6 +825,9 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   f->no_fused2d = std::getenv("SGWG_NO_FUSED2D") != nullptr;
   CK(cudaEventCreate(&f->ev0));
   CK(cudaEventCreate(&f->ev1));
+  CK(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&f->evfork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&f->evjoin, cudaEventDisableTiming));
   int st = build_tasks(f);
   if (st != SGWG_OK) return st;
   CK(cudaMalloc(&f->dmem, sizeof(MemberDesc) * std::max(1, f->nm)));
@@ -1518,6 +1536,9 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->slab_out);
   cudaEventDestroy(f->ev0);
   cudaEventDestroy(f->ev1);
+  cudaEventDestroy(f->evfork);
+  cudaEventDestroy(f->evjoin);
+  cudaStreamDestroy(f->side);
   delete f;
   return SGWG_OK;
 }
