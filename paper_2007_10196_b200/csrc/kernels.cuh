@@ -911,8 +911,25 @@ __device__ __forceinline__ void tile_body(const Stage2DParams& p, const MemberDe
   }
 }
 
+// half-size tiles (1024 points, 256 threads): two CTAs per SM, so one CTA's
+// staging / epilogue overlaps the other's sweeps (large families; the
+// 2048-point tiles above stay for the persistent small-family kernel)
 template <bool BURGERS>
-__global__ void __launch_bounds__(kFastThreads, 1) stage2d_fast_kernel(const Stage2DParams p) {
+__device__ __forceinline__ void tile_body_half(const Stage2DParams& p, const MemberDesc* M,
+                                               int4 tk, double* sm) {
+  switch (tk.w) {  // TX*TY = 1024, 256 threads
+    case 4: stage2d_fast_body<BURGERS, false, 32, 32>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 5: stage2d_fast_body<BURGERS, false, 16, 64>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 6: stage2d_fast_body<BURGERS, false, 64, 16>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 7: stage2d_fast_body<BURGERS, false, 8, 128>(p, M, tk.x, tk.y, tk.z, sm); break;
+    default: stage2d_fast_body<BURGERS, false, 128, 8>(p, M, tk.x, tk.y, tk.z, sm); break;
+  }
+}
+constexpr int kHalfThreads = kFastThreads / 2;
+
+template <bool BURGERS, bool HALF>
+__global__ void __launch_bounds__(HALF ? kHalfThreads : kFastThreads, HALF ? 2 : 1)
+    stage2d_fast_kernel(const Stage2DParams p) {
   pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
@@ -921,7 +938,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) stage2d_fast_kernel(const Sta
   extern __shared__ double sm[];
   if (p.amax_zero != nullptr && blockIdx.x == 0)
     for (int i = threadIdx.x; i < p.nmembers; i += blockDim.x) p.amax_zero[i] = 0ull;
-  tile_body<BURGERS, false>(p, M, tk, sm);
+  if (HALF)
+    tile_body_half<BURGERS>(p, M, tk, sm);
+  else
+    tile_body<BURGERS, false>(p, M, tk, sm);
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
 }
 
@@ -2112,10 +2132,16 @@ cudaError_t launch_vm_fields(const VmParams& p, int nmembers, int smem, cudaStre
 
 cudaError_t configure() {
 #if SGWG_FAST
-  cudaError_t e0 = cudaFuncSetAttribute(stage2d_fast_kernel<true>,
+  cudaError_t e0 = cudaFuncSetAttribute(stage2d_fast_kernel<true, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(stage2d_fast_kernel<false>,
+  e0 = cudaFuncSetAttribute(stage2d_fast_kernel<false, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage2d_fast_kernel<true, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage2d_fast_kernel<false, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(stage3d_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2144,10 +2170,19 @@ cudaError_t configure() {
 cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
 #if SGWG_FAST
+  if (p.half_tiles) {
+    if (p.burgers)
+      return launch_k(stage2d_fast_kernel<true, true>, dim3(nblocks), dim3(kHalfThreads), smem,
+                      s, p);
+    return launch_k(stage2d_fast_kernel<false, true>, dim3(nblocks), dim3(kHalfThreads), smem, s,
+                    p);
+  }
   if (p.burgers)
-    return launch_k(stage2d_fast_kernel<true>, dim3(nblocks), dim3(kFastThreads), smem, s, p);
+    return launch_k(stage2d_fast_kernel<true, false>, dim3(nblocks), dim3(kFastThreads), smem, s,
+                    p);
   else
-    return launch_k(stage2d_fast_kernel<false>, dim3(nblocks), dim3(kFastThreads), smem, s, p);
+    return launch_k(stage2d_fast_kernel<false, false>, dim3(nblocks), dim3(kFastThreads), smem,
+                    s, p);
 #else
   if (p.burgers)
     return launch_k(stage2d_kernel<true>, dim3(nblocks), dim3(256), smem, s, p);

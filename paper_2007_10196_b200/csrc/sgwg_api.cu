@@ -226,6 +226,9 @@ struct sgwg_family {
   int smem2d = 0;
   int4* dtiles2d_fast = nullptr;
   int ntiles2d_fast = 0;
+  int4* dtiles2d_half = nullptr;  // 1024-point tiles of the stage kernel (two CTAs per SM)
+  int ntiles2d_half = 0;
+  int smem2d_half = 0;
   int smem2d_fast = 0;
   int4* dtiles3d_fast = nullptr;  // fast 3D stage tiles (advection)
   int ntiles3d_fast = 0;
@@ -288,6 +291,16 @@ void account_timed(sgwg_family* f, int stage, int npass_dims, bool last, float m
     f->stats.pass_flops += pts * (stage == 1 ? 2.0 : 5.0);
     f->stats.pass_bytes += pts * (stage == 1 ? 16.0 : 24.0);
   }
+}
+
+// fast 2D stage kernel on 1024-point tiles (two CTAs per SM); SGWG_TILE2D=2048
+// selects the 2048-point tiles (one CTA per SM) for experiments
+bool half_tiles_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("SGWG_TILE2D");
+    return (e != nullptr && std::string(e) == "2048") ? 0 : 1;
+  }();
+  return v != 0;
 }
 
 // fast 4D plane path (kernels.cuh plane_fast_kernel)
@@ -476,6 +489,14 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     const bool fastk = arith_of(f) == SGWG_ARITH_FAST;
     p.mem = f->dmem;
     p.tiles = fastk ? f->dtiles2d_fast : f->dtiles2d;
+    int nt = fastk ? f->ntiles2d_fast : f->ntiles2d;
+    size_t smem = (size_t)(fastk ? f->smem2d_fast : f->smem2d) * sizeof(double);
+    if (fastk && half_tiles_enabled()) {
+      p.tiles = f->dtiles2d_half;
+      p.half_tiles = 1;
+      nt = f->ntiles2d_half;
+      smem = (size_t)f->smem2d_half * sizeof(double);
+    }
     p.burgers = burgers;
     p.flux0 = order[0].flux;
     p.flux1 = order[1].flux;
@@ -499,10 +520,8 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     p.dtp = dtp;
     p.counter = f->counter;
     if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
-    CK(fastk ? fast::launch_stage2d(p, f->ntiles2d_fast,
-                                    (size_t)f->smem2d_fast * sizeof(double), f->ctx->stream)
-             : exact::launch_stage2d(p, f->ntiles2d, (size_t)f->smem2d * sizeof(double),
-                                     f->ctx->stream));
+    CK(fastk ? fast::launch_stage2d(p, nt, smem, f->ctx->stream)
+             : exact::launch_stage2d(p, nt, smem, f->ctx->stream));
     if (timed) {
       CK(cudaEventRecord(f->ev1, f->ctx->stream));
       CK(cudaEventSynchronize(f->ev1));
@@ -684,6 +703,34 @@ int build_tasks(sgwg_family* f) {
     f->smem2d_fast = sfmax;
     CK(cudaMalloc(&f->dtiles2d_fast, sizeof(int4) * std::max<size_t>(1, tf.size())));
     CK(cudaMemcpy(f->dtiles2d_fast, tf.data(), sizeof(int4) * tf.size(), cudaMemcpyHostToDevice));
+    // stage-kernel tiles: 1024 points in {(32,32),(16,64),(64,16),(8,128),(128,8)}
+    // (kernels.cuh tile_body_half, shape codes 4..8)
+    static const int shh[5][2] = {{32, 32}, {16, 64}, {64, 16}, {8, 128}, {128, 8}};
+    std::vector<int4> th;
+    int shmax = 0;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      const MemberDesc& M = f->hmem[mi];
+      int best = 0;
+      long long bw = -1;
+      for (int s = 0; s < 5; ++s) {
+        const long long cov = (long long)((M.ext[0] + shh[s][0] - 1) / shh[s][0]) * shh[s][0] *
+                              ((M.ext[1] + shh[s][1] - 1) / shh[s][1]) * shh[s][1];
+        if (bw < 0 || cov < bw) {
+          bw = cov;
+          best = s;
+        }
+      }
+      const int TX = shh[best][0], TY = shh[best][1];
+      const int PY = ((TY + 6) % 2 == 0) ? TY + 7 : TY + 6;
+      const int sm = 2 * (TX + 6) * PY + 2 * TX * (TY + 1) + TX + TY;
+      shmax = std::max(shmax, sm);
+      for (int i0 = 0; i0 < M.ext[0]; i0 += TX)
+        for (int j0 = 0; j0 < M.ext[1]; j0 += TY) th.push_back(make_int4(mi, i0, j0, 4 + best));
+    }
+    f->ntiles2d_half = (int)th.size();
+    f->smem2d_half = shmax;
+    CK(cudaMalloc(&f->dtiles2d_half, sizeof(int4) * std::max<size_t>(1, th.size())));
+    CK(cudaMemcpy(f->dtiles2d_half, th.data(), sizeof(int4) * th.size(), cudaMemcpyHostToDevice));
   }
   if (f->d == 3 && !f->no_fused2d) {  // fast 3D stage tiles: 2048 points, 3 shapes
     static const int shp3[3][3] = {{8, 16, 16}, {16, 8, 16}, {16, 16, 8}};
@@ -1508,6 +1555,7 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->counter);
   cudaFree(f->dtiles2d);
   cudaFree(f->dtiles2d_fast);
+  cudaFree(f->dtiles2d_half);
   cudaFree(f->dtiles3d_fast);
   cudaFree(f->dptiles[0]);
   cudaFree(f->dptiles[1]);

@@ -127,6 +127,7 @@ struct Stage2DParams {
   int resident;       // one tile per CTA: stage input / u^n kept in shared memory
   int resident_load;  // first stage of the launch: fill the resident copy from HBM
   int trace_ss;       // step * 3 + stage - 1 (phase-trace experiment builds)
+  int half_tiles;     // fast stage kernel on 1024-point tiles (two CTAs per SM)
 };
 
 struct PersistParams {
