@@ -748,21 +748,22 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   const double* u = p.uin + M->offset;
   const double alpha = BURGERS ? __longlong_as_double((long long)p.amax_in[mi]) : 0.0;
   const int bc0 = M->bc[0], bc1 = M->bc[1];
-  // global index of tile-relative padded position (a, b) with the boundary
-  // treatment of weno.hpp:131-136 (periodic wrap / zero ghosts); -1 = zero.
-  auto gindex = [&](int a, int b) -> int {
-    int gi = i0 - 3 + a, gj = j0 - 3 + b;
-    if (gi < 0 || gi >= n0) {
-      if (bc0 != 0) return -1;
-      gi %= n0;
-      if (gi < 0) gi += n0;
-    }
-    if (gj < 0 || gj >= n1) {
-      if (bc1 != 0) return -1;
-      gj %= n1;
-      if (gj < 0) gj += n1;
-    }
-    return gi * n1 + gj;
+  // global row offset / column of tile-relative padded position a / b with the
+  // boundary treatment of weno.hpp:131-136 (periodic wrap / zero ghosts), -1 =
+  // zero.  Valid outputs read at most 3 points past a member edge (periodic
+  // lines have n >= 6); positions further out are padding of a partial tile
+  // and read as zero.  Branch-free: no modulo on the runtime extents.
+  auto grow = [&](int a) -> int {
+    const int gi = i0 - 3 + a;
+    const int w = (gi < 0) ? gi + n0 : (gi >= n0 ? gi - n0 : gi);
+    const bool z = (gi < 0 || gi >= n0) && (bc0 != 0 || gi >= n0 + 3);
+    return z ? -1 : w * n1;
+  };
+  auto gcol = [&](int b) -> int {
+    const int gj = j0 - 3 + b;
+    const int w = (gj < 0) ? gj + n1 : (gj >= n1 ? gj - n1 : gj);
+    const bool z = (gj < 0 || gj >= n1) && (bc1 != 0 || gj >= n1 + 3);
+    return z ? -1 : w;
   };
   auto split_store = [&](int a, int b, double uj) {
     if (BURGERS) {
@@ -774,11 +775,16 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
       FP[a * PY + b] = uj;
     }
   };
-  // tile interior: NE points per thread (also the epilogue's u_in), then the
-  // 3-wide halos of the two axes; all loads issued before any use
+  // tile interior: NE points per thread in one column (j = tid % TY, rows
+  // tid / TY + e * RS; also the epilogue's points and u_in), then the 3-wide
+  // halos of the two axes; all loads issued before any use
   constexpr int NE = TX * TY / NT;
-  constexpr int NH = 6 * (TX + TY);
+  constexpr int RS = NT / TY;  // row step of a thread's interior points
+  static_assert(NT % TY == 0, "tile width must divide the thread count");
+  constexpr int NHR = 6 * TY, NH = 6 * (TX + TY);
   constexpr int NHL = (NH + NT - 1) / NT;
+  const int tj = tid % TY, tr = tid / TY;
+  const int ccol = gcol(tj + 3);
   double vin[NE], pre_n[NE], vh[NHL];
   int ih[NHL];
   // resident tile (persistent launch, one tile per CTA): the tile's own stage
@@ -789,15 +795,17 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   const bool resident = PERSIST && p.resident;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    const int q = tid + e * NT;
-    const bool inside = (i0 + q / TY < n0) && (j0 + q % TY < n1);
+    const int q = tid + e * NT, ti = tr + e * RS;
+    const bool inside = (i0 + ti < n0) && (j0 + tj < n1);
     if (resident && !p.resident_load && inside) {
       vin[e] = UC[q];
       pre_n[e] = UN[q];
     } else {
-      const int g = gindex(q / TY + 3, q % TY + 3);
-      vin[e] = (g >= 0) ? ldx<PERSIST>(u + g) : 0.0;
-      pre_n[e] = (p.stage > 1 && g >= 0) ? ldx<PERSIST>(p.un + M->offset + g) : 0.0;
+      const int ro = grow(ti + 3);
+      const bool ok = ro >= 0 && ccol >= 0;
+      const int g = ro + ccol;
+      vin[e] = ok ? ldx<PERSIST>(u + g) : 0.0;
+      pre_n[e] = (p.stage > 1 && ok) ? ldx<PERSIST>(p.un + M->offset + g) : 0.0;
       if (resident && inside) {
         UC[q] = vin[e];
         UN[q] = (p.stage == 1) ? vin[e] : pre_n[e];
@@ -807,28 +815,35 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
 #pragma unroll
   for (int e = 0; e < NHL; ++e) {
     const int h = tid + e * NT;
-    int a = 0, b = 0;
-    if (h < 6 * TY) {
+    int a, b;
+    if (h < NHR) {  // 3 rows above / below: (r6, column), columns fastest
       const int r6 = h / TY;
       a = (r6 < 3) ? r6 : TX + r6;
       b = h % TY + 3;
-    } else {
-      const int h2 = h - 6 * TY, c6 = h2 % 6;
+    } else {  // 3 columns left / right: (row, c6), c6 fastest
+      const int h2 = h - NHR, c6 = h2 % 6;
       a = h2 / 6 + 3;
       b = (c6 < 3) ? c6 : TY + c6;
     }
-    ih[e] = (h < NH) ? a * 1024 + b : -1;
-    const int g = (h < NH) ? gindex(a, b) : -1;
-    vh[e] = (g >= 0) ? ldx<PERSIST>(u + g) : 0.0;
+    const int ro = (h < NH) ? grow(a) : -1, co = gcol(b);
+    ih[e] = (h < NH) ? a * PY + b : -1;
+    vh[e] = (ro >= 0 && co >= 0) ? ldx<PERSIST>(u + ro + co) : 0.0;
   }
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const int q = tid + e * NT;
-    split_store(q / TY + 3, q % TY + 3, vin[e]);
-  }
+  for (int e = 0; e < NE; ++e) split_store(tr + e * RS + 3, tj + 3, vin[e]);
 #pragma unroll
   for (int e = 0; e < NHL; ++e)
-    if (ih[e] >= 0) split_store(ih[e] >> 10, ih[e] & 1023, vh[e]);
+    if (ih[e] >= 0) {
+      const double uj = vh[e];
+      if (BURGERS) {
+        const double f = 0.5 * uj * uj;
+        const double fpj = 0.5 * (f + alpha * uj);
+        FP[ih[e]] = fpj;
+        FM[ih[e]] = f - fpj;
+      } else {
+        FP[ih[e]] = uj;
+      }
+    }
   __syncthreads();
   if (PERSIST) SGWG_MARK(p.trace_ss, 1);
   const double eps4 = 4.0 * p.eps;
@@ -854,16 +869,17 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   __syncthreads();
   if (PERSIST) SGWG_MARK(p.trace_ss, 2);
   // epilogue: k = (0 - du_x) - du_y, RK stage, coalesced along j
-  double lmax = 0.0;
+  // max|out| as the u64 bit pattern (non-negative doubles order as integers)
+  unsigned long long lmax = 0ull;
   const StepCtl* ctl = p.ctl;
   const double dt = PERSIST ? p.dt_value : ((ctl != nullptr) ? ctl->dt : 0.0);
+  double* outp = p.out + M->offset + (long long)(i0 + tr) * n1 + (j0 + tj);
+  const bool colok = j0 + tj < n1;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    const int q = tid + e * NT;
-    const int ti = q / TY, tj = q % TY;
-    if (i0 + ti >= n0 || j0 + tj >= n1) continue;
+    const int ti = tr + e * RS;
+    if (!colok || i0 + ti >= n0) continue;
     const double kv = (0.0 - DX[ti * DP + tj]) - DY[ti * DP + tj];
-    const long long gi = M->offset + (long long)(i0 + ti) * n1 + (j0 + tj);
     double o;
     if (p.stage == 0) {
       o = kv;
@@ -880,22 +896,28 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
       else
         o = fma(1.0 / 3.0, pre_n[e], (2.0 / 3.0) * fma(dt, kv, ui));
     }
-    p.out[gi] = o;
+    outp[(long long)e * RS * n1] = o;
     if (resident) {  // next stage's input (and u^{n+1} after stage 3) stay on chip
+      const int q = tid + e * NT;
       UC[q] = o;
       if (p.stage == 3) UN[q] = o;
     }
-    lmax = fmax(lmax, fabs(o));
+    const unsigned long long ob = (unsigned long long)__double_as_longlong(fabs(o));
+    lmax = (ob > lmax) ? ob : lmax;
   }
   if (p.track_max) {  // one atomic per CTA (max is exact in any order)
-    __shared__ double wmax[kFastThreads / 32];
-    lmax = warp_max(lmax);
-    if ((tid & 31) == 0) wmax[tid >> 5] = lmax;
+    __shared__ unsigned long long wmax[kFastThreads / 32];
+    // exact u64 warp max from two 32-bit reductions (high word, then the low
+    // word among the lanes holding the maximal high word)
+    const unsigned hi = (unsigned)(lmax >> 32);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)lmax : 0u);
+    if ((tid & 31) == 0) wmax[tid >> 5] = ((unsigned long long)mh << 32) | ml;
     __syncthreads();
     if (tid == 0) {
-      double m = 0.0;
-      for (int w = 0; w < NT / 32; ++w) m = fmax(m, wmax[w]);
-      atomicMax(p.amax_out + mi, (unsigned long long)__double_as_longlong(m));
+      unsigned long long m = 0ull;
+      for (int w = 0; w < NT / 32; ++w) m = (wmax[w] > m) ? wmax[w] : m;
+      atomicMax(p.amax_out + mi, m);
     }
   }
 }
