@@ -936,15 +936,15 @@ __device__ __forceinline__ void tile_body(const Stage2DParams& p, const MemberDe
 // half-size tiles (1024 points, 256 threads): two CTAs per SM, so one CTA's
 // staging / epilogue overlaps the other's sweeps (large families; the
 // 2048-point tiles above stay for the persistent small-family kernel)
-template <bool BURGERS>
+template <bool BURGERS, bool PERSIST = false>
 __device__ __forceinline__ void tile_body_half(const Stage2DParams& p, const MemberDesc* M,
                                                int4 tk, double* sm) {
   switch (tk.w) {  // TX*TY = 1024, 256 threads
-    case 4: stage2d_fast_body<BURGERS, false, 32, 32>(p, M, tk.x, tk.y, tk.z, sm); break;
-    case 5: stage2d_fast_body<BURGERS, false, 16, 64>(p, M, tk.x, tk.y, tk.z, sm); break;
-    case 6: stage2d_fast_body<BURGERS, false, 64, 16>(p, M, tk.x, tk.y, tk.z, sm); break;
-    case 7: stage2d_fast_body<BURGERS, false, 8, 128>(p, M, tk.x, tk.y, tk.z, sm); break;
-    default: stage2d_fast_body<BURGERS, false, 128, 8>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 4: stage2d_fast_body<BURGERS, PERSIST, 32, 32>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 5: stage2d_fast_body<BURGERS, PERSIST, 16, 64>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 6: stage2d_fast_body<BURGERS, PERSIST, 64, 16>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 7: stage2d_fast_body<BURGERS, PERSIST, 8, 128>(p, M, tk.x, tk.y, tk.z, sm); break;
+    default: stage2d_fast_body<BURGERS, PERSIST, 128, 8>(p, M, tk.x, tk.y, tk.z, sm); break;
   }
 }
 constexpr int kHalfThreads = kFastThreads / 2;
@@ -1707,8 +1707,8 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
 // post-barrier data (deterministic, so all CTAs agree) on its own copy of the
 // step-control block, and CTA 0 publishes it.  Loads of data written by other
 // CTAs in this launch go through L2 (ld.global.cg).
-template <bool BURGERS>
-__global__ void __launch_bounds__(kFastThreads, 1)
+template <bool BURGERS, bool HALF>
+__global__ void __launch_bounds__(HALF ? kHalfThreads : kFastThreads, HALF ? 2 : 1)
     evolve2d_persistent_kernel(const PersistParams pp) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1746,7 +1746,10 @@ __global__ void __launch_bounds__(kFastThreads, 1)
           pp.base.amax_zero[(size_t)((s + 1) % 3) * nm + i] = 0ull;
       for (int t = blockIdx.x; t < pp.base.ntiles; t += gridDim.x) {
         const int4 tk = pp.base.tiles[t];
-        tile_body<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
+        if (HALF)
+          tile_body_half<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
+        else
+          tile_body<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
         __syncthreads();
       }
       SGWG_MARK(p.trace_ss, 3);
@@ -1789,21 +1792,22 @@ int plane_smem_doubles(int nv, int tx, int ty) { return PlaneGeom(nv, tx, ty).sm
 
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s) {
   void* args[] = {(void*)&p};
-  if (p.base.burgers)
-    return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<true>, nblocks,
-                                       kFastThreads,
-                                       args, smem, s);
-  return cudaLaunchCooperativeKernel((void*)evolve2d_persistent_kernel<false>, nblocks,
-                                     kFastThreads, args,
-                                     smem, s);
+  const bool h = p.base.half_tiles != 0;
+  const void* fn = p.base.burgers ? (h ? (const void*)evolve2d_persistent_kernel<true, true>
+                                       : (const void*)evolve2d_persistent_kernel<true, false>)
+                                  : (h ? (const void*)evolve2d_persistent_kernel<false, true>
+                                       : (const void*)evolve2d_persistent_kernel<false, false>);
+  return cudaLaunchCooperativeKernel(fn, nblocks, h ? kHalfThreads : kFastThreads, args, smem, s);
 }
 
-int persist2d_max_blocks(int burgers, size_t smem) {
+int persist2d_max_blocks(int burgers, int half, size_t smem) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, burgers ? (const void*)evolve2d_persistent_kernel<true>
-                       : (const void*)evolve2d_persistent_kernel<false>,
-      kFastThreads, smem);
+  const void* fn = burgers ? (half ? (const void*)evolve2d_persistent_kernel<true, true>
+                                   : (const void*)evolve2d_persistent_kernel<true, false>)
+                           : (half ? (const void*)evolve2d_persistent_kernel<false, true>
+                                   : (const void*)evolve2d_persistent_kernel<false, false>);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, half ? kHalfThreads : kFastThreads,
+                                                smem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2175,10 +2179,16 @@ cudaError_t configure() {
   e0 = cudaFuncSetAttribute(stage3d_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (2 * kPipe3DBox + 3 * kPipe3DDn) * (int)sizeof(double));
   if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true>,
+  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true, false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<false>,
+  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<false, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<false, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
 #endif

@@ -1841,19 +1841,28 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   // small 2D families (fast build, single rank): persistent cooperative kernel
   PersistParams pp{};
   int persist_blocks = 0;
-  // + the resident tile (stage input and u^n, 2 x 2048 doubles)
-  const size_t persist_smem = ((size_t)f->smem2d_fast + 2 * 2048) * sizeof(double);
-  if (arith_of(f) == SGWG_ARITH_FAST && f->d == 2 && f->ntiles2d_fast > 0 && dt_fusable(f) &&
+  // 1024-point tiles, two CTAs per SM (measured: C1 34.2 -> 30.1 ms, C2 34.6 -> 34.3 ms
+  // against 2048-point tiles, one per SM; SGWG_PERSIST_HALF=0 selects those)
+  const char* ph = std::getenv("SGWG_PERSIST_HALF");
+  const bool phalf = !(ph != nullptr && ph[0] == '0');
+  const int pntiles = phalf ? f->ntiles2d_half : f->ntiles2d_fast;
+  // + the resident tile (stage input and u^n)
+  const size_t persist_smem =
+      phalf ? ((size_t)f->smem2d_half + 2 * 1024) * sizeof(double)
+            : ((size_t)f->smem2d_fast + 2 * 2048) * sizeof(double);
+  if (arith_of(f) == SGWG_ARITH_FAST && f->d == 2 && pntiles > 0 && dt_fusable(f) &&
       !f->ctx->profile && std::getenv("SGWG_NO_PERSIST") == nullptr) {
     // one tile per CTA (tiles resident in shared memory across stages); larger
     // families run faster as graph-captured stage launches (measured: S2)
-    const int maxb = fast::persist2d_max_blocks(f->model.kind == SGWG_BURGERS, persist_smem);
-    persist_blocks = (f->ntiles2d_fast <= maxb) ? f->ntiles2d_fast : 0;
+    const int maxb =
+        fast::persist2d_max_blocks(f->model.kind == SGWG_BURGERS, phalf ? 1 : 0, persist_smem);
+    persist_blocks = (pntiles <= maxb) ? pntiles : 0;
     const auto order = pass_order(f);
     Stage2DParams& p = pp.base;
     p.mem = f->dmem;
-    p.tiles = f->dtiles2d_fast;
-    p.ntiles = f->ntiles2d_fast;
+    p.tiles = phalf ? f->dtiles2d_half : f->dtiles2d_fast;
+    p.ntiles = pntiles;
+    p.half_tiles = phalf ? 1 : 0;
     p.burgers = f->model.kind == SGWG_BURGERS;
     p.flux0 = order[0].flux;
     p.flux1 = order[1].flux;
@@ -1870,7 +1879,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
     p.track_max = p.burgers;
     p.fail = f->fail;
     p.dtp = f->d_dtp;
-    p.resident = (f->ntiles2d_fast <= persist_blocks &&
+    p.resident = (pntiles <= persist_blocks &&
                   std::getenv("SGWG_NO_RESIDENT") == nullptr) ? 1 : 0;
     pp.u = f->u;
     pp.A = f->A;

@@ -292,7 +292,7 @@ cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cud
 cudaError_t launch_plane(const PlaneParams& p, int nblocks, size_t smem, cudaStream_t s);
 int plane_smem_doubles(int nv, int tx, int ty);
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s);
-int persist2d_max_blocks(int burgers, size_t smem);
+int persist2d_max_blocks(int burgers, int half, size_t smem);
 }  // namespace fast
 
 // exact-arithmetic scalar kernels (k_exact.cu)
