@@ -109,6 +109,12 @@ def kernel_name(cfg, arith):
     if cfg["d"] == 2:
         k = "stage2d_fast_kernel" if arith == "fast" else "stage2d_kernel"
         return f"{k}<{phys}> (both WENO5 sweeps + RK3 stage, all members, 1 launch)"
+    if arith == "fast" and cfg["d"] == 3 and cfg["kind"] == 0:
+        return ("stage3d_pipe_kernel<Advect> (persistent, cp.async-pipelined; all three WENO5 "
+                "sweeps + RK3 stage of all members, 1 launch)")
+    if arith == "fast" and cfg["d"] == 4 and cfg["kind"] in (0, 3):
+        return (f"plane_fast_kernel<{phys}> (fast; 2 launches per stage: dims (0,1) -> K, "
+                "dims (2,3) + RK3 stage + charge-density partials)")
     return (f"pass_kernel<{phys}> ({arith}; one WENO5 direction of all members per launch, "
             "RK3 stage fused into the last direction)")
 
