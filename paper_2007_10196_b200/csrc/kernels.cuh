@@ -1218,37 +1218,62 @@ __device__ __forceinline__ int gidx3(const MemberDesc* M, int i0, int j0, int l0
   return (gi * n1 + gj) * n2 + gl;
 }
 
+// one padded coordinate of a 3D box: member index (periodic wrap, |excursion|
+// <= 3 < n) or -1 (zero ghost)
+__device__ __forceinline__ int wrap1(int g, int n, int bc) {
+  if (g >= 0 && g < n) return g;
+  if (bc != 0) return -1;
+  return (g < 0) ? g + n : g - n;
+}
+
 template <int TX, int TY, int TZ>
 __device__ __forceinline__ void stage3d_issue(const Stage2DParams& p, const MemberDesc* M, int i0,
                                               int j0, int l0, double* U) {
   using G = Box3<TX, TY, TZ>;
   const double* u = p.uin + M->offset;
   const int tid = threadIdx.x;
-  for (int q = tid; q < G::NPTS; q += G::NT) {
-    const int a = q / (TY * TZ), b = (q / TZ) % TY, c = q % TZ;
-    const int g = gidx3(M, i0, j0, l0, a + 3, b + 3, c + 3);
-    cp_async8(U + ((a + 3) * G::PY + (b + 3)) * G::PZ + (c + 3), u + max(g, 0), g >= 0);
+  const int n0 = M->ext[0], n1 = M->ext[1], n2 = M->ext[2];
+  const int s0 = n1 * n2;
+  // a box inside its member (every tile of the BASELINE families): interior
+  // points need no boundary rule, a face point only the rule of its face axis
+  const bool full = (i0 + TX <= n0) && (j0 + TY <= n1) && (l0 + TZ <= n2);
+  const int base = (i0 * n1 + j0) * n2 + l0;
+#pragma unroll
+  for (int e = 0; e < (G::NPTS + G::NT - 1) / G::NT; ++e) {
+    const int q = tid + e * G::NT;
+    if (q < G::NPTS) {
+      const int a = q / (TY * TZ), b = (q / TZ) % TY, c = q % TZ;
+      const int g = full ? base + a * s0 + b * n2 + c : gidx3(M, i0, j0, l0, a + 3, b + 3, c + 3);
+      cp_async8(U + ((a + 3) * G::PY + (b + 3)) * G::PZ + (c + 3), u + max(g, 0), g >= 0);
+    }
   }
   constexpr int FX = 6 * TY * TZ, FY = 6 * TX * TZ, FZ = 6 * TX * TY;
+  const int bc0 = M->bc[0], bc1 = M->bc[1], bc2 = M->bc[2];
   for (int h = tid; h < FX + FY + FZ; h += G::NT) {
-    int a, b, c;
+    int a, b, c, g;
     if (h < FX) {
       const int r6 = h / (TY * TZ), rem = h % (TY * TZ);
       a = (r6 < 3) ? r6 : TX + r6;
       b = rem / TZ + 3;
       c = rem % TZ + 3;
+      const int gi = wrap1(i0 - 3 + a, n0, bc0);
+      g = (gi >= 0) ? (gi * n1 + j0 + b - 3) * n2 + l0 + c - 3 : -1;
     } else if (h < FX + FY) {
       const int h2 = h - FX, r6 = h2 / (TX * TZ), rem = h2 % (TX * TZ);
       b = (r6 < 3) ? r6 : TY + r6;
       a = rem / TZ + 3;
       c = rem % TZ + 3;
+      const int gj = wrap1(j0 - 3 + b, n1, bc1);
+      g = (gj >= 0) ? ((i0 + a - 3) * n1 + gj) * n2 + l0 + c - 3 : -1;
     } else {
       const int h3 = h - FX - FY, r6 = h3 / (TX * TY), rem = h3 % (TX * TY);
       c = (r6 < 3) ? r6 : TZ + r6;
       a = rem / TY + 3;
       b = rem % TY + 3;
+      const int gl = wrap1(l0 - 3 + c, n2, bc2);
+      g = (gl >= 0) ? ((i0 + a - 3) * n1 + j0 + b - 3) * n2 + gl : -1;
     }
-    const int g = gidx3(M, i0, j0, l0, a, b, c);
+    if (!full) g = gidx3(M, i0, j0, l0, a, b, c);
     cp_async8(U + (a * G::PY + b) * G::PZ + c, u + max(g, 0), g >= 0);
   }
 }
@@ -1297,12 +1322,27 @@ __device__ __forceinline__ void stage3d_compute(const Stage2DParams& p, const Me
   const StepCtl* ctl = p.ctl;
   const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
   const int n0 = M->ext[0], n1 = M->ext[1], n2 = M->ext[2];
-  for (int q = tid; q < G::NPTS; q += G::NT) {
+  // all u^n loads of the thread's points in flight before any use
+  constexpr int NE = (G::NPTS + G::NT - 1) / G::NT;
+  const double* unb = p.un + M->offset;
+  double* outb = p.out + M->offset;
+  int gq[NE];
+  double unv[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int q = tid + e * G::NT;
     const int a = q / (TY * TZ), b = (q / TZ) % TY, c = q % TZ;
-    if (i0 + a >= n0 || j0 + b >= n1 || l0 + c >= n2) continue;
+    const bool ok = q < G::NPTS && i0 + a < n0 && j0 + b < n1 && l0 + c < n2;
+    gq[e] = ok ? ((i0 + a) * n1 + (j0 + b)) * n2 + (l0 + c) : -1;
+    unv[e] = (ok && p.stage > 1) ? __ldg(unb + gq[e]) : 0.0;
+  }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    if (gq[e] < 0) continue;
+    const int q = tid + e * G::NT;
+    const int a = q / (TY * TZ), b = (q / TZ) % TY, c = q % TZ;
     const int dq = (a * TY + b) * DZP + c;
     const double kv = ((0.0 - DX[dq]) - DY[dq]) - DZ[dq];
-    const long long gi = M->offset + ((long long)(i0 + a) * n1 + (j0 + b)) * n2 + (l0 + c);
     double o;
     if (p.stage == 0) {
       o = kv;
@@ -1316,11 +1356,11 @@ __device__ __forceinline__ void stage3d_compute(const Stage2DParams& p, const Me
       if (p.stage == 1)
         o = fma(dt, kv, ui);
       else if (p.stage == 2)
-        o = fma(0.75, __ldg(p.un + gi), 0.25 * fma(dt, kv, ui));
+        o = fma(0.75, unv[e], 0.25 * fma(dt, kv, ui));
       else
-        o = fma(1.0 / 3.0, __ldg(p.un + gi), (2.0 / 3.0) * fma(dt, kv, ui));
+        o = fma(1.0 / 3.0, unv[e], (2.0 / 3.0) * fma(dt, kv, ui));
     }
-    p.out[gi] = o;
+    outb[gq[e]] = o;
   }
 }
 

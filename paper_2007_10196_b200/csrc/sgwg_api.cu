@@ -740,6 +740,7 @@ int build_tasks(sgwg_family* f) {
     for (int mi = 0; mi < f->nm; ++mi) {
       const MemberDesc& M = f->hmem[mi];
       if (M.ext[0] >= 65536 || M.ext[1] >= 65536) ok = false;
+      if (M.npts >= (1LL << 31)) ok = false;  // 32-bit member-local offsets in the kernel
       int best = 0;
       long long bw = -1;
       for (int s = 0; s < 3; ++s) {
