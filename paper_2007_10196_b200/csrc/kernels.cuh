@@ -949,6 +949,34 @@ __device__ __forceinline__ void tile_body_half(const Stage2DParams& p, const Mem
 }
 constexpr int kHalfThreads = kFastThreads / 2;
 
+// quarter-size tiles (512 points, 128 threads): four CTAs per SM
+template <bool BURGERS, bool PERSIST = false>
+__device__ __forceinline__ void tile_body_quarter(const Stage2DParams& p, const MemberDesc* M,
+                                                  int4 tk, double* sm) {
+  switch (tk.w) {  // TX*TY = 512, 128 threads
+    case 8: stage2d_fast_body<BURGERS, PERSIST, 16, 32>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 9: stage2d_fast_body<BURGERS, PERSIST, 32, 16>(p, M, tk.x, tk.y, tk.z, sm); break;
+    case 10: stage2d_fast_body<BURGERS, PERSIST, 8, 64>(p, M, tk.x, tk.y, tk.z, sm); break;
+    default: stage2d_fast_body<BURGERS, PERSIST, 64, 8>(p, M, tk.x, tk.y, tk.z, sm); break;
+  }
+}
+constexpr int kQuarterThreads = kFastThreads / 4;
+
+template <bool BURGERS>
+__global__ void __launch_bounds__(kQuarterThreads, 4)
+    stage2d_quarter_kernel(const Stage2DParams p) {
+  pdl_wait();
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  const int4 tk = p.tiles[blockIdx.x];
+  const MemberDesc* M = p.mem + tk.x;
+  extern __shared__ double sm[];
+  if (p.amax_zero != nullptr && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < p.nmembers; i += blockDim.x) p.amax_zero[i] = 0ull;
+  tile_body_quarter<BURGERS>(p, M, tk, sm);
+  if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+
 template <bool BURGERS, bool HALF>
 __global__ void __launch_bounds__(HALF ? kHalfThreads : kFastThreads, HALF ? 2 : 1)
     stage2d_fast_kernel(const Stage2DParams p) {
@@ -1747,8 +1775,9 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
 // post-barrier data (deterministic, so all CTAs agree) on its own copy of the
 // step-control block, and CTA 0 publishes it.  Loads of data written by other
 // CTAs in this launch go through L2 (ld.global.cg).
-template <bool BURGERS, bool HALF>
-__global__ void __launch_bounds__(HALF ? kHalfThreads : kFastThreads, HALF ? 2 : 1)
+// Q = tile divisor: 2048 / Q-point tiles, Q CTAs of kFastThreads / Q threads per SM
+template <bool BURGERS, int Q>
+__global__ void __launch_bounds__(kFastThreads / Q, Q)
     evolve2d_persistent_kernel(const PersistParams pp) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1786,7 +1815,9 @@ __global__ void __launch_bounds__(HALF ? kHalfThreads : kFastThreads, HALF ? 2 :
           pp.base.amax_zero[(size_t)((s + 1) % 3) * nm + i] = 0ull;
       for (int t = blockIdx.x; t < pp.base.ntiles; t += gridDim.x) {
         const int4 tk = pp.base.tiles[t];
-        if (HALF)
+        if (Q == 4)
+          tile_body_quarter<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
+        else if (Q == 2)
           tile_body_half<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
         else
           tile_body<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
@@ -1830,24 +1861,26 @@ cudaError_t launch_plane(const PlaneParams& p, int nblocks, size_t smem, cudaStr
 
 int plane_smem_doubles(int nv, int tx, int ty) { return PlaneGeom(nv, tx, ty).smem_doubles(); }
 
+template <bool B>
+const void* persist_fn(int q) {
+  return (q == 4) ? (const void*)evolve2d_persistent_kernel<B, 4>
+                  : (q == 2) ? (const void*)evolve2d_persistent_kernel<B, 2>
+                             : (const void*)evolve2d_persistent_kernel<B, 1>;
+}
+
+// p.base.half_tiles: 0 = 2048-point tiles, 1 = 1024, 2 = 512
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s) {
   void* args[] = {(void*)&p};
-  const bool h = p.base.half_tiles != 0;
-  const void* fn = p.base.burgers ? (h ? (const void*)evolve2d_persistent_kernel<true, true>
-                                       : (const void*)evolve2d_persistent_kernel<true, false>)
-                                  : (h ? (const void*)evolve2d_persistent_kernel<false, true>
-                                       : (const void*)evolve2d_persistent_kernel<false, false>);
-  return cudaLaunchCooperativeKernel(fn, nblocks, h ? kHalfThreads : kFastThreads, args, smem, s);
+  const int q = 1 << p.base.half_tiles;
+  const void* fn = p.base.burgers ? persist_fn<true>(q) : persist_fn<false>(q);
+  return cudaLaunchCooperativeKernel(fn, nblocks, kFastThreads / q, args, smem, s);
 }
 
 int persist2d_max_blocks(int burgers, int half, size_t smem) {
   int per_sm = 0;
-  const void* fn = burgers ? (half ? (const void*)evolve2d_persistent_kernel<true, true>
-                                   : (const void*)evolve2d_persistent_kernel<true, false>)
-                           : (half ? (const void*)evolve2d_persistent_kernel<false, true>
-                                   : (const void*)evolve2d_persistent_kernel<false, false>);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, half ? kHalfThreads : kFastThreads,
-                                                smem);
+  const int q = 1 << half;
+  const void* fn = burgers ? persist_fn<true>(q) : persist_fn<false>(q);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFastThreads / q, smem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2204,6 +2237,12 @@ cudaError_t configure() {
   e0 = cudaFuncSetAttribute(stage2d_fast_kernel<false, false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage2d_quarter_kernel<true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage2d_quarter_kernel<false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(stage2d_fast_kernel<true, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   if (e0 != cudaSuccess) return e0;
@@ -2219,18 +2258,14 @@ cudaError_t configure() {
   e0 = cudaFuncSetAttribute(stage3d_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (2 * kPipe3DBox + 3 * kPipe3DDn) * (int)sizeof(double));
   if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<false, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<true, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(evolve2d_persistent_kernel<false, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e0 != cudaSuccess) return e0;
+  for (int q = 1; q <= 4; q *= 2) {
+    e0 = cudaFuncSetAttribute(persist_fn<true>(q), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              112 * 1024);
+    if (e0 != cudaSuccess) return e0;
+    e0 = cudaFuncSetAttribute(persist_fn<false>(q), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              112 * 1024);
+    if (e0 != cudaSuccess) return e0;
+  }
 #endif
   cudaError_t e = cudaFuncSetAttribute(pass_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -2242,7 +2277,14 @@ cudaError_t configure() {
 cudaError_t launch_stage2d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
 #if SGWG_FAST
-  if (p.half_tiles) {
+  if (p.half_tiles == 2) {  // four CTAs per SM
+    if (p.burgers)
+      return launch_k(stage2d_quarter_kernel<true>, dim3(nblocks), dim3(kQuarterThreads), smem,
+                      s, p);
+    return launch_k(stage2d_quarter_kernel<false>, dim3(nblocks), dim3(kQuarterThreads), smem, s,
+                    p);
+  }
+  if (p.half_tiles) {  // two CTAs per SM
     if (p.burgers)
       return launch_k(stage2d_fast_kernel<true, true>, dim3(nblocks), dim3(kHalfThreads), smem,
                       s, p);

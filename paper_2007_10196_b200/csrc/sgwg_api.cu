@@ -229,6 +229,9 @@ struct sgwg_family {
   int4* dtiles2d_half = nullptr;  // 1024-point tiles of the stage kernel (two CTAs per SM)
   int ntiles2d_half = 0;
   int smem2d_half = 0;
+  int4* dtiles2d_q = nullptr;     // 512-point tiles (four CTAs per SM)
+  int ntiles2d_q = 0;
+  int smem2d_q = 0;
   int smem2d_fast = 0;
   int4* dtiles3d_fast = nullptr;  // fast 3D stage tiles (advection)
   int ntiles3d_fast = 0;
@@ -293,14 +296,17 @@ void account_timed(sgwg_family* f, int stage, int npass_dims, bool last, float m
   }
 }
 
-// fast 2D stage kernel on 1024-point tiles (two CTAs per SM); SGWG_TILE2D=2048
-// selects the 2048-point tiles (one CTA per SM) for experiments
-bool half_tiles_enabled() {
+// tile size of the fast 2D stage kernel: 512 points, four CTAs per SM (measured:
+// S2 stage 358 -> 319 us, C4 3.17 -> 2.90 s against 1024-point tiles, two per
+// SM); SGWG_TILE2D=1024 / 2048 select the larger tiles
+int stage_tile_code() {
   static const int v = [] {
     const char* e = std::getenv("SGWG_TILE2D");
-    return (e != nullptr && std::string(e) == "2048") ? 0 : 1;
+    if (e != nullptr && std::string(e) == "2048") return 0;
+    if (e != nullptr && std::string(e) == "1024") return 1;
+    return 2;
   }();
-  return v != 0;
+  return v;
 }
 
 // fast 4D plane path (kernels.cuh plane_fast_kernel)
@@ -491,7 +497,12 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     p.tiles = fastk ? f->dtiles2d_fast : f->dtiles2d;
     int nt = fastk ? f->ntiles2d_fast : f->ntiles2d;
     size_t smem = (size_t)(fastk ? f->smem2d_fast : f->smem2d) * sizeof(double);
-    if (fastk && half_tiles_enabled()) {
+    if (fastk && stage_tile_code() == 2) {
+      p.tiles = f->dtiles2d_q;
+      p.half_tiles = 2;
+      nt = f->ntiles2d_q;
+      smem = (size_t)f->smem2d_q * sizeof(double);
+    } else if (fastk && stage_tile_code() == 1) {
       p.tiles = f->dtiles2d_half;
       p.half_tiles = 1;
       nt = f->ntiles2d_half;
@@ -731,6 +742,32 @@ int build_tasks(sgwg_family* f) {
     f->smem2d_half = shmax;
     CK(cudaMalloc(&f->dtiles2d_half, sizeof(int4) * std::max<size_t>(1, th.size())));
     CK(cudaMemcpy(f->dtiles2d_half, th.data(), sizeof(int4) * th.size(), cudaMemcpyHostToDevice));
+    static const int shq[4][2] = {{16, 32}, {32, 16}, {8, 64}, {64, 8}};
+    std::vector<int4> tq;
+    int sqmax = 0;
+    for (int mi = 0; mi < f->nm; ++mi) {
+      const MemberDesc& M = f->hmem[mi];
+      int best = 0;
+      long long bw = -1;
+      for (int s = 0; s < 4; ++s) {
+        const long long cov = (long long)((M.ext[0] + shq[s][0] - 1) / shq[s][0]) * shq[s][0] *
+                              ((M.ext[1] + shq[s][1] - 1) / shq[s][1]) * shq[s][1];
+        if (bw < 0 || cov < bw) {
+          bw = cov;
+          best = s;
+        }
+      }
+      const int TX = shq[best][0], TY = shq[best][1];
+      const int PY = ((TY + 6) % 2 == 0) ? TY + 7 : TY + 6;
+      const int sm = 2 * (TX + 6) * PY + 2 * TX * (TY + 1) + TX + TY;
+      sqmax = std::max(sqmax, sm);
+      for (int i0 = 0; i0 < M.ext[0]; i0 += TX)
+        for (int j0 = 0; j0 < M.ext[1]; j0 += TY) tq.push_back(make_int4(mi, i0, j0, 8 + best));
+    }
+    f->ntiles2d_q = (int)tq.size();
+    f->smem2d_q = sqmax;
+    CK(cudaMalloc(&f->dtiles2d_q, sizeof(int4) * std::max<size_t>(1, tq.size())));
+    CK(cudaMemcpy(f->dtiles2d_q, tq.data(), sizeof(int4) * tq.size(), cudaMemcpyHostToDevice));
   }
   if (f->d == 3 && !f->no_fused2d) {  // fast 3D stage tiles: 2048 points, 3 shapes
     static const int shp3[3][3] = {{8, 16, 16}, {16, 8, 16}, {16, 16, 8}};
@@ -1557,6 +1594,7 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dtiles2d);
   cudaFree(f->dtiles2d_fast);
   cudaFree(f->dtiles2d_half);
+  cudaFree(f->dtiles2d_q);
   cudaFree(f->dtiles3d_fast);
   cudaFree(f->dptiles[0]);
   cudaFree(f->dptiles[1]);
@@ -1842,28 +1880,42 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   // small 2D families (fast build, single rank): persistent cooperative kernel
   PersistParams pp{};
   int persist_blocks = 0;
-  // 1024-point tiles, two CTAs per SM (measured: C1 34.2 -> 30.1 ms, C2 34.6 -> 34.3 ms
-  // against 2048-point tiles, one per SM; SGWG_PERSIST_HALF=0 selects those)
-  const char* ph = std::getenv("SGWG_PERSIST_HALF");
-  const bool phalf = !(ph != nullptr && ph[0] == '0');
-  const int pntiles = phalf ? f->ntiles2d_half : f->ntiles2d_fast;
+  // 1024-point tiles, two CTAs per SM (measured: C2 34.6 -> 34.3 ms against 2048-point
+  // tiles, one per SM; 512-point tiles 35.7 ms), 512-point tiles, four per SM, when
+  // the family has fewer 1024-point tiles than SMs (C1 30.2 -> 27.6 ms);
+  // SGWG_PERSIST_TILE=2048 / 1024 / 512 force one
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int pcode = (f->ntiles2d_half < nsm) ? 2 : 1;
+  if (const char* e = std::getenv("SGWG_PERSIST_TILE")) {
+    if (std::string(e) == "2048") pcode = 0;
+    if (std::string(e) == "1024") pcode = 1;
+    if (std::string(e) == "512") pcode = 2;
+  }
+  const int pntiles = (pcode == 2) ? f->ntiles2d_q : (pcode == 1) ? f->ntiles2d_half
+                                                                  : f->ntiles2d_fast;
+  const int pts_tile = 2048 >> pcode;
   // + the resident tile (stage input and u^n)
   const size_t persist_smem =
-      phalf ? ((size_t)f->smem2d_half + 2 * 1024) * sizeof(double)
-            : ((size_t)f->smem2d_fast + 2 * 2048) * sizeof(double);
+      ((size_t)((pcode == 2) ? f->smem2d_q : (pcode == 1) ? f->smem2d_half : f->smem2d_fast) +
+       2 * pts_tile) * sizeof(double);
   if (arith_of(f) == SGWG_ARITH_FAST && f->d == 2 && pntiles > 0 && dt_fusable(f) &&
       !f->ctx->profile && std::getenv("SGWG_NO_PERSIST") == nullptr) {
     // one tile per CTA (tiles resident in shared memory across stages); larger
     // families run faster as graph-captured stage launches (measured: S2)
     const int maxb =
-        fast::persist2d_max_blocks(f->model.kind == SGWG_BURGERS, phalf ? 1 : 0, persist_smem);
+        fast::persist2d_max_blocks(f->model.kind == SGWG_BURGERS, pcode, persist_smem);
     persist_blocks = (pntiles <= maxb) ? pntiles : 0;
     const auto order = pass_order(f);
     Stage2DParams& p = pp.base;
     p.mem = f->dmem;
-    p.tiles = phalf ? f->dtiles2d_half : f->dtiles2d_fast;
+    p.tiles = (pcode == 2) ? f->dtiles2d_q : (pcode == 1) ? f->dtiles2d_half : f->dtiles2d_fast;
     p.ntiles = pntiles;
-    p.half_tiles = phalf ? 1 : 0;
+    p.half_tiles = pcode;
     p.burgers = f->model.kind == SGWG_BURGERS;
     p.flux0 = order[0].flux;
     p.flux1 = order[1].flux;
