@@ -1225,6 +1225,8 @@ struct Box3 {
 };
 constexpr int kPipe3DBox = 7260;   // max Box3::BOX of the three tile shapes
 constexpr int kPipe3DDn = 2304;    // max Box3::DN
+constexpr int kPipe3DBoxH = 4620;  // 1024-point tiles (8,8,16), (8,16,8), (16,8,8)
+constexpr int kPipe3DDnH = 1152;
 
 // gindex of the padded box position (a, b, c) (weno.hpp:131-141 boundary rule)
 __device__ __forceinline__ int gidx3(const MemberDesc* M, int i0, int j0, int l0, int a, int b,
@@ -1398,17 +1400,24 @@ __device__ __forceinline__ void stage3d_issue_any(const Stage2DParams& p, int4 t
   switch (tk.z & 0xff) {
     case 0: stage3d_issue<8, 16, 16>(p, M, i0, j0, l0, U); break;
     case 1: stage3d_issue<16, 8, 16>(p, M, i0, j0, l0, U); break;
-    default: stage3d_issue<16, 16, 8>(p, M, i0, j0, l0, U); break;
+    case 2: stage3d_issue<16, 16, 8>(p, M, i0, j0, l0, U); break;
+    case 3: stage3d_issue<8, 8, 16>(p, M, i0, j0, l0, U); break;
+    case 4: stage3d_issue<8, 16, 8>(p, M, i0, j0, l0, U); break;
+    default: stage3d_issue<16, 8, 8>(p, M, i0, j0, l0, U); break;
   }
 }
 
-__global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_pipe_kernel(const Stage2DParams p) {
+// Q = 1: 2048-point tiles, 768 threads, one CTA per SM; Q = 2: 1024-point
+// tiles (shape codes 3..5), 384 threads, two CTAs per SM
+template <int Q>
+__global__ void __launch_bounds__(kStage3DThreads / Q, Q) stage3d_pipe_kernel(const Stage2DParams p) {
   pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
   extern __shared__ double sm[];
-  double* Ub[2] = {sm, sm + kPipe3DBox};
-  double* D = sm + 2 * kPipe3DBox;
+  constexpr int BOX = (Q == 1) ? kPipe3DBox : kPipe3DBoxH;
+  double* Ub[2] = {sm, sm + BOX};
+  double* D = sm + 2 * BOX;
   int t = blockIdx.x;
   if (t < p.ntiles) stage3d_issue_any(p, p.tiles[t], Ub[0]);
   cp_async_commit();
@@ -1421,10 +1430,18 @@ __global__ void __launch_bounds__(kStage3DThreads, 1) stage3d_pipe_kernel(const 
     const int4 tk = p.tiles[t];
     const MemberDesc* M = p.mem + tk.x;
     const int i0 = tk.y >> 16, j0 = tk.y & 0xffff, l0 = tk.z >> 8;
-    switch (tk.z & 0xff) {
-      case 0: stage3d_compute<8, 16, 16>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
-      case 1: stage3d_compute<16, 8, 16>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
-      default: stage3d_compute<16, 16, 8>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+    if (Q == 1) {
+      switch (tk.z & 0xff) {
+        case 0: stage3d_compute<8, 16, 16>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+        case 1: stage3d_compute<16, 8, 16>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+        default: stage3d_compute<16, 16, 8>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+      }
+    } else {
+      switch (tk.z & 0xff) {
+        case 3: stage3d_compute<8, 8, 16>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+        case 4: stage3d_compute<8, 16, 8>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+        default: stage3d_compute<16, 8, 8>(p, M, tk.x, i0, j0, l0, Ub[k & 1], D); break;
+      }
     }
     __syncthreads();  // box k&1 and D are reused by the next tiles
   }
@@ -1842,13 +1859,17 @@ __global__ void __launch_bounds__(kFastThreads / Q, Q)
 cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
   const char* e = getenv("SGWG_3D_PIPE");
-  if (!(e && e[0] == '0')) {  // persistent, pipelined: one CTA per SM
+  if (p.half_tiles || !(e && e[0] == '0')) {  // persistent, pipelined
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     Stage2DParams q = p;
     q.ntiles = nblocks;
-    return launch_k(stage3d_pipe_kernel, dim3(min(nblocks, sms)), dim3(kStage3DThreads),
+    if (p.half_tiles)  // 1024-point tiles, two CTAs per SM
+      return launch_k(stage3d_pipe_kernel<2>, dim3(min(nblocks, 2 * sms)),
+                      dim3(kStage3DThreads / 2),
+                      (2 * kPipe3DBoxH + 3 * kPipe3DDnH) * sizeof(double), s, q);
+    return launch_k(stage3d_pipe_kernel<1>, dim3(min(nblocks, sms)), dim3(kStage3DThreads),
                     (2 * kPipe3DBox + 3 * kPipe3DDn) * sizeof(double), s, q);
   }
   return launch_k(stage3d_fast_kernel, dim3(nblocks), dim3(kStage3DThreads), smem, s, p);
@@ -2255,8 +2276,11 @@ cudaError_t configure() {
   e0 = cudaFuncSetAttribute(plane_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             200 * 1024);
   if (e0 != cudaSuccess) return e0;
-  e0 = cudaFuncSetAttribute(stage3d_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e0 = cudaFuncSetAttribute(stage3d_pipe_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (2 * kPipe3DBox + 3 * kPipe3DDn) * (int)sizeof(double));
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage3d_pipe_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (2 * kPipe3DBoxH + 3 * kPipe3DDnH) * (int)sizeof(double));
   if (e0 != cudaSuccess) return e0;
   for (int q = 1; q <= 4; q *= 2) {
     e0 = cudaFuncSetAttribute(persist_fn<true>(q), cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -236,6 +236,7 @@ struct sgwg_family {
   int4* dtiles3d_fast = nullptr;  // fast 3D stage tiles (advection)
   int ntiles3d_fast = 0;
   int smem3d_fast = 0;
+  int tiles3d_half = 0;  // 1024-point 3D tiles (pipelined kernel, two CTAs per SM)
   PlaneTile* dptiles[2] = {nullptr, nullptr};  // fast 4D plane tiles (pairs (0,1), (2,3))
   int nptiles[2] = {0, 0};
   int psmem = 0;
@@ -477,6 +478,7 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     p.fail = f->fail;
     p.dtp = dtp;
     p.counter = f->counter;
+    p.half_tiles = f->tiles3d_half;
     if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
     CK(fast::launch_stage3d(p, f->ntiles3d_fast, (size_t)f->smem3d_fast * sizeof(double),
                             f->ctx->stream));
@@ -769,8 +771,14 @@ int build_tasks(sgwg_family* f) {
     CK(cudaMalloc(&f->dtiles2d_q, sizeof(int4) * std::max<size_t>(1, tq.size())));
     CK(cudaMemcpy(f->dtiles2d_q, tq.data(), sizeof(int4) * tq.size(), cudaMemcpyHostToDevice));
   }
-  if (f->d == 3 && !f->no_fused2d) {  // fast 3D stage tiles: 2048 points, 3 shapes
-    static const int shp3[3][3] = {{8, 16, 16}, {16, 8, 16}, {16, 16, 8}};
+  if (f->d == 3 && !f->no_fused2d) {  // fast 3D stage tiles, 3 shapes
+    // default 1024-point tiles, shape codes 3..5, pipelined kernel with two CTAs per SM
+    // (measured: C3 171.2 -> 164.9 ms, S3 39.2 -> 38.5 ms); SGWG_3D_TILE=2048: 2048 points
+    static const int shp3f[3][3] = {{8, 16, 16}, {16, 8, 16}, {16, 16, 8}};
+    static const int shp3h[3][3] = {{8, 8, 16}, {8, 16, 8}, {16, 8, 8}};
+    const char* e3 = std::getenv("SGWG_3D_TILE");
+    f->tiles3d_half = (e3 != nullptr && std::string(e3) == "2048") ? 0 : 1;
+    const int(*shp3)[3] = f->tiles3d_half ? shp3h : shp3f;
     std::vector<int4> t3;
     int smax = 0;
     bool ok = true;
@@ -796,7 +804,7 @@ int build_tasks(sgwg_family* f) {
       for (int i0 = 0; i0 < M.ext[0]; i0 += TX)
         for (int j0 = 0; j0 < M.ext[1]; j0 += TY)
           for (int l0 = 0; l0 < M.ext[2]; l0 += TZ)
-            t3.push_back(make_int4(mi, (i0 << 16) | j0, (l0 << 8) | best, 0));
+            t3.push_back(make_int4(mi, (i0 << 16) | j0, (l0 << 8) | (best + 3 * f->tiles3d_half), 0));
     }
     if (ok) {
       f->ntiles3d_fast = (int)t3.size();
