@@ -1467,7 +1467,10 @@ __global__ void __launch_bounds__(kStage3DThreads / Q, Q) stage3d_pipe_kernel(co
 #ifndef SGWG_PLANE_MINB
 #define SGWG_PLANE_MINB 3
 #endif
-constexpr int kPlaneThreads = 256;
+#ifndef SGWG_PLANE_THREADS
+#define SGWG_PLANE_THREADS 256
+#endif
+constexpr int kPlaneThreads = SGWG_PLANE_THREADS;
 constexpr int kPlaneMaxE = 8;  // tile points <= kPlaneThreads * kPlaneMaxE
 
 // q / n for 0 <= q < 2^21, 0 < n < 2^12 via a float reciprocal (exact: the quotient
