@@ -342,6 +342,7 @@ def run_b200(args):
     combine_ms = max_over_ranks(st["combine_ms"])
 
     # ---- end to end through the public API with host buffers (e2e) ----
+    one_sim(host_io=True)  # untimed warm-up of the host-buffer path
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()

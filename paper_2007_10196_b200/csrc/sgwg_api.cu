@@ -301,13 +301,10 @@ void account_timed(sgwg_family* f, int stage, int npass_dims, bool last, float m
 // S2 stage 358 -> 319 us, C4 3.17 -> 2.90 s against 1024-point tiles, two per
 // SM); SGWG_TILE2D=1024 / 2048 select the larger tiles
 int stage_tile_code() {
-  static const int v = [] {
-    const char* e = std::getenv("SGWG_TILE2D");
-    if (e != nullptr && std::string(e) == "2048") return 0;
-    if (e != nullptr && std::string(e) == "1024") return 1;
-    return 2;
-  }();
-  return v;
+  const char* e = std::getenv("SGWG_TILE2D");
+  if (e != nullptr && std::string(e) == "2048") return 0;
+  if (e != nullptr && std::string(e) == "1024") return 1;
+  return 2;
 }
 
 // fast 4D plane path (kernels.cuh plane_fast_kernel)

@@ -85,3 +85,30 @@ def test_combine_fast(ctx_fast, oracle):
     fam.upload(s)
     for mode in (O.WENO, O.LAGRANGE):
         assert maxabs(fam.combine(mode, 1e-6), oracle.combine(dom, s, mode, 1e-6)) < 1e-12
+
+
+# Every tile-size variant of the fast 2D / 3D stage kernels and of the
+# persistent 2D evolve against the oracle (the defaults pick one per family
+# size: 512-point stage tiles, 1024- or 512-point persistent tiles, 1024-point
+# 3D tiles; the others stay selectable and must stay correct).
+@pytest.mark.parametrize("env,name,over,T", [
+    ({"SGWG_NO_PERSIST": "1", "SGWG_TILE2D": "2048"}, "C2", {"nl": 3, "root": [16, 16]}, 0.02),
+    ({"SGWG_NO_PERSIST": "1", "SGWG_TILE2D": "1024"}, "C2", {"nl": 3, "root": [16, 16]}, 0.02),
+    ({"SGWG_NO_PERSIST": "1", "SGWG_TILE2D": "512"}, "C2", {"nl": 3, "root": [16, 16]}, 0.02),
+    ({"SGWG_TILE2D": "2048"}, "C4", {"nl": 3, "root": [16, 16]}, 0.2),
+    ({"SGWG_TILE2D": "1024"}, "C4", {"nl": 3, "root": [16, 16]}, 0.2),
+    ({"SGWG_PERSIST_TILE": "2048"}, "C2", {"nl": 4, "root": [16, 16]}, 0.02),
+    ({"SGWG_PERSIST_TILE": "1024"}, "C2", {"nl": 4, "root": [16, 16]}, 0.02),
+    ({"SGWG_PERSIST_TILE": "512"}, "C2", {"nl": 4, "root": [16, 16]}, 0.02),
+    ({"SGWG_3D_TILE": "2048"}, "C3", {"nl": 3, "root": [16, 16, 16]}, 0.004),
+    ({"SGWG_3D_TILE": "1024"}, "C3", {"nl": 3, "root": [16, 16, 16]}, 0.004),
+])
+def test_tile_variants_fast(ctx_fast, oracle, monkeypatch, env, name, over, T):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = configs.config(name, **over)
+    got, want, gd, wd, gc, wc = _evolve_both(ctx_fast, oracle, cfg, T)
+    assert len(gd) == len(wd) > 2
+    assert maxabs(gd, wd) < 1e-14
+    assert maxabs(got, want) < TOL
+    assert maxabs(gc[-1], wc[-1]) < TOL
