@@ -33,13 +33,17 @@ __device__ __forceinline__ int bitrev(int x, int bits) {
 }
 
 // radix-2 FFTs of all lines along `axis` (1 = x2, contiguous) of NA complex
-// n1 x n2 arrays (re[k], im[k]) at once (one barrier per butterfly stage for
-// all of them); n1 = 2^b1, n2 = 2^b2.  DIF (forward, sign -1): natural order in,
-// bit-reversed order out; DIT (inverse, sign +1, unnormalised): bit-reversed in,
-// natural out -- so no bit-reversal pass is needed, and the spectral step works
-// in bit-reversed order.  Twiddles from the stage-major table
-// T[half + pos] = e^{i pi pos/half} (consecutive lanes read consecutive entries:
-// no shared-memory bank conflicts).
+// n1 x n2 arrays (re[k], im[k]) at once; n1 = 2^b1, n2 = 2^b2.  DIF (forward,
+// sign -1): natural order in, bit-reversed order out; DIT (inverse, sign +1,
+// unnormalised): bit-reversed in, natural out -- so no bit-reversal pass is
+// needed, and the spectral step works in bit-reversed order.  Twiddles from the
+// stage-major table T[half + pos] = e^{i pi pos/half} (consecutive lanes read
+// consecutive entries: no shared-memory bank conflicts).
+// Two consecutive radix-2 stages are done per barrier: a thread loads the four
+// elements the two stages couple, applies both stages in registers and stores
+// them back -- the same floating-point operations in the same order as two
+// separate stages (bitwise identical), half the barriers and shared-memory
+// round trips; an odd stage count leaves one single stage.
 template <int NA, bool DIF>
 __device__ inline void fft_lines(double* const* re, double* const* im, int b1, int b2, int axis,
                                  const double* tc, const double* ts) {
@@ -53,7 +57,73 @@ __device__ inline void fft_lines(double* const* re, double* const* im, int b1, i
   // lanes walk positions along contiguous lines (axis 1) and walk lines when
   // the lines are strided (axis 0), so shared-memory accesses stay conflict-free
   const int lbits = b1 + b2 - bits;  // log2(number of lines)
-  for (int st = 0; st < bits; ++st) {
+  // (a, b) -> (a + b, (a - b) w)   [DIF]   /   (a + b w, a - b w)   [DIT]
+  auto bfly = [&](double& ar, double& ai, double& xr, double& xi, double c, double s) {
+    if (DIF) {
+      const double dr = ar - xr, di = ai - xi;
+      ar = ar + xr;
+      ai = ai + xi;
+      xr = dr * c - di * s;
+      xi = dr * s + di * c;
+    } else {
+      const double br = xr * c - xi * s, bi = xr * s + xi * c;
+      xr = ar - br;
+      xi = ai - bi;
+      ar = ar + br;
+      ai = ai + bi;
+    }
+  };
+  int st = 0;
+  for (; st + 1 < bits; st += 2) {  // stage pairs
+    // DIF: halves h, h/2 (h = 2^(bits-1-st)); DIT: halves h, 2h (h = 2^st)
+    const int lh = DIF ? bits - 1 - st : st;
+    const int h = 1 << lh;
+    const int qb = DIF ? lh - 1 : lh;  // log2(quads per group)
+    for (int bf = threadIdx.x; bf < nx / 4; bf += blockDim.x) {
+      const int line = axis ? bf >> (bits - 2) : bf & ((1 << lbits) - 1);
+      const int q = axis ? bf & ((len >> 2) - 1) : bf >> lbits;
+      const int grp = q >> qb, pos = q & ((1 << qb) - 1);
+      int ia, ib, ic, id;  // element indices
+      double c1, s1, c2, s2, c3, s3;
+      if (DIF) {  // group of 2h: a = p, b = p + h/2, c = p + h, d = p + 3h/2
+        ia = base_of(line) + ((grp << (lh + 1)) + pos) * stride;
+        ib = ia + (h >> 1) * stride;
+        ic = ia + h * stride;
+        id = ib + h * stride;
+        c1 = tc[h + pos], s1 = sign * ts[h + pos];                        // (a, c)
+        c2 = tc[h + pos + (h >> 1)], s2 = sign * ts[h + pos + (h >> 1)];  // (b, d)
+        c3 = tc[(h >> 1) + pos], s3 = sign * ts[(h >> 1) + pos];          // (a, b), (c, d)
+      } else {    // group of 4h: a = p, b = p + h, c = p + 2h, d = p + 3h
+        ia = base_of(line) + ((grp << (lh + 2)) + pos) * stride;
+        ib = ia + h * stride;
+        ic = ib + h * stride;
+        id = ic + h * stride;
+        c1 = tc[h + pos], s1 = sign * ts[h + pos];                        // (a, b), (c, d)
+        c2 = tc[2 * h + pos], s2 = sign * ts[2 * h + pos];                // (a, c)
+        c3 = tc[2 * h + pos + h], s3 = sign * ts[2 * h + pos + h];        // (b, d)
+      }
+#pragma unroll
+      for (int k = 0; k < NA; ++k) {
+        double ar = re[k][ia], ai = im[k][ia], br = re[k][ib], bi = im[k][ib];
+        double cr = re[k][ic], ci = im[k][ic], dr = re[k][id], di = im[k][id];
+        if (DIF) {
+          bfly(ar, ai, cr, ci, c1, s1);
+          bfly(br, bi, dr, di, c2, s2);
+          bfly(ar, ai, br, bi, c3, s3);
+          bfly(cr, ci, dr, di, c3, s3);
+        } else {
+          bfly(ar, ai, br, bi, c1, s1);
+          bfly(cr, ci, dr, di, c1, s1);
+          bfly(ar, ai, cr, ci, c2, s2);
+          bfly(br, bi, dr, di, c3, s3);
+        }
+        re[k][ia] = ar, im[k][ia] = ai, re[k][ib] = br, im[k][ib] = bi;
+        re[k][ic] = cr, im[k][ic] = ci, re[k][id] = dr, im[k][id] = di;
+      }
+    }
+    __syncthreads();
+  }
+  if (st < bits) {  // last single stage
     const int lh = DIF ? bits - 1 - st : st;
     const int half = 1 << lh;
     for (int bf = threadIdx.x; bf < nx / 2; bf += blockDim.x) {
@@ -65,21 +135,9 @@ __device__ inline void fft_lines(double* const* re, double* const* im, int b1, i
       const double c = tc[half + pos], s = sign * ts[half + pos];  // e^{sign i pi pos/half}
 #pragma unroll
       for (int k = 0; k < NA; ++k) {
-        const double ar = re[k][i0], ai = im[k][i0];
-        const double xr = re[k][i1], xi = im[k][i1];
-        if (DIF) {  // (a, b) -> (a + b, (a - b) w)
-          const double dr = ar - xr, di = ai - xi;
-          re[k][i0] = ar + xr;
-          im[k][i0] = ai + xi;
-          re[k][i1] = dr * c - di * s;
-          im[k][i1] = dr * s + di * c;
-        } else {    // (a, b) -> (a + b w, a - b w)
-          const double br = xr * c - xi * s, bi = xr * s + xi * c;
-          re[k][i0] = ar + br;
-          im[k][i0] = ai + bi;
-          re[k][i1] = ar - br;
-          im[k][i1] = ai - bi;
-        }
+        double ar = re[k][i0], ai = im[k][i0], xr = re[k][i1], xi = im[k][i1];
+        bfly(ar, ai, xr, xi, c, s);
+        re[k][i0] = ar, im[k][i0] = ai, re[k][i1] = xr, im[k][i1] = xi;
       }
     }
     __syncthreads();
