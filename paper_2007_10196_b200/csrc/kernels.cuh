@@ -1624,6 +1624,15 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
       ij[e] = (i << 16) | j;
     }
   }
+  // zero ghosts of a whole zero-BC dimension (the velocity planes): one
+  // vectorised clear of the staging planes instead of per-point edge tests
+  const bool zA = wholeA && bca != 0, zB = wholeB && bcb != 0;
+  if (zA || zB) {
+    double2* z = reinterpret_cast<double2*>(FP);
+    const int n2 = (V * plane + 1) / 2;  // (one spare double of DX, rewritten by the sweeps)
+    for (int q = tid; q < n2; q += kPlaneThreads) z[q] = make_double2(0.0, 0.0);
+    __syncthreads();
+  }
   // halos along a window-split dimension: 3 rows above/below (a), 3 columns
   // left/right (b) of every plane, from L2/HBM (periodic wrap or zero ghosts)
   const int HA = wholeA ? 0 : 6 * TY, HB = wholeB ? 0 : 6 * TX;
@@ -1688,15 +1697,13 @@ __global__ void __launch_bounds__(kPlaneThreads, SGWG_PLANE_MINB) plane_fast_ker
     const double val = vin[e];
     const int si = sidx[e], i = ij[e] >> 16, j = ij[e] & 0xffff;
     FP[si] = val;
-    if (wholeA) {
-      const double g = (bca != 0) ? 0.0 : val;
-      if (i < 3) FP[si + upA] = g;
-      if (i >= TX - 3) FP[si + dnA] = g;
+    if (wholeA && !zA) {  // periodic image
+      if (i < 3) FP[si + upA] = val;
+      if (i >= TX - 3) FP[si + dnA] = val;
     }
-    if (wholeB) {
-      const double g = (bcb != 0) ? 0.0 : val;
-      if (j < 3) FP[si + upB] = g;
-      if (j >= TY - 3) FP[si + dnB] = g;
+    if (wholeB && !zB) {
+      if (j < 3) FP[si + upB] = val;
+      if (j >= TY - 3) FP[si + dnB] = val;
     }
   }
   __syncthreads();
