@@ -210,28 +210,45 @@ __device__ inline void field_member(const FieldParams& p, int mi, double* sh, do
   double* twc = sh + 6 * nx;  // stage-major twiddles, 2H each
   double* tws = twc + 2 * H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int xi = threadIdx.x; xi < nx; xi += blockDim.x) {
-    const double* pt = p.rho_parts + (M->xoff + xi) * kRhoParts;
-    double v[kRhoParts];  // all partial loads in flight, then summed in part order
-#pragma unroll
-    for (int t = 0; t < kRhoParts; ++t) v[t] = (t < M->rparts) ? fld_ld<COH>(pt + t) : 0.0;
-    double acc = v[0];
-#pragma unroll
-    for (int t = 1; t < kRhoParts; ++t)
-      if (t < M->rparts) acc += v[t];
-    const double r = 1.0 - acc;
-    p.rho[M->xoff + xi] = r;
-    rr[xi] = r;
-    ri[xi] = 0.0;
-  }
+  // the phase's loads (charge-density partials of two x points, two twiddle
+  // entries per thread and round) all in flight before any use
   // twiddles: T[half + pos] = e^{i pi pos/half} = family table entry
-  // e^{i pi q/hmax}, q = pos hmax/half (half = 1 .. H)
-  for (int e = threadIdx.x; e < 2 * H; e += blockDim.x) {
-    if (e == 0) continue;
-    const int half = 1 << (31 - __clz(e)), pos = e - half;
-    const int q = pos * (p.hmax / half);
-    twc[e] = fld_ld<COH>(p.twid + q);
-    tws[e] = fld_ld<COH>(p.twid + p.hmax + q);
+  // e^{i pi q/hmax}, q = pos hmax/half (half = 1 .. H; hmax a power of two)
+  const int lhmax = 31 - __clz(p.hmax);
+  const int span = 2 * blockDim.x;
+  for (int r0 = 0; r0 < max(nx, 2 * H); r0 += span) {
+    double v[2][kRhoParts], c[2], sn[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = r0 + threadIdx.x + u * blockDim.x;
+      const bool okt = e > 0 && e < 2 * H;
+      const int k = 31 - __clz(max(e, 1));
+      const int q = (e - (1 << k)) << (lhmax - k);
+      c[u] = okt ? fld_ld<COH>(p.twid + q) : 0.0;
+      sn[u] = okt ? fld_ld<COH>(p.twid + p.hmax + q) : 0.0;
+      const double* pt = p.rho_parts + (M->xoff + e) * kRhoParts;
+#pragma unroll
+      for (int t = 0; t < kRhoParts; ++t)
+        v[u][t] = (e < nx && t < M->rparts) ? fld_ld<COH>(pt + t) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = r0 + threadIdx.x + u * blockDim.x;
+      if (e > 0 && e < 2 * H) {
+        twc[e] = c[u];
+        tws[e] = sn[u];
+      }
+      if (e < nx) {
+        double acc = v[u][0];
+#pragma unroll
+        for (int t = 1; t < kRhoParts; ++t)
+          if (t < M->rparts) acc += v[u][t];
+        const double r = 1.0 - acc;
+        p.rho[M->xoff + e] = r;
+        rr[e] = r;
+        ri[e] = 0.0;
+      }
+    }
   }
   __syncthreads();
   SGWG_FMARK(mi, 1);
