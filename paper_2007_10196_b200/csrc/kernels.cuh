@@ -1866,8 +1866,32 @@ __global__ void __launch_bounds__(kFastThreads / Q, Q)
   }
 }
 
+// 512-point tiles (8 x 8 x 8), one per CTA, 192 threads, four CTAs per SM: the
+// staging of one CTA overlaps the others' sweeps (no software pipeline)
+constexpr int kSmall3DSmem = Box3<8, 8, 8>::BOX + 3 * Box3<8, 8, 8>::DN;
+__global__ void __launch_bounds__(kStage3DThreads / 4, 4) stage3d_small_kernel(const Stage2DParams p) {
+  pdl_wait();
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  extern __shared__ double sm[];
+  const int4 tk = p.tiles[blockIdx.x];
+  const MemberDesc* M = p.mem + tk.x;
+  const int i0 = tk.y >> 16, j0 = tk.y & 0xffff, l0 = tk.z >> 8;
+  double* U = sm;
+  double* D = sm + Box3<8, 8, 8>::BOX;
+  stage3d_issue<8, 8, 8>(p, M, i0, j0, l0, U);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  stage3d_compute<8, 8, 8>(p, M, tk.x, i0, j0, l0, U, D);
+  if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+
 cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
+  if (p.half_tiles == 2)
+    return launch_k(stage3d_small_kernel, dim3(nblocks), dim3(kStage3DThreads / 4),
+                    kSmall3DSmem * sizeof(double), s, p);
   const char* e = getenv("SGWG_3D_PIPE");
   if (p.half_tiles || !(e && e[0] == '0')) {  // persistent, pipelined
     int dev = 0, sms = 148;
@@ -2285,6 +2309,9 @@ cudaError_t configure() {
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(plane_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             200 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = cudaFuncSetAttribute(stage3d_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kSmall3DSmem * (int)sizeof(double));
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(stage3d_pipe_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (2 * kPipe3DBox + 3 * kPipe3DDn) * (int)sizeof(double));

@@ -769,13 +769,18 @@ int build_tasks(sgwg_family* f) {
     CK(cudaMemcpy(f->dtiles2d_q, tq.data(), sizeof(int4) * tq.size(), cudaMemcpyHostToDevice));
   }
   if (f->d == 3 && !f->no_fused2d) {  // fast 3D stage tiles, 3 shapes
-    // default 1024-point tiles, shape codes 3..5, pipelined kernel with two CTAs per SM
-    // (measured: C3 171.2 -> 164.9 ms, S3 39.2 -> 38.5 ms); SGWG_3D_TILE=2048: 2048 points
+    // default 512-point tiles (8x8x8, shape code 6), one per CTA, four CTAs per SM
+    // (measured: C3 165.3 -> 155.3 ms, S3 stage 1246 -> 1066 us against the pipelined kernel
+    // on 1024-point tiles, two CTAs per SM, shape codes 3..5: SGWG_3D_TILE=1024; 2048-point
+    // tiles, one CTA per SM: SGWG_3D_TILE=2048)
     static const int shp3f[3][3] = {{8, 16, 16}, {16, 8, 16}, {16, 16, 8}};
     static const int shp3h[3][3] = {{8, 8, 16}, {8, 16, 8}, {16, 8, 8}};
+    static const int shp3q[3][3] = {{8, 8, 8}, {8, 8, 8}, {8, 8, 8}};
     const char* e3 = std::getenv("SGWG_3D_TILE");
-    f->tiles3d_half = (e3 != nullptr && std::string(e3) == "2048") ? 0 : 1;
-    const int(*shp3)[3] = f->tiles3d_half ? shp3h : shp3f;
+    f->tiles3d_half = 2;
+    if (e3 != nullptr && std::string(e3) == "1024") f->tiles3d_half = 1;
+    if (e3 != nullptr && std::string(e3) == "2048") f->tiles3d_half = 0;
+    const int(*shp3)[3] = (f->tiles3d_half == 2) ? shp3q : f->tiles3d_half ? shp3h : shp3f;
     std::vector<int4> t3;
     int smax = 0;
     bool ok = true;
@@ -801,7 +806,8 @@ int build_tasks(sgwg_family* f) {
       for (int i0 = 0; i0 < M.ext[0]; i0 += TX)
         for (int j0 = 0; j0 < M.ext[1]; j0 += TY)
           for (int l0 = 0; l0 < M.ext[2]; l0 += TZ)
-            t3.push_back(make_int4(mi, (i0 << 16) | j0, (l0 << 8) | (best + 3 * f->tiles3d_half), 0));
+            t3.push_back(make_int4(mi, (i0 << 16) | j0,
+                                   (l0 << 8) | (f->tiles3d_half == 2 ? 6 : best + 3 * f->tiles3d_half), 0));
     }
     if (ok) {
       f->ntiles3d_fast = (int)t3.size();

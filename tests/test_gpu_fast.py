@@ -89,7 +89,7 @@ def test_combine_fast(ctx_fast, oracle):
 
 # Every tile-size variant of the fast 2D / 3D stage kernels and of the
 # persistent 2D evolve against the oracle (the defaults pick one per family
-# size: 512-point stage tiles, 1024- or 512-point persistent tiles, 1024-point
+# size: 512-point stage tiles, 1024- or 512-point persistent tiles, 512-point
 # 3D tiles; the others stay selectable and must stay correct).
 @pytest.mark.parametrize("env,name,over,T", [
     ({"SGWG_NO_PERSIST": "1", "SGWG_TILE2D": "2048"}, "C2", {"nl": 3, "root": [16, 16]}, 0.02),
@@ -102,6 +102,7 @@ def test_combine_fast(ctx_fast, oracle):
     ({"SGWG_PERSIST_TILE": "512"}, "C2", {"nl": 4, "root": [16, 16]}, 0.02),
     ({"SGWG_3D_TILE": "2048"}, "C3", {"nl": 3, "root": [16, 16, 16]}, 0.004),
     ({"SGWG_3D_TILE": "1024"}, "C3", {"nl": 3, "root": [16, 16, 16]}, 0.004),
+    ({"SGWG_3D_TILE": "512"}, "C3", {"nl": 3, "root": [16, 16, 16]}, 0.004),
 ])
 def test_tile_variants_fast(ctx_fast, oracle, monkeypatch, env, name, over, T):
     for k, v in env.items():
