@@ -19,7 +19,10 @@
 
 namespace sgwg {
 
-constexpr int kFieldThreads = 512;
+#ifndef SGWG_FIELD_THREADS
+#define SGWG_FIELD_THREADS 512
+#endif
+constexpr int kFieldThreads = SGWG_FIELD_THREADS;
 constexpr int kFieldMaxX = 2048;
 constexpr int kFieldSmemDoubles = 6 * kFieldMaxX + 2 * kFieldMaxX;  // + 2 x 2H twiddles
 
