@@ -1848,7 +1848,7 @@ __global__ void __launch_bounds__(kFastThreads / Q, Q)
           tile_body_half<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
         else
           tile_body<BURGERS, true>(p, pp.base.mem + tk.x, tk, sm);
-        __syncthreads();
+        if (t + (int)gridDim.x < pp.base.ntiles) __syncthreads();  // (grid.sync has one)
       }
       SGWG_MARK(p.trace_ss, 3);
       grid.sync();
