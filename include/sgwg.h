@@ -131,6 +131,9 @@ typedef void (*sgwg_stop_cb)(double t, void* user);
 /* Bind a CUDA device (one process per GPU).  Replaces nothing in the
  * reference (it is single-process CPU; parallel.hpp:12-31 thread fan-out). */
 int sgwg_init(int device, sgwg_ctx** out);
+/* Frees the context.  While families created on it are still open the call is
+ * deferred: the context (and its stream) is freed by the last
+ * sgwg_family_destroy. */
 int sgwg_shutdown(sgwg_ctx* ctx);
 const char* sgwg_last_error(void);
 int sgwg_version(void);
@@ -254,8 +257,8 @@ int sgwg_vp_field(sgwg_family* fam, double* rho, size_t nrho, double* E, size_t 
 /* Per-step field energy of the last sgwg_evolve (BASELINE C4 "log|E|_2 recorded
  * per step"): out[s] = ||E_c||_2 at the start of step s, E_c = sum_m c_m I_m(E_m)
  * on the finest x-grid (I_m: separable degree-4 Lagrange interpolation,
- * interp.hpp:36-53), ||.||_2 with the finest x-spacings.  Local members only in
- * a sharded family. */
+ * interp.hpp:36-53), ||.||_2 with the finest x-spacings.  SGWG_EUNSUPPORTED on
+ * a sharded family (the record would cover the local members only). */
 int sgwg_field_energy(sgwg_family* fam, double* out, size_t cap, size_t* n);
 
 /* ---- host-side initial data: initialize_family (models.hpp:855-871) ------- */

@@ -207,6 +207,45 @@ class Oracle(_Lib):
         L.sgwo_family_wave_speeds.restype = C.c_int
         L.sgwo_restrict_preset.argtypes = [C.c_int, C.POINTER(Domain), _IP, _DP]
         L.sgwo_restrict_preset.restype = C.c_int
+        L.sgwo_set_threads.argtypes = [C.c_int]
+        L.sgwo_set_threads.restype = None
+        L.sgwo_combine_box.argtypes = [C.POINTER(Domain), _DP, C.c_int, C.c_double, _IP, _IP, _DP]
+        L.sgwo_combine_box.restype = C.c_int
+        L.sgwo_field_energy.argtypes = [C.POINTER(Domain), C.c_int, _DP]
+        L.sgwo_field_energy.restype = C.c_double
+        L.sgwo_set_energy_record.argtypes = [_DP, C.c_long]
+        L.sgwo_set_energy_record.restype = None
+        self._energy_buf = None
+
+    def combine_box(self, dom, states, lo, hi, mode=WENO, eps=1e-6):
+        """the combined solution on the finest-grid box [lo, hi) (bitwise = combine)"""
+        states = np.ascontiguousarray(states, dtype=np.float64)
+        lo = np.ascontiguousarray(lo, dtype=np.int32)
+        hi = np.ascontiguousarray(hi, dtype=np.int32)
+        out = np.zeros(int(np.prod(hi - lo)))
+        if self.lib.sgwo_combine_box(C.byref(dom), _dp(states), mode, eps, _ip(lo), _ip(hi),
+                                     _dp(out)):
+            raise ValueError("combine_box failed")
+        return out.reshape(tuple(int(h - l) for l, h in zip(lo, hi)))
+
+    def field_energy(self, dom, space_dim, states):
+        states = np.ascontiguousarray(states, dtype=np.float64)
+        return float(self.lib.sgwo_field_energy(C.byref(dom), space_dim, _dp(states)))
+
+    def record_energy(self, cap):
+        """start a per-step field-energy record in evolve (None: stop); returns the buffer"""
+        if cap is None:
+            self.lib.sgwo_set_energy_record(None, 0)
+            self._energy_buf = None
+            return None
+        self._energy_buf = np.zeros(int(cap))
+        self.lib.sgwo_set_energy_record(_dp(self._energy_buf), int(cap))
+        return self._energy_buf
+
+    def set_threads(self, n):
+        """member-level OpenMP threads (bitwise-identical results for any n)"""
+        self.lib.sgwo_set_threads(int(n))
+        return self
 
     def total_points(self, dom):
         return int(self.lib.sgwo_family_total_points(C.byref(dom)))

@@ -23,6 +23,13 @@
 
 static double sqr(double x) { return x * x; } /* weno.hpp:31 */
 
+/* Member-level parallelism of the oracle (OpenMP; 1 = serial, the default).
+ * Members are independent within a step given dt (timestep.hpp:156-165 loops
+ * over them serially), so every result is bitwise the same for any count. */
+static int g_threads = 1;
+void sgwo_set_threads(int n) { g_threads = (n < 1) ? 1 : n; }
+int sgwo_get_threads(void) { return g_threads; }
+
 /* ------------------------------------------------------------------------ */
 /* grid.hpp                                                                  */
 /* ------------------------------------------------------------------------ */
@@ -355,6 +362,21 @@ static void free_coords(double** c, int d) {
 static void spectral_poisson(int dxs, const int* n, const double* L, const double* rho, double* E) {
   const int n1 = n[0], n2 = (dxs == 2) ? n[1] : 1;
   const size_t N = (size_t)n1 * (size_t)n2;
+  /* twiddle tables: the same cos, sin of 2 pi ph / n that the sums used inline */
+  double* c1t = (double*)malloc(sizeof(double) * (size_t)n1);
+  double* s1t = (double*)malloc(sizeof(double) * (size_t)n1);
+  double* c2t = (double*)malloc(sizeof(double) * (size_t)n2);
+  double* s2t = (double*)malloc(sizeof(double) * (size_t)n2);
+  for (int ph = 0; ph < n1; ++ph) {
+    const double th = 2.0 * M_PI * (double)ph / (double)n1;
+    c1t[ph] = cos(th);
+    s1t[ph] = sin(th);
+  }
+  for (int ph = 0; ph < n2; ++ph) {
+    const double th = 2.0 * M_PI * (double)ph / (double)n2;
+    c2t[ph] = cos(th);
+    s2t[ph] = sin(th);
+  }
   double* rr = (double*)calloc(N, sizeof(double));
   double* ri = (double*)calloc(N, sizeof(double));
   /* forward DFT, dimension 1 (fast) then dimension 0 */
@@ -365,10 +387,9 @@ static void spectral_poisson(int dxs, const int* n, const double* L, const doubl
       double sr = 0.0, si = 0.0;
       for (int b = 0; b < n2; ++b) {
         long ph = ((long)k2 * b) % n2;
-        double th = 2.0 * M_PI * (double)ph / (double)n2;
         double v = rho[(size_t)a * n2 + b];
-        sr += v * cos(th);
-        si -= v * sin(th);
+        sr += v * c2t[ph];
+        si -= v * s2t[ph];
       }
       tr[(size_t)a * n2 + k2] = sr;
       ti[(size_t)a * n2 + k2] = si;
@@ -378,8 +399,7 @@ static void spectral_poisson(int dxs, const int* n, const double* L, const doubl
       double sr = 0.0, si = 0.0;
       for (int a = 0; a < n1; ++a) {
         long ph = ((long)k1 * a) % n1;
-        double th = 2.0 * M_PI * (double)ph / (double)n1;
-        double c = cos(th), s = -sin(th);
+        double c = c1t[ph], s = -s1t[ph];
         double xr = tr[(size_t)a * n2 + k2], xi = ti[(size_t)a * n2 + k2];
         sr += xr * c - xi * s;
         si += xr * s + xi * c;
@@ -416,8 +436,7 @@ static void spectral_poisson(int dxs, const int* n, const double* L, const doubl
         double sr = 0.0, si = 0.0;
         for (int k2 = 0; k2 < n2; ++k2) {
           long ph = ((long)k2 * b) % n2;
-          double th = 2.0 * M_PI * (double)ph / (double)n2;
-          double c = cos(th), s = sin(th);
+          double c = c2t[ph], s = s2t[ph];
           double xr = tr[(size_t)k1 * n2 + k2], xi = ti[(size_t)k1 * n2 + k2];
           sr += xr * c - xi * s;
           si += xr * s + xi * c;
@@ -430,8 +449,7 @@ static void spectral_poisson(int dxs, const int* n, const double* L, const doubl
         double sr = 0.0;
         for (int k1 = 0; k1 < n1; ++k1) {
           long ph = ((long)k1 * a) % n1;
-          double th = 2.0 * M_PI * (double)ph / (double)n1;
-          sr += ur[(size_t)k1 * n2 + b] * cos(th) - ui[(size_t)k1 * n2 + b] * sin(th);
+          sr += ur[(size_t)k1 * n2 + b] * c1t[ph] - ui[(size_t)k1 * n2 + b] * s1t[ph];
         }
         E[(size_t)comp * N + (size_t)a * n2 + b] = sr / (double)N;
       }
@@ -442,6 +460,10 @@ static void spectral_poisson(int dxs, const int* n, const double* L, const doubl
   free(ri);
   free(tr);
   free(ti);
+  free(c1t);
+  free(s1t);
+  free(c2t);
+  free(s2t);
 }
 
 static int vp_field_geom(const sgwo_domain* dom, const geom_t* g, int dxs, const double* f,
@@ -639,8 +661,16 @@ int sgwo_family_wave_speeds(const sgwo_domain* dom, const sgwo_model* model, con
         }
       }
     if (model->kind == SGWO_VLASOV_POISSON) {
-      /* family max |E_j| over members (new physics) */
+      /* family max |E_j| over members (new physics); per-member maxima in
+       * parallel, folded in member order */
+      size_t* offs = (size_t*)malloc(sizeof(size_t) * (size_t)nm);
+      double* mx = (double*)calloc((size_t)nm * 4, sizeof(double));
       size_t off = 0;
+      for (int m = 0; m < nm; ++m) {
+        offs[m] = off;
+        off += sgwo_member_points(dom, lv + m * d);
+      }
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
       for (int m = 0; m < nm; ++m) {
         geom_t g;
         make_geom(dom, lv + m * d, &g);
@@ -649,19 +679,109 @@ int sgwo_family_wave_speeds(const sgwo_domain* dom, const sgwo_model* model, con
         size_t nx = g.total / vn;
         double* E = (double*)malloc(sizeof(double) * nx * (size_t)dxs);
         double* rho = (double*)malloc(sizeof(double) * nx);
-        vp_field_geom(dom, &g, dxs, states + off, rho, E);
-        for (int j = 0; j < dxs; ++j) {
-          double a = max_abs(E + (size_t)j * nx, nx);
-          speeds[dxs + j] = (speeds[dxs + j] < a) ? a : speeds[dxs + j];
-        }
+        vp_field_geom(dom, &g, dxs, states + offs[m], rho, E);
+        for (int j = 0; j < dxs; ++j) mx[m * 4 + j] = max_abs(E + (size_t)j * nx, nx);
         free(E);
         free(rho);
-        off += g.total;
       }
+      for (int m = 0; m < nm; ++m)
+        for (int j = 0; j < dxs; ++j) {
+          const double a = mx[m * 4 + j];
+          speeds[dxs + j] = (speeds[dxs + j] < a) ? a : speeds[dxs + j];
+        }
+      free(offs);
+      free(mx);
     }
   }
   free(lv);
   return SGWO_OK;
+}
+
+/* Per-step field-energy record of the Vlasov-Poisson evolve (new physics, the
+ * device record sgwg_field_energy): ||E_c||_2 on the finest x-grid with
+ * E_c = sum_m c_m I_m(E_m), I_m separable degree-4 Lagrange upsampling
+ * (interp.hpp:36-53; dimension 1 first in 2D), members in order. */
+double sgwo_field_energy(const sgwo_domain* dom, int space_dim, const double* states) {
+  const int d = dom->d, dxs = space_dim;
+  int* lv;
+  int nm = family_levels(dom, &lv);
+  long long coef[4];
+  sgwo_combination_coefficients(d, dom->nl, coef);
+  int nf[2] = {dom->root_cells[0] << dom->nl, dxs == 2 ? dom->root_cells[1] << dom->nl : 1};
+  const size_t NF = (size_t)nf[0] * (size_t)nf[1];
+  size_t* offs = (size_t*)malloc(sizeof(size_t) * (size_t)nm);
+  size_t off = 0;
+  for (int m = 0; m < nm; ++m) {
+    offs[m] = off;
+    off += sgwo_member_points(dom, lv + m * d);
+  }
+  double** fine = (double**)malloc(sizeof(double*) * (size_t)nm);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+  for (int m = 0; m < nm; ++m) {
+    geom_t g;
+    make_geom(dom, lv + m * d, &g);
+    size_t vn = 1;
+    for (int k = dxs; k < d; ++k) vn *= (size_t)g.points[k];
+    const size_t nx = g.total / vn;
+    double* E = (double*)malloc(sizeof(double) * nx * (size_t)dxs);
+    double* rho = (double*)malloc(sizeof(double) * nx);
+    vp_field_geom(dom, &g, dxs, states + offs[m], rho, E);
+    const int n0 = g.points[0], n1 = (dxs == 2) ? g.points[1] : 1;
+    const int m0 = dom->nl - lv[m * d], m1 = (dxs == 2) ? dom->nl - lv[m * d + 1] : 0;
+    double* out = (double*)malloc(sizeof(double) * NF * (size_t)dxs);
+    double* rows = (double*)malloc(sizeof(double) * (size_t)n0 * (size_t)nf[1]);
+    double* col = (double*)malloc(sizeof(double) * (size_t)(n0 > nf[0] ? n0 : nf[0]));
+    double* col2 = (double*)malloc(sizeof(double) * (size_t)nf[0]);
+    for (int c = 0; c < dxs; ++c) {
+      const double* Ec = E + (size_t)c * nx;
+      for (int i = 0; i < n0; ++i) {
+        if (m1 > 0)
+          sgwo_upsample_line(Ec + (size_t)i * n1, n1, rows + (size_t)i * nf[1], nf[1], m1,
+                             SGWO_PERIODIC, SGWO_INTERP_LAGRANGE, 0.0);
+        else
+          memcpy(rows + (size_t)i * nf[1], Ec + (size_t)i * n1, sizeof(double) * (size_t)n1);
+      }
+      for (int j = 0; j < nf[1]; ++j) {
+        for (int i = 0; i < n0; ++i) col[i] = rows[(size_t)i * nf[1] + j];
+        if (m0 > 0)
+          sgwo_upsample_line(col, n0, col2, nf[0], m0, SGWO_PERIODIC, SGWO_INTERP_LAGRANGE, 0.0);
+        else
+          memcpy(col2, col, sizeof(double) * (size_t)nf[0]);
+        for (int i = 0; i < nf[0]; ++i) out[(size_t)c * NF + (size_t)i * nf[1] + j] = col2[i];
+      }
+    }
+    free(rows);
+    free(col);
+    free(col2);
+    free(E);
+    free(rho);
+    fine[m] = out;
+  }
+  double* acc = (double*)calloc(NF * (size_t)dxs, sizeof(double));
+  for (int m = 0; m < nm; ++m) {
+    int s = 0;
+    for (int k = 0; k < d; ++k) s += lv[m * d + k];
+    const double c = (double)coef[dom->nl - s];
+    for (size_t i = 0; i < NF * (size_t)dxs; ++i) acc[i] += c * fine[m][i];
+    free(fine[m]);
+  }
+  double hv = (dom->upper[0] - dom->lower[0]) / nf[0];
+  if (dxs == 2) hv *= (dom->upper[1] - dom->lower[1]) / nf[1];
+  double e = 0.0;
+  for (size_t i = 0; i < NF * (size_t)dxs; ++i) e += acc[i] * acc[i];
+  free(acc);
+  free(fine);
+  free(offs);
+  free(lv);
+  return sqrt(e * hv);
+}
+
+/* optional per-step energy record of sgwo_evolve (Vlasov-Poisson models) */
+static double* g_energy = NULL;
+static long g_energy_cap = 0;
+void sgwo_set_energy_record(double* buf, long cap) {
+  g_energy = buf;
+  g_energy_cap = (buf != NULL) ? cap : 0;
 }
 
 static int cmp_double(const void* a, const void* b) {
@@ -718,20 +838,43 @@ int sgwo_evolve(const sgwo_domain* dom, const sgwo_model* model, const sgwo_poli
     if (stop > tfinal + eps_t) break;
     while (stop - t > eps_t) {
       double speeds[4];
+      if (g_energy != NULL && model->kind == SGWO_VLASOV_POISSON && step_index < g_energy_cap)
+        g_energy[step_index] = sgwo_field_energy(dom, model->space_dim, states);
       sgwo_family_wave_speeds(dom, model, states, speeds);
       double dt = sgwo_compute_dt(pol, speeds, fsp, d, stop - t);
       if (stop - (t + dt) <= eps_t) dt = stop - t;
-      for (int m = 0; m < nm; ++m) {
-        int f = sgwo_rk3_step(dom, lv + m * d, model, states + off[m], dt);
-        if (f) {
-          if (fail_member) *fail_member = m;
-          if (fail_step) *fail_step = step_index;
-          if (fail_stage) *fail_stage = f;
-          status = SGWO_ENONFINITE;
-          break;
+      int first_fail = nm, fail_code = 0;
+      if (g_threads <= 1) {
+        for (int m = 0; m < nm; ++m) {
+          int f = sgwo_rk3_step(dom, lv + m * d, model, states + off[m], dt);
+          if (f) {
+            first_fail = m;
+            fail_code = f;
+            break;
+          }
         }
+      } else {
+        /* members in parallel; the failure reported is the first member in
+         * order (the serial loop's), later members' states are then unspecified
+         * as after the reference's exception */
+        int* codes = (int*)calloc((size_t)nm, sizeof(int));
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+        for (int m = 0; m < nm; ++m) codes[m] = sgwo_rk3_step(dom, lv + m * d, model, states + off[m], dt);
+        for (int m = 0; m < nm; ++m)
+          if (codes[m]) {
+            first_fail = m;
+            fail_code = codes[m];
+            break;
+          }
+        free(codes);
       }
-      if (status != SGWO_OK) break;
+      if (first_fail < nm) {
+        if (fail_member) *fail_member = first_fail;
+        if (fail_step) *fail_step = step_index;
+        if (fail_stage) *fail_stage = fail_code;
+        status = SGWO_ENONFINITE;
+        break;
+      }
       t += dt;
       if (dts && step_index < cap) dts[step_index] = dt;
       ++step_index;
@@ -872,6 +1015,178 @@ int sgwo_prolong(const sgwo_domain* dom, const int* level, const double* src, in
   return SGWO_OK;
 }
 
+/* One output point j of sgwo_upsample_line (interp.hpp:151-189): the same
+ * OffsetTable offsets, stencil gather, smoothness indicators and expression
+ * order, so the value is bitwise that of the whole-line routine. */
+static double upsample_at(const double* src, int n_src, int j, int m, int bc, int mode,
+                          double eps) {
+  const int f = 1 << m;
+  const int r = j & (f - 1);
+  if (r == 0) return src[(j >> m) % n_src];
+  int di;
+  double t, c[3];
+  if (mode == SGWO_INTERP_WENO) {
+    di = (r >= f / 2) ? 1 : 0;
+    t = (double)r / f - di;
+  } else {
+    di = 0;
+    t = (double)r / f;
+  }
+  interp_weights(t, c);
+  const int i = (j >> m) + di;
+  double stencil[5], beta[3] = {0, 0, 0};
+  for (int s = 0; s < 5; ++s) {
+    int q = i - 2 + s;
+    if (bc == SGWO_PERIODIC)
+      stencil[s] = src[((q % n_src) + n_src) % n_src];
+    else
+      stencil[s] = (q >= 0 && q < n_src) ? src[q] : 0.0;
+  }
+  if (mode == SGWO_INTERP_WENO) sgwo_smoothness_indicators(stencil, beta);
+  double p[3];
+  substencil_values(stencil, t, p);
+  if (mode == SGWO_INTERP_LAGRANGE) return c[0] * p[0] + c[1] * p[1] + c[2] * p[2];
+  const double a0 = c[0] / sqr(eps + beta[0]);
+  const double a1 = c[1] / sqr(eps + beta[1]);
+  const double a2 = c[2] / sqr(eps + beta[2]);
+  return (a0 * p[0] + a1 * p[1] + a2 * p[2]) / (a0 + a1 + a2);
+}
+
+/* source indices of a member line that the outputs [lo, hi) read (sorted, unique) */
+static int needed_sources(int n_src, int m, int bc, int mode, int lo, int hi, int* out) {
+  char* need = (char*)calloc((size_t)n_src, 1);
+  const int f = 1 << m;
+  for (int j = lo; j < hi; ++j) {
+    const int r = j & (f - 1);
+    if (r == 0) {
+      need[(j >> m) % n_src] = 1;
+      continue;
+    }
+    const int di = (mode == SGWO_INTERP_WENO && r >= f / 2) ? 1 : 0;
+    const int i = (j >> m) + di;
+    for (int s = 0; s < 5; ++s) {
+      int q = i - 2 + s;
+      if (bc == SGWO_PERIODIC)
+        need[((q % n_src) + n_src) % n_src] = 1;
+      else if (q >= 0 && q < n_src)
+        need[q] = 1;
+    }
+  }
+  int c = 0;
+  for (int q = 0; q < n_src; ++q)
+    if (need[q]) out[c++] = q;
+  free(need);
+  return c;
+}
+
+/* The combined solution (combine.hpp:95-122) on the finest-grid box
+ * [lo_k, hi_k): each member prolonged (interp.hpp:197-250, dimensions in
+ * order) only on the lines the box depends on, then acc += c * p in member
+ * order -- bitwise the corresponding entries of sgwo_combine, at a cost
+ * proportional to the box (cut planes of BASELINE C5, whose full finest grid
+ * is 34.6 GB).  out: row-major over the box. */
+int sgwo_combine_box(const sgwo_domain* dom, const double* states, int mode, double eps,
+                     const int* lo, const int* hi, double* out) {
+  const int d = dom->d;
+  int* lv;
+  int nm = family_levels(dom, &lv);
+  if (nm <= 0) return SGWO_EINVAL;
+  int fl[4], fpts[4];
+  double fsp[4];
+  for (int k = 0; k < d; ++k) fl[k] = dom->nl;
+  sgwo_member_geometry(dom, fl, fpts, fsp);
+  size_t nbox = 1;
+  for (int k = 0; k < d; ++k) {
+    if (lo[k] < 0 || hi[k] > fpts[k] || lo[k] >= hi[k]) {
+      free(lv);
+      return SGWO_EINVAL;
+    }
+    nbox *= (size_t)(hi[k] - lo[k]);
+  }
+  long long coef[4];
+  sgwo_combination_coefficients(d, dom->nl, coef);
+  size_t* offs = (size_t*)malloc(sizeof(size_t) * (size_t)nm);
+  size_t off = 0;
+  for (int m = 0; m < nm; ++m) {
+    offs[m] = off;
+    off += sgwo_member_points(dom, lv + m * d);
+  }
+  double** vals = (double**)malloc(sizeof(double*) * (size_t)nm);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+  for (int mi = 0; mi < nm; ++mi) {
+    const int* level = lv + mi * d;
+    int pts[4];
+    double sp[4];
+    sgwo_member_geometry(dom, level, pts, sp);
+    /* per dimension: the working index list (sources before the dimension is
+     * processed, box outputs after) */
+    int* idx[4];
+    int ext[4], msh[4];
+    for (int k = 0; k < d; ++k) {
+      msh[k] = dom->nl - level[k];
+      idx[k] = (int*)malloc(sizeof(int) * (size_t)(pts[k] > fpts[k] ? pts[k] : fpts[k]));
+      ext[k] = needed_sources(pts[k], msh[k], dom->bc[k], mode, lo[k], hi[k], idx[k]);
+    }
+    /* gather the member sub-array */
+    size_t n = 1;
+    for (int k = 0; k < d; ++k) n *= (size_t)ext[k];
+    double* cur = (double*)malloc(sizeof(double) * n);
+    size_t mstr[4];
+    mstr[d - 1] = 1;
+    for (int k = d - 2; k >= 0; --k) mstr[k] = mstr[k + 1] * (size_t)pts[k + 1];
+    {
+      int it[4] = {0, 0, 0, 0};
+      for (size_t lin = 0; lin < n; ++lin) {
+        size_t src = 0;
+        for (int k = 0; k < d; ++k) src += (size_t)idx[k][it[k]] * mstr[k];
+        cur[lin] = states[offs[mi] + src];
+        for (int k = d - 1; k >= 0; --k) {
+          if (++it[k] < ext[k]) break;
+          it[k] = 0;
+        }
+      }
+    }
+    int lmax = 1;
+    for (int k = 0; k < d; ++k) lmax = (pts[k] > lmax) ? pts[k] : lmax;
+    double* line = (double*)malloc(sizeof(double) * (size_t)lmax);
+    for (int k = 0; k < d; ++k) {
+      const int nb = hi[k] - lo[k];
+      size_t outer = 1, inner = 1;
+      for (int q = 0; q < k; ++q) outer *= (size_t)ext[q];
+      for (int q = k + 1; q < d; ++q) inner *= (size_t)ext[q];
+      double* next = (double*)malloc(sizeof(double) * outer * (size_t)nb * inner);
+      for (size_t o = 0; o < outer; ++o)
+        for (size_t in = 0; in < inner; ++in) {
+          for (int q = 0; q < pts[k]; ++q) line[q] = 0.0; /* entries never read */
+          for (int a = 0; a < ext[k]; ++a)
+            line[idx[k][a]] = cur[(o * (size_t)ext[k] + (size_t)a) * inner + in];
+          for (int b = 0; b < nb; ++b)
+            next[(o * (size_t)nb + (size_t)b) * inner + in] =
+                (msh[k] == 0) ? line[lo[k] + b]
+                              : upsample_at(line, pts[k], lo[k] + b, msh[k], dom->bc[k], mode, eps);
+        }
+      free(cur);
+      cur = next;
+      ext[k] = nb;
+    }
+    vals[mi] = cur;
+    free(line);
+    for (int k = 0; k < d; ++k) free(idx[k]);
+  }
+  for (size_t i = 0; i < nbox; ++i) out[i] = 0.0;
+  for (int mi = 0; mi < nm; ++mi) {
+    int s = 0;
+    for (int k = 0; k < d; ++k) s += lv[mi * d + k];
+    const double c = (double)coef[dom->nl - s];
+    for (size_t i = 0; i < nbox; ++i) out[i] += c * vals[mi][i];
+    free(vals[mi]);
+  }
+  free(vals);
+  free(offs);
+  free(lv);
+  return SGWO_OK;
+}
+
 /* combine.hpp:95-122 */
 int sgwo_combine(const sgwo_domain* dom, const double* states, int mode, double eps, double* out) {
   const int d = dom->d;
@@ -882,17 +1197,37 @@ int sgwo_combine(const sgwo_domain* dom, const double* states, int mode, double 
   sgwo_combination_coefficients(d, dom->nl, coef);
   const size_t nt = sgwo_finest_points(dom);
   memset(out, 0, sizeof(double) * nt);
-  double* p = (double*)malloc(sizeof(double) * nt);
+  size_t* offs = (size_t*)malloc(sizeof(size_t) * (size_t)nm);
+  double* cs = (double*)malloc(sizeof(double) * (size_t)nm);
   size_t off = 0;
   for (int m = 0; m < nm; ++m) {
     int s = 0;
     for (int k = 0; k < d; ++k) s += lv[m * d + k];
-    const double c = (double)coef[dom->nl - s];
-    sgwo_prolong(dom, lv + m * d, states + off, mode, eps, p);
-    for (size_t i = 0; i < nt; ++i) out[i] += c * p[i];
+    cs[m] = (double)coef[dom->nl - s];
+    offs[m] = off;
     off += sgwo_member_points(dom, lv + m * d);
   }
+  /* batches of members prolonged in parallel, accumulated in member order
+   * (acc += c * p, combine.hpp:115-120) */
+  const int nb = (g_threads < nm) ? g_threads : nm;
+  double** p = (double**)malloc(sizeof(double*) * (size_t)nb);
+  for (int b = 0; b < nb; ++b) p[b] = (double*)malloc(sizeof(double) * nt);
+  for (int m0 = 0; m0 < nm; m0 += nb) {
+    const int cnt = (nm - m0 < nb) ? nm - m0 : nb;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+    for (int b = 0; b < cnt; ++b)
+      sgwo_prolong(dom, lv + (m0 + b) * d, states + offs[m0 + b], mode, eps, p[b]);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (size_t i = 0; i < nt; ++i) {
+      double acc = out[i];
+      for (int b = 0; b < cnt; ++b) acc += cs[m0 + b] * p[b][i];
+      out[i] = acc;
+    }
+  }
+  for (int b = 0; b < nb; ++b) free(p[b]);
   free(p);
+  free(offs);
+  free(cs);
   free(lv);
   return SGWO_OK;
 }

@@ -109,6 +109,11 @@ int sgwo_family_wave_speeds(const sgwo_domain* dom, const sgwo_model* model, con
 /* timestep.hpp:126-174 evolve_family over the packed member states (member order =
  * sorted levels).  dts/cap receive the dt sequence; nsteps its length.  On a
  * non-finite tendency returns SGWO_ENONFINITE with fail_{member,step,stage}. */
+/* member-level OpenMP threads of sgwo_evolve / sgwo_combine (default 1);
+ * results are bitwise independent of the count */
+void sgwo_set_threads(int n);
+int sgwo_get_threads(void);
+
 int sgwo_evolve(const sgwo_domain* dom, const sgwo_model* model, const sgwo_policy* pol,
                 double* states, double tfinal, const double* stops, int nstops, sgwo_stop_cb cb,
                 void* user, double* dts, long cap, long* nsteps, int* fail_member,
@@ -123,6 +128,17 @@ int sgwo_upsample_line(const double* src, int n_src, double* dst, int n_dst, int
 /* combine.hpp:95-122 */
 int sgwo_combine(const sgwo_domain* dom, const double* states, int interp_mode, double eps,
                  double* out);
+
+/* The combined solution on the finest-grid box [lo_k, hi_k) (row-major), each
+ * member prolonged only on the lines the box reads: bitwise equal to the same
+ * entries of sgwo_combine (cut planes of configurations whose finest grid is
+ * too large to materialise). */
+int sgwo_combine_box(const sgwo_domain* dom, const double* states, int interp_mode, double eps,
+                     const int* lo, const int* hi, double* out);
+/* Vlasov-Poisson field-energy record (sgwg_field_energy's definition) of the
+ * packed family states, and an optional per-step record filled by sgwo_evolve. */
+double sgwo_field_energy(const sgwo_domain* dom, int space_dim, const double* states);
+void sgwo_set_energy_record(double* buf, long cap);
 
 size_t sgwo_family_total_points(const sgwo_domain* dom);
 size_t sgwo_finest_points(const sgwo_domain* dom);

@@ -114,6 +114,8 @@ struct sgwg_ctx {
   int arith = SGWG_ARITH_EXACT;
   int profile = 0;
   int sm_count = 148;
+  int families = 0;      // open families created on this context
+  bool closing = false;  // sgwg_shutdown called while families were open
 };
 
 struct StageBufs {
@@ -873,6 +875,7 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   }
   sgwg_family* f = new sgwg_family();
   f->ctx = ctx;
+  ++ctx->families;
   f->dom = *dom;
   f->d = dom->d;
   f->nl = dom->nl;
@@ -1469,6 +1472,8 @@ int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, dou
   const long long nout = (b - a) * per_row;
   if (f->slab_out_doubles < nout && !out_is_device) {
     cudaFree(f->slab_out);
+    f->slab_out = nullptr;
+    f->slab_out_doubles = 0;
     CK(cudaMalloc(&f->slab_out, sizeof(double) * nout));
     f->slab_out_doubles = nout;
   }
@@ -1538,6 +1543,10 @@ int sgwg_init(int device, sgwg_ctx** out) {
 
 int sgwg_shutdown(sgwg_ctx* ctx) {
   if (ctx == nullptr) return SGWG_OK;
+  if (ctx->families > 0) {  // deferred: the last sgwg_family_destroy frees the context
+    ctx->closing = true;
+    return SGWG_OK;
+  }
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return SGWG_OK;
@@ -1637,7 +1646,12 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaEventDestroy(f->evfork);
   cudaEventDestroy(f->evjoin);
   cudaStreamDestroy(f->side);
+  sgwg_ctx* ctx = f->ctx;
   delete f;
+  if (--ctx->families == 0 && ctx->closing) {
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  }
   return SGWG_OK;
 }
 
@@ -2071,6 +2085,11 @@ int sgwg_field_energy(sgwg_family* f, double* out, size_t cap, size_t* n) {
   if (f == nullptr || out == nullptr) return fail_with(SGWG_EINVAL, "null argument");
   if (f->model.kind != SGWG_VLASOV_POISSON || f->fe == nullptr)
     return fail_with(SGWG_EINVAL, "field_energy: no Vlasov-Poisson evolve recorded");
+  // the record combines E over this rank's members only; the cross-rank sum
+  // of the combined field is not formed, so a sharded family has no record
+  if (f->comm != nullptr && f->nranks > 1)
+    return fail_with(SGWG_EUNSUPPORTED,
+                     "field_energy: not available on a sharded family (per-rank partial E)");
   const size_t steps = (size_t)std::min<long long>(f->stats.steps, f->fe_cap);
   const size_t m = std::min(cap, steps);
   if (m > 0) CK(cudaMemcpy(out, f->fe, sizeof(double) * m, cudaMemcpyDeviceToHost));
@@ -2324,35 +2343,45 @@ int sgwg_write_snapshot(sgwg_family* f, int mode, double eps, const char* path) 
     std::memcpy(hdr + 12 + 4 * k, &e, 4);
     std::memcpy(hdr + 32 + 8 * k, &f->fine_h[k], 8);
   }
-  // sharded family: every rank takes part in the combination's all-reduce, rank 0 writes
+  // sharded family: every rank takes part in the combination's all-reduce, rank 0 writes.
+  // The writer's I/O failures are deferred (io_st) so that it still joins every
+  // collective of the slab loop -- returning early would leave the other ranks
+  // blocked inside ncclAllReduce.
   const bool writer = (f->comm == nullptr || f->rank == 0);
   FILE* fp = writer ? std::fopen(path, "wb") : nullptr;
+  int io_st = SGWG_OK;
   if (writer && fp == nullptr)
-    return fail_with(SGWG_EINVAL, std::string("write_snapshot: cannot open ") + path);
-  int st = (!writer || std::fwrite(hdr, 1, sizeof(hdr), fp) == sizeof(hdr))
-               ? SGWG_OK
-               : fail_with(SGWG_EINVAL, "write_snapshot: write failed");
+    io_st = fail_with(SGWG_EINVAL, std::string("write_snapshot: cannot open ") + path);
+  if (io_st == SGWG_OK && writer && std::fwrite(hdr, 1, sizeof(hdr), fp) != sizeof(hdr))
+    io_st = fail_with(SGWG_EINVAL, "write_snapshot: write failed");
   double* host = nullptr;
   long long host_n = 0;
-  if (st == SGWG_OK)
-    st = for_each_combined_slab(f, mode, eps, [&](const double* dev, long long, long long n) -> int {
-      if (!writer) return SGWG_OK;
-      if (host_n < n) {
-        cudaFreeHost(host);
-        host = nullptr;
-        CK(cudaMallocHost(&host, sizeof(double) * n));
-        host_n = n;
+  int st = for_each_combined_slab(f, mode, eps, [&](const double* dev, long long, long long n) -> int {
+    if (!writer || io_st != SGWG_OK) return SGWG_OK;
+    if (host_n < n) {
+      cudaFreeHost(host);
+      host = nullptr;
+      host_n = 0;
+      if (cudaMallocHost(&host, sizeof(double) * n) != cudaSuccess) {
+        io_st = fail_with(SGWG_ECUDA, "write_snapshot: pinned host buffer");
+        return SGWG_OK;
       }
-      CK(cudaMemcpyAsync(host, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, f->ctx->stream));
-      CK(cudaStreamSynchronize(f->ctx->stream));
-      if (std::fwrite(host, sizeof(double), (size_t)n, fp) != (size_t)n)
-        return fail_with(SGWG_EINVAL, "write_snapshot: write failed");
+      host_n = n;
+    }
+    if (cudaMemcpyAsync(host, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, f->ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(f->ctx->stream) != cudaSuccess) {
+      io_st = fail_with(SGWG_ECUDA, "write_snapshot: device-to-host copy");
       return SGWG_OK;
-    });
+    }
+    if (std::fwrite(host, sizeof(double), (size_t)n, fp) != (size_t)n)
+      io_st = fail_with(SGWG_EINVAL, "write_snapshot: write failed");
+    return SGWG_OK;
+  });
   cudaFreeHost(host);
-  if (fp != nullptr && std::fclose(fp) != 0 && st == SGWG_OK)
-    st = fail_with(SGWG_EINVAL, "write_snapshot: close failed");
-  return st;
+  if (fp != nullptr && std::fclose(fp) != 0 && io_st == SGWG_OK)
+    io_st = fail_with(SGWG_EINVAL, "write_snapshot: close failed");
+  return (st != SGWG_OK) ? st : io_st;
 }
 
 int sgwg_combine(sgwg_family* f, int mode, double eps, double* out, size_t n, int out_is_device) {

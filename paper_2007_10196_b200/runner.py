@@ -115,43 +115,10 @@ def run(cfg: dict, roots: Optional[Sequence[int]] = None, grid_mode: str = "spar
             c["reference_spacing"] = min((c["upper"][k] - c["lower"][k]) / nr / (1 << c["nl"])
                                          for k in range(d))
             fam = sgwg.Family.from_config(ctx, c, single=(grid_mode == "single"))
-            fam.initialize(c["ic"])
-            result["finest_nh"] = nr << c["nl"]
-            series = []
-
-            def record(t, fam=fam, c=c, series=series):
-                st = fam.combined_stats(c["interp"], c["epsilon"])
-                series.append({"t": t, "mass": st["mass"], "min": st["min"], "max": st["max"]})
-                if out_dir:
-                    tag = "%.6f" % t
-                    fam.write_snapshot(os.path.join(out_dir, f"snapshot_t{tag}.sgw5"),
-                                       c["interp"], c["epsilon"])
-                    for name, da, db, fixed in cut_planes(c, fam):
-                        plane = fam.cut_plane(da, db, fixed, c["interp"], c["epsilon"])
-                        write_plane_csv(os.path.join(out_dir, f"{name}_t{tag}.csv"), c, fam,
-                                        da, db, plane)
-
-            if not table and (0.0 in stops or c["tfinal"] == 0.0):
-                record(0.0)
-            t0 = time.perf_counter()
-            if c["tfinal"] > 0.0:
-                fam.evolve_config(c, tfinal=c["tfinal"], stops=[] if table else stops,
-                                  on_stop=None if table else record)
-            if table:
-                st = fam.combined_stats(c["interp"], c["epsilon"], exact_preset=c["ic"],
-                                        t=c["tfinal"])
-            t1 = time.perf_counter()
-            result["wall_seconds"] = t1 - t0
-            if table:
-                row = {"grid": nr << c["nl"], "l1": st["l1"], "linf": st["linf"],
-                       "wall_seconds": t1 - t0, "order_l1": None, "order_linf": None}
-                if result["rows"]:
-                    prev = result["rows"][-1]
-                    row["order_l1"] = float(np.log2(prev["l1"] / row["l1"]))
-                    row["order_linf"] = float(np.log2(prev["linf"] / row["linf"]))
-                result["rows"].append(row)
-            else:
-                result["series"] = series
+            try:
+                _run_one(fam, c, nr, table, stops, out_dir, result)
+            finally:
+                fam.close()  # before ctx.close(): the family's stream lives in the context
     finally:
         if own:
             ctx.close()
@@ -171,6 +138,47 @@ def run(cfg: dict, roots: Optional[Sequence[int]] = None, grid_mode: str = "spar
                                             else "weno"))
             fh.write("wall_seconds,%.5e\n" % result["wall_seconds"])
     return result
+
+
+def _run_one(fam, c, nr, table, stops, out_dir, result):
+    """One root of run()'s refinement loop (runner.hpp:293-365) on an open family."""
+    fam.initialize(c["ic"])
+    result["finest_nh"] = nr << c["nl"]
+    series = []
+
+    def record(t, fam=fam, c=c, series=series):
+        st = fam.combined_stats(c["interp"], c["epsilon"])
+        series.append({"t": t, "mass": st["mass"], "min": st["min"], "max": st["max"]})
+        if out_dir:
+            tag = "%.6f" % t
+            fam.write_snapshot(os.path.join(out_dir, f"snapshot_t{tag}.sgw5"),
+                               c["interp"], c["epsilon"])
+            for name, da, db, fixed in cut_planes(c, fam):
+                plane = fam.cut_plane(da, db, fixed, c["interp"], c["epsilon"])
+                write_plane_csv(os.path.join(out_dir, f"{name}_t{tag}.csv"), c, fam,
+                                da, db, plane)
+
+    if not table and (0.0 in stops or c["tfinal"] == 0.0):
+        record(0.0)
+    t0 = time.perf_counter()
+    if c["tfinal"] > 0.0:
+        fam.evolve_config(c, tfinal=c["tfinal"], stops=[] if table else stops,
+                          on_stop=None if table else record)
+    if table:
+        st = fam.combined_stats(c["interp"], c["epsilon"], exact_preset=c["ic"],
+                                t=c["tfinal"])
+    t1 = time.perf_counter()
+    result["wall_seconds"] = t1 - t0
+    if table:
+        row = {"grid": nr << c["nl"], "l1": st["l1"], "linf": st["linf"],
+               "wall_seconds": t1 - t0, "order_l1": None, "order_linf": None}
+        if result["rows"]:
+            prev = result["rows"][-1]
+            row["order_l1"] = float(np.log2(prev["l1"] / row["l1"]))
+            row["order_linf"] = float(np.log2(prev["linf"] / row["linf"]))
+        result["rows"].append(row)
+    else:
+        result["series"] = series
 
 
 def compare_runs(dir_a: str, dir_b: str) -> dict:
