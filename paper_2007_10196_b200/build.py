@@ -33,7 +33,8 @@ UNITS = {
     "k_diag.cu": ["--fmad=true"],
     "sgwg_api.cu": ["--fmad=false"],
 }
-HEADERS = ["kernels.cuh", "sgwg_internal.h", "dt_device.cuh", "field_device.cuh", "pdl.cuh"]
+HEADERS = ["kernels.cuh", "sgwg_internal.h", "dt_device.cuh", "field_device.cuh", "pdl.cuh",
+           "plane4d.cuh"]
 
 
 def _stale(obj, deps):

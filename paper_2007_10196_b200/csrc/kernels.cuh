@@ -2284,6 +2284,10 @@ cudaError_t launch_vm_fields(const VmParams& p, int nmembers, int smem, cudaStre
   return launch_k(vm_fields_kernel, dim3(nmembers), dim3(256), (size_t)smem, s, p);
 }
 
+#if SGWG_FAST
+#include "plane4d.cuh"
+#endif
+
 cudaError_t configure() {
 #if SGWG_FAST
   cudaError_t e0 = cudaFuncSetAttribute(stage2d_fast_kernel<true, false>,
@@ -2309,6 +2313,8 @@ cudaError_t configure() {
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(plane_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             200 * 1024);
+  if (e0 != cudaSuccess) return e0;
+  e0 = configure_plane4();
   if (e0 != cudaSuccess) return e0;
   e0 = cudaFuncSetAttribute(stage3d_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kSmall3DSmem * (int)sizeof(double));

@@ -242,6 +242,9 @@ struct sgwg_family {
   PlaneTile* dptiles[2] = {nullptr, nullptr};  // fast 4D plane tiles (pairs (0,1), (2,3))
   int nptiles[2] = {0, 0};
   int psmem = 0;
+  int4* dp4tiles[2] = {nullptr, nullptr};  // whole-plane 4D tiles (plane4d.cuh): x pass, v pass
+  int np4tiles[2] = {0, 0};
+  int p4smem[2] = {0, 0};                  // dynamic shared memory (doubles) per pass
   double* rho_parts = nullptr;      // Vlasov-Poisson charge-density partial sums
   double* twid = nullptr;           // FFT twiddle table (2 x hmax)
   int hmax = 1;
@@ -312,6 +315,11 @@ int stage_tile_code() {
 // fast 4D plane path (kernels.cuh plane_fast_kernel)
 bool plane_path(const sgwg_family* f) {
   return f->d == 4 && f->nptiles[0] > 0 && f->nptiles[1] > 0 && arith_of(f) == SGWG_ARITH_FAST;
+}
+// fast 4D whole-plane path (plane4d.cuh), preferred when the family qualifies
+bool plane4_path(const sgwg_family* f) {
+  return f->d == 4 && f->np4tiles[0] > 0 && f->np4tiles[1] > 0 &&
+         arith_of(f) == SGWG_ARITH_FAST;
 }
 
 // Vlasov-Poisson field of `state`.  The charge density comes from the
@@ -413,7 +421,49 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     f->stats.kernel_launches++;
   }
   // every path below but the plane path writes a state without its rho partials
-  if (stage > 0 && !plane_path(f)) f->parts_of = nullptr;
+  if (stage > 0 && !plane_path(f) && !plane4_path(f)) f->parts_of = nullptr;
+  if (plane4_path(f)) {  // fast 4D on whole planes: x pass -> K, v pass + RK stage + rho
+    const bool vp = (m.kind == SGWG_VLASOV_POISSON);
+    Plane4Params p{};
+    p.mem = f->dmem;
+    p.stage = stage;
+    p.linear = (m.weno_mode == SGWG_WENO_LINEAR);
+    p.eps = m.epsilon;
+    p.space_dim = m.space_dim;
+    p.uin = b.uin;
+    p.un = b.un;
+    p.out = b.out;
+    p.kbuf = f->K;
+    p.efield = f->E;
+    p.ctl = f->ctl;
+    p.fail = f->fail;
+    p.counter = f->counter;
+    for (int pass = 0; pass < 2; ++pass) {
+      p.tiles = f->dp4tiles[pass];
+      if (vp) {
+        p.flux_a = p.flux_b = (pass == 0) ? kFluxKinX : kFluxKinVP;
+      } else {
+        p.flux_a = p.flux_b = kFluxAdvect;
+        p.c_a = m.speeds[2 * pass];
+        p.c_b = m.speeds[2 * pass + 1];
+      }
+      p.rho_parts = (pass == 1 && vp) ? f->rho_parts : nullptr;
+      p.dtp = (pass == 1) ? dtp : nullptr;
+      if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
+      CK(fast::launch_plane4(p, pass, f->np4tiles[pass], (size_t)f->p4smem[pass] * sizeof(double),
+                             f->ctx->stream));
+      if (timed) {
+        CK(cudaEventRecord(f->ev1, f->ctx->stream));
+        CK(cudaEventSynchronize(f->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+        account_timed(f, stage, 2, pass == 1, ms);
+      }
+      f->stats.kernel_launches++;
+    }
+    if (stage > 0) f->parts_of = vp ? b.out : nullptr;
+    return SGWG_OK;
+  }
   if (plane_path(f)) {  // fast 4D: dims (0,1) -> K, dims (2,3) + RK stage
     const bool vp = (m.kind == SGWG_VLASOV_POISSON);
     PlaneParams p{};
@@ -931,7 +981,9 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   if (st != SGWG_OK) return st;
   CK(cudaMalloc(&f->dmem, sizeof(MemberDesc) * std::max(1, f->nm)));
   CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
-  const size_t bytes = sizeof(double) * std::max<long long>(1, f->total);
+  // (+2 doubles: the whole-plane 4D pass stages 16-byte-aligned spans that may
+  // round one double past a member's end)
+  const size_t bytes = sizeof(double) * (std::max<long long>(1, f->total) + 2);
   CK(cudaMalloc(&f->u, bytes));
   CK(cudaMalloc(&f->A, bytes));
   CK(cudaMalloc(&f->B, bytes));
@@ -1173,6 +1225,66 @@ int build_plane_tiles(sgwg_family* f) {
   return SGWG_OK;
 }
 
+// Whole-plane 4D tiles (plane4d.cuh).  The family qualifies when dims (0, 1)
+// are periodic with power-of-two extents >= 8 and an x-plane of <= 2048
+// points, and dims (2, 3) are zero-ghost lines of 8m + 1 >= 9 points with a
+// velocity plane of < 4096 points (every BASELINE C5 member; SGWG_PLANE4=0
+// keeps the windowed plane kernels).  x pass: the whole x-plane times C
+// consecutive velocity points, X C ~ 4096; v pass: G whole velocity planes,
+// G V ~ SGWG_P4_VTARGET (3072) points.  One charge-density partial per x point.
+int build_plane4_tiles(sgwg_family* f) {
+  for (int pass = 0; pass < 2; ++pass) {
+    cudaFree(f->dp4tiles[pass]);
+    f->dp4tiles[pass] = nullptr;
+    f->np4tiles[pass] = 0;
+    f->p4smem[pass] = 0;
+  }
+  const sgwg_model& m = f->model;
+  if (f->d != 4 || f->no_fused2d || f->nm == 0 || arith_of(f) != SGWG_ARITH_FAST) return SGWG_OK;
+  if (m.kind != SGWG_ADVECTION && !(m.kind == SGWG_VLASOV_POISSON && m.space_dim == 2))
+    return SGWG_OK;
+  if (const char* e = std::getenv("SGWG_PLANE4"))
+    if (e[0] == '0') return SGWG_OK;
+  if (f->dom.bc[0] != SGWG_PERIODIC || f->dom.bc[1] != SGWG_PERIODIC ||
+      f->dom.bc[2] != SGWG_ZERO || f->dom.bc[3] != SGWG_ZERO)
+    return SGWG_OK;
+  auto pow2 = [](int n) { return n >= 8 && (n & (n - 1)) == 0; };
+  for (const auto& M : f->hmem) {
+    const int X = M.ext[0] * M.ext[1], V = M.ext[2] * M.ext[3];
+    if (!pow2(M.ext[0]) || !pow2(M.ext[1]) || X > 2048) return SGWG_OK;
+    if (M.ext[2] < 9 || M.ext[3] < 9 || (M.ext[2] & 7) != 1 || (M.ext[3] & 7) != 1 || V >= 4096)
+      return SGWG_OK;
+  }
+  int vtarget = 3072;
+  if (const char* e = std::getenv("SGWG_P4_VTARGET")) vtarget = std::max(64, std::atoi(e));
+  int xtarget = 4096;
+  if (const char* e = std::getenv("SGWG_P4_XTARGET")) xtarget = std::max(128, std::atoi(e));
+  std::vector<int4> t[2];
+  for (int mi = 0; mi < f->nm; ++mi) {
+    const MemberDesc& M = f->hmem[mi];
+    const int X = M.ext[0] * M.ext[1], V = M.ext[2] * M.ext[3];
+    int cs = 1;
+    while (cs < 6 && (X << (cs + 1)) <= xtarget) ++cs;
+    const int C = 1 << cs;
+    for (int v0 = 0; v0 < V; v0 += C) t[0].push_back(make_int4(mi, v0, std::min(C, V - v0), cs));
+    f->p4smem[0] = std::max(f->p4smem[0], 2 * (X << cs));
+    const int G = std::max(1, std::min(kP4MaxG, vtarget / V));
+    for (int x0 = 0; x0 < X; x0 += G) {
+      const int g = std::min(G, X - x0);
+      t[1].push_back(make_int4(mi, x0, g, 0));
+      f->p4smem[1] = std::max(f->p4smem[1], 3 * ((g * V + 3) & ~1));
+    }
+  }
+  for (int mi = 0; mi < f->nm; ++mi) f->hmem[mi].rparts = 1;
+  CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
+  for (int pass = 0; pass < 2; ++pass) {
+    f->np4tiles[pass] = (int)t[pass].size();
+    TRY(upload_vec(&f->dp4tiles[pass], t[pass]));
+  }
+  f->parts_of = nullptr;
+  return SGWG_OK;
+}
+
 void clear_graphs(sgwg_family* f) {
   for (auto& kv : f->graphs) cudaGraphExecDestroy(kv.second);
   f->graphs.clear();
@@ -1208,7 +1320,7 @@ int launches_per_step(const sgwg_family* f) {
   const bool fused3d = f->d == 3 && f->ntiles3d_fast > 0 && arith_of(f) == SGWG_ARITH_FAST &&
                        f->model.kind == SGWG_ADVECTION;
   const int np = ((f->d == 2 && f->ntiles2d > 0) || fused3d) ? 1
-                 : plane_path(f)                             ? 2
+                 : (plane_path(f) || plane4_path(f))         ? 2
                                                              : (int)pass_order(f).size();
   int n = 3 * np;
   if (!dt_fusable(f)) n += 1;
@@ -1216,7 +1328,7 @@ int launches_per_step(const sgwg_family* f) {
   if (f->model.kind == SGWG_VLASOV_POISSON) {  // (moment +) field per stage, energy per step
     const long long fine_x = (long long)f->fine_ext[0] *
                              ((f->model.space_dim == 2) ? f->fine_ext[1] : 1);
-    n += (plane_path(f) ? 3 : 6) + ((fine_x * f->nm > (1LL << 20)) ? 2 : 1);
+    n += ((plane_path(f) || plane4_path(f)) ? 3 : 6) + ((fine_x * f->nm > (1LL << 20)) ? 2 : 1);
   }
   if (f->comm != nullptr) n += 1;
   return n;
@@ -1618,6 +1730,8 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dtiles3d_fast);
   cudaFree(f->dptiles[0]);
   cudaFree(f->dptiles[1]);
+  cudaFree(f->dp4tiles[0]);
+  cudaFree(f->dp4tiles[1]);
   cudaFree(f->rho_parts);
   cudaFree(f->twid);
   cudaFree(f->Fu);
@@ -1767,6 +1881,7 @@ int sgwg_set_model(sgwg_family* f, const sgwg_model* m) {
   if (m->kind == SGWG_VLASOV_POISSON) TRY(setup_vp(f));
   if (m->kind == SGWG_VLASOV_MAXWELL) TRY(setup_vm(f));
   TRY(build_plane_tiles(f));
+  TRY(build_plane4_tiles(f));
   if (m->kind == SGWG_VLASOV_POISSON) TRY(build_moment_tasks(f));
   clear_graphs(f);
   return SGWG_OK;
@@ -1993,7 +2108,8 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
           int chunk = 1;
           while (chunk * 2 <= left && chunk < 64) chunk *= 2;
           // captured steps take the rho partials of u^n as given
-          if (f->model.kind == SGWG_VLASOV_POISSON && plane_path(f) && f->parts_of != f->u)
+          if (f->model.kind == SGWG_VLASOV_POISSON && (plane_path(f) || plane4_path(f)) &&
+              f->parts_of != f->u)
             TRY(launch_field_for(f, f->u, 0));
           cudaGraphExec_t ge;
           TRY(get_graph(f, chunk, &ge));

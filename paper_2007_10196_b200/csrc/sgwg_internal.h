@@ -52,6 +52,7 @@ struct MemberDesc {
 // t < MemberDesc::rparts (one partial per velocity-plane tile, fixed order)
 constexpr int kRhoParts = 8;
 constexpr int kPlaneMaxV = 32;  // planes per fast 4D plane tile
+constexpr int kP4MaxG = 64;     // x points per whole-plane 4D v-pass tile (plane4d.cuh)
 
 // Step control block (timestep.hpp:126-174 loop state), device resident.
 struct StepCtl {
@@ -164,6 +165,29 @@ struct PlaneParams {
   const StepCtl* ctl;
   unsigned long long* fail;
   double* rho_parts;       // pr = 1, Vlasov-Poisson: sum_v w_v out per (x point, part)
+  const struct DtParams* dtp;
+  unsigned int* counter;
+};
+
+// fast 4D stage on whole planes (plane4d.cuh): x pass tiles (mi, v0, nc, log2 C),
+// v pass tiles (mi, x0, G, -)
+struct Plane4Params {
+  const MemberDesc* mem;
+  const int4* tiles;
+  int flux_a, flux_b;      // FluxKind of the lower / upper dimension of the pass
+  double c_a, c_b;         // advection speeds
+  int stage;               // 1..3, 0 = tendency only
+  int linear;
+  double eps;
+  int space_dim;
+  const double* uin;
+  const double* un;
+  double* out;
+  double* kbuf;
+  const double* efield;
+  const StepCtl* ctl;
+  unsigned long long* fail;
+  double* rho_parts;       // v pass, Vlasov-Poisson: sum_v w_v out per x point (part 0)
   const struct DtParams* dtp;
   unsigned int* counter;
 };
@@ -291,6 +315,8 @@ namespace fast {
 cudaError_t launch_stage3d(const Stage2DParams& p, int nblocks, size_t smem, cudaStream_t s);
 cudaError_t launch_plane(const PlaneParams& p, int nblocks, size_t smem, cudaStream_t s);
 int plane_smem_doubles(int nv, int tx, int ty);
+cudaError_t launch_plane4(const Plane4Params& p, int pass, int nblocks, size_t smem, cudaStream_t s);
+cudaError_t configure_plane4();
 cudaError_t launch_persist2d(const PersistParams& p, int nblocks, size_t smem, cudaStream_t s);
 int persist2d_max_blocks(int burgers, int half, size_t smem);
 }  // namespace fast

@@ -42,11 +42,14 @@ def test_vp_c5_small_evolve(ctx, oracle):
     assert maxabs(gc[-1], wc[-1]) < 1e-10
 
 
-@pytest.mark.parametrize("cap", [None, "256"])
-def test_vp_c5_small_evolve_fast(ctx_fast, oracle, monkeypatch, cap):
+@pytest.mark.parametrize("cap,plane4", [(None, "1"), (None, "0"), ("256", "0")])
+def test_vp_c5_small_evolve_fast(ctx_fast, oracle, monkeypatch, cap, plane4):
     """Fast build, 2D2V: the two plane launches per stage (dims (x1,x2) ->
-    tendency, dims (v1,v2) + RK stage + charge-density partials); cap 256
-    splits velocity planes into several windows (several partials per x)."""
+    tendency, dims (v1,v2) + RK stage + charge density).  plane4 = 1: the
+    whole-plane kernels (plane4d.cuh, the default for C5-shaped families);
+    plane4 = 0: the windowed plane kernels, cap 256 splitting velocity planes
+    into several windows (several partials per x)."""
+    monkeypatch.setenv("SGWG_PLANE4", plane4)
     if cap is not None:
         monkeypatch.setenv("SGWG_PLANE_CAP", cap)
     cfg = configs.config("C5", **C5_SMALL)
@@ -57,10 +60,12 @@ def test_vp_c5_small_evolve_fast(ctx_fast, oracle, monkeypatch, cap):
     assert maxabs(gc[-1], wc[-1]) < 1e-10
 
 
-def test_vp_c5_partials_track_state(ctx_fast, oracle, monkeypatch):
+@pytest.mark.parametrize("plane4", ["1", "0"])
+def test_vp_c5_partials_track_state(ctx_fast, oracle, monkeypatch, plane4):
     """The charge density the field solve uses after an evolve comes from the
     plane kernel's partial sums; after an upload it must be recomputed."""
     monkeypatch.setenv("SGWG_PLANE_CAP", "512")
+    monkeypatch.setenv("SGWG_PLANE4", plane4)
     cfg = configs.config("C5", **C5_SMALL)
     dom, model, pol = oracle_objs(cfg)
     fam = gpu_family(ctx_fast, cfg)
@@ -93,8 +98,11 @@ def test_vp_c5_partials_track_state(ctx_fast, oracle, monkeypatch):
     assert maxabs(fam.download(), fam2.download()) == 0.0
 
 
-def test_advection_4d_evolve_fast(ctx_fast, oracle):
-    """4D constant-speed advection through the plane launches (fused dt)."""
+@pytest.mark.parametrize("plane4", ["1", "0"])
+def test_advection_4d_evolve_fast(ctx_fast, oracle, monkeypatch, plane4):
+    """4D constant-speed advection through the plane launches (fused dt),
+    both directions of every sweep (whole-plane and windowed kernels)."""
+    monkeypatch.setenv("SGWG_PLANE4", plane4)
     cfg = configs.config("C3", d=4, nl=3, lower=[0.0] * 4, upper=[2.0] * 4, root=[8] * 4,
                          bc=[0, 0, 1, 1], speeds=[1.0, -1.0, 0.5, -0.25])
     T = 4 * cfg["reference_spacing"] ** (5.0 / 3.0)
