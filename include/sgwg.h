@@ -119,6 +119,17 @@ typedef struct {
   double pass_bytes;          /* algorithmic HBM bytes of those launches */
 } sgwg_stats;
 
+/* profile mode (sgwg_set_profile): per-kernel event time of every launch of
+ * the last evolves and the kernel's algorithmic work per launch (SURVEY 8(d)
+ * counting), for the roofline of the stage kernels */
+typedef struct {
+  char name[48];
+  double ms_sum;
+  long long launches;
+  double flops_per_launch;
+  double bytes_per_launch;
+} sgwg_kernel_timing;
+
 typedef struct sgwg_ctx sgwg_ctx;
 typedef struct sgwg_family sgwg_family;
 
@@ -260,6 +271,11 @@ int sgwg_vp_field(sgwg_family* fam, double* rho, size_t nrho, double* E, size_t 
  * interp.hpp:36-53), ||.||_2 with the finest x-spacings.  SGWG_EUNSUPPORTED on
  * a sharded family (the record would cover the local members only). */
 int sgwg_field_energy(sgwg_family* fam, double* out, size_t cap, size_t* n);
+/* profile-mode kernel table (entries sorted by name; *n = entries available) */
+int sgwg_kernel_profile(const sgwg_family* fam, sgwg_kernel_timing* out, int cap, int* n);
+int sgwg_kernel_profile_reset(sgwg_family* fam);
+/* the stage kernel(s) the family's evolve launches (fixed at sgwg_set_model) */
+const char* sgwg_stage_kernels(const sgwg_family* fam);
 
 /* ---- host-side initial data: initialize_family (models.hpp:855-871) ------- */
 /* Initial-condition presets of BASELINE C1-C5 and the paper examples,

@@ -215,6 +215,8 @@ class Oracle(_Lib):
         L.sgwo_field_energy.restype = C.c_double
         L.sgwo_set_energy_record.argtypes = [_DP, C.c_long]
         L.sgwo_set_energy_record.restype = None
+        L.sgwo_set_max_steps.argtypes = [C.c_long]
+        L.sgwo_set_max_steps.restype = None
         self._energy_buf = None
 
     def combine_box(self, dom, states, lo, hi, mode=WENO, eps=1e-6):
@@ -241,6 +243,11 @@ class Oracle(_Lib):
         self._energy_buf = np.zeros(int(cap))
         self.lib.sgwo_set_energy_record(_dp(self._energy_buf), int(cap))
         return self._energy_buf
+
+    def set_max_steps(self, n):
+        """stop evolve after n steps (0: no limit)"""
+        self.lib.sgwo_set_max_steps(int(n))
+        return self
 
     def set_threads(self, n):
         """member-level OpenMP threads (bitwise-identical results for any n)"""

@@ -776,6 +776,10 @@ double sgwo_field_energy(const sgwo_domain* dom, int space_dim, const double* st
   return sqrt(e * hv);
 }
 
+/* optional step limit of sgwo_evolve (0 = none): bounded CPU samples of a run */
+static long g_max_steps = 0;
+void sgwo_set_max_steps(long n) { g_max_steps = (n < 0) ? 0 : n; }
+
 /* optional per-step energy record of sgwo_evolve (Vlasov-Poisson models) */
 static double* g_energy = NULL;
 static long g_energy_cap = 0;
@@ -837,6 +841,7 @@ int sgwo_evolve(const sgwo_domain* dom, const sgwo_model* model, const sgwo_poli
     const double stop = stops[si];
     if (stop > tfinal + eps_t) break;
     while (stop - t > eps_t) {
+      if (g_max_steps > 0 && step_index >= g_max_steps) break;
       double speeds[4];
       if (g_energy != NULL && model->kind == SGWO_VLASOV_POISSON && step_index < g_energy_cap)
         g_energy[step_index] = sgwo_field_energy(dom, model->space_dim, states);
@@ -880,6 +885,7 @@ int sgwo_evolve(const sgwo_domain* dom, const sgwo_model* model, const sgwo_poli
       ++step_index;
     }
     if (status != SGWO_OK) break;
+    if (g_max_steps > 0 && step_index >= g_max_steps && stop - t > eps_t) break;
     t = stop;
     if (cb) cb(t, user);
   }

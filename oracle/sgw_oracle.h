@@ -139,6 +139,8 @@ int sgwo_combine_box(const sgwo_domain* dom, const double* states, int interp_mo
  * packed family states, and an optional per-step record filled by sgwo_evolve. */
 double sgwo_field_energy(const sgwo_domain* dom, int space_dim, const double* states);
 void sgwo_set_energy_record(double* buf, long cap);
+/* stop sgwo_evolve after n steps (0 = no limit; bounded CPU baselines) */
+void sgwo_set_max_steps(long n);
 
 size_t sgwo_family_total_points(const sgwo_domain* dom);
 size_t sgwo_finest_points(const sgwo_domain* dom);

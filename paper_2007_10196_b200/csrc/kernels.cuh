@@ -2177,6 +2177,194 @@ __global__ void __launch_bounds__(256) final_kernel(const FinalParams p) {
   }
 }
 
+#if SGWG_FAST
+// ---------------------------------------------------------------------------
+// Fast final pass of the combination (last dimension of prolong fused with
+// acc += c p over members, combine.hpp:113-120 / interp.hpp:151-189).
+// A thread owns 8 consecutive fine points of one finest row; a warp takes the
+// same 8-point chunk of 32 rows, so the refinement phase of the chunk (which
+// fine points are copies, which stencil centre and offset t each uses) is a
+// compile-time property of the instantiation <M, PH> (2^M refinement, chunk
+// phase PH = (8 c mod 2^M) / 8).  Per stencil centre the smoothness
+// indicators are computed once and the three nonlinear weights are put over a
+// common denominator; the linear weights C_k(t) and substencil coefficients
+// are literals.  ~24 fp64 operations per interpolated fine point.
+// ---------------------------------------------------------------------------
+template <int M, int PH, int MODE>
+__device__ __forceinline__ void final_chunk(const double* __restrict__ line, int n_src, int bc,
+                                            int ib, double coef, double eps, double* acc) {
+  constexpr int F = 1 << M;
+  constexpr int W0 = 8 * PH;  // offset of the chunk's first fine point within its block
+  // window offsets (relative to ib) of every source value the chunk reads
+  constexpr int OMIN = -2;
+  constexpr int OMAX = ((W0 + 7) >> M) + 1 + 2;
+  constexpr int NW = OMAX - OMIN + 1;
+  double s[NW];
+#pragma unroll
+  for (int o = 0; o < NW; ++o) {
+    int q = ib + OMIN + o;
+    if (q < 0 || q >= n_src) {
+      if (bc == 0) {
+        q = (q < 0) ? q + n_src : q - n_src;
+        s[o] = __ldg(line + q);
+      } else {
+        s[o] = 0.0;
+      }
+    } else {
+      s[o] = __ldg(line + q);
+    }
+  }
+  // per stencil centre (window index c - OMIN): Q_k = prod_{l != k} (eps + b_l)^2
+  constexpr int NC = ((W0 + 7) >> M) + 2;
+  double Q0[NC], Q1[NC], Q2[NC];
+  if (MODE == 1) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int z = c - OMIN;
+      const double s0 = s[z - 2], s1 = s[z - 1], s2 = s[z], s3 = s[z + 1], s4 = s[z + 2];
+      const double d0 = s0 - 2.0 * s1 + s2, g0 = s0 - 4.0 * s1 + 3.0 * s2;
+      const double d1 = s1 - 2.0 * s2 + s3, g1 = s1 - s3;
+      const double d2 = s2 - 2.0 * s3 + s4, g2 = 3.0 * s2 - 4.0 * s3 + s4;
+      const double e0 = fma(13.0 / 12.0 * d0, d0, fma(0.25 * g0, g0, eps));
+      const double e1 = fma(13.0 / 12.0 * d1, d1, fma(0.25 * g1, g1, eps));
+      const double e2 = fma(13.0 / 12.0 * d2, d2, fma(0.25 * g2, g2, eps));
+      const double q0 = e0 * e0, q1 = e1 * e1, q2 = e2 * e2;
+      Q0[c] = q1 * q2;
+      Q1[c] = q0 * q2;
+      Q2[c] = q0 * q1;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int w = W0 + u;
+    const int r = w & (F - 1);
+    const int jj = w >> M;
+    if (r == 0) {  // copy: src[(j >> m) % n_src]
+      acc[u] = fma(coef, s[jj - OMIN], acc[u]);
+      continue;
+    }
+    const int di = (MODE == 1 && r >= F / 2) ? 1 : 0;
+    const double t = (double)r / F - di;
+    const int co = jj + di;
+    const int z = co - OMIN;
+    const double s0 = s[z - 2], s1 = s[z - 1], s2 = s[z], s3 = s[z + 1], s4 = s[z + 2];
+    const double p0 =
+        s0 * (0.5 * (t + 1.0) * t) - s1 * ((t + 2.0) * t) + s2 * (0.5 * (t + 2.0) * (t + 1.0));
+    const double p1 =
+        s1 * (0.5 * t * (t - 1.0)) - s2 * ((t + 1.0) * (t - 1.0)) + s3 * (0.5 * (t + 1.0) * t);
+    const double p2 =
+        s2 * (0.5 * (t - 1.0) * (t - 2.0)) - s3 * (t * (t - 2.0)) + s4 * (0.5 * t * (t - 1.0));
+    const double c0 = (t - 1.0) * (t - 2.0) / 12.0, c1 = (4.0 - t * t) / 6.0,
+                 c2 = (t + 2.0) * (t + 1.0) / 12.0;
+    double v;
+    if (MODE == 1) {
+      const double a0 = c0 * Q0[co], a1 = c1 * Q1[co], a2 = c2 * Q2[co];
+      v = fma(a0, p0, fma(a1, p1, a2 * p2)) * fast_rcp(a0 + a1 + a2);
+    } else {
+      v = fma(c0, p0, fma(c1, p1, c2 * p2));
+    }
+    acc[u] = fma(coef, v, acc[u]);
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void final_chunk_dispatch(int m, int c, const double* line, int n_src,
+                                                     int bc, double coef, double eps,
+                                                     double* acc) {
+  const int j0 = 8 * c;
+  switch (m) {
+    case 1: final_chunk<1, 0, MODE>(line, n_src, bc, j0 >> 1, coef, eps, acc); break;
+    case 2: final_chunk<2, 0, MODE>(line, n_src, bc, j0 >> 2, coef, eps, acc); break;
+    case 3: final_chunk<3, 0, MODE>(line, n_src, bc, j0 >> 3, coef, eps, acc); break;
+    case 4:
+      if (c & 1)
+        final_chunk<4, 1, MODE>(line, n_src, bc, j0 >> 4, coef, eps, acc);
+      else
+        final_chunk<4, 0, MODE>(line, n_src, bc, j0 >> 4, coef, eps, acc);
+      break;
+    case 5:
+      switch (c & 3) {
+        case 0: final_chunk<5, 0, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
+        case 1: final_chunk<5, 1, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
+        case 2: final_chunk<5, 2, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
+        default: final_chunk<5, 3, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
+      }
+      break;
+    default:
+      break;
+  }
+}
+
+// the chunk in the reference form (interp_point), when the common-denominator
+// weights overflowed (|u| >~ 1e38)
+template <int MODE>
+__device__ __noinline__ void final_chunk_ref(const double* const* srcs, const double* coef,
+                                             const int* mref, const int* mext, int nm,
+                                             int fine_last, int bc, double eps, double* out,
+                                             long long row, int c) {
+  for (int u = 0; u < 8; ++u) {
+    const int j = 8 * c + u;
+    if (j >= fine_last) break;
+    double a = 0.0;
+    for (int mi = 0; mi < nm; ++mi) {
+      const int m = mref[mi];
+      const double* src = srcs[mi];
+      const double v = (m == 0) ? src[row * fine_last + j]
+                                : interp_point(src, row * mext[mi], 1, mext[mi], j, m, bc, MODE,
+                                               eps);
+      a = fma(coef[mi], v, a);
+    }
+    out[row * fine_last + j] = a;
+  }
+}
+
+// grid-stride over (32-row block, chunk) warp items
+template <int MODE>
+__global__ void __launch_bounds__(256) final_fast_kernel(const FinalParams p) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int nch = (p.fine_last + 7) >> 3;  // chunks per row (the last may be partial)
+  const long long rows = p.nfine / p.fine_last;
+  const long long rblocks = (rows + 31) >> 5;
+  const long long items = rblocks * nch;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items;
+       it += wstride) {
+    const int c = (int)(it % nch);  // warp-uniform chunk
+    const long long row = (it / nch) * 32 + lane;
+    if (row >= rows) continue;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int mi = 0; mi < p.nm; ++mi) {
+      const int m = p.mrefine[mi];
+      const double cf = p.coef[mi];
+      if (m == 0) {  // member at the finest level along the last dimension: copy
+        const double* src = p.src[mi] + row * p.fine_last + 8 * c;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (8 * c + u < p.fine_last) acc[u] = fma(cf, __ldg(src + u), acc[u]);
+        continue;
+      }
+      const int n_src = p.msrc_ext[mi];
+      final_chunk_dispatch<MODE>(m, c, p.src[mi] + row * n_src, n_src, p.bc_last, cf, p.eps, acc);
+    }
+    int ex = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ex = max(ex, __double2hiint(acc[u]) & 0x7ff00000);
+    if (ex == 0x7ff00000) {  // overflowed common-denominator weights
+      final_chunk_ref<MODE>(p.src, p.coef, p.mrefine, p.msrc_ext, p.nm, p.fine_last, p.bc_last,
+                            p.eps, p.out, row, c);
+      continue;
+    }
+    double* out = p.out + row * p.fine_last + 8 * c;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (8 * c + u < p.fine_last) out[u] = acc[u];
+  }
+}
+#endif
+
 // ---------------------------------------------------------------------------
 // Vlasov-Maxwell field lines (vm_rhs_into, models.hpp:437-505 + SspRk3::step)
 // ---------------------------------------------------------------------------
@@ -2389,6 +2577,22 @@ cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s
 
 cudaError_t launch_final(const FinalParams& p, cudaStream_t s) {
   if (p.nfine <= 0) return cudaSuccess;
+#if SGWG_FAST
+  // chunked kernel: rows of 8m (+1) fine points, refinement <= 2^5 in the last
+  // dimension; else (or SGWG_FINAL_GENERIC=1) the generic one
+  bool chunked = !p.assign && p.nm_host == p.nm &&
+                 ((p.fine_last - (p.bc_last != 0 ? 1 : 0)) % 8 == 0) &&
+                 std::getenv("SGWG_FINAL_GENERIC") == nullptr;
+  for (int mi = 0; chunked && mi < p.nm_host; ++mi) chunked = p.mref_host[mi] <= 5;
+  if (chunked) {
+    const long long rows = p.nfine / p.fine_last;
+    const long long items = ((rows + 31) / 32) * ((p.fine_last + 7) / 8);
+    long long blocks = (items + 7) / 8;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    return p.mode == 1 ? launch_k(final_fast_kernel<1>, dim3((int)blocks), dim3(256), 0, s, p)
+                       : launch_k(final_fast_kernel<0>, dim3((int)blocks), dim3(256), 0, s, p);
+  }
+#endif
   long long blocks = (p.nfine + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   return launch_k(final_kernel, dim3((int)blocks), dim3(256), 0, s, p);

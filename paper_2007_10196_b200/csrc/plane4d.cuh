@@ -67,8 +67,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 // _negative, weno.hpp:60-80): taken only when the fast form overflowed
 // (|u| >~ 1e36 makes the common-denominator weights infinite, the reference's
 // separate divides do not).
-template <int RUN, int GL, int GR, bool ZERO, bool ACC>
-__device__ __noinline__ void adv_run_ref(const double* __restrict__ P, int st, int wrap, double c,
+template <int RUN, int GL, int GR, bool ZERO>
+__device__ __forceinline__ void adv_run_ref(const double* __restrict__ P, int st, int wrap, double c,
                                          double eps, int linear, double inv_h,
                                          double* __restrict__ out, int ost) {
   constexpr int NV = RUN + 6;
@@ -89,13 +89,7 @@ __device__ __noinline__ void adv_run_ref(const double* __restrict__ P, int st, i
     const int i = t + 2, m = t + 3;
     const double F = rev ? recon_ref(f[m + 2], f[m + 1], f[m], f[m - 1], f[m - 2], eps, linear)
                          : recon_ref(f[i - 2], f[i - 1], f[i], f[i + 1], f[i + 2], eps, linear);
-    if (t > 0) {
-      const double du = (F - Fp) * inv_h;
-      if (ACC)
-        out[(t - 1) * ost] += du;
-      else
-        out[(t - 1) * ost] = du;
-    }
+    if (t > 0) out[(t - 1) * ost] = (F - Fp) * inv_h;
     Fp = F;
   }
 }
@@ -104,12 +98,12 @@ __device__ __noinline__ void adv_run_ref(const double* __restrict__ P, int st, i
 // RUN consecutive points of one line.  P: the window's first value (physical
 // point 8r - 3 of the line), st: smem stride along the line.  GL / GR values at
 // the window ends are ghosts: zeros (ZERO) or the periodic image at -/+ wrap.
-// Writes out[k*ost] = du (ACC: out[k*ost] += du).  Downwind lines (c < 0) use
+// Writes out[k*ost] = du.  Downwind lines (c < 0) use
 // the mirrored reconstruction on the same physically ordered window.
-template <int RUN, int GL, int GR, bool ZERO, bool LINEAR, bool ACC>
-__device__ __noinline__ void adv_run(const double* __restrict__ P, int st, int wrap, double c,
-                                     double eps, double inv_h, double* __restrict__ out,
-                                     int ost) {
+template <int RUN, int GL, int GR, bool ZERO, bool LINEAR>
+__device__ __noinline__ bool adv_run_fast(const double* __restrict__ P, int st, int wrap, double c,
+                                          double eps, double inv_h, double* __restrict__ out,
+                                          int ost) {
   constexpr int NV = RUN + 6;
   double f[NV];
 #pragma unroll
@@ -130,15 +124,19 @@ __device__ __noinline__ void adv_run(const double* __restrict__ P, int st, int w
   }
 #pragma unroll
   for (int q = 1; q < NV; ++q) dd[q] = f[q] - f[q - 1];
-  double du[RUN];
   double Fp = 0.0;
+  int ex = 0;  // max exponent field of the outputs (overflow guard)
   if (!(c < 0.0)) {
 #pragma unroll
     for (int t = 0; t <= RUN; ++t) {
       const int i = t + 2;
       const double F = recon_roles<LINEAR>(f[i], D[i - 1], D[i], D[i + 1], K[i - 1], K[i],
                                            K[i + 1], dd[i], dd[i + 1]);
-      if (t > 0) du[t - 1] = (F - Fp) * inv_h;
+      if (t > 0) {
+        const double du = (F - Fp) * inv_h;
+        ex = max(ex, __double2hiint(du) & 0x7ff00000);
+        out[(t - 1) * ost] = du;
+      }
       Fp = F;
     }
   } else {
@@ -147,98 +145,87 @@ __device__ __noinline__ void adv_run(const double* __restrict__ P, int st, int w
       const int m = t + 3;
       const double F = recon_roles<LINEAR>(f[m], D[m + 1], D[m], D[m - 1], K[m + 1], K[m],
                                            K[m - 1], -dd[m + 1], -dd[m]);
-      if (t > 0) du[t - 1] = (F - Fp) * inv_h;
+      if (t > 0) {
+        const double du = (F - Fp) * inv_h;
+        ex = max(ex, __double2hiint(du) & 0x7ff00000);
+        out[(t - 1) * ost] = du;
+      }
       Fp = F;
     }
   }
-  // overflow guard on the integer pipe: a non-finite du (all exponent bits
-  // set) sends the run through the reference form
-  int ex = 0;
-#pragma unroll
-  for (int k = 0; k < RUN; ++k) ex = max(ex, __double2hiint(du[k]) & 0x7ff00000);
-  if (ex == 0x7ff00000) {
-    adv_run_ref<RUN, GL, GR, ZERO, ACC>(P, st, wrap, c, eps, LINEAR, inv_h, out, ost);
-    return;
-  }
-#pragma unroll
-  for (int k = 0; k < RUN; ++k) {
-    if (ACC)
-      out[k * ost] += du[k];
-    else
-      out[k * ost] = du[k];
-  }
+  // overflow guard: a non-finite du (all exponent bits set, tracked on the
+  // integer pipe) re-runs the window in the reference form, overwriting the
+  // outputs (inlined: the run stays a leaf function)
+  if (ex == 0x7ff00000) adv_run_ref<RUN, GL, GR, ZERO>(P, st, wrap, c, eps, LINEAR, inv_h, out, ost);
+  return false;
 }
 
-// A sweep over `nlines` lines of n points, as warp tasks of 32 lines sharing
-// one run-position class.  Periodic lines have n = 8m; zero-ghost lines
-// n = 8m + 1 (8m points in runs + a one-point tail).
-struct SweepGeom {
-  int nlines, m;
-  int zero;      // zero ghosts (else periodic)
-  float inv_nl;  // 1 / nlines (qdiv)
+template <int RUN, int GL, int GR, bool ZERO, bool LINEAR>
+__device__ __forceinline__ void adv_run(const double* __restrict__ P, int st, int wrap, double c,
+                                        double eps, double inv_h, double* __restrict__ out,
+                                        int ost) {
+  adv_run_fast<RUN, GL, GR, ZERO, LINEAR>(P, st, wrap, c, eps, inv_h, out, ost);
+}
+
+// ---------------------------------------------------------------------------
+// Warp tasks.  A task is 32 consecutive lines of one sweep (one per lane) and
+// a range of <= kP4RunsPerTask consecutive runs along them: the line address
+// is decoded once per task, the runs follow by pointer steps, and the run
+// position -- first (left ghosts), middle, last (right ghosts), the tail point
+// of a zero-ghost line of 8m + 1 points -- is warp-uniform, so the ghost
+// pattern is a compile-time property of the adv_run instantiation each run
+// calls.  The task table is built once per CTA in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kP4MaxTasks = 512;
+constexpr int kP4RunsPerTask = 4;
+
+struct P4Tasks {
+  int nlines[2], m[2];
+  float inv_nl[2];
+  int ntask;
+  int task[kP4MaxTasks];  // sweep << 30 | line block << 12 | first run << 6 | end run
 };
 
-// class c of a sweep -> (first run, number of runs); classes:
-// 0 first run, 1 middle runs, 2 last run, 3 tail (zero) / unused; m == 1:
-// class 0 is the single run (both ends), class 2 unused.
-__device__ __forceinline__ void class_runs(const SweepGeom& g, int c, int& r0, int& nr) {
-  if (c == 0) {
-    r0 = 0;
-    nr = 1;
-  } else if (c == 1) {
-    r0 = 1;
-    nr = max(0, g.m - 2);
-  } else if (c == 2) {
-    r0 = g.m - 1;
-    nr = (g.m >= 2) ? 1 : 0;
-  } else {
-    r0 = g.m;
-    nr = g.zero ? 1 : 0;
+__device__ __forceinline__ void add_sweep(P4Tasks& T, int s, int nlines, int m, bool zero) {
+  T.nlines[s] = nlines;
+  T.m[s] = m;
+  const int nruns = m + (zero ? 1 : 0);
+  const int nb = (nlines + 31) >> 5;
+  for (int r0 = 0; r0 < nruns; r0 += kP4RunsPerTask) {
+    const int r1 = min(nruns, r0 + kP4RunsPerTask);
+    for (int b = 0; b < nb && T.ntask < kP4MaxTasks; ++b)
+      T.task[T.ntask++] = (s << 30) | (b << 12) | (r0 << 6) | r1;
   }
 }
 
-template <bool ZERO, bool LINEAR, bool ACC>
-__device__ __forceinline__ void run_dispatch(int cls, int m, const double* P, int st, int wrap,
-                                             double c, double eps, double inv_h, double* out) {
+// adv_run instantiation of run r of a line with m full runs: 0 middle, 1 first,
+// 2 last, 3 single (both ends), 4 zero-ghost tail point
+__device__ __forceinline__ int run_inst(int r, int m) {
+  if (r == m) return 4;
+  if (m == 1) return 3;
+  if (r == 0) return 1;
+  if (r == m - 1) return 2;
+  return 0;
+}
+
+template <bool ZERO, bool LINEAR>
+__device__ __forceinline__ void run_dispatch(int inst, const double* P, int st, int wrap, double c,
+                                             double eps, double inv_h, double* out) {
   if constexpr (ZERO) {
-    if (cls == 3)
-      adv_run<1, 0, 3, true, LINEAR, ACC>(P, st, 0, c, eps, inv_h, out, st);
-    else if (cls == 1)
-      adv_run<8, 0, 0, true, LINEAR, ACC>(P, st, 0, c, eps, inv_h, out, st);
-    else if (cls == 0 && m == 1)
-      adv_run<8, 3, 2, true, LINEAR, ACC>(P, st, 0, c, eps, inv_h, out, st);
-    else if (cls == 0)
-      adv_run<8, 3, 0, true, LINEAR, ACC>(P, st, 0, c, eps, inv_h, out, st);
-    else
-      adv_run<8, 0, 2, true, LINEAR, ACC>(P, st, 0, c, eps, inv_h, out, st);
+    switch (inst) {
+      case 0: adv_run<8, 0, 0, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
+      case 1: adv_run<8, 3, 0, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
+      case 2: adv_run<8, 0, 2, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
+      case 3: adv_run<8, 3, 2, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
+      default: adv_run<1, 0, 3, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
+    }
   } else {
-    if (cls == 1)
-      adv_run<8, 0, 0, true, LINEAR, ACC>(P, st, 0, c, eps, inv_h, out, st);
-    else if (cls == 0 && m == 1)
-      adv_run<8, 3, 3, false, LINEAR, ACC>(P, st, wrap, c, eps, inv_h, out, st);
-    else if (cls == 0)
-      adv_run<8, 3, 0, false, LINEAR, ACC>(P, st, wrap, c, eps, inv_h, out, st);
-    else
-      adv_run<8, 0, 3, false, LINEAR, ACC>(P, st, wrap, c, eps, inv_h, out, st);
-  }
-}
-
-// warp tasks of one or two sweeps: task t -> (sweep s, class c, chunk)
-struct TaskMap {
-  int cum[9];  // cumulative warp tasks over (sweep, class)
-  int r0[8], nr[8];
-};
-
-__device__ __forceinline__ void make_taskmap(TaskMap& tm, const SweepGeom* g, int nsweeps) {
-  tm.cum[0] = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int s = k >> 2;
-    int r0 = 0, nr = 0;
-    if (s < nsweeps) class_runs(g[s], k & 3, r0, nr);
-    tm.r0[k] = r0;
-    tm.nr[k] = nr;
-    tm.cum[k + 1] = tm.cum[k] + ((s < nsweeps) ? (nr * g[s].nlines + 31) >> 5 : 0);
+    switch (inst) {
+      case 0: adv_run<8, 0, 0, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
+      case 1: adv_run<8, 3, 0, false, LINEAR>(P, st, wrap, c, eps, inv_h, out, st); break;
+      case 2: adv_run<8, 0, 3, false, LINEAR>(P, st, wrap, c, eps, inv_h, out, st); break;
+      default: adv_run<8, 3, 3, false, LINEAR>(P, st, wrap, c, eps, inv_h, out, st); break;
+    }
   }
 }
 
@@ -258,67 +245,91 @@ __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_kernel(const Plane4Para
   const int NT = (n1 * n2) << cs;
   extern __shared__ __align__(16) double sm[];
   double* U = sm;
-  double* D = sm + NT;
+  double* D1 = sm + NT;  // d/dx1
+  double* D2 = D1 + NT;  // d/dx2
   __shared__ double ca[kP4MaxC], cb[kP4MaxC];
+  __shared__ P4Tasks T;
   const int tid = threadIdx.x;
-  const double* src = p.uin + M->offset + v0;
-  for (int e = tid; e < NT; e += kP4Threads) {
-    const int pp = e >> cs, c = e & (C - 1);
-    cp_async8(U + e, src + pp * V + min(c, nc - 1), c < nc);
+  {
+    const double* src = p.uin + M->offset + v0;
+    const int cm = nc - 1;
+    for (int e = tid; e < NT; e += kP4Threads) {
+      const int c = e & (C - 1);
+      cp_async8(U + e, src + (e >> cs) * V + min(c, cm), c < nc);
+    }
+    cp_async_commit();
   }
-  cp_async_commit();
   if (tid < C) {  // x_j lines at velocity point vl: coefficient v_j (models.hpp:341-344)
     const int vl = v0 + min(tid, nc - 1);
     const int i3 = vl / n4;
     ca[tid] = line_coef(p.flux_a, M, 0, p.space_dim, i3, p.c_a, p.efield);
     cb[tid] = line_coef(p.flux_b, M, 1, p.space_dim, vl - i3 * n4, p.c_b, p.efield);
   }
+  if (tid == 0) {
+    // sweep 0: x1 lines (x2, c) = l, stride n2 C, n1 points; sweep 1: x2 lines
+    // (x1, c), stride C, n2 points
+    T.ntask = 0;
+    add_sweep(T, 0, n2 << cs, n1 >> 3, false);
+    add_sweep(T, 1, n1 << cs, n2 >> 3, false);
+  }
   cp_async_wait<0>();
   __syncthreads();
   const int lane = tid & 31, warp = tid >> 5;
-  // phase A: x2 lines (x1, c), stride C, n2 points; phase B: x1 lines (x2, c) = l,
-  // stride n2 C, n1 points, accumulated
-  for (int ph = 0; ph < 2; ++ph) {
-    SweepGeom g;
-    g.nlines = (ph == 0 ? n1 : n2) << cs;
-    g.m = (ph == 0 ? n2 : n1) >> 3;
-    g.zero = 0;
-    g.inv_nl = 1.0f / (float)g.nlines;
-    __shared__ TaskMap tm;
-    if (tid == 0) make_taskmap(tm, &g, 1);
-    __syncthreads();
-    const int st = (ph == 0) ? C : (n2 << cs);
-    const int wrap = (ph == 0 ? n2 : n1) * st;
-    const double inv_h = M->inv_h[ph == 0 ? 1 : 0];
-    for (int t = warp; t < tm.cum[4]; t += kP4Threads / 32) {
-      int k = 0;
-      while (t >= tm.cum[k + 1]) ++k;
-      const int i = ((t - tm.cum[k]) << 5) + lane;
-      if (i >= tm.nr[k] * g.nlines) continue;
-      const int q = qdiv(i, g.inv_nl);
-      const int l = i - q * g.nlines, r = tm.r0[k] + q;
-      const int c = l & (C - 1);
-      const int base = (ph == 0) ? (l >> cs) * (n2 << cs) + c : l;
-      const double* P = U + base + (8 * r - 3) * st;
-      double* o = D + base + 8 * r * st;
-      if (ph == 0)
-        run_dispatch<false, LINEAR, false>(k, g.m, P, st, wrap, cb[c], p.eps, inv_h, o);
-      else
-        run_dispatch<false, LINEAR, true>(k, g.m, P, st, wrap, ca[c], p.eps, inv_h, o);
+  const int st0 = n2 << cs, wrap0 = n1 * st0, wrap1 = n2 << cs;
+  const double ih1 = M->inv_h[0], ih2 = M->inv_h[1], eps = p.eps;
+  for (int t = warp; t < T.ntask; t += kP4Threads / 32) {
+    const int e = T.task[t];
+    const int sw = e >> 30, r0 = (e >> 6) & 63, r1 = e & 63;
+    const int l = (((e >> 12) & 0x3ffff) << 5) + lane;
+    if (l >= T.nlines[sw]) continue;
+    const int m = T.m[sw];
+    const int c = l & (C - 1);
+    if (sw == 0) {
+      const double cf = ca[c];
+      for (int r = r0; r < r1; ++r)
+        run_dispatch<false, LINEAR>(run_inst(r, m), U + l + (8 * r - 3) * st0, st0, wrap0,
+                                           cf, eps, ih1, D1 + l + 8 * r * st0);
+    } else {
+      const int base = (l >> cs) * wrap1 + c;
+      const double cf = cb[c];
+      for (int r = r0; r < r1; ++r)
+        run_dispatch<false, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * C, C, wrap1,
+                                           cf, eps, ih2, D2 + base + 8 * r * C);
     }
-    __syncthreads();
   }
-  // K = (0 - dx1) - dx2 (in the order dx2 + dx1 of the sweeps; fast build)
+  __syncthreads();
+  // K = (0 - dx1) - dx2 (models.hpp:187-197 order)
   double* kb = p.kbuf + M->offset + v0;
   for (int e = tid; e < NT; e += kP4Threads) {
-    const int pp = e >> cs, c = e & (C - 1);
-    if (c < nc) kb[pp * V + c] = 0.0 - D[e];
+    const int c = e & (C - 1);
+    if (c < nc) kb[(e >> cs) * V + c] = (0.0 - D1[e]) - D2[e];
   }
 }
 
 // ---------------------------------------------------------------------------
 // v pass: dims (2, 3) of G whole velocity planes + RK stage + charge density
 // ---------------------------------------------------------------------------
+template <int STAGE, bool MOMENT>
+__device__ __forceinline__ void vpass_epilogue(int NT, const double* U, const double* Kt,
+                                               const double* UNt, double* DV1, const double* DV2,
+                                               double* out, double dt, int& ex) {
+  for (int e = threadIdx.x; e < NT; e += kP4Threads) {
+    const double kv = (Kt[e] - DV1[e]) - DV2[e];
+    ex = max(ex, __double2hiint(kv) & 0x7ff00000);
+    double o;
+    if (STAGE == 0)
+      o = kv;
+    else if (STAGE == 1)
+      o = fma(dt, kv, U[e]);
+    else if (STAGE == 2)
+      o = fma(0.75, UNt[e], 0.25 * fma(dt, kv, U[e]));
+    else
+      o = fma(1.0 / 3.0, UNt[e], (2.0 / 3.0) * fma(dt, kv, U[e]));
+    out[e] = o;
+    if (MOMENT) DV1[e] = o;
+  }
+}
+
 template <bool LINEAR>
 __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Params p) {
   pdl_wait();
@@ -331,125 +342,132 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
   const int V = n3 * n4;
   const int NT = G * V;
   extern __shared__ __align__(16) double sm[];
-  __shared__ unsigned long long bar;
+  __shared__ unsigned long long bar[2];
   __shared__ double ce1[kP4MaxG], ce2[kP4MaxG];
+  __shared__ P4Tasks T;
   const int tid = threadIdx.x;
+  const int stage = p.stage;
   const long long gs = M->offset + (long long)x0 * V;  // tile start (doubles)
   const long long ga = gs & ~1LL;                         // 16-byte aligned start
   const int shift = (int)(gs - ga);
   const unsigned nbytes = (unsigned)((((gs + NT + 1) & ~1LL) - ga) * 8);
   const int pitch = (NT + 3) & ~1;
+  // [u^(s) | K | u^n | dv1 | dv2], the first three staged by bulk copies with
+  // the tile's alignment shift
   double* U = sm + shift;
-  double* DV1 = sm + pitch;
-  double* DV2 = DV1 + pitch;
-  if (tid == 0) mbar_init(&bar, 1);
+  double* Kt = sm + pitch + shift;
+  double* UNt = sm + 2 * pitch + shift;
+  double* DV1 = sm + 3 * pitch;
+  double* DV2 = sm + 4 * pitch;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
   __syncthreads();
-  if (tid == 0) bulk_g2s(sm, p.uin + ga, nbytes, &bar);
+  if (tid == 0) {
+    bulk_g2s(sm, p.uin + ga, nbytes, &bar[0]);
+    if (stage > 1) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[1])),
+                   "r"(2 * nbytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(sm + pitch)),
+          "l"(p.kbuf + ga), "r"(nbytes), "r"(smem_u32(&bar[1]))
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(sm + 2 * pitch)),
+          "l"(p.un + ga), "r"(nbytes), "r"(smem_u32(&bar[1]))
+          : "memory");
+    } else {
+      bulk_g2s(sm + pitch, p.kbuf + ga, nbytes, &bar[1]);
+    }
+    // sweep 0: v2 lines (rows rho = g n3 + i3), unit stride, n4 points;
+    // sweep 1: v1 lines (columns kappa = g n4 + i4), stride n4, n3 points
+    T.ntask = 0;
+    add_sweep(T, 0, G * n3, n4 >> 3, true);
+    add_sweep(T, 1, G * n4, n3 >> 3, true);
+  }
   if (tid < G) {  // v_j lines at x point x0+tid: -E_j(x) (VP) or the advection speed
     ce1[tid] = line_coef(p.flux_a, M, 2, p.space_dim, x0 + tid, p.c_a, p.efield);
     ce2[tid] = line_coef(p.flux_b, M, 3, p.space_dim, x0 + tid, p.c_b, p.efield);
   }
   __syncthreads();
-  mbar_wait(&bar, 0);
+  mbar_wait(&bar[0], 0);
   const int lane = tid & 31, warp = tid >> 5;
   {
-    // sweep 0: v2 lines (rows rho = g n3 + i3), unit stride, n4 points;
-    // sweep 1: v1 lines (columns kappa = g n4 + i4), stride n4, n3 points
-    SweepGeom g[2];
-    g[0].nlines = G * n3;
-    g[0].m = n4 >> 3;
-    g[1].nlines = G * n4;
-    g[1].m = n3 >> 3;
-    g[0].zero = g[1].zero = 1;
-    g[0].inv_nl = 1.0f / (float)g[0].nlines;
-    g[1].inv_nl = 1.0f / (float)g[1].nlines;
-    __shared__ TaskMap tm;
-    if (tid == 0) make_taskmap(tm, g, 2);
-    __syncthreads();
     const float i3f = 1.0f / (float)n3, i4f = 1.0f / (float)n4;
-    const double ih3 = M->inv_h[2], ih4 = M->inv_h[3];
-    for (int t = warp; t < tm.cum[8]; t += kP4Threads / 32) {
-      int k = 0;
-      while (t >= tm.cum[k + 1]) ++k;
-      const int s = k >> 2, cls = k & 3;
-      const int i = ((t - tm.cum[k]) << 5) + lane;
-      if (i >= tm.nr[k] * g[s].nlines) continue;
-      const int q = qdiv(i, g[s].inv_nl);
-      const int l = i - q * g[s].nlines, r = tm.r0[k] + q;
-      if (s == 0) {
-        const int gx = qdiv(l, i3f);
-        const int base = l * n4 + 8 * r;
-        run_dispatch<true, LINEAR, false>(cls, g[0].m, U + base - 3, 1, 0, ce2[gx], p.eps, ih4,
-                                          DV2 + base);
+    const double ih3 = M->inv_h[2], ih4 = M->inv_h[3], eps = p.eps;
+    for (int t = warp; t < T.ntask; t += kP4Threads / 32) {
+      const int e = T.task[t];
+      const int sw = e >> 30, r0 = (e >> 6) & 63, r1 = e & 63;
+      const int l = (((e >> 12) & 0x3ffff) << 5) + lane;
+      if (l >= T.nlines[sw]) continue;
+      const int m = T.m[sw];
+      if (sw == 0) {
+        const int base = l * n4;
+        const double cf = ce2[qdiv(l, i3f)];
+        for (int r = r0; r < r1; ++r)
+          run_dispatch<true, LINEAR>(run_inst(r, m), U + base + 8 * r - 3, 1, 0, cf, eps,
+                                            ih4, DV2 + base + 8 * r);
       } else {
         const int gx = qdiv(l, i4f);
-        const int base = gx * V + (l - gx * n4) + 8 * r * n4;
-        run_dispatch<true, LINEAR, false>(cls, g[1].m, U + base - 3 * n4, n4, 0, ce1[gx], p.eps,
-                                          ih3, DV1 + base);
+        const int base = gx * V + (l - gx * n4);
+        const double cf = ce1[gx];
+        for (int r = r0; r < r1; ++r)
+          run_dispatch<true, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * n4, n4, 0, cf,
+                                            eps, ih3, DV1 + base + 8 * r * n4);
       }
     }
   }
+  mbar_wait(&bar[1], 0);
   __syncthreads();
-  // epilogue: k = (K - dv1) - dv2, RK stage (timestep.hpp:86-104), non-finite
-  // check, output; trapezoid-weighted stage output for the charge density
-  const double* kb = p.kbuf + gs;
-  const double* un = p.un + gs;
-  double* out = p.out + gs;
+  // epilogue: k = (K - dv1) - dv2, RK stage (timestep.hpp:86-104), output
   const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
-  const bool moment = (p.rho_parts != nullptr) && (p.stage > 0);
-  const float iVf = 1.0f / (float)V, i4f = 1.0f / (float)n4;
-  const double h3 = M->h[2], h4 = M->h[3];
-  bool bad = false;
-  for (int e0 = tid; e0 < NT; e0 += 4 * kP4Threads) {
-    double kin[4], unv[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int e = e0 + j * kP4Threads;
-      kin[j] = (e < NT) ? __ldg(kb + e) : 0.0;
-      unv[j] = (e < NT && p.stage > 1) ? __ldg(un + e) : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int e = e0 + j * kP4Threads;
-      if (e >= NT) break;
-      const double kv = (kin[j] - DV1[e]) - DV2[e];
-      double o;
-      if (p.stage == 0) {
-        o = kv;
-      } else {
-        bad |= !isfinite(kv);
-        const double ui = U[e];
-        if (p.stage == 1)
-          o = fma(dt, kv, ui);
-        else if (p.stage == 2)
-          o = fma(0.75, unv[j], 0.25 * fma(dt, kv, ui));
-        else
-          o = fma(1.0 / 3.0, unv[j], (2.0 / 3.0) * fma(dt, kv, ui));
-      }
-      out[e] = o;
-      if (moment) {  // trapezoid weights of the velocity block (models.hpp:64-71,240-257)
-        const int gx = qdiv(e, iVf), rr = e - gx * V;
-        const int a = qdiv(rr, i4f), b = rr - a * n4;
-        const double wa = (a == 0 || a == n3 - 1) ? 0.5 * h3 : h3;
-        const double wb = (b == 0 || b == n4 - 1) ? 0.5 * h4 : h4;
-        DV1[e] = (wa * wb) * o;
-      }
-    }
+  const bool moment = (p.rho_parts != nullptr) && (stage > 0);
+  double* out = p.out + gs;
+  int ex = 0;
+  if (moment) {
+    if (stage == 1)
+      vpass_epilogue<1, true>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
+    else if (stage == 2)
+      vpass_epilogue<2, true>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
+    else
+      vpass_epilogue<3, true>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
+  } else {
+    if (stage == 0)
+      vpass_epilogue<0, false>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
+    else if (stage == 1)
+      vpass_epilogue<1, false>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
+    else if (stage == 2)
+      vpass_epilogue<2, false>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
+    else
+      vpass_epilogue<3, false>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
   }
-  if (bad) {
+  if (stage > 0 && ex == 0x7ff00000) {  // non-finite tendency (tendency_finite, timestep.hpp:71-75)
     const unsigned long long code =
-        (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)p.stage;
+        (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)stage;
     atomicMin(p.fail + tk.x, code);
   }
-  if (moment) {  // one warp per x point, fixed order
+  if (moment) {
+    // charge density of the stage output per x point (moment_density,
+    // models.hpp:294-306) with the trapezoid weights (models.hpp:64-71,240-257)
+    // h3 h4 f(a) f(b), f = 1/2 at the zero-ghost ends: the plane sum minus half
+    // the edge rows / columns plus a quarter of the corners.  One warp per x point.
     __syncthreads();
+    const double hh = M->h[2] * M->h[3];
     for (int gx = warp; gx < G; gx += kP4Threads / 32) {
       const double* w = DV1 + gx * V;
-      double acc = 0.0;
-      for (int e = lane; e < V; e += 32) acc += w[e];
+      double all = 0.0, edge = 0.0;
+      for (int e = lane; e < V; e += 32) all += w[e];
+      for (int e = lane; e < n4; e += 32) edge += w[e] + w[(n3 - 1) * n4 + e];
+      for (int e = lane; e < n3; e += 32) edge += w[e * n4] + w[e * n4 + n4 - 1];
+      double corner = (lane == 0) ? (w[0] + w[n4 - 1]) + (w[(n3 - 1) * n4] + w[V - 1]) : 0.0;
+      double acc = fma(-0.5, edge, fma(0.25, corner, all));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) p.rho_parts[(M->xoff + x0 + gx) * kRhoParts] = acc;
+      if (lane == 0) p.rho_parts[(M->xoff + x0 + gx) * kRhoParts] = hh * acc;
     }
   }
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);

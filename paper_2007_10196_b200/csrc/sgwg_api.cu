@@ -148,6 +148,7 @@ struct ProlongPlan {
   double* fcoef = nullptr;
   int* fext = nullptr;
   int* fref = nullptr;
+  std::vector<int> href;  // host copy of fref (launch-time kernel choice)
   int nm = 0;
   long long row_a = 0, row_b = 0;  // dimension-0 fine rows covered
 };
@@ -242,6 +243,11 @@ struct sgwg_family {
   PlaneTile* dptiles[2] = {nullptr, nullptr};  // fast 4D plane tiles (pairs (0,1), (2,3))
   int nptiles[2] = {0, 0};
   int psmem = 0;
+  // fast build, state magnitude >= kOverflowGuard: the step kernels of this
+  // call run in the reference arithmetic (overflow_guard)
+  bool exact_override = false;
+  // profile mode: per-kernel event times and algorithmic counts (sgwg_kernel_profile)
+  std::map<std::string, sgwg_kernel_timing> kprof;
   int4* dp4tiles[2] = {nullptr, nullptr};  // whole-plane 4D tiles (plane4d.cuh): x pass, v pass
   int np4tiles[2] = {0, 0};
   int p4smem[2] = {0, 0};                  // dynamic shared memory (doubles) per pass
@@ -255,7 +261,9 @@ struct sgwg_family {
 
 namespace {
 
-int arith_of(const sgwg_family* f) { return f->ctx->arith; }
+int arith_of(const sgwg_family* f) {
+  return f->exact_override ? SGWG_ARITH_EXACT : f->ctx->arith;
+}
 
 cudaError_t do_launch_pass(const sgwg_family* f, const PassParams& p, int kdim) {
   // split-flux arrays (+ a du array in the fast kernel) + coefficients + line bases
@@ -285,6 +293,15 @@ std::vector<PassDesc> pass_order(const sgwg_family* f) {
     }
   }
   return v;
+}
+
+void account_kernel(sgwg_family* f, const char* name, double ms, double flops, double bytes) {
+  sgwg_kernel_timing& k = f->kprof[name];
+  std::snprintf(k.name, sizeof(k.name), "%s", name);
+  k.ms_sum += ms;
+  k.launches += 1;
+  k.flops_per_launch = flops;
+  k.bytes_per_launch = bytes;
 }
 
 void account_timed(sgwg_family* f, int stage, int npass_dims, bool last, float ms) {
@@ -458,6 +475,16 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
         account_timed(f, stage, 2, pass == 1, ms);
+        // algorithmic counts per launch: 70 flops per point and
+        // direction; x pass + K (1), v pass + accumulate (2) + RK stage (2/5/5) +
+        // charge density (2); HBM: u^(s) in, K out | u^(s), K, (u^n) in, out out
+        const double pts = (double)f->total;
+        const double rk = (stage == 0) ? 0.0 : (stage == 1 ? 2.0 : 5.0);
+        if (pass == 0)
+          account_kernel(f, "xpass4d_kernel", ms, pts * 141.0, pts * 16.0);
+        else
+          account_kernel(f, "vpass4d_kernel", ms, pts * (142.0 + rk + (vp ? 2.0 : 0.0)),
+                         pts * (stage > 1 ? 32.0 : 24.0));
       }
       f->stats.kernel_launches++;
     }
@@ -641,6 +668,38 @@ int launch_member_max_slot0(sgwg_family* f) {
   CK(cudaMemsetAsync(f->amax, 0, sizeof(unsigned long long) * 3 * f->nm, f->ctx->stream));
   CK(launch_member_max(f->dmem, f->nm, f->dmax_tasks, f->nmax_tasks, f->u, f->amax,
                        f->ctx->stream));
+  return SGWG_OK;
+}
+
+// Overflow guard of the fast build.  Its reconstructions put the three WENO
+// weights over one common denominator (one reciprocal instead of four
+// divides), which overflows for |u| >~ 1e36 where the reference's separate
+// divides (weno.hpp:60-72) stay finite.  Every evolve / rk3_step / rhs call
+// first reduces max|u| over the family (one small kernel); at or above 1e30
+// the step kernels of the call run in the reference arithmetic instead, so the
+// fast build never reports a non-finite tendency the reference would not.
+// (The 4D whole-plane and combination kernels also re-run an overflowed window
+// in the reference form themselves.)
+constexpr double kOverflowGuard = 1e30;
+void clear_graphs(sgwg_family* f);
+int overflow_guard(sgwg_family* f) {
+  bool on = false;
+  if (f->ctx->arith == SGWG_ARITH_FAST && f->nm > 0) {
+    TRY(launch_member_max_slot0(f));
+    std::vector<unsigned long long> mx(f->nm);
+    CK(cudaMemcpyAsync(mx.data(), f->amax, sizeof(unsigned long long) * f->nm,
+                       cudaMemcpyDeviceToHost, f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    for (unsigned long long b : mx) {
+      double v;
+      std::memcpy(&v, &b, sizeof(v));
+      if (!(v < kOverflowGuard)) on = true;  // (NaN included: the reference path reports it)
+    }
+  }
+  if (on != f->exact_override) {
+    f->exact_override = on;
+    clear_graphs(f);
+  }
   return SGWG_OK;
 }
 
@@ -1232,6 +1291,7 @@ int build_plane_tiles(sgwg_family* f) {
 // keeps the windowed plane kernels).  x pass: the whole x-plane times C
 // consecutive velocity points, X C ~ 4096; v pass: G whole velocity planes,
 // G V ~ SGWG_P4_VTARGET (3072) points.  One charge-density partial per x point.
+constexpr int kP4MaxTasksHost = 512;  // plane4d.cuh kP4MaxTasks
 int build_plane4_tiles(sgwg_family* f) {
   for (int pass = 0; pass < 2; ++pass) {
     cudaFree(f->dp4tiles[pass]);
@@ -1255,7 +1315,7 @@ int build_plane4_tiles(sgwg_family* f) {
     if (M.ext[2] < 9 || M.ext[3] < 9 || (M.ext[2] & 7) != 1 || (M.ext[3] & 7) != 1 || V >= 4096)
       return SGWG_OK;
   }
-  int vtarget = 3072;
+  int vtarget = 2400;
   if (const char* e = std::getenv("SGWG_P4_VTARGET")) vtarget = std::max(64, std::atoi(e));
   int xtarget = 4096;
   if (const char* e = std::getenv("SGWG_P4_XTARGET")) xtarget = std::max(128, std::atoi(e));
@@ -1267,13 +1327,23 @@ int build_plane4_tiles(sgwg_family* f) {
     while (cs < 6 && (X << (cs + 1)) <= xtarget) ++cs;
     const int C = 1 << cs;
     for (int v0 = 0; v0 < V; v0 += C) t[0].push_back(make_int4(mi, v0, std::min(C, V - v0), cs));
-    f->p4smem[0] = std::max(f->p4smem[0], 2 * (X << cs));
+    f->p4smem[0] = std::max(f->p4smem[0], 3 * (X << cs));  // u, d/dx1, d/dx2
     const int G = std::max(1, std::min(kP4MaxG, vtarget / V));
     for (int x0 = 0; x0 < X; x0 += G) {
       const int g = std::min(G, X - x0);
       t[1].push_back(make_int4(mi, x0, g, 0));
-      f->p4smem[1] = std::max(f->p4smem[1], 3 * ((g * V + 3) & ~1));
+      f->p4smem[1] = std::max(f->p4smem[1], 5 * ((g * V + 3) & ~1));  // u, K, u^n, dv1, dv2
     }
+    // warp tasks per CTA (plane4d.cuh add_sweep): runs x lines / 32 + partial chunks
+    auto tasks = [](int nlines, int m, bool zero) {
+      return ((nlines + 31) / 32) * ((m + (zero ? 1 : 0) + 3) / 4);  // kP4RunsPerTask = 4
+    };
+    const int G0 = std::min(G, X);
+    if (tasks(M.ext[1] << cs, M.ext[0] / 8, false) + tasks(M.ext[0] << cs, M.ext[1] / 8, false) >
+            kP4MaxTasksHost ||
+        tasks(G0 * M.ext[2], M.ext[3] / 8, true) + tasks(G0 * M.ext[3], M.ext[2] / 8, true) >
+            kP4MaxTasksHost)
+      return SGWG_OK;
   }
   for (int mi = 0; mi < f->nm; ++mi) f->hmem[mi].rparts = 1;
   CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
@@ -1495,6 +1565,7 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long lo
   TRY(upload_vec(&pl->fcoef, fcoef));
   TRY(upload_vec(&pl->fext, fext));
   TRY(upload_vec(&pl->fref, fref));
+  pl->href = fref;
   *out = pl;
   return SGWG_OK;
 }
@@ -1532,6 +1603,8 @@ int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, 
   fp.msrc_ext = pl->fext;
   fp.mrefine = pl->fref;
   fp.nm = pl->nm;
+  fp.nm_host = (int)pl->href.size();
+  fp.mref_host = pl->href.data();
   fp.d = d;
   fp.nl = f->nl;
   fp.fine_last = f->fine_ext[d - 1];
@@ -1920,6 +1993,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   if (pol->mode == SGWG_DT_CFL && !(pol->cfl > 0.0))
     return fail_with(SGWG_EINVAL, "compute_dt: cfl must be positive");
   CK(cudaSetDevice(f->ctx->device));
+  TRY(overflow_guard(f));
   cudaStream_t s = f->ctx->stream;
   // stop list (timestep.hpp:133-142)
   const double eps_dedupe = 1e-12 * std::max(1.0, tfinal);
@@ -2158,6 +2232,7 @@ int sgwg_rk3_step(sgwg_family* f, double dt, sgwg_failure* fail) {
   TRY(require_model(f));
   if (!(dt > 0.0)) return fail_with(SGWG_EINVAL, "ssp_rk3_step: dt must be positive");
   CK(cudaSetDevice(f->ctx->device));
+  TRY(overflow_guard(f));
   cudaStream_t s = f->ctx->stream;
   std::memset(f->hctl, 0, sizeof(StepCtl));
   f->hctl->active = 1;
@@ -2251,6 +2326,7 @@ int sgwg_rhs(sgwg_family* f, double* out, size_t n, int out_is_device) {
     return fail_with(SGWG_EINVAL, "rhs: size must equal the packed member states");
   TRY(require_model(f));
   CK(cudaSetDevice(f->ctx->device));
+  TRY(overflow_guard(f));
   cudaStream_t s = f->ctx->stream;
   std::memset(f->hctl, 0, sizeof(StepCtl));
   f->hctl->active = 1;
@@ -2360,6 +2436,8 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
   sp.t = t;
   sp.partial = f->diag_scratch;
   double mass = 0.0, mn = INFINITY, mx = -INFINITY, l1 = 0.0, linf = 0.0;
+  f->stats.combine_launches = 0;
+  CK(cudaEventRecord(f->ev0, f->ctx->stream));
   TRY(for_each_combined_slab(f, mode, eps, [&](const double* dev, long long first, long long n) -> int {
     StatsParams q = sp;
     q.field = dev;
@@ -2367,6 +2445,7 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
     q.n = n;
     double h5[5];
     CK(launch_stats(q, f->diag_scratch + stats_partial_doubles() - 5, f->ctx->stream));
+    f->stats.combine_launches += 2;
     CK(cudaMemcpyAsync(h5, f->diag_scratch + stats_partial_doubles() - 5, sizeof(h5),
                        cudaMemcpyDeviceToHost, f->ctx->stream));
     CK(cudaStreamSynchronize(f->ctx->stream));
@@ -2377,6 +2456,11 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
     linf = std::max(linf, h5[4]);
     return SGWG_OK;
   }));
+  CK(cudaEventRecord(f->ev1, f->ctx->stream));
+  CK(cudaEventSynchronize(f->ev1));
+  float cms = 0.f;
+  CK(cudaEventElapsedTime(&cms, f->ev0, f->ev1));
+  f->stats.combine_ms = cms;
   out->mass = mass;
   out->min = mn;
   out->max = mx;
@@ -2384,6 +2468,37 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
   out->l1 = (exact_preset >= 0) ? l1 / (double)f->finest : NAN;
   out->linf = (exact_preset >= 0) ? linf : NAN;
   return SGWG_OK;
+}
+
+int sgwg_kernel_profile(const sgwg_family* f, sgwg_kernel_timing* out, int cap, int* n) {
+  if (f == nullptr || n == nullptr || (cap > 0 && out == nullptr))
+    return fail_with(SGWG_EINVAL, "null argument");
+  int i = 0;
+  for (const auto& kv : f->kprof) {
+    if (i < cap) out[i] = kv.second;
+    ++i;
+  }
+  *n = i;
+  return SGWG_OK;
+}
+
+int sgwg_kernel_profile_reset(sgwg_family* f) {
+  if (f == nullptr) return fail_with(SGWG_EINVAL, "null argument");
+  f->kprof.clear();
+  return SGWG_OK;
+}
+
+const char* sgwg_stage_kernels(const sgwg_family* f) {
+  if (f == nullptr || !f->has_model) return "";
+  const bool fast = arith_of(f) == SGWG_ARITH_FAST;
+  if (plane4_path(f)) return "xpass4d_kernel + vpass4d_kernel";
+  if (plane_path(f)) return "plane_fast_kernel (x2)";
+  if (f->d == 3 && f->ntiles3d_fast > 0 && fast && f->model.kind == SGWG_ADVECTION)
+    return "stage3d_small_kernel";
+  if (f->d == 2 && f->ntiles2d > 0)
+    return fast ? "stage2d_quarter_kernel (evolve: evolve2d_persistent_kernel when co-resident)"
+                : "stage2d_kernel";
+  return "pass_kernel";
 }
 
 int sgwg_eval_points(sgwg_family* f, int mode, double eps, const int* idx, size_t npoints,

@@ -243,6 +243,8 @@ struct FinalParams {
   double eps;
   int assign;              // 1: out = p (prolong of one member, no accumulation)
   double* out;
+  int nm_host;             // host copy of the refinement exponents (launch-time dispatch)
+  const int* mref_host;
 };
 
 struct EvalParams {        // combined field at single finest-grid points

@@ -74,6 +74,11 @@ class Stats(C.Structure):
                 ("pass_flops", C.c_double), ("pass_bytes", C.c_double)]
 
 
+class KernelTiming(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("ms_sum", C.c_double), ("launches", C.c_longlong),
+                ("flops_per_launch", C.c_double), ("bytes_per_launch", C.c_double)]
+
+
 STOP_CB = C.CFUNCTYPE(None, C.c_double, C.c_void_p)
 IC_CB = C.CFUNCTYPE(C.c_double, C.POINTER(C.c_double), C.c_int, C.c_void_p)
 _DP = C.POINTER(C.c_double)
@@ -125,6 +130,9 @@ SIGNATURES = {
     "sgwg_eval_points": (C.c_int, [_VP, C.c_int, C.c_double, C.POINTER(C.c_int), C.c_size_t,
                                    _DP]),
     "sgwg_write_snapshot": (C.c_int, [_VP, C.c_int, C.c_double, C.c_char_p]),
+    "sgwg_kernel_profile": (C.c_int, [_VP, _VP, C.c_int, _IP]),
+    "sgwg_kernel_profile_reset": (C.c_int, [_VP]),
+    "sgwg_stage_kernels": (C.c_char_p, [_VP]),
 }
 
 
@@ -454,6 +462,23 @@ class Family:
         ms, fl, by = C.c_double(0), C.c_double(0), C.c_double(0)
         _check(load().sgwg_time_stage(self.h, reps, C.byref(ms), C.byref(fl), C.byref(by)))
         return ms.value, fl.value, by.value
+
+    def kernel_profile(self) -> list:
+        """profile mode: [{name, ms_sum, launches, flops_per_launch, bytes_per_launch}]"""
+        n = C.c_int(0)
+        _check(load().sgwg_kernel_profile(self.h, None, 0, C.byref(n)))
+        arr = (KernelTiming * max(1, n.value))()
+        _check(load().sgwg_kernel_profile(self.h, arr, n.value, C.byref(n)))
+        return [{"name": k.name.decode(), "ms_sum": k.ms_sum, "launches": k.launches,
+                 "flops_per_launch": k.flops_per_launch, "bytes_per_launch": k.bytes_per_launch}
+                for k in arr[:n.value]]
+
+    def kernel_profile_reset(self):
+        _check(load().sgwg_kernel_profile_reset(self.h))
+
+    @property
+    def stage_kernels(self) -> str:
+        return (load().sgwg_stage_kernels(self.h) or b"").decode()
 
     def stats(self) -> dict:
         s = Stats()
