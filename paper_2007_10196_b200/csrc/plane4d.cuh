@@ -167,36 +167,151 @@ __device__ __forceinline__ void adv_run(const double* __restrict__ P, int st, in
   adv_run_fast<RUN, GL, GR, ZERO, LINEAR>(P, st, wrap, c, eps, inv_h, out, ost);
 }
 
-// ---------------------------------------------------------------------------
-// Warp tasks.  A task is 32 consecutive lines of one sweep (one per lane) and
-// a range of <= kP4RunsPerTask consecutive runs along them: the line address
-// is decoded once per task, the runs follow by pointer steps, and the run
-// position -- first (left ghosts), middle, last (right ghosts), the tail point
-// of a zero-ghost line of 8m + 1 points -- is warp-uniform, so the ghost
-// pattern is a compile-time property of the adv_run instantiation each run
-// calls.  The task table is built once per CTA in shared memory.
-// ---------------------------------------------------------------------------
-constexpr int kP4MaxTasks = 512;
-constexpr int kP4RunsPerTask = 4;
-
-struct P4Tasks {
-  int nlines[2], m[2];
-  float inv_nl[2];
-  int ntask;
-  int task[kP4MaxTasks];  // sweep << 30 | line block << 12 | first run << 6 | end run
-};
-
-__device__ __forceinline__ void add_sweep(P4Tasks& T, int s, int nlines, int m, bool zero) {
-  T.nlines[s] = nlines;
-  T.m[s] = m;
-  const int nruns = m + (zero ? 1 : 0);
-  const int nb = (nlines + 31) >> 5;
-  for (int r0 = 0; r0 < nruns; r0 += kP4RunsPerTask) {
-    const int r1 = min(nruns, r0 + kP4RunsPerTask);
-    for (int b = 0; b < nb && T.ntask < kP4MaxTasks; ++b)
-      T.task[T.ntask++] = (s << 30) | (b << 12) | (r0 << 6) | r1;
+// Masked form: one instantiation per (RUN, ghost kind) -- the ghost counts
+// gl (left) / gr (right) of the run are runtime values (integer selects on the
+// six window ends), so every full run of a sweep shares one body: a small hot
+// code footprint (the instruction cache was the vpass's second stall reason
+// with one body per ghost pattern).  Ghost values are zeros (ZERO) or the
+// periodic image at -/+ wrap; a masked zero ghost reads the run's own first
+// point (a valid address) and discards it.
+template <int RUN, bool ZERO>
+__device__ __forceinline__ void load_window_masked(double* f, const double* __restrict__ P, int st,
+                                                   int wrap, int gl, int gr, double c) {
+  constexpr int NV = RUN + 6;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const bool lg = (q < 3) && (q < gl);
+    const bool rg = (q >= NV - 3) && (q >= NV - gr);
+    int idx = q * st;
+    if (ZERO) {
+      if (lg || rg) idx = 3 * st;
+    } else {
+      if (lg) idx += wrap;
+      if (rg) idx -= wrap;
+    }
+    const double v = c * P[idx];
+    f[q] = (ZERO && (lg || rg)) ? 0.0 : v;
   }
 }
+
+template <int RUN, bool ZERO, bool LINEAR>
+__device__ __noinline__ void adv_run_ref_masked(const double* __restrict__ P, int st, int wrap,
+                                                int gl, int gr, double c, double eps,
+                                                double inv_h, double* __restrict__ out, int ost) {
+  constexpr int NV = RUN + 6;
+  double f[NV];
+  load_window_masked<RUN, ZERO>(f, P, st, wrap, gl, gr, c);
+  const bool rev = c < 0.0;
+  double Fp = 0.0;
+#pragma unroll
+  for (int t = 0; t <= RUN; ++t) {
+    const int i = t + 2, m = t + 3;
+    const double F = rev ? recon_ref(f[m + 2], f[m + 1], f[m], f[m - 1], f[m - 2], eps, LINEAR)
+                         : recon_ref(f[i - 2], f[i - 1], f[i], f[i + 1], f[i + 2], eps, LINEAR);
+    if (t > 0) out[(t - 1) * ost] = (F - Fp) * inv_h;
+    Fp = F;
+  }
+}
+
+template <int RUN, bool ZERO, bool LINEAR>
+__device__ __noinline__ void adv_run_masked(const double* __restrict__ P, int st, int wrap, int gl,
+                                            int gr, double c, double eps, double inv_h,
+                                            double* __restrict__ out, int ost) {
+  constexpr int NV = RUN + 6;
+  double f[NV];
+  load_window_masked<RUN, ZERO>(f, P, st, wrap, gl, gr, c);
+  const double eps4 = 4.0 * eps;
+  double D[NV], K[NV], dd[NV];
+#pragma unroll
+  for (int q = 1; q < NV - 1; ++q) {
+    D[q] = fma(-2.0, f[q], f[q - 1] + f[q + 1]);
+    K[q] = fma(13.0 / 3.0 * D[q], D[q], eps4);
+  }
+#pragma unroll
+  for (int q = 1; q < NV; ++q) dd[q] = f[q] - f[q - 1];
+  double Fp = 0.0;
+  int ex = 0;  // max exponent field of the outputs (overflow guard)
+  if (!(c < 0.0)) {
+#pragma unroll
+    for (int t = 0; t <= RUN; ++t) {
+      const int i = t + 2;
+      const double F = recon_roles<LINEAR>(f[i], D[i - 1], D[i], D[i + 1], K[i - 1], K[i],
+                                           K[i + 1], dd[i], dd[i + 1]);
+      if (t > 0) {
+        const double du = (F - Fp) * inv_h;
+        ex = max(ex, __double2hiint(du) & 0x7ff00000);
+        out[(t - 1) * ost] = du;
+      }
+      Fp = F;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t <= RUN; ++t) {
+      const int m = t + 3;
+      const double F = recon_roles<LINEAR>(f[m], D[m + 1], D[m], D[m - 1], K[m + 1], K[m],
+                                           K[m - 1], -dd[m + 1], -dd[m]);
+      if (t > 0) {
+        const double du = (F - Fp) * inv_h;
+        ex = max(ex, __double2hiint(du) & 0x7ff00000);
+        out[(t - 1) * ost] = du;
+      }
+      Fp = F;
+    }
+  }
+  if (ex == 0x7ff00000)
+    adv_run_ref_masked<RUN, ZERO, LINEAR>(P, st, wrap, gl, gr, c, eps, inv_h, out, ost);
+}
+
+// run r of a line with m full runs (r == m: the zero-ghost tail point)
+template <bool ZERO, bool LINEAR>
+__device__ __forceinline__ void run_masked(int r, int m, const double* P, int st, int wrap,
+                                           double c, double eps, double inv_h, double* out) {
+  if (ZERO && r == m) {
+    adv_run_masked<1, true, LINEAR>(P, st, 0, 0, 3, c, eps, inv_h, out, st);
+    return;
+  }
+  const int gl = (r == 0) ? 3 : 0;
+  const int gr = (r == m - 1) ? (ZERO ? 2 : 3) : 0;
+  adv_run_masked<8, ZERO, LINEAR>(P, st, wrap, gl, gr, c, eps, inv_h, out, st);
+}
+
+// ---------------------------------------------------------------------------
+// Warp tasks.  A task is 32 consecutive lines of one sweep (one per lane) and
+// a range of <= rpt consecutive runs along them (rpt = 1 by default: equal-cost
+// tasks, so the round-robin assignment to warps is balanced to one run): the
+// line address is decoded once per task, the runs follow by pointer steps,
+// and the run position -- first (left ghosts), middle, last (right ghosts),
+// the tail point of a zero-ghost line of 8m + 1 points -- is warp-uniform, so
+// the ghost pattern is a compile-time property of the adv_run instantiation
+// each run calls.  Tasks are decoded arithmetically by every warp (no table,
+// no serial set-up before the CTA's first barrier).
+// ---------------------------------------------------------------------------
+struct P4Sweeps {
+  int nlines[2], m[2], nb[2], nt0, ntask, nruns[2], rpt;
+  float inv_nb[2];
+  __device__ void set(int s, int nlines_, int m_, bool zero) {
+    nlines[s] = nlines_;
+    m[s] = m_;
+    nb[s] = (nlines_ + 31) >> 5;
+    nruns[s] = m_ + (zero ? 1 : 0);
+    inv_nb[s] = 1.0f / (float)nb[s];
+  }
+  __device__ void finish(int rpt_) {
+    rpt = rpt_;
+    const int c0 = (nruns[0] + rpt - 1) / rpt, c1 = (nruns[1] + rpt - 1) / rpt;
+    nt0 = nb[0] * c0;
+    ntask = nt0 + nb[1] * c1;
+  }
+  // task t -> sweep, line (lane's), run range [r0, r1)
+  __device__ __forceinline__ void decode(int t, int lane, int& sw, int& l, int& r0, int& r1) const {
+    sw = (t >= nt0) ? 1 : 0;
+    const int u = sw ? t - nt0 : t;
+    const int q = qdiv(u, inv_nb[sw]);
+    l = ((u - q * nb[sw]) << 5) + lane;
+    r0 = q * rpt;
+    r1 = min(nruns[sw], r0 + rpt);
+  }
+};
 
 // adv_run instantiation of run r of a line with m full runs: 0 middle, 1 first,
 // 2 last, 3 single (both ends), 4 zero-ghost tail point
@@ -248,7 +363,6 @@ __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_kernel(const Plane4Para
   double* D1 = sm + NT;  // d/dx1
   double* D2 = D1 + NT;  // d/dx2
   __shared__ double ca[kP4MaxC], cb[kP4MaxC];
-  __shared__ P4Tasks T;
   const int tid = threadIdx.x;
   {
     const double* src = p.uin + M->offset + v0;
@@ -265,36 +379,42 @@ __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_kernel(const Plane4Para
     ca[tid] = line_coef(p.flux_a, M, 0, p.space_dim, i3, p.c_a, p.efield);
     cb[tid] = line_coef(p.flux_b, M, 1, p.space_dim, vl - i3 * n4, p.c_b, p.efield);
   }
-  if (tid == 0) {
-    // sweep 0: x1 lines (x2, c) = l, stride n2 C, n1 points; sweep 1: x2 lines
-    // (x1, c), stride C, n2 points
-    T.ntask = 0;
-    add_sweep(T, 0, n2 << cs, n1 >> 3, false);
-    add_sweep(T, 1, n1 << cs, n2 >> 3, false);
-  }
+  // sweep 0: x1 lines (x2, c) = l, stride n2 C, n1 points; sweep 1: x2 lines
+  // (x1, c), stride C, n2 points
+  P4Sweeps T;
+  T.set(0, n2 << cs, n1 >> 3, false);
+  T.set(1, n1 << cs, n2 >> 3, false);
+  T.finish(p.rpt);
   cp_async_wait<0>();
   __syncthreads();
   const int lane = tid & 31, warp = tid >> 5;
   const int st0 = n2 << cs, wrap0 = n1 * st0, wrap1 = n2 << cs;
   const double ih1 = M->inv_h[0], ih2 = M->inv_h[1], eps = p.eps;
-  for (int t = warp; t < T.ntask; t += kP4Threads / 32) {
-    const int e = T.task[t];
-    const int sw = e >> 30, r0 = (e >> 6) & 63, r1 = e & 63;
-    const int l = (((e >> 12) & 0x3ffff) << 5) + lane;
+  for (int t = (p.dbg & 1) ? T.ntask : warp; t < T.ntask; t += kP4Threads / 32) {
+    int sw, l, r0, r1;
+    T.decode(t, lane, sw, l, r0, r1);
     if (l >= T.nlines[sw]) continue;
     const int m = T.m[sw];
     const int c = l & (C - 1);
     if (sw == 0) {
       const double cf = ca[c];
       for (int r = r0; r < r1; ++r)
-        run_dispatch<false, LINEAR>(run_inst(r, m), U + l + (8 * r - 3) * st0, st0, wrap0,
-                                           cf, eps, ih1, D1 + l + 8 * r * st0);
+        if (p.masked)
+          run_masked<false, LINEAR>(r, m, U + l + (8 * r - 3) * st0, st0, wrap0, cf, eps, ih1,
+                                    D1 + l + 8 * r * st0);
+        else
+          run_dispatch<false, LINEAR>(run_inst(r, m), U + l + (8 * r - 3) * st0, st0, wrap0,
+                                      cf, eps, ih1, D1 + l + 8 * r * st0);
     } else {
       const int base = (l >> cs) * wrap1 + c;
       const double cf = cb[c];
       for (int r = r0; r < r1; ++r)
-        run_dispatch<false, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * C, C, wrap1,
-                                           cf, eps, ih2, D2 + base + 8 * r * C);
+        if (p.masked)
+          run_masked<false, LINEAR>(r, m, U + base + (8 * r - 3) * C, C, wrap1, cf, eps, ih2,
+                                    D2 + base + 8 * r * C);
+        else
+          run_dispatch<false, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * C, C, wrap1,
+                                      cf, eps, ih2, D2 + base + 8 * r * C);
     }
   }
   __syncthreads();
@@ -344,7 +464,6 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
   extern __shared__ __align__(16) double sm[];
   __shared__ unsigned long long bar[2];
   __shared__ double ce1[kP4MaxG], ce2[kP4MaxG];
-  __shared__ P4Tasks T;
   const int tid = threadIdx.x;
   const int stage = p.stage;
   const long long gs = M->offset + (long long)x0 * V;  // tile start (doubles)
@@ -359,14 +478,13 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
   double* UNt = sm + 2 * pitch + shift;
   double* DV1 = sm + 3 * pitch;
   double* DV2 = sm + 4 * pitch;
-  if (tid == 0) {
+  if (tid == 0) {  // the CTA barrier below publishes the initialised mbarriers
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (tid == 0) {
     bulk_g2s(sm, p.uin + ga, nbytes, &bar[0]);
-    if (stage > 1) {
+    if (p.dbg & 4) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar[1])) : "memory");
+    } else if (stage > 1) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[1])),
                    "r"(2 * nbytes)
                    : "memory");
@@ -383,12 +501,13 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
     } else {
       bulk_g2s(sm + pitch, p.kbuf + ga, nbytes, &bar[1]);
     }
-    // sweep 0: v2 lines (rows rho = g n3 + i3), unit stride, n4 points;
-    // sweep 1: v1 lines (columns kappa = g n4 + i4), stride n4, n3 points
-    T.ntask = 0;
-    add_sweep(T, 0, G * n3, n4 >> 3, true);
-    add_sweep(T, 1, G * n4, n3 >> 3, true);
   }
+  // sweep 0: v2 lines (rows rho = g n3 + i3), unit stride, n4 points;
+  // sweep 1: v1 lines (columns kappa = g n4 + i4), stride n4, n3 points
+  P4Sweeps T;
+  T.set(0, G * n3, n4 >> 3, true);
+  T.set(1, G * n4, n3 >> 3, true);
+  T.finish(p.rpt);
   if (tid < G) {  // v_j lines at x point x0+tid: -E_j(x) (VP) or the advection speed
     ce1[tid] = line_coef(p.flux_a, M, 2, p.space_dim, x0 + tid, p.c_a, p.efield);
     ce2[tid] = line_coef(p.flux_b, M, 3, p.space_dim, x0 + tid, p.c_b, p.efield);
@@ -399,25 +518,32 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
   {
     const float i3f = 1.0f / (float)n3, i4f = 1.0f / (float)n4;
     const double ih3 = M->inv_h[2], ih4 = M->inv_h[3], eps = p.eps;
-    for (int t = warp; t < T.ntask; t += kP4Threads / 32) {
-      const int e = T.task[t];
-      const int sw = e >> 30, r0 = (e >> 6) & 63, r1 = e & 63;
-      const int l = (((e >> 12) & 0x3ffff) << 5) + lane;
+    for (int t = (p.dbg & 1) ? T.ntask : warp; t < T.ntask; t += kP4Threads / 32) {
+      int sw, l, r0, r1;
+      T.decode(t, lane, sw, l, r0, r1);
       if (l >= T.nlines[sw]) continue;
       const int m = T.m[sw];
       if (sw == 0) {
         const int base = l * n4;
         const double cf = ce2[qdiv(l, i3f)];
         for (int r = r0; r < r1; ++r)
-          run_dispatch<true, LINEAR>(run_inst(r, m), U + base + 8 * r - 3, 1, 0, cf, eps,
-                                            ih4, DV2 + base + 8 * r);
+          if (p.masked)
+            run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, cf, eps, ih4,
+                                     DV2 + base + 8 * r);
+          else
+            run_dispatch<true, LINEAR>(run_inst(r, m), U + base + 8 * r - 3, 1, 0, cf, eps,
+                                       ih4, DV2 + base + 8 * r);
       } else {
         const int gx = qdiv(l, i4f);
         const int base = gx * V + (l - gx * n4);
         const double cf = ce1[gx];
         for (int r = r0; r < r1; ++r)
-          run_dispatch<true, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * n4, n4, 0, cf,
-                                            eps, ih3, DV1 + base + 8 * r * n4);
+          if (p.masked)
+            run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, cf, eps, ih3,
+                                     DV1 + base + 8 * r * n4);
+          else
+            run_dispatch<true, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * n4, n4, 0, cf,
+                                       eps, ih3, DV1 + base + 8 * r * n4);
       }
     }
   }
@@ -428,6 +554,7 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
   const bool moment = (p.rho_parts != nullptr) && (stage > 0);
   double* out = p.out + gs;
   int ex = 0;
+  if (p.dbg & 2) return;
   if (moment) {
     if (stage == 1)
       vpass_epilogue<1, true>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);

@@ -217,6 +217,7 @@ struct sgwg_family {
   int nranks = 1, rank = 0;
   sgwg_stats stats{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evs0 = nullptr, evs1 = nullptr;  // whole combined_stats span (ev0/ev1 time each slab)
   cudaStream_t side = nullptr;                 // off-critical-path work (energy record)
   cudaEvent_t evfork = nullptr, evjoin = nullptr;
   // current policy for graph building
@@ -455,6 +456,11 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     p.ctl = f->ctl;
     p.fail = f->fail;
     p.counter = f->counter;
+    p.rpt = 1;
+    if (const char* e = std::getenv("SGWG_P4_RPT")) p.rpt = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("SGWG_P4_DBG")) p.dbg = std::atoi(e);
+    p.masked = 1;
+    if (const char* e = std::getenv("SGWG_P4_MASKED")) p.masked = std::atoi(e);
     for (int pass = 0; pass < 2; ++pass) {
       p.tiles = f->dp4tiles[pass];
       if (vp) {
@@ -1033,6 +1039,8 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   f->no_fused2d = std::getenv("SGWG_NO_FUSED2D") != nullptr;
   CK(cudaEventCreate(&f->ev0));
   CK(cudaEventCreate(&f->ev1));
+  CK(cudaEventCreate(&f->evs0));
+  CK(cudaEventCreate(&f->evs1));
   CK(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&f->evfork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&f->evjoin, cudaEventDisableTiming));
@@ -1291,7 +1299,6 @@ int build_plane_tiles(sgwg_family* f) {
 // keeps the windowed plane kernels).  x pass: the whole x-plane times C
 // consecutive velocity points, X C ~ 4096; v pass: G whole velocity planes,
 // G V ~ SGWG_P4_VTARGET (3072) points.  One charge-density partial per x point.
-constexpr int kP4MaxTasksHost = 512;  // plane4d.cuh kP4MaxTasks
 int build_plane4_tiles(sgwg_family* f) {
   for (int pass = 0; pass < 2; ++pass) {
     cudaFree(f->dp4tiles[pass]);
@@ -1334,16 +1341,6 @@ int build_plane4_tiles(sgwg_family* f) {
       t[1].push_back(make_int4(mi, x0, g, 0));
       f->p4smem[1] = std::max(f->p4smem[1], 5 * ((g * V + 3) & ~1));  // u, K, u^n, dv1, dv2
     }
-    // warp tasks per CTA (plane4d.cuh add_sweep): runs x lines / 32 + partial chunks
-    auto tasks = [](int nlines, int m, bool zero) {
-      return ((nlines + 31) / 32) * ((m + (zero ? 1 : 0) + 3) / 4);  // kP4RunsPerTask = 4
-    };
-    const int G0 = std::min(G, X);
-    if (tasks(M.ext[1] << cs, M.ext[0] / 8, false) + tasks(M.ext[0] << cs, M.ext[1] / 8, false) >
-            kP4MaxTasksHost ||
-        tasks(G0 * M.ext[2], M.ext[3] / 8, true) + tasks(G0 * M.ext[3], M.ext[2] / 8, true) >
-            kP4MaxTasksHost)
-      return SGWG_OK;
   }
   for (int mi = 0; mi < f->nm; ++mi) f->hmem[mi].rparts = 1;
   CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
@@ -1830,6 +1827,8 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->slab_out);
   cudaEventDestroy(f->ev0);
   cudaEventDestroy(f->ev1);
+  cudaEventDestroy(f->evs0);
+  cudaEventDestroy(f->evs1);
   cudaEventDestroy(f->evfork);
   cudaEventDestroy(f->evjoin);
   cudaStreamDestroy(f->side);
@@ -2437,7 +2436,7 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
   sp.partial = f->diag_scratch;
   double mass = 0.0, mn = INFINITY, mx = -INFINITY, l1 = 0.0, linf = 0.0;
   f->stats.combine_launches = 0;
-  CK(cudaEventRecord(f->ev0, f->ctx->stream));
+  CK(cudaEventRecord(f->evs0, f->ctx->stream));
   TRY(for_each_combined_slab(f, mode, eps, [&](const double* dev, long long first, long long n) -> int {
     StatsParams q = sp;
     q.field = dev;
@@ -2456,10 +2455,10 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
     linf = std::max(linf, h5[4]);
     return SGWG_OK;
   }));
-  CK(cudaEventRecord(f->ev1, f->ctx->stream));
-  CK(cudaEventSynchronize(f->ev1));
+  CK(cudaEventRecord(f->evs1, f->ctx->stream));
+  CK(cudaEventSynchronize(f->evs1));
   float cms = 0.f;
-  CK(cudaEventElapsedTime(&cms, f->ev0, f->ev1));
+  CK(cudaEventElapsedTime(&cms, f->evs0, f->evs1));
   f->stats.combine_ms = cms;
   out->mass = mass;
   out->min = mn;

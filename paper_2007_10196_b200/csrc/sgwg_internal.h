@@ -190,6 +190,9 @@ struct Plane4Params {
   double* rho_parts;       // v pass, Vlasov-Poisson: sum_v w_v out per x point (part 0)
   const struct DtParams* dtp;
   unsigned int* counter;
+  int rpt;                 // runs per warp task (plane4d.cuh P4Sweeps)
+  int masked;              // 1: one sweep body with runtime ghost masks (default), 0: per-pattern bodies
+  int dbg;                 // timing experiments only (SGWG_P4_DBG): 1 no sweeps, 2 no epilogue, 4 no K/u^n copies
 };
 
 // Vlasov-Maxwell field lines (vm_rhs_into, models.hpp:437-505): per member the
