@@ -9,4 +9,7 @@
 extern "C" int sgwg_trace_dump(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, sgwg::fast::sgwg_trace, sizeof(sgwg::fast::sgwg_trace));
 }
+extern "C" int sgwg_p4trace_dump(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, sgwg::fast::sgwg_p4trace, sizeof(sgwg::fast::sgwg_p4trace));
+}
 #endif

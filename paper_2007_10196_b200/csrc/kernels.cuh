@@ -2191,8 +2191,8 @@ __global__ void __launch_bounds__(256) final_kernel(const FinalParams p) {
 // are literals.  ~24 fp64 operations per interpolated fine point.
 // ---------------------------------------------------------------------------
 template <int M, int PH, int MODE>
-__device__ __forceinline__ void final_chunk(const double* __restrict__ line, int n_src, int bc,
-                                            int ib, double coef, double eps, double* acc) {
+__device__ __forceinline__ void final_chunk(const double* __restrict__ line, long long st, int n_src,
+                                            int bc, int ib, double coef, double eps, double* acc) {
   constexpr int F = 1 << M;
   constexpr int W0 = 8 * PH;  // offset of the chunk's first fine point within its block
   // window offsets (relative to ib) of every source value the chunk reads
@@ -2206,12 +2206,12 @@ __device__ __forceinline__ void final_chunk(const double* __restrict__ line, int
     if (q < 0 || q >= n_src) {
       if (bc == 0) {
         q = (q < 0) ? q + n_src : q - n_src;
-        s[o] = __ldg(line + q);
+        s[o] = __ldg(line + q * st);
       } else {
         s[o] = 0.0;
       }
     } else {
-      s[o] = __ldg(line + q);
+      s[o] = __ldg(line + q * st);
     }
   }
   // per stencil centre (window index c - OMIN): Q_k = prod_{l != k} (eps + b_l)^2
@@ -2267,31 +2267,147 @@ __device__ __forceinline__ void final_chunk(const double* __restrict__ line, int
   }
 }
 
-template <int MODE>
-__device__ __forceinline__ void final_chunk_dispatch(int m, int c, const double* line, int n_src,
-                                                     int bc, double coef, double eps,
-                                                     double* acc) {
-  const int j0 = 8 * c;
-  switch (m) {
-    case 1: final_chunk<1, 0, MODE>(line, n_src, bc, j0 >> 1, coef, eps, acc); break;
-    case 2: final_chunk<2, 0, MODE>(line, n_src, bc, j0 >> 2, coef, eps, acc); break;
-    case 3: final_chunk<3, 0, MODE>(line, n_src, bc, j0 >> 3, coef, eps, acc); break;
-    case 4:
-      if (c & 1)
-        final_chunk<4, 1, MODE>(line, n_src, bc, j0 >> 4, coef, eps, acc);
-      else
-        final_chunk<4, 0, MODE>(line, n_src, bc, j0 >> 4, coef, eps, acc);
-      break;
-    case 5:
-      switch (c & 3) {
-        case 0: final_chunk<5, 0, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
-        case 1: final_chunk<5, 1, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
-        case 2: final_chunk<5, 2, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
-        default: final_chunk<5, 3, MODE>(line, n_src, bc, j0 >> 5, coef, eps, acc); break;
+// Chunk of 8 fine points [j0, j0 + 8) along a line refined by 2^m >= 8: every
+// point lies in the source interval [ib, ib + 1), ib = j0 >> m, so the window
+// is the 6 values ib-2 .. ib+3 and the stencil centre is ib or ib + 1 (WENO:
+// r >= 2^m / 2, interp.hpp:124-146).  The per-offset coefficients -- the
+// substencil polynomials p_k(t) as point weights and the linear weights C_k(t)
+// (interp.hpp:36-53, 119-122) -- come from a constant table indexed by the
+// warp-uniform (m, r), so one body serves every m in 3..7 and chunk phase
+// (the per-phase instantiations of final_chunk were the final pass's
+// instruction-cache stall).  The smoothness indicators of the two centres are
+// computed once per chunk.
+constexpr int kInterpTabMaxM = 7;
+__constant__ double c_itab[2][256][12];  // [mode][(1 << m) + r]: a0..a2 b1..b3 e2..e4 c0..c2
+
+void fill_interp_table(double* tab /* [2][256][12] */) {
+  for (int mode = 0; mode < 2; ++mode)
+    for (int m = 1; m <= kInterpTabMaxM; ++m) {
+      const int F = 1 << m;
+      for (int r = 1; r < F; ++r) {
+        const int di = (mode == 1 && r >= F / 2) ? 1 : 0;
+        const double t = (double)r / F - di;
+        double* e = tab + ((mode * 256) + F + r) * 12;
+        e[0] = 0.5 * (t + 1.0) * t;
+        e[1] = -(t + 2.0) * t;
+        e[2] = 0.5 * (t + 2.0) * (t + 1.0);
+        e[3] = 0.5 * t * (t - 1.0);
+        e[4] = -(t + 1.0) * (t - 1.0);
+        e[5] = 0.5 * (t + 1.0) * t;
+        e[6] = 0.5 * (t - 1.0) * (t - 2.0);
+        e[7] = -t * (t - 2.0);
+        e[8] = 0.5 * t * (t - 1.0);
+        e[9] = (t - 1.0) * (t - 2.0) / 12.0;
+        e[10] = (4.0 - t * t) / 6.0;
+        e[11] = (t + 2.0) * (t + 1.0) / 12.0;
       }
-      break;
-    default:
-      break;
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void weno_q(const double* s, double eps, double& Q0, double& Q1,
+                                       double& Q2) {
+  const double s0 = s[0], s1 = s[1], s2 = s[2], s3 = s[3], s4 = s[4];
+  const double d0 = s0 - 2.0 * s1 + s2, g0 = s0 - 4.0 * s1 + 3.0 * s2;
+  const double d1 = s1 - 2.0 * s2 + s3, g1 = s1 - s3;
+  const double d2 = s2 - 2.0 * s3 + s4, g2 = 3.0 * s2 - 4.0 * s3 + s4;
+  const double e0 = fma(13.0 / 12.0 * d0, d0, fma(0.25 * g0, g0, eps));
+  const double e1 = fma(13.0 / 12.0 * d1, d1, fma(0.25 * g1, g1, eps));
+  const double e2 = fma(13.0 / 12.0 * d2, d2, fma(0.25 * g2, g2, eps));
+  const double q0 = e0 * e0, q1 = e1 * e1, q2 = e2 * e2;
+  Q0 = q1 * q2;
+  Q1 = q0 * q2;
+  Q2 = q0 * q1;
+}
+
+// the points u in [U0, U1) of the chunk with stencil values s0..s4 and weights
+// Q (one centre): acc[u] += coef * P(u)
+template <int MODE, int U0, int U1>
+__device__ __forceinline__ void chunk_points(const double* __restrict__ tab, int j0, int F, int np,
+                                             double s0, double s1, double s2, double s3, double s4,
+                                             double Q0, double Q1, double Q2, double coef,
+                                             double* acc) {
+#pragma unroll
+  for (int u = U0; u < U1; ++u) {
+    if (u >= np) break;
+    const int r = (j0 + u) & (F - 1);
+    if (r == 0) {  // copy: src[j >> m] (the window's centre ib)
+      acc[u] = fma(coef, s2, acc[u]);
+      continue;
+    }
+    const double* e = tab + r * 12;
+    const double p0 = fma(s0, e[0], fma(s1, e[1], s2 * e[2]));
+    const double p1 = fma(s1, e[3], fma(s2, e[4], s3 * e[5]));
+    const double p2 = fma(s2, e[6], fma(s3, e[7], s4 * e[8]));
+    double v;
+    if (MODE == 1) {
+      const double a0 = e[9] * Q0, a1 = e[10] * Q1, a2 = e[11] * Q2;
+      v = fma(a0, p0, fma(a1, p1, a2 * p2)) * fast_rcp(a0 + a1 + a2);
+    } else {
+      v = fma(e[9], p0, fma(e[10], p1, e[11] * p2));
+    }
+    acc[u] = fma(coef, v, acc[u]);
+  }
+}
+
+// NP <= 8 points of the chunk are formed (line tails); acc[u] += coef * P(u).
+// For m >= 4 the chunk lies in one half of its source interval, so one stencil
+// centre (ib, or ib + 1 when WENO's r >= 2^m / 2) serves all 8 points; for m = 3
+// points 0-3 use ib and 4-7 use ib + 1.
+template <int MODE>
+__device__ __forceinline__ void chunk_generic(const double* __restrict__ line, long long st,
+                                              int n_src, int bc, int m, int j0, int np,
+                                              double coef, double eps, double* acc) {
+  const int F = 1 << m;
+  const int ib = j0 >> m;
+  double s[6];
+#pragma unroll
+  for (int o = 0; o < 6; ++o) {
+    int q = ib - 2 + o;
+    const bool out = (q < 0 || q >= n_src);
+    if (out && bc == 0) q = (q < 0) ? q + n_src : q - n_src;
+    s[o] = (out && bc != 0) ? 0.0 : __ldg(line + q * st);
+  }
+  const double* tab = &c_itab[MODE][F][0];
+  double Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;
+  if (m > 3) {
+    const bool hi = (MODE == 1) && (((j0 & (F - 1)) << 1) >= F);  // chunk-uniform centre
+    const double s0 = hi ? s[1] : s[0], s1 = hi ? s[2] : s[1], s2 = hi ? s[3] : s[2],
+                 s3 = hi ? s[4] : s[3], s4 = hi ? s[5] : s[4];
+    if (MODE == 1) {
+      const double w[5] = {s0, s1, s2, s3, s4};
+      weno_q<MODE>(w, eps, Q0, Q1, Q2);
+    }
+    // r == 0 copies (j0 % F == 0) take the centre ib: hi is false there
+    chunk_points<MODE, 0, 8>(tab, j0, F, np, s0, s1, s2, s3, s4, Q0, Q1, Q2, coef, acc);
+  } else {
+    if (MODE == 1) weno_q<MODE>(s, eps, Q0, Q1, Q2);
+    chunk_points<MODE, 0, 4>(tab, j0, F, np, s[0], s[1], s[2], s[3], s[4], Q0, Q1, Q2, coef, acc);
+    if (MODE == 1) {
+      weno_q<MODE>(s + 1, eps, Q0, Q1, Q2);
+      chunk_points<MODE, 4, 8>(tab, j0, F, np, s[1], s[2], s[3], s[4], s[5], Q0, Q1, Q2, coef,
+                               acc);
+    } else {
+      chunk_points<MODE, 4, 8>(tab, j0, F, np, s[0], s[1], s[2], s[3], s[4], Q0, Q1, Q2, coef,
+                               acc);
+    }
+  }
+}
+
+// chunk [j0, j0 + np) of a line refined by 2^m (1 <= m <= 7, j0 % 8 == 0)
+template <int MODE>
+__device__ __forceinline__ void interp_chunk(int m, int j0, int np, const double* line,
+                                             long long st, int n_src, int bc, double coef,
+                                             double eps, double* acc) {
+  if (m >= 3) {
+    chunk_generic<MODE>(line, st, n_src, bc, m, j0, np, coef, eps, acc);
+  } else {
+    // np < 8 only at a zero-ghost line's last point (fine extent 8k + 1): the
+    // full chunk's extra points read in-range or zero windows and are discarded
+    if (m == 1)
+      final_chunk<1, 0, MODE>(line, st, n_src, bc, j0 >> 1, coef, eps, acc);
+    else
+      final_chunk<2, 0, MODE>(line, st, n_src, bc, j0 >> 2, coef, eps, acc);
   }
 }
 
@@ -2319,8 +2435,11 @@ __device__ __noinline__ void final_chunk_ref(const double* const* srcs, const do
 }
 
 // grid-stride over (32-row block, chunk) warp items
+#ifndef SGWG_FINAL_MINB
+#define SGWG_FINAL_MINB 3
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(256) final_fast_kernel(const FinalParams p) {
+__global__ void __launch_bounds__(256, SGWG_FINAL_MINB) final_fast_kernel(const FinalParams p) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
   const int nch = (p.fine_last + 7) >> 3;  // chunks per row (the last may be partial)
@@ -2347,7 +2466,8 @@ __global__ void __launch_bounds__(256) final_fast_kernel(const FinalParams p) {
         continue;
       }
       const int n_src = p.msrc_ext[mi];
-      final_chunk_dispatch<MODE>(m, c, p.src[mi] + row * n_src, n_src, p.bc_last, cf, p.eps, acc);
+      interp_chunk<MODE>(m, 8 * c, min(8, p.fine_last - 8 * c), p.src[mi] + row * n_src, 1, n_src,
+                         p.bc_last, cf, p.eps, acc);
     }
     int ex = 0;
 #pragma unroll
@@ -2361,6 +2481,66 @@ __global__ void __launch_bounds__(256) final_fast_kernel(const FinalParams p) {
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (8 * c + u < p.fine_last) out[u] = acc[u];
+  }
+}
+
+// Fast prolongation of dimension k < d-1 (interp.hpp:217-244) for all member
+// slots of a plan: a thread forms one 8-point chunk of one line along k, a
+// warp the same chunk of 32 consecutive lines (consecutive inner index: the
+// loads and stores of a warp are unit-stride across lanes), the chunk phase
+// is warp-uniform.  Work item = (slot, chunk, 32-line block), chunk-major
+// within a slot; slot found by binary search of the item prefix.
+template <int MODE>
+__global__ void __launch_bounds__(256) upsample_fast_kernel(const UpsampleParams p) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  const int k = p.kdim;
+  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       it < p.nitems; it += wstride) {
+    int lo = 0, hi = p.nslots - 1;  // last slot with item0 <= it
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.slot_item0[mid] <= it) lo = mid; else hi = mid - 1;
+    }
+    const int slot = lo;
+    const int* ext = p.slot_ext + 4 * slot;
+    long long inner = 1, outer = 1;
+    for (int q = 0; q < 4; ++q) {
+      if (q > k) inner *= ext[q];
+      if (q < k) outer *= ext[q];
+    }
+    const long long nlines = outer * inner;
+    const long long nblk = (nlines + 31) >> 5;
+    const long long local = it - p.slot_item0[slot];
+    const int ci = (int)(local / nblk);
+    const long long line = (local - ci * nblk) * 32 + lane;
+    if (line >= nlines) continue;
+    const int n_src = ext[k];
+    const int ndst = (k == 0) ? p.nrows0 : p.fine_ext;      // dst extent along k
+    const int jlo = (k == 0) ? p.jrow0 : 0;                 // fine index of dst row 0
+    const int j0 = ((jlo >> 3) + ci) * 8;                   // chunk start (fine index)
+    const int a = max(j0, jlo), b = min(j0 + 8, jlo + ndst);  // points of this slab
+    const int m = p.nl - p.mem[p.slot_member[slot]].level[k];
+    const long long o = line / inner, i = line - o * inner;
+    const double* src = p.src[slot] + o * (long long)n_src * inner + i;
+    double* dst = p.dst[slot] + (o * (long long)ndst - jlo) * inner + i;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    interp_chunk<MODE>(m, j0, 8, src, inner, n_src, p.bc, 1.0, p.eps, acc);
+    int ex = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ex = max(ex, __double2hiint(acc[u]) & 0x7ff00000);
+    if (ex == 0x7ff00000) {  // overflowed common-denominator weights: reference form
+      const long long base = o * (long long)n_src * inner + i;
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u >= a && j0 + u < b)
+          acc[u] = interp_point(p.src[slot], base, inner, n_src, j0 + u, m, p.bc, MODE, p.eps);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u >= a && j0 + u < b) dst[(long long)(j0 + u) * inner] = acc[u];
   }
 }
 #endif
@@ -2504,6 +2684,12 @@ cudaError_t configure() {
   if (e0 != cudaSuccess) return e0;
   e0 = configure_plane4();
   if (e0 != cudaSuccess) return e0;
+  {
+    static double tab[2 * 256 * 12];
+    fill_interp_table(tab);
+    e0 = cudaMemcpyToSymbol(c_itab, tab, sizeof(tab));
+    if (e0 != cudaSuccess) return e0;
+  }
   e0 = cudaFuncSetAttribute(stage3d_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kSmall3DSmem * (int)sizeof(double));
   if (e0 != cudaSuccess) return e0;
@@ -2572,6 +2758,14 @@ cudaError_t launch_pass(const PassParams& p, int nblocks, size_t smem, cudaStrea
 
 cudaError_t launch_upsample(const UpsampleParams& p, int nblocks, cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
+#if SGWG_FAST
+  if (p.nitems > 0) {  // chunked form (every member refinement of the pass <= 2^7)
+    long long blocks = (p.nitems + 7) / 8;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    return p.mode == 1 ? launch_k(upsample_fast_kernel<1>, dim3((int)blocks), dim3(256), 0, s, p)
+                       : launch_k(upsample_fast_kernel<0>, dim3((int)blocks), dim3(256), 0, s, p);
+  }
+#endif
   return launch_k(upsample_kernel, dim3(nblocks), dim3(256), 0, s, p);
 }
 
@@ -2583,7 +2777,7 @@ cudaError_t launch_final(const FinalParams& p, cudaStream_t s) {
   bool chunked = !p.assign && p.nm_host == p.nm &&
                  ((p.fine_last - (p.bc_last != 0 ? 1 : 0)) % 8 == 0) &&
                  std::getenv("SGWG_FINAL_GENERIC") == nullptr;
-  for (int mi = 0; chunked && mi < p.nm_host; ++mi) chunked = p.mref_host[mi] <= 5;
+  for (int mi = 0; chunked && mi < p.nm_host; ++mi) chunked = p.mref_host[mi] <= kInterpTabMaxM;
   if (chunked) {
     const long long rows = p.nfine / p.fine_last;
     const long long items = ((rows + 31) / 32) * ((p.fine_last + 7) / 8);

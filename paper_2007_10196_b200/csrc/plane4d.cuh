@@ -28,8 +28,44 @@
 // lines: odd row pitch or unit stride).
 #pragma once
 
-constexpr int kP4Threads = 256;
+#ifndef SGWG_P4_THREADS
+#define SGWG_P4_THREADS 256
+#endif
+#ifndef SGWG_P4_MINB
+#define SGWG_P4_MINB 2
+#endif
+constexpr int kP4Threads = SGWG_P4_THREADS;
 constexpr int kP4MaxC = 64;   // velocity points per x-pass tile
+
+#ifdef SGWG_TRACE
+// experiment builds only: per-CTA phase stamps of the plane kernels
+// [pass][cta][0: globaltimer start, 1..7: clock64 at marks 0..6, 8: smid, 9: globaltimer at mark 5]
+constexpr int kP4TraceCtas = 8192;
+__device__ long long sgwg_p4trace[2][kP4TraceCtas][10];
+#define P4MARK(pass, k)                                                      \
+  do {                                                                       \
+    if (threadIdx.x == 0 && blockIdx.x < kP4TraceCtas) {                     \
+      if ((k) == 0) {                                                        \
+        long long g;                                                         \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));                \
+        unsigned sid;                                                        \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sid));                     \
+        sgwg_p4trace[pass][blockIdx.x][0] = g;                               \
+        sgwg_p4trace[pass][blockIdx.x][8] = sid;                             \
+      }                                                                      \
+      if ((k) == 5) {                                                        \
+        long long g;                                                         \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));                \
+        sgwg_p4trace[pass][blockIdx.x][9] = g;                               \
+      }                                                                      \
+      sgwg_p4trace[pass][blockIdx.x][(k) + 1] = clock64();                   \
+    }                                                                        \
+  } while (0)
+#else
+#define P4MARK(pass, k) \
+  do {                  \
+  } while (0)
+#endif
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -287,29 +323,35 @@ __device__ __forceinline__ void run_masked(int r, int m, const double* P, int st
 // no serial set-up before the CTA's first barrier).
 // ---------------------------------------------------------------------------
 struct P4Sweeps {
-  int nlines[2], m[2], nb[2], nt0, ntask, nruns[2], rpt;
-  float inv_nb[2];
+  // per sweep s = 0, 1 as scalars (a runtime-indexed array would live in local memory)
+  int nl0, nl1, m0, m1, nb0, nb1, nr0, nr1, nt0, ntask, rpt;
+  float inb0, inb1;
   __device__ void set(int s, int nlines_, int m_, bool zero) {
-    nlines[s] = nlines_;
-    m[s] = m_;
-    nb[s] = (nlines_ + 31) >> 5;
-    nruns[s] = m_ + (zero ? 1 : 0);
-    inv_nb[s] = 1.0f / (float)nb[s];
+    const int nb = (nlines_ + 31) >> 5, nr = m_ + (zero ? 1 : 0);
+    if (s == 0) {
+      nl0 = nlines_, m0 = m_, nb0 = nb, nr0 = nr, inb0 = 1.0f / (float)nb;
+    } else {
+      nl1 = nlines_, m1 = m_, nb1 = nb, nr1 = nr, inb1 = 1.0f / (float)nb;
+    }
   }
   __device__ void finish(int rpt_) {
     rpt = rpt_;
-    const int c0 = (nruns[0] + rpt - 1) / rpt, c1 = (nruns[1] + rpt - 1) / rpt;
-    nt0 = nb[0] * c0;
-    ntask = nt0 + nb[1] * c1;
+    const int c0 = (nr0 + rpt - 1) / rpt, c1 = (nr1 + rpt - 1) / rpt;
+    nt0 = nb0 * c0;
+    ntask = nt0 + nb1 * c1;
   }
-  // task t -> sweep, line (lane's), run range [r0, r1)
-  __device__ __forceinline__ void decode(int t, int lane, int& sw, int& l, int& r0, int& r1) const {
+  // task t -> sweep, line (lane's), run range [r0, r1), the sweep's line count and runs
+  __device__ __forceinline__ void decode(int t, int lane, int& sw, int& l, int& r0, int& r1,
+                                         int& nlines, int& m) const {
     sw = (t >= nt0) ? 1 : 0;
     const int u = sw ? t - nt0 : t;
-    const int q = qdiv(u, inv_nb[sw]);
-    l = ((u - q * nb[sw]) << 5) + lane;
+    const int nb = sw ? nb1 : nb0;
+    const int q = qdiv(u, sw ? inb1 : inb0);
+    l = ((u - q * nb) << 5) + lane;
     r0 = q * rpt;
-    r1 = min(nruns[sw], r0 + rpt);
+    r1 = min(sw ? nr1 : nr0, r0 + rpt);
+    nlines = sw ? nl1 : nl0;
+    m = sw ? m1 : m0;
   }
 };
 
@@ -348,10 +390,11 @@ __device__ __forceinline__ void run_dispatch(int inst, const double* P, int st, 
 // x pass: dims (0, 1) of C velocity points over the whole periodic x-plane
 // ---------------------------------------------------------------------------
 template <bool LINEAR>
-__global__ void __launch_bounds__(kP4Threads, 2) xpass4d_kernel(const Plane4Params p) {
+__global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) xpass4d_kernel(const Plane4Params p) {
   pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
+  P4MARK(0, 0);
   const int4 tk = p.tiles[blockIdx.x];
   const MemberDesc* M = p.mem + tk.x;
   const int v0 = tk.y, nc = tk.z, cs = tk.w, C = 1 << cs;
@@ -385,16 +428,17 @@ __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_kernel(const Plane4Para
   T.set(0, n2 << cs, n1 >> 3, false);
   T.set(1, n1 << cs, n2 >> 3, false);
   T.finish(p.rpt);
+  P4MARK(0, 1);
   cp_async_wait<0>();
   __syncthreads();
+  P4MARK(0, 2);
   const int lane = tid & 31, warp = tid >> 5;
   const int st0 = n2 << cs, wrap0 = n1 * st0, wrap1 = n2 << cs;
   const double ih1 = M->inv_h[0], ih2 = M->inv_h[1], eps = p.eps;
   for (int t = (p.dbg & 1) ? T.ntask : warp; t < T.ntask; t += kP4Threads / 32) {
-    int sw, l, r0, r1;
-    T.decode(t, lane, sw, l, r0, r1);
-    if (l >= T.nlines[sw]) continue;
-    const int m = T.m[sw];
+    int sw, l, r0, r1, nlines, m;
+    T.decode(t, lane, sw, l, r0, r1, nlines, m);
+    if (l >= nlines) continue;
     const int c = l & (C - 1);
     if (sw == 0) {
       const double cf = ca[c];
@@ -417,13 +461,16 @@ __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_kernel(const Plane4Para
                                       cf, eps, ih2, D2 + base + 8 * r * C);
     }
   }
+  P4MARK(0, 3);
   __syncthreads();
+  P4MARK(0, 4);
   // K = (0 - dx1) - dx2 (models.hpp:187-197 order)
   double* kb = p.kbuf + M->offset + v0;
   for (int e = tid; e < NT; e += kP4Threads) {
     const int c = e & (C - 1);
     if (c < nc) kb[(e >> cs) * V + c] = (0.0 - D1[e]) - D2[e];
   }
+  P4MARK(0, 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -451,10 +498,11 @@ __device__ __forceinline__ void vpass_epilogue(int NT, const double* U, const do
 }
 
 template <bool LINEAR>
-__global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Params p) {
+__global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) vpass4d_kernel(const Plane4Params p) {
   pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
+  P4MARK(1, 0);
   const int4 tk = p.tiles[blockIdx.x];
   const MemberDesc* M = p.mem + tk.x;
   const int x0 = tk.y, G = tk.z;
@@ -513,16 +561,17 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
     ce2[tid] = line_coef(p.flux_b, M, 3, p.space_dim, x0 + tid, p.c_b, p.efield);
   }
   __syncthreads();
+  P4MARK(1, 1);
   mbar_wait(&bar[0], 0);
+  P4MARK(1, 2);
   const int lane = tid & 31, warp = tid >> 5;
   {
     const float i3f = 1.0f / (float)n3, i4f = 1.0f / (float)n4;
     const double ih3 = M->inv_h[2], ih4 = M->inv_h[3], eps = p.eps;
     for (int t = (p.dbg & 1) ? T.ntask : warp; t < T.ntask; t += kP4Threads / 32) {
-      int sw, l, r0, r1;
-      T.decode(t, lane, sw, l, r0, r1);
-      if (l >= T.nlines[sw]) continue;
-      const int m = T.m[sw];
+      int sw, l, r0, r1, nlines, m;
+      T.decode(t, lane, sw, l, r0, r1, nlines, m);
+      if (l >= nlines) continue;
       if (sw == 0) {
         const int base = l * n4;
         const double cf = ce2[qdiv(l, i3f)];
@@ -547,8 +596,10 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
       }
     }
   }
+  P4MARK(1, 3);
   mbar_wait(&bar[1], 0);
   __syncthreads();
+  P4MARK(1, 4);
   // epilogue: k = (K - dv1) - dv2, RK stage (timestep.hpp:86-104), output
   const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
   const bool moment = (p.rho_parts != nullptr) && (stage > 0);
@@ -572,6 +623,7 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
     else
       vpass_epilogue<3, false>(NT, U, Kt, UNt, DV1, DV2, out, dt, ex);
   }
+  P4MARK(1, 6);
   if (stage > 0 && ex == 0x7ff00000) {  // non-finite tendency (tendency_finite, timestep.hpp:71-75)
     const unsigned long long code =
         (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)stage;
@@ -597,6 +649,295 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_kernel(const Plane4Para
       if (lane == 0) p.rho_parts[(M->xoff + x0 + gx) * kRhoParts] = hh * acc;
     }
   }
+  P4MARK(1, 5);
+  if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent, software-pipelined v pass (default).  A phase trace of the
+// one-tile-per-CTA form (tools/trace_p4.py) put ~45 % of a CTA's time outside
+// the sweeps: a chain of dependent global loads before the first barrier
+// (tile -> member -> E field, ~4.7 K cycles), the epilogue (~2 K) and the
+// charge-density reduction (~3.5 K).  Here CTAs (two per SM) loop over the
+// tile list and everything a tile needs is fetched one tile ahead: its
+// descriptor (thread 0, stored to a 3-slot ring in shared memory), its u^(s)
+// (bulk copy into the other U slot during the current sweeps), its K / u^n
+// (bulk copies after the current epilogue) and its E-field line coefficients
+// (loaded after the current epilogue).  The epilogue stores w_3 w_4 f of the
+// stage output (trapezoid weights, models.hpp:64-71,240-257) so the charge
+// density is a plain per-plane sum (4 accumulators per lane).
+// smem: [U0 | U1 | K | u^n | dv1 | dv2], each p.vpitch doubles.
+// ---------------------------------------------------------------------------
+struct VInfo {
+  long long gs, ga;  // tile start (doubles) and its 16-byte aligned floor
+  long long xoff;    // member's first x point in the packed x-grid buffers
+  double ih3, ih4, hh;
+  int mi, x0, G, n3, n4, V, NT, shift, nx;
+  unsigned nbytes;
+  __device__ void load(const Plane4Params& p, int t) {
+    const int4 tk = p.tiles[t];
+    const MemberDesc* M = p.mem + tk.x;
+    mi = tk.x;
+    x0 = tk.y;
+    G = tk.z;
+    n3 = M->ext[2];
+    n4 = M->ext[3];
+    V = n3 * n4;
+    NT = G * V;
+    gs = M->offset + (long long)x0 * V;
+    ga = gs & ~1LL;
+    shift = (int)(gs - ga);
+    nbytes = (unsigned)((((gs + NT + 1) & ~1LL) - ga) * 8);
+    xoff = M->xoff;
+    nx = M->nx;
+    ih3 = M->inv_h[2];
+    ih4 = M->inv_h[3];
+    hh = M->h[2] * M->h[3];
+  }
+};
+
+__device__ __forceinline__ void bulk_g2s_noexpect(void* dst, const void* src, unsigned bytes,
+                                                  unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// thread 0: K (and u^n for stages 2, 3) of tile v into the K / u^n slots
+__device__ __forceinline__ void vp_issue_ku(const Plane4Params& p, const VInfo& v, double* Ks,
+                                            double* UNs, unsigned long long* bar) {
+  const bool un = p.stage > 1;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(un ? 2 * v.nbytes : v.nbytes)
+               : "memory");
+  bulk_g2s_noexpect(Ks, p.kbuf + v.ga, v.nbytes, bar);
+  if (un) bulk_g2s_noexpect(UNs, p.un + v.ga, v.nbytes, bar);
+}
+
+// the sweeps of one tile (both directions, all warps); U = the tile's u^(s)
+template <bool LINEAR>
+__device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps, const double* U,
+                                            double* DV1, double* DV2, const double* ce1,
+                                            const double* ce2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = vi->G, n3 = vi->n3, n4 = vi->n4, V = vi->V;
+  P4Sweeps T;
+  T.set(0, G * n3, n4 >> 3, true);
+  T.set(1, G * n4, n3 >> 3, true);
+  T.finish(rpt);
+  const float i3f = 1.0f / (float)n3, i4f = 1.0f / (float)n4;
+  const double ih3 = vi->ih3, ih4 = vi->ih4;
+  for (int q = warp; q < T.ntask; q += kP4Threads / 32) {
+    int sw, l, r0, r1, nlines, m;
+    T.decode(q, lane, sw, l, r0, r1, nlines, m);
+    if (l >= nlines) continue;
+    if (sw == 0) {
+      const int base = l * n4;
+      const double cf = ce2[qdiv(l, i3f)];
+      for (int r = r0; r < r1; ++r)
+        run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, cf, eps, ih4,
+                                 DV2 + base + 8 * r);
+    } else {
+      const int gx = qdiv(l, i4f);
+      const int base = gx * V + (l - gx * n4);
+      const double cf = ce1[gx];
+      for (int r = r0; r < r1; ++r)
+        run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, cf, eps, ih3,
+                                 DV1 + base + 8 * r * n4);
+    }
+  }
+}
+
+// k = (K - dv1) - dv2, RK stage (timestep.hpp:86-104), output; MOMENT: DV1[e] = w3 w4 f
+template <int STAGE, bool MOMENT>
+__device__ __forceinline__ int vp_epilogue(const VInfo* vi, const double* U, const double* Kt,
+                                           const double* UNt, double* DV1, const double* DV2,
+                                           double* out, double dt) {
+  const int NT = vi->NT, V = vi->V, n3 = vi->n3, n4 = vi->n4;
+  const float iVf = 1.0f / (float)V, i4f = 1.0f / (float)n4;
+  int ex = 0;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < NT; e += kP4Threads) {
+    const double kv = (Kt[e] - DV1[e]) - DV2[e];
+    ex = max(ex, __double2hiint(kv) & 0x7ff00000);
+    double o;
+    if (STAGE == 0)
+      o = kv;
+    else if (STAGE == 1)
+      o = fma(dt, kv, U[e]);
+    else if (STAGE == 2)
+      o = fma(0.75, UNt[e], 0.25 * fma(dt, kv, U[e]));
+    else
+      o = fma(1.0 / 3.0, UNt[e], (2.0 / 3.0) * fma(dt, kv, U[e]));
+    out[e] = o;
+    if (MOMENT) {
+      const int g = qdiv(e, iVf), rem = e - g * V, i3 = qdiv(rem, i4f), i4 = rem - i3 * n4;
+      const double w3 = (i3 == 0 || i3 == n3 - 1) ? 0.5 : 1.0;
+      const double w4 = (i4 == 0 || i4 == n4 - 1) ? 0.5 : 1.0;
+      DV1[e] = (w3 * w4) * o;
+    }
+  }
+  return ex;
+}
+
+template <bool LINEAR>
+__global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Plane4Params p) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ unsigned long long bar[3];  // U0, U1, K/u^n
+  __shared__ double ce1[2][kP4MaxG], ce2[2][kP4MaxG];
+  __shared__ VInfo info[3];              // tile `it` uses slot it % 3
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pitch = p.vpitch;
+  double* Ks = sm + 2 * pitch;
+  double* UNs = sm + 3 * pitch;
+  double* DV1 = sm + 4 * pitch;
+  double* DV2 = sm + 5 * pitch;
+  const int stride = gridDim.x, nt = p.ntiles;
+  int t = blockIdx.x;
+  if (t >= nt) return;
+  // static tile data before the dependency wait (overlaps the previous kernel under PDL)
+  if (tid == 0) {
+    info[0].load(p, t);
+    if (t + stride < nt) info[1].load(p, t + stride);
+  }
+  pdl_wait();
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  const int stage = p.stage;
+  const bool moment = (p.rho_parts != nullptr) && (stage > 0);
+  __syncthreads();
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    bulk_g2s(sm, p.uin + info[0].ga, info[0].nbytes, &bar[0]);
+    vp_issue_ku(p, info[0], Ks, UNs, &bar[2]);
+  }
+  if (tid < info[0].G) {  // v_j lines at x point x0+tid: -E_j(x) (VP) or the advection speed
+    const MemberDesc* M = p.mem + info[0].mi;
+    ce1[0][tid] = line_coef(p.flux_a, M, 2, p.space_dim, info[0].x0 + tid, p.c_a, p.efield);
+    ce2[0][tid] = line_coef(p.flux_b, M, 3, p.space_dim, info[0].x0 + tid, p.c_b, p.efield);
+  }
+  const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
+#ifdef SGWG_TRACE
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64(), tn_;
+#define P4PH(k)                 \
+  do {                          \
+    tn_ = clock64();            \
+    ph[k] += tn_ - tc;          \
+    tc = tn_;                   \
+  } while (0)
+#else
+#define P4PH(k) \
+  do {          \
+  } while (0)
+#endif
+  for (int it = 0; t < nt; t += stride, ++it) {
+    // it: local tile counter -- U slot it & 1 (parity (it >> 1) & 1), K/u^n parity it & 1
+    const int b = it & 1;
+    const int t1 = t + stride, t2 = t + 2 * stride;
+    const VInfo* vi = &info[it % 3];
+    // [A]: ce / info of this tile published (and, at it = 0, the mbarriers);
+    // the previous tile is completely done with the other U slot and dv1
+    __syncthreads();
+    P4PH(0);
+    VInfo n2;
+    if (tid == 0) {
+      if (t1 < nt) {
+        const VInfo* v1 = &info[(it + 1) % 3];
+        bulk_g2s(sm + (b ^ 1) * pitch, p.uin + v1->ga, v1->nbytes, &bar[b ^ 1]);
+      }
+      if (t2 < nt) n2.load(p, t2);  // consumed after the sweeps
+    }
+    // the next tile's line coefficients: loads in flight during the sweeps
+    double nce1 = 0.0, nce2 = 0.0;
+    const VInfo* v1 = &info[(it + 1) % 3];
+    const bool ldce = (t1 < nt) && (tid < v1->G);
+    if (ldce) {
+      if (p.flux_a == kFluxKinVP) {  // -E_j(x) (models.hpp:346-349 with the Poisson field)
+        const double* E = p.efield + v1->xoff * p.space_dim + v1->x0 + tid;
+        nce1 = -E[0];
+        nce2 = -E[v1->nx];
+      } else {
+        const MemberDesc* M = p.mem + v1->mi;
+        nce1 = line_coef(p.flux_a, M, 2, p.space_dim, v1->x0 + tid, p.c_a, p.efield);
+        nce2 = line_coef(p.flux_b, M, 3, p.space_dim, v1->x0 + tid, p.c_b, p.efield);
+      }
+    }
+    const double* U = sm + b * pitch + vi->shift;
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    P4PH(1);
+    vp_tile_sweeps<LINEAR>(vi, p.rpt, p.eps, U, DV1, DV2, ce1[b], ce2[b]);
+    P4PH(2);
+    if (ldce) {  // ce[b ^ 1] is not read before barrier A of the next tile
+      ce1[b ^ 1][tid] = nce1;
+      ce2[b ^ 1][tid] = nce2;
+    }
+    mbar_wait(&bar[2], it & 1);
+    P4PH(3);
+    // [B]: dv1 / dv2 complete, K / u^n landed
+    __syncthreads();
+    P4PH(4);
+    if (tid == 0 && t2 < nt) info[(it + 2) % 3] = n2;
+
+    double* out = p.out + vi->gs;
+    const double* Kt = Ks + vi->shift;
+    const double* UNt = UNs + vi->shift;
+    int ex;
+    if (moment) {
+      ex = (stage == 1)   ? vp_epilogue<1, true>(vi, U, Kt, UNt, DV1, DV2, out, dt)
+           : (stage == 2) ? vp_epilogue<2, true>(vi, U, Kt, UNt, DV1, DV2, out, dt)
+                          : vp_epilogue<3, true>(vi, U, Kt, UNt, DV1, DV2, out, dt);
+    } else {
+      ex = (stage == 0)   ? vp_epilogue<0, false>(vi, U, Kt, UNt, DV1, DV2, out, dt)
+           : (stage == 1) ? vp_epilogue<1, false>(vi, U, Kt, UNt, DV1, DV2, out, dt)
+           : (stage == 2) ? vp_epilogue<2, false>(vi, U, Kt, UNt, DV1, DV2, out, dt)
+                          : vp_epilogue<3, false>(vi, U, Kt, UNt, DV1, DV2, out, dt);
+    }
+    if (stage > 0 && ex == 0x7ff00000) {  // non-finite tendency (tendency_finite, timestep.hpp:71-75)
+      const unsigned long long code =
+          (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)stage;
+      atomicMin(p.fail + vi->mi, code);
+    }
+
+    P4PH(5);
+    // [C]: K / u^n slots free, w f of the stage output in dv1
+    __syncthreads();
+    P4PH(6);
+    if (tid == 0 && t1 < nt) vp_issue_ku(p, info[(it + 1) % 3], Ks, UNs, &bar[2]);
+    if (moment) {
+      // charge density of the stage output per x point (moment_density, models.hpp:294-306)
+      const int V = vi->V;
+      for (int gx = warp; gx < vi->G; gx += kP4Threads / 32) {
+        const double* w = DV1 + gx * V;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int e = lane;
+        for (; e + 96 < V; e += 128) {
+          a0 += w[e];
+          a1 += w[e + 32];
+          a2 += w[e + 64];
+          a3 += w[e + 96];
+        }
+        if (e < V) a0 += w[e];
+        if (e + 32 < V) a1 += w[e + 32];
+        if (e + 64 < V) a2 += w[e + 64];
+        double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) p.rho_parts[(vi->xoff + vi->x0 + gx) * kRhoParts] = vi->hh * acc;
+      }
+    }
+    P4PH(7);
+  }
+#ifdef SGWG_TRACE
+  if (tid == 0 && blockIdx.x < kP4TraceCtas)
+    for (int k = 0; k < 8; ++k) sgwg_p4trace[1][blockIdx.x][k] = ph[k];
+  if (tid == 32 && blockIdx.x < kP4TraceCtas)  // warp 1's view of the same phases
+    for (int k = 0; k < 2; ++k) sgwg_p4trace[1][blockIdx.x][8 + k] = ph[2 + k];
+#endif
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
 }
 
@@ -606,6 +947,12 @@ cudaError_t launch_plane4(const Plane4Params& p, int pass, int nblocks, size_t s
   if (pass == 0)
     return p.linear ? launch_k(xpass4d_kernel<true>, dim3(nblocks), dim3(kP4Threads), smem, s, p)
                     : launch_k(xpass4d_kernel<false>, dim3(nblocks), dim3(kP4Threads), smem, s, p);
+  if (p.vpitch > 0) {  // persistent form: nblocks = min(tiles, 2 x SMs) CTAs
+    return p.linear
+               ? launch_k(vpass4d_persist_kernel<true>, dim3(nblocks), dim3(kP4Threads), smem, s, p)
+               : launch_k(vpass4d_persist_kernel<false>, dim3(nblocks), dim3(kP4Threads), smem, s,
+                          p);
+  }
   return p.linear ? launch_k(vpass4d_kernel<true>, dim3(nblocks), dim3(kP4Threads), smem, s, p)
                   : launch_k(vpass4d_kernel<false>, dim3(nblocks), dim3(kP4Threads), smem, s, p);
 }
@@ -613,6 +960,11 @@ cudaError_t launch_plane4(const Plane4Params& p, int pass, int nblocks, size_t s
 cudaError_t configure_plane4() {
   const int maxs = 200 * 1024;
   cudaError_t e;
+  // two ~113 KB CTAs per SM need the full shared-memory carveout
+  cudaFuncSetAttribute(vpass4d_persist_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       100);
+  cudaFuncSetAttribute(vpass4d_persist_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       100);
   if ((e = cudaFuncSetAttribute(xpass4d_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 maxs)) != cudaSuccess)
     return e;
@@ -621,6 +973,12 @@ cudaError_t configure_plane4() {
     return e;
   if ((e = cudaFuncSetAttribute(vpass4d_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 maxs)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(vpass4d_persist_kernel<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, maxs)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(vpass4d_persist_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, maxs)) != cudaSuccess)
     return e;
   return cudaFuncSetAttribute(vpass4d_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               maxs);

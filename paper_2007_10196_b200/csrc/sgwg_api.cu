@@ -141,6 +141,9 @@ struct ProlongPlan {
     int* slot_member = nullptr;
     long long* slot_n = nullptr;
     int* slot_ext = nullptr;
+    long long* item0 = nullptr;  // fast chunked form: first work item of each slot
+    long long nitems = 0;        // 0: generic upsample kernel
+    int nrows0 = 0;              // dimension-0 pass: output rows of the slab
   } dims[kMaxD];
   std::vector<double*> owned;
   // final pass
@@ -204,6 +207,9 @@ struct sgwg_family {
   long long graph_key_policy = -1;
   // prolongation plans
   ProlongPlan* full_plan = nullptr;
+  // row-slab plans of the whole family over slab_arena, by (row_a, row_b): built
+  // once (a plan is ~30 small device tables) and reused by every later combination
+  std::map<std::pair<long long, long long>, ProlongPlan*> slab_plans;
   double* fine_buf = nullptr;
   double* diag_slab = nullptr;     // combined-field slab for diagnostics / snapshots
   long long diag_slab_doubles = 0;
@@ -252,6 +258,7 @@ struct sgwg_family {
   int4* dp4tiles[2] = {nullptr, nullptr};  // whole-plane 4D tiles (plane4d.cuh): x pass, v pass
   int np4tiles[2] = {0, 0};
   int p4smem[2] = {0, 0};                  // dynamic shared memory (doubles) per pass
+  int p4vpitch = 0;                        // > 0: persistent v pass, slot pitch (doubles)
   double* rho_parts = nullptr;      // Vlasov-Poisson charge-density partial sums
   double* twid = nullptr;           // FFT twiddle table (2 x hmax)
   int hmax = 1;
@@ -473,7 +480,14 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
       p.rho_parts = (pass == 1 && vp) ? f->rho_parts : nullptr;
       p.dtp = (pass == 1) ? dtp : nullptr;
       if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
-      CK(fast::launch_plane4(p, pass, f->np4tiles[pass], (size_t)f->p4smem[pass] * sizeof(double),
+      int nblk = f->np4tiles[pass];
+      p.vpitch = 0;
+      p.ntiles = nblk;
+      if (pass == 1 && f->p4vpitch > 0) {
+        p.vpitch = f->p4vpitch;
+        nblk = std::min(nblk, 2 * f->ctx->sm_count);
+      }
+      CK(fast::launch_plane4(p, pass, nblk, (size_t)f->p4smem[pass] * sizeof(double),
                              f->ctx->stream));
       if (timed) {
         CK(cudaEventRecord(f->ev1, f->ctx->stream));
@@ -1322,7 +1336,10 @@ int build_plane4_tiles(sgwg_family* f) {
     if (M.ext[2] < 9 || M.ext[3] < 9 || (M.ext[2] & 7) != 1 || (M.ext[3] & 7) != 1 || V >= 4096)
       return SGWG_OK;
   }
-  int vtarget = 2400;
+  // persistent v pass (SGWG_P4_PERSIST, default on): six tile slots per CTA, two CTAs per SM
+  bool persist = true;
+  if (const char* e = std::getenv("SGWG_P4_PERSIST")) persist = (e[0] != '0');
+  int vtarget = persist ? 2300 : 2400;
   if (const char* e = std::getenv("SGWG_P4_VTARGET")) vtarget = std::max(64, std::atoi(e));
   int xtarget = 4096;
   if (const char* e = std::getenv("SGWG_P4_XTARGET")) xtarget = std::max(128, std::atoi(e));
@@ -1330,7 +1347,7 @@ int build_plane4_tiles(sgwg_family* f) {
   for (int mi = 0; mi < f->nm; ++mi) {
     const MemberDesc& M = f->hmem[mi];
     const int X = M.ext[0] * M.ext[1], V = M.ext[2] * M.ext[3];
-    int cs = 1;
+    int cs = ((X << 1) <= xtarget) ? 1 : 0;
     while (cs < 6 && (X << (cs + 1)) <= xtarget) ++cs;
     const int C = 1 << cs;
     for (int v0 = 0; v0 < V; v0 += C) t[0].push_back(make_int4(mi, v0, std::min(C, V - v0), cs));
@@ -1340,6 +1357,19 @@ int build_plane4_tiles(sgwg_family* f) {
       const int g = std::min(G, X - x0);
       t[1].push_back(make_int4(mi, x0, g, 0));
       f->p4smem[1] = std::max(f->p4smem[1], 5 * ((g * V + 3) & ~1));  // u, K, u^n, dv1, dv2
+    }
+  }
+  f->p4vpitch = 0;
+  if (persist) {
+    int pitch = 0;
+    for (const int4& q : t[1]) {
+      const int V = f->hmem[q.x].ext[2] * f->hmem[q.x].ext[3];
+      pitch = std::max(pitch, (q.z * V + 3) & ~1);
+    }
+    // 6 slots + ~2.5 KB static + 1 KB reserved per CTA, two CTAs in 228 KB
+    if (6LL * pitch * 8 + 2600 <= 115712) {
+      f->p4vpitch = pitch;
+      f->p4smem[1] = 6 * pitch;
     }
   }
   for (int mi = 0; mi < f->nm; ++mi) f->hmem[mi].rparts = 1;
@@ -1437,6 +1467,7 @@ void free_plan(ProlongPlan* pl) {
     cudaFree(dm.slot_member);
     cudaFree(dm.slot_n);
     cudaFree(dm.slot_ext);
+    cudaFree(dm.item0);
   }
   for (double* p : pl->owned) cudaFree(p);
   cudaFree(pl->fsrc);
@@ -1516,10 +1547,24 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long lo
     std::vector<const double*> src;
     std::vector<double*> dst;
     std::vector<int> smember, sext;
-    std::vector<long long> sn;
+    std::vector<long long> sn, item0;
+    long long nitems = 0;
+    bool chunked = (arith_of(f) == SGWG_ARITH_FAST);
     for (size_t s = 0; s < mis.size(); ++s) {
       const MemberDesc& M = f->hmem[mis[s]];
       if (f->nl - M.level[k] == 0) continue;  // interp.hpp:219
+      if (f->nl - M.level[k] > 7) chunked = false;  // kInterpTabMaxM
+      {  // chunked work items: 8-point chunks along k x 32-line blocks
+        long long outer = 1, inner = 1;
+        for (int q = 0; q < d; ++q) {
+          if (q < k) outer *= ext[s][q];
+          if (q > k) inner *= ext[s][q];
+        }
+        const long long nch = (k == 0) ? (((b - 1) >> 3) - (a >> 3) + 1)
+                                       : ((f->fine_ext[k] + 7) / 8);
+        item0.push_back(nitems);
+        nitems += nch * ((outer * inner + 31) / 32);
+      }
       long long n = 1;
       for (int q = 0; q < d; ++q)
         n *= (q == k) ? (k == 0 ? (b - a) : f->fine_ext[k]) : ext[s][q];
@@ -1538,6 +1583,9 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long lo
     auto& dm = pl->dims[k];
     dm.nslots = (int)src.size();
     dm.ntasks = (int)tasks.size();
+    dm.nitems = chunked ? nitems : 0;
+    dm.nrows0 = (int)(b - a);
+    TRY(upload_vec(&dm.item0, item0));
     TRY(upload_vec(&dm.tasks, tasks));
     TRY(upload_vec(&dm.src, src));
     TRY(upload_vec(&dm.dst, dst));
@@ -1589,6 +1637,10 @@ int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, 
     p.mode = mode;
     p.eps = eps;
     p.chunk = kUpsampleChunk;
+    p.slot_item0 = dm.item0;
+    p.nitems = std::getenv("SGWG_UPSAMPLE_GENERIC") ? 0 : dm.nitems;
+    p.nslots = dm.nslots;
+    p.nrows0 = dm.nrows0;
     CK(fast_mode ? fast::launch_upsample(p, dm.ntasks, f->ctx->stream)
                  : exact::launch_upsample(p, dm.ntasks, f->ctx->stream));
     f->stats.combine_launches++;
@@ -1644,6 +1696,8 @@ int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, dou
                       long long a, long long b, double* out, int out_is_device) {
   const long long need = plan_doubles(f, mis, a, b);
   if (f->slab_arena_doubles < need) {
+    for (auto& kv : f->slab_plans) free_plan(kv.second);  // carved from the old arena
+    f->slab_plans.clear();
     cudaFree(f->slab_arena);
     f->slab_arena = nullptr;
     f->slab_arena_doubles = 0;
@@ -1661,7 +1715,15 @@ int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, dou
   }
   double* dst = out_is_device ? out : f->slab_out;
   ProlongPlan* pl = nullptr;
-  TRY(build_plan(f, mis, a, b, f->slab_arena, &pl));
+  const bool cache = ((int)mis.size() == f->nm);
+  if (cache) {
+    auto it = f->slab_plans.find(std::make_pair(a, b));
+    if (it != f->slab_plans.end()) pl = it->second;
+  }
+  if (pl == nullptr) {
+    TRY(build_plan(f, mis, a, b, f->slab_arena, &pl));
+    if (cache) f->slab_plans[std::make_pair(a, b)] = pl;
+  }
   CK(cudaEventRecord(f->ev0, f->ctx->stream));
   int st = run_plan(f, pl, mode, eps, 0, dst);
   if (st == SGWG_OK && f->comm != nullptr && f->nranks > 1) {
@@ -1677,7 +1739,7 @@ int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, dou
     f->stats.combine_ms = ms;
     st = copy_out(f, dst, out, (size_t)nout, out_is_device);
   }
-  free_plan(pl);
+  if (!cache) free_plan(pl);
   return st;
 }
 
@@ -1780,6 +1842,8 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaStreamSynchronize(f->ctx->stream);
   clear_graphs(f);
   free_plan(f->full_plan);
+  for (auto& kv : f->slab_plans) free_plan(kv.second);
+  f->slab_plans.clear();
   if (f->comm) ncclCommDestroy(f->comm);
   for (int k = 0; k < kMaxD; ++k) cudaFree(f->dtasks[k]);
   cudaFree(f->dmax_tasks);

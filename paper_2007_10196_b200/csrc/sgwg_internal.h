@@ -191,6 +191,8 @@ struct Plane4Params {
   const struct DtParams* dtp;
   unsigned int* counter;
   int rpt;                 // runs per warp task (plane4d.cuh P4Sweeps)
+  int vpitch;              // > 0: persistent v pass (vpass4d_persist_kernel), slot pitch in doubles
+  int ntiles;              // v-pass tiles (persistent form)
   int masked;              // 1: one sweep body with runtime ghost masks (default), 0: per-pattern bodies
   int dbg;                 // timing experiments only (SGWG_P4_DBG): 1 no sweeps, 2 no epilogue, 4 no K/u^n copies
 };
@@ -227,6 +229,11 @@ struct UpsampleParams {
   double eps;
   int chunk;
   int jrow0;               // dimension-0 slab: fine index of the first output row
+  // fast chunked form (upsample_fast_kernel): items = (slot, 8-point chunk, 32 lines)
+  const long long* slot_item0;  // first item of each slot (prefix), nslots entries
+  long long nitems;        // 0: the generic kernel
+  int nslots;
+  int nrows0;              // k == 0: output rows of the slab
 };
 
 struct FinalParams {

@@ -1,8 +1,9 @@
 """Fast-build kernels against their reference forms and the oracle:
 
-* the chunked final combination pass (kernels.cuh final_fast_kernel: 8-point
-  chunks, per-centre smoothness indicators, common-denominator weights)
-  against the generic per-point kernel (SGWG_FINAL_GENERIC=1) and the oracle,
+* the chunked combination passes (kernels.cuh upsample_fast_kernel and
+  final_fast_kernel: 8-point chunks, per-centre smoothness indicators,
+  common-denominator weights, tabulated per-offset coefficients) against the
+  generic per-point kernels (SGWG_UPSAMPLE_GENERIC=1, SGWG_FINAL_GENERIC=1) and the oracle,
   both interpolation modes, periodic and zero-ghost last dimensions;
 * overflow guard: states of magnitude ~1e40, where the fast build's
   common-denominator WENO weights overflow but the reference's separate
@@ -43,8 +44,10 @@ def test_final_chunked_matches_generic_and_oracle(ctx_fast, oracle, monkeypatch,
     fam.upload(s)
     got = fam.combine(cfg["interp"], cfg["epsilon"])
     monkeypatch.setenv("SGWG_FINAL_GENERIC", "1")
+    monkeypatch.setenv("SGWG_UPSAMPLE_GENERIC", "1")
     gen = fam.combine(cfg["interp"], cfg["epsilon"])
     monkeypatch.delenv("SGWG_FINAL_GENERIC")
+    monkeypatch.delenv("SGWG_UPSAMPLE_GENERIC")
     dom, _, _ = oracle_objs(cfg)
     want = oracle.combine(dom, s, cfg["interp"], cfg["epsilon"])
     scale = max(1.0, float(np.max(np.abs(want))))
