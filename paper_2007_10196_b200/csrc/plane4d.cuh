@@ -311,6 +311,79 @@ __device__ __forceinline__ void run_masked(int r, int m, const double* P, int st
   adv_run_masked<8, ZERO, LINEAR>(P, st, wrap, gl, gr, c, eps, inv_h, out, st);
 }
 
+// K-output form of a periodic full run (the persistent x pass's second sweep):
+// instead of du into shared memory, K = (0 - d1) - du (models.hpp:187-197
+// order) straight to global memory: d1 = the first sweep's derivative at the
+// run's points (shared memory, stride ost), gout / gst = K at the run's points.
+template <bool LINEAR>
+__device__ __noinline__ void adv_run_kout_ref(const double* __restrict__ P, int st, int wrap, int gl,
+                                              int gr, double c, double eps, double inv_h,
+                                              const double* __restrict__ d1, int ost,
+                                              double* __restrict__ gout, long long gst) {
+  constexpr int RUN = 8, NV = RUN + 6;
+  double f[NV];
+  load_window_masked<RUN, false>(f, P, st, wrap, gl, gr, c);
+  const bool rev = c < 0.0;
+  double Fp = 0.0;
+#pragma unroll
+  for (int t = 0; t <= RUN; ++t) {
+    const int i = t + 2, m = t + 3;
+    const double F = rev ? recon_ref(f[m + 2], f[m + 1], f[m], f[m - 1], f[m - 2], eps, LINEAR)
+                         : recon_ref(f[i - 2], f[i - 1], f[i], f[i + 1], f[i + 2], eps, LINEAR);
+    if (t > 0) gout[(t - 1) * gst] = (0.0 - d1[(t - 1) * ost]) - (F - Fp) * inv_h;
+    Fp = F;
+  }
+}
+
+template <bool LINEAR>
+__device__ __noinline__ void adv_run_kout(const double* __restrict__ P, int st, int wrap, int gl,
+                                          int gr, double c, double eps, double inv_h,
+                                          const double* __restrict__ d1, int ost,
+                                          double* __restrict__ gout, long long gst) {
+  constexpr int RUN = 8, NV = RUN + 6;
+  double f[NV];
+  load_window_masked<RUN, false>(f, P, st, wrap, gl, gr, c);
+  const double eps4 = 4.0 * eps;
+  double D[NV], K[NV], dd[NV];
+#pragma unroll
+  for (int q = 1; q < NV - 1; ++q) {
+    D[q] = fma(-2.0, f[q], f[q - 1] + f[q + 1]);
+    K[q] = fma(13.0 / 3.0 * D[q], D[q], eps4);
+  }
+#pragma unroll
+  for (int q = 1; q < NV; ++q) dd[q] = f[q] - f[q - 1];
+  double du[RUN];
+  double Fp = 0.0;
+  int ex = 0;
+  if (!(c < 0.0)) {
+#pragma unroll
+    for (int t = 0; t <= RUN; ++t) {
+      const int i = t + 2;
+      const double F = recon_roles<LINEAR>(f[i], D[i - 1], D[i], D[i + 1], K[i - 1], K[i],
+                                           K[i + 1], dd[i], dd[i + 1]);
+      if (t > 0) du[t - 1] = (F - Fp) * inv_h;
+      Fp = F;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t <= RUN; ++t) {
+      const int m = t + 3;
+      const double F = recon_roles<LINEAR>(f[m], D[m + 1], D[m], D[m - 1], K[m + 1], K[m],
+                                           K[m - 1], -dd[m + 1], -dd[m]);
+      if (t > 0) du[t - 1] = (F - Fp) * inv_h;
+      Fp = F;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < RUN; ++t) ex = max(ex, __double2hiint(du[t]) & 0x7ff00000);
+  if (ex == 0x7ff00000) {
+    adv_run_kout_ref<LINEAR>(P, st, wrap, gl, gr, c, eps, inv_h, d1, ost, gout, gst);
+    return;
+  }
+#pragma unroll
+  for (int t = 0; t < RUN; ++t) gout[t * gst] = (0.0 - d1[t * ost]) - du[t];
+}
+
 // ---------------------------------------------------------------------------
 // Warp tasks.  A task is 32 consecutive lines of one sweep (one per lane) and
 // a range of <= rpt consecutive runs along them (rpt = 1 by default: equal-cost
@@ -941,12 +1014,137 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent x pass (default; SGWG_P4_PERSIST=0 keeps xpass4d_kernel).  The
+// phase trace of the one-tile-per-CTA form: issue of the strided gather +
+// descriptor chain ~21 % of a CTA's time, the K store loop ~14 %.  Here CTAs
+// (two per SM) loop over the tiles; the gather of tile i+1 (cp.async into the
+// other U slot) is issued right after tile i's first barrier and lands during
+// tile i's sweeps; the x1 sweep writes d/dx1 to shared memory, and the x2
+// sweep, after a barrier, stores K = (0 - d/dx1) - d/dx2 straight to global
+// memory (no d/dx2 array, no separate store phase).
+// smem: [U0 | U1 | d/dx1], each p.xpitch doubles.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void xp_issue_gather(const Plane4Params& p, int t, double* Ub) {
+  const int4 tk = p.tiles[t];
+  const MemberDesc* M = p.mem + tk.x;
+  const int v0 = tk.y, nc = tk.z, cs = tk.w, C = 1 << cs;
+  const int V = M->ext[2] * M->ext[3];
+  const int NT = (M->ext[0] * M->ext[1]) << cs;
+  const double* src = p.uin + M->offset + v0;
+  const int cm = nc - 1;
+  for (int e = threadIdx.x; e < NT; e += kP4Threads) {
+    const int c = e & (C - 1);
+    cp_async8(Ub + e, src + (e >> cs) * V + min(c, cm), c < nc);
+  }
+}
+
+__device__ __forceinline__ void xp_coefs(const Plane4Params& p, int t, double* ca, double* cb) {
+  const int4 tk = p.tiles[t];
+  const MemberDesc* M = p.mem + tk.x;
+  const int v0 = tk.y, nc = tk.z, C = 1 << tk.w, n4 = M->ext[3];
+  const int tid = threadIdx.x;
+  if (tid < C) {  // x_j lines at velocity point vl: coefficient v_j (models.hpp:341-344)
+    const int vl = v0 + min(tid, nc - 1);
+    const int i3 = vl / n4;
+    ca[tid] = line_coef(p.flux_a, M, 0, p.space_dim, i3, p.c_a, p.efield);
+    cb[tid] = line_coef(p.flux_b, M, 1, p.space_dim, vl - i3 * n4, p.c_b, p.efield);
+  }
+}
+
+template <bool LINEAR>
+__global__ void __launch_bounds__(kP4Threads, 2) xpass4d_persist_kernel(const Plane4Params p) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double ca[2][kP4MaxC], cb[2][kP4MaxC];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pitch = p.xpitch;
+  double* D1 = sm + 2 * pitch;
+  const int stride = gridDim.x, nt = p.ntiles;
+  int t = blockIdx.x;
+  if (t >= nt) return;
+  xp_coefs(p, t, ca[0], cb[0]);  // static (x coordinates / advection speeds)
+  pdl_wait();
+  const StepCtl* ctl = p.ctl;
+  if (ctl != nullptr && !ctl->active) return;
+  xp_issue_gather(p, t, sm);
+  cp_async_commit();
+  const double eps = p.eps;
+  for (int it = 0; t < nt; t += stride, ++it) {
+    const int b = it & 1;
+    const int t1 = t + stride;
+    cp_async_wait<0>();
+    // [A]: this tile's u (every thread's copies) and coefficients visible; the
+    // previous tile's x2 sweep is done with the other U slot and d/dx1
+    __syncthreads();
+    if (t1 < nt && !(p.dbg & 8)) {
+      xp_issue_gather(p, t1, sm + (b ^ 1) * pitch);
+      xp_coefs(p, t1, ca[b ^ 1], cb[b ^ 1]);
+    }
+    if (!(p.dbg & 8)) cp_async_commit();
+    const int4 tk = p.tiles[t];
+    const MemberDesc* M = p.mem + tk.x;
+    const int v0 = tk.y, cs = tk.w, C = 1 << cs, nc = tk.z;
+    const int n1 = M->ext[0], n2 = M->ext[1];
+    const int V = M->ext[2] * M->ext[3];
+    const double* U = sm + b * pitch;
+    const double* cfa = ca[b];
+    const double* cfb = cb[b];
+    const int st0 = n2 << cs, wrap0 = n1 * st0, wrap1 = n2 << cs;
+    // x1 sweep: lines (x2, c) = l, stride n2 C, n1 points -> d/dx1
+    {
+      const double ih1 = M->inv_h[0];
+      const int nl = n2 << cs, m = n1 >> 3, nb = (nl + 31) >> 5, ntask = nb * m;
+      const float inb = 1.0f / (float)nb;
+      for (int q = warp; q < ntask; q += kP4Threads / 32) {
+        const int r = qdiv(q, inb), l = ((q - r * nb) << 5) + lane;
+        if (l >= nl) continue;
+        run_masked<false, LINEAR>(r, m, U + l + (8 * r - 3) * st0, st0, wrap0, cfa[l & (C - 1)],
+                                  eps, ih1, D1 + l + 8 * r * st0);
+      }
+    }
+    // [B]: d/dx1 complete
+    __syncthreads();
+    if (p.dbg & 8) {  // experiment: gather of the next tile issued after the x1 sweep
+      if (t1 < nt) {
+        xp_issue_gather(p, t1, sm + (b ^ 1) * pitch);
+        xp_coefs(p, t1, ca[b ^ 1], cb[b ^ 1]);
+      }
+      cp_async_commit();
+    }
+    // x2 sweep: lines (x1, c), stride C, n2 points -> K to global
+    {
+      const double ih2 = M->inv_h[1];
+      const int nl = n1 << cs, m = n2 >> 3, nb = (nl + 31) >> 5, ntask = nb * m;
+      const float inb = 1.0f / (float)nb;
+      double* kb = p.kbuf + M->offset + v0;
+      for (int q = warp; q < ntask; q += kP4Threads / 32) {
+        const int r = qdiv(q, inb), l = ((q - r * nb) << 5) + lane;
+        if (l >= nl) continue;
+        const int c = l & (C - 1), x1 = l >> cs;
+        if (c >= nc) continue;  // padded velocity point of a partial tile
+        const int base = x1 * wrap1 + c;
+        const int gl = (r == 0) ? 3 : 0, gr = (r == m - 1) ? 3 : 0;
+        adv_run_kout<LINEAR>(U + base + (8 * r - 3) * C, C, wrap1, gl, gr, cfb[c], eps, ih2,
+                             D1 + base + 8 * r * C, C,
+                             kb + ((long long)x1 * n2 + 8 * r) * V + c, V);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 cudaError_t launch_plane4(const Plane4Params& p, int pass, int nblocks, size_t smem,
                           cudaStream_t s) {
   if (nblocks <= 0) return cudaSuccess;
-  if (pass == 0)
+  if (pass == 0) {
+    if (p.xpitch > 0)
+      return p.linear
+                 ? launch_k(xpass4d_persist_kernel<true>, dim3(nblocks), dim3(kP4Threads), smem, s, p)
+                 : launch_k(xpass4d_persist_kernel<false>, dim3(nblocks), dim3(kP4Threads), smem, s,
+                            p);
     return p.linear ? launch_k(xpass4d_kernel<true>, dim3(nblocks), dim3(kP4Threads), smem, s, p)
                     : launch_k(xpass4d_kernel<false>, dim3(nblocks), dim3(kP4Threads), smem, s, p);
+  }
   if (p.vpitch > 0) {  // persistent form: nblocks = min(tiles, 2 x SMs) CTAs
     return p.linear
                ? launch_k(vpass4d_persist_kernel<true>, dim3(nblocks), dim3(kP4Threads), smem, s, p)
@@ -960,6 +1158,14 @@ cudaError_t launch_plane4(const Plane4Params& p, int pass, int nblocks, size_t s
 cudaError_t configure_plane4() {
   const int maxs = 200 * 1024;
   cudaError_t e;
+  cudaFuncSetAttribute(xpass4d_persist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       maxs);
+  cudaFuncSetAttribute(xpass4d_persist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       maxs);
+  cudaFuncSetAttribute(xpass4d_persist_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       100);
+  cudaFuncSetAttribute(xpass4d_persist_kernel<false>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   // two ~113 KB CTAs per SM need the full shared-memory carveout
   cudaFuncSetAttribute(vpass4d_persist_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        100);

@@ -259,6 +259,7 @@ struct sgwg_family {
   int np4tiles[2] = {0, 0};
   int p4smem[2] = {0, 0};                  // dynamic shared memory (doubles) per pass
   int p4vpitch = 0;                        // > 0: persistent v pass, slot pitch (doubles)
+  int p4xpitch = 0;                        // > 0: persistent x pass, slot pitch (doubles)
   double* rho_parts = nullptr;      // Vlasov-Poisson charge-density partial sums
   double* twid = nullptr;           // FFT twiddle table (2 x hmax)
   int hmax = 1;
@@ -482,9 +483,14 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
       if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
       int nblk = f->np4tiles[pass];
       p.vpitch = 0;
+      p.xpitch = 0;
       p.ntiles = nblk;
       if (pass == 1 && f->p4vpitch > 0) {
         p.vpitch = f->p4vpitch;
+        nblk = std::min(nblk, 2 * f->ctx->sm_count);
+      }
+      if (pass == 0 && f->p4xpitch > 0) {
+        p.xpitch = f->p4xpitch;
         nblk = std::min(nblk, 2 * f->ctx->sm_count);
       }
       CK(fast::launch_plane4(p, pass, nblk, (size_t)f->p4smem[pass] * sizeof(double),
@@ -1360,7 +1366,19 @@ int build_plane4_tiles(sgwg_family* f) {
     }
   }
   f->p4vpitch = 0;
+  f->p4xpitch = 0;
   if (persist) {
+    int xp = 0;
+    for (const int4& q : t[0]) xp = std::max(xp, (f->hmem[q.x].ext[0] * f->hmem[q.x].ext[1]) << q.w);
+    xp = (xp + 1) & ~1;
+    // U0, U1, d/dx1 + ~1.2 KB static + 1 KB reserved per CTA, two CTAs in 228 KB.
+    // Opt-in (SGWG_P4_XPERSIST=1): measured slower than the one-tile-per-CTA x pass
+    // on C5 (150 vs 138 us per launch), unlike the v pass (209 vs 218 us)
+    const char* xe = std::getenv("SGWG_P4_XPERSIST");
+    if (xe != nullptr && xe[0] == '1' && 3LL * xp * 8 + 1300 <= 115712) {
+      f->p4xpitch = xp;
+      f->p4smem[0] = 3 * xp;
+    }
     int pitch = 0;
     for (const int4& q : t[1]) {
       const int V = f->hmem[q.x].ext[2] * f->hmem[q.x].ext[3];

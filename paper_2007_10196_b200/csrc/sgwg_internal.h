@@ -191,6 +191,7 @@ struct Plane4Params {
   const struct DtParams* dtp;
   unsigned int* counter;
   int rpt;                 // runs per warp task (plane4d.cuh P4Sweeps)
+  int xpitch;              // > 0: persistent x pass (xpass4d_persist_kernel), slot pitch in doubles
   int vpitch;              // > 0: persistent v pass (vpass4d_persist_kernel), slot pitch in doubles
   int ntiles;              // v-pass tiles (persistent form)
   int masked;              // 1: one sweep body with runtime ghost masks (default), 0: per-pattern bodies
