@@ -2466,6 +2466,9 @@ __global__ void __launch_bounds__(256, SGWG_FINAL_MINB) final_fast_kernel(const 
         continue;
       }
       const int n_src = p.msrc_ext[mi];
+      SGWG_DCHECK(m >= 1 && m <= kInterpTabMaxM && ((n_src - (p.bc_last != 0 ? 1 : 0)) << m) ==
+                                                        p.fine_last - (p.bc_last != 0 ? 1 : 0),
+                  "final pass refinement");
       interp_chunk<MODE>(m, 8 * c, min(8, p.fine_last - 8 * c), p.src[mi] + row * n_src, 1, n_src,
                          p.bc_last, cf, p.eps, acc);
     }
@@ -2525,6 +2528,9 @@ __global__ void __launch_bounds__(256) upsample_fast_kernel(const UpsampleParams
     const long long o = line / inner, i = line - o * inner;
     const double* src = p.src[slot] + o * (long long)n_src * inner + i;
     double* dst = p.dst[slot] + (o * (long long)ndst - jlo) * inner + i;
+    SGWG_DCHECK(m >= 1 && m <= kInterpTabMaxM && j0 + 8 > jlo && j0 < jlo + ndst,
+                "upsample chunk outside the slab");
+    SGWG_DCHECK((o + 1) * (long long)ndst * inner <= p.slot_n[slot], "upsample dst slot");
     double acc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = 0.0;

@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) xpass4d_kernel(const
   double* U = sm;
   double* D1 = sm + NT;  // d/dx1
   double* D2 = D1 + NT;  // d/dx2
+  SGWG_DCHECK(v0 + nc <= V && nc <= C && C <= kP4MaxC, "xpass tile velocity range");
   __shared__ double ca[kP4MaxC], cb[kP4MaxC];
   const int tid = threadIdx.x;
   {
@@ -808,6 +809,7 @@ __device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps
     if (l >= nlines) continue;
     if (sw == 0) {
       const int base = l * n4;
+      SGWG_DCHECK(qdiv(l, i3f) == l / n3 && base + 8 * (r1 - 1) < G * V, "vpass row run");
       const double cf = ce2[qdiv(l, i3f)];
       for (int r = r0; r < r1; ++r)
         run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, cf, eps, ih4,
@@ -815,6 +817,7 @@ __device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps
     } else {
       const int gx = qdiv(l, i4f);
       const int base = gx * V + (l - gx * n4);
+      SGWG_DCHECK(gx == l / n4 && gx < G && base + 8 * (r1 - 1) * n4 < G * V, "vpass column run");
       const double cf = ce1[gx];
       for (int r = r0; r < r1; ++r)
         run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, cf, eps, ih3,
@@ -941,6 +944,11 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
       }
     }
     const double* U = sm + b * pitch + vi->shift;
+    SGWG_DCHECK(vi->shift + vi->NT <= pitch && (long long)vi->nbytes <= 8LL * pitch,
+                "vpass tile exceeds its shared-memory slot");
+    SGWG_DCHECK(vi->gs + vi->NT <= p.mem[vi->mi].offset + p.mem[vi->mi].npts,
+                "vpass tile exceeds its member");
+    SGWG_DCHECK(vi->G <= kP4MaxG, "vpass tile has too many x points");
     mbar_wait(&bar[b], (it >> 1) & 1);
     P4PH(1);
     vp_tile_sweeps<LINEAR>(vi, p.rpt, p.eps, U, DV1, DV2, ce1[b], ce2[b]);

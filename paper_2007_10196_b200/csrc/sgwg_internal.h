@@ -6,6 +6,7 @@
 // member row-major with dimension 0 slowest (grid.hpp:102-108).  Three such
 // buffers (u^n, stage A, stage B) plus one tendency buffer K hold a step.
 #pragma once
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,6 +28,23 @@ enum FluxKind : int {
 };
 
 // One component grid on the device (GridGeometry, grid.hpp:85-136).
+// Device-side invariant checks of the experiment build -DSGWG_CHECK (compute-sanitizer is not
+// available on the GPU pool): a failed check prints its tag and traps.
+#ifdef SGWG_CHECK
+#define SGWG_DCHECK(cond, tag)                                                          \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("SGWG_DCHECK failed: %s (block %d thread %d)\n", tag, (int)blockIdx.x,     \
+             (int)threadIdx.x);                                                         \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define SGWG_DCHECK(cond, tag) \
+  do {                         \
+  } while (0)
+#endif
+
 struct MemberDesc {
   long long offset;        // first point in the packed state buffers
   long long npts;
