@@ -221,6 +221,16 @@ int sgwg_combine(sgwg_family* fam, int interp_mode, double eps, double* out, siz
  * (BASELINE C5: 4.3e9 points) and how a sharded output is produced. */
 int sgwg_combine_rows(sgwg_family* fam, int interp_mode, double eps, long long row_begin,
                       long long row_end, double* out, size_t n, int out_is_device);
+/* This rank's share of the combination, the result left sharded (option B for a
+ * family with a multi-rank communicator): every rank gathers all member
+ * states (NCCL broadcasts of the shards) and combines ITS dimension-0 rows
+ * [*row_begin, *row_end) -- rows * rank / nranks .. rows * (rank + 1) / nranks -- for
+ * every member in family order, so the rows are bitwise those of the one-GPU
+ * combine(set, mode, eps) (combine.hpp:95-122).  Without a communicator: all rows.
+ * out == NULL only reports the row range; else n = (row_end - row_begin) x points per
+ * dimension-0 row.  Collective over the communicator. */
+int sgwg_combine_local(sgwg_family* fam, int interp_mode, double eps, double* out, size_t n,
+                       int out_is_device, long long* row_begin, long long* row_end);
 /* prolong (interp.hpp:197-250) of one local member onto the finest grid. */
 int sgwg_prolong(sgwg_family* fam, int mi, int interp_mode, double eps, double* out, size_t n,
                  int out_is_device);

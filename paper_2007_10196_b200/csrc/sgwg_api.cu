@@ -210,6 +210,15 @@ struct sgwg_family {
   // row-slab plans of the whole family over slab_arena, by (row_a, row_b): built
   // once (a plan is ~30 small device tables) and reused by every later combination
   std::map<std::pair<long long, long long>, ProlongPlan*> slab_plans;
+  // option B for sharded families (gather_view): every member's state on every rank,
+  // combined in dimension-0 row slabs split over the ranks
+  std::vector<int> gsel;                   // global member index of each local member
+  bool gview = false;
+  std::vector<MemberDesc> ghmem;           // all members in family order, offsets into gu
+  MemberDesc* gdmem = nullptr;
+  double* gu = nullptr;
+  std::vector<long long> grank_off, grank_cnt;  // per-rank block of gu (doubles)
+  std::map<std::pair<long long, long long>, ProlongPlan*> gslab_plans;
   double* fine_buf = nullptr;
   double* diag_slab = nullptr;     // combined-field slab for diagnostics / snapshots
   long long diag_slab_doubles = 0;
@@ -980,6 +989,34 @@ int check_domain(const sgwg_domain* dom) {
   return SGWG_OK;
 }
 
+// geometry of the component grid at levels lv (GridGeometry::make, grid.hpp:110-133),
+// its state at `off` in a packed buffer
+MemberDesc geom_desc(const sgwg_domain* dom, const std::array<int, 4>& lv, long long off) {
+  const int d = dom->d;
+  MemberDesc M{};
+  M.offset = off;
+  M.npts = 1;
+  for (int k = 0; k < kMaxD; ++k) {
+    M.ext[k] = 1;
+    M.h[k] = 1.0;
+    M.inv_h[k] = 1.0;
+  }
+  for (int k = 0; k < d; ++k) {
+    const int cells = dom->root_cells[k] << lv[k];
+    M.ext[k] = cells + (dom->bc[k] == SGWG_ZERO ? 1 : 0);
+    M.bc[k] = dom->bc[k];
+    M.level[k] = lv[k];
+    M.h[k] = std::ldexp((dom->upper[k] - dom->lower[k]) / dom->root_cells[k], -lv[k]);
+    M.inv_h[k] = 1.0 / M.h[k];
+    M.lower[k] = dom->lower[k];
+    M.npts *= M.ext[k];
+  }
+  M.stride[d - 1] = 1;
+  for (int k = d - 2; k >= 0; --k) M.stride[k] = M.stride[k + 1] * M.ext[k + 1];
+  for (int k = d; k < kMaxD; ++k) M.stride[k] = 1;
+  return M;
+}
+
 int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int count,
                   sgwg_family** out, bool single = false) {
   if (ctx == nullptr || out == nullptr) return fail_with(SGWG_EINVAL, "null argument");
@@ -1027,28 +1064,8 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   for (int k = 0; k < d; ++k) f->finest *= f->fine_ext[k];
   long long off = 0;
   for (int gi : sel) {
-    MemberDesc M{};
     const auto& lv = all[gi];
-    M.offset = off;
-    M.npts = 1;
-    for (int k = 0; k < kMaxD; ++k) {
-      M.ext[k] = 1;
-      M.h[k] = 1.0;
-      M.inv_h[k] = 1.0;
-    }
-    for (int k = 0; k < d; ++k) {  // GridGeometry::make (grid.hpp:110-133)
-      const int cells = dom->root_cells[k] << lv[k];
-      M.ext[k] = cells + (dom->bc[k] == SGWG_ZERO ? 1 : 0);
-      M.bc[k] = dom->bc[k];
-      M.level[k] = lv[k];
-      M.h[k] = std::ldexp((dom->upper[k] - dom->lower[k]) / dom->root_cells[k], -lv[k]);
-      M.inv_h[k] = 1.0 / M.h[k];
-      M.lower[k] = dom->lower[k];
-      M.npts *= M.ext[k];
-    }
-    M.stride[d - 1] = 1;
-    for (int k = d - 2; k >= 0; --k) M.stride[k] = M.stride[k + 1] * M.ext[k + 1];
-    for (int k = d; k < kMaxD; ++k) M.stride[k] = 1;
+    const MemberDesc M = geom_desc(dom, lv, off);
     f->hmem.push_back(M);
     f->gidx.push_back(gi);
     f->levels.push_back(lv);
@@ -1504,12 +1521,126 @@ int upload_vec(T** dptr, const std::vector<T>& v) {
 
 constexpr int kUpsampleChunk = 2048;
 
+// ---------------------------------------------------------------------------
+// Option B for sharded families: prolongation is dimension-
+// sequential with dimension 0 first (interp.hpp:217-244), so the finest grid
+// splits into independent dimension-0 row slabs.  Every rank gathers all
+// member states (C5: 96.5 MB) and combines ITS rows for every member, in
+// family order -- bitwise the single-GPU result, no all-reduce of the finest
+// grid (C5: 34.6 GB).  Used by sgwg_combined_stats (5 doubles reduced across
+// ranks), sgwg_eval_points (every rank evaluates all points) and
+// sgwg_combine_local (this rank's rows, the result left sharded); forced for a
+// one-rank communicator by SGWG_OPTION_B=1, disabled by SGWG_COMBINE_ALLREDUCE=1.
+// ---------------------------------------------------------------------------
+bool use_option_b(const sgwg_family* f) {
+  if (f->comm == nullptr || f->single || f->state_total != f->total || f->d < 2) return false;
+  if (std::getenv("SGWG_COMBINE_ALLREDUCE") != nullptr) return false;
+  if (f->nranks > 1) return true;
+  const char* e = std::getenv("SGWG_OPTION_B");
+  return e != nullptr && e[0] == '1';
+}
+
+// rows [a, b) of dimension 0 that rank r combines
+void option_b_rows(const sgwg_family* f, int r, long long* a, long long* b) {
+  const long long rows = f->fine_ext[0];
+  *a = rows * r / f->nranks;
+  *b = rows * (r + 1) / f->nranks;
+}
+
+// the layout of the gathered states (once per family): owners from an NCCL
+// all-gather of ownership flags; rank r's block holds its members in family
+// order, exactly its local state buffer
+int build_gathered_view(sgwg_family* f) {
+  if (f->gview) return SGWG_OK;
+  const int nfull = f->nfull, R = f->nranks;
+  cudaStream_t s = f->ctx->stream;
+  std::vector<int> own(nfull, 0), all((size_t)nfull * R, 0);
+  for (int g : f->gidx) own[g] = 1;
+  int *down = nullptr, *dall = nullptr;
+  CK(cudaMalloc(&down, sizeof(int) * nfull));
+  CK(cudaMalloc(&dall, sizeof(int) * nfull * R));
+  CK(cudaMemcpyAsync(down, own.data(), sizeof(int) * nfull, cudaMemcpyHostToDevice, s));
+  ncclResult_t nr = ncclAllGather(down, dall, nfull, ncclInt32, f->comm, s);
+  if (nr == ncclSuccess) {
+    CK(cudaMemcpyAsync(all.data(), dall, sizeof(int) * nfull * R, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  cudaFree(down);
+  cudaFree(dall);
+  if (nr != ncclSuccess) return fail_with(SGWG_ENCCL, ncclGetErrorString(nr));
+  const auto levels = enumerate_levels(f->d, f->nl);
+  std::vector<int> owner(nfull, -1);
+  for (int g = 0; g < nfull; ++g)
+    for (int r = 0; r < R; ++r)
+      if (all[(size_t)r * nfull + g]) {
+        if (owner[g] >= 0) return fail_with(SGWG_EINVAL, "shards overlap: a member on two ranks");
+        owner[g] = r;
+      }
+  for (int g = 0; g < nfull; ++g)
+    if (owner[g] < 0) return fail_with(SGWG_EINVAL, "shards do not cover the family");
+  f->grank_cnt.assign(R, 0);
+  f->ghmem.clear();
+  std::vector<long long> local(nfull);
+  for (int g = 0; g < nfull; ++g) {
+    f->ghmem.push_back(geom_desc(&f->dom, levels[g], 0));
+    local[g] = f->grank_cnt[owner[g]];
+    f->grank_cnt[owner[g]] += f->ghmem.back().npts;
+  }
+  f->grank_off.assign(R, 0);
+  for (int r = 1; r < R; ++r) f->grank_off[r] = f->grank_off[r - 1] + f->grank_cnt[r - 1];
+  const long long total = f->grank_off[R - 1] + f->grank_cnt[R - 1];
+  for (int g = 0; g < nfull; ++g) f->ghmem[g].offset = f->grank_off[owner[g]] + local[g];
+  if (f->grank_cnt[f->rank] != f->total)
+    return fail_with(SGWG_EINVAL, "gathered view: this rank's block differs from its states");
+  CK(cudaMalloc(&f->gu, sizeof(double) * std::max(1LL, total)));
+  TRY(upload_vec(&f->gdmem, f->ghmem));
+  f->gview = true;
+  return SGWG_OK;
+}
+
+// every rank's member states into gu (grouped broadcasts: blocks differ in size)
+int gather_states(sgwg_family* f) {
+  TRY(build_gathered_view(f));
+  cudaStream_t s = f->ctx->stream;
+  CKN(ncclGroupStart());
+  for (int r = 0; r < f->nranks; ++r) {
+    double* dst = f->gu + f->grank_off[r];
+    const void* src = (r == f->rank) ? (const void*)f->u : (const void*)dst;
+    ncclResult_t nr = ncclBroadcast(src, dst, (size_t)f->grank_cnt[r], ncclDouble, r, f->comm, s);
+    if (nr != ncclSuccess) {
+      ncclGroupEnd();
+      return fail_with(SGWG_ENCCL, ncclGetErrorString(nr));
+    }
+  }
+  CKN(ncclGroupEnd());
+  return SGWG_OK;
+}
+
 // doubles of intermediate storage a plan for fine rows [a, b) of dimension 0 needs
-long long plan_doubles(const sgwg_family* f, const std::vector<int>& mis, long long a, long long b) {
+// The members a combination reads: the family's own (local) members, or -- for a
+// sharded family combined by row slabs (option B) -- every member of the family,
+// gathered from all ranks (gview).  partial: the sum covers only this rank's
+// members (all-reduced across ranks afterwards).
+struct CombView {
+  const std::vector<MemberDesc>* hmem;
+  const MemberDesc* dmem;
+  const double* u;
+  std::map<std::pair<long long, long long>, ProlongPlan*>* cache;
+  bool partial;
+};
+CombView local_view(sgwg_family* f) {
+  return CombView{&f->hmem, f->dmem, f->u, &f->slab_plans, true};
+}
+CombView gathered_view(sgwg_family* f) {
+  return CombView{&f->ghmem, f->gdmem, f->gu, &f->gslab_plans, false};
+}
+
+long long plan_doubles(const sgwg_family* f, const CombView& v, const std::vector<int>& mis,
+                       long long a, long long b) {
   const int d = f->d;
   long long tot = 0;
   for (int mi : mis) {
-    const MemberDesc& M = f->hmem[mi];
+    const MemberDesc& M = (*v.hmem)[mi];
     long long ext[4];
     for (int q = 0; q < 4; ++q) ext[q] = (q < d) ? M.ext[q] : 1;
     for (int k = 0; k + 1 < d; ++k) {
@@ -1525,6 +1656,9 @@ long long plan_doubles(const sgwg_family* f, const std::vector<int>& mis, long l
   }
   return tot;
 }
+long long plan_doubles(sgwg_family* f, const std::vector<int>& mis, long long a, long long b) {
+  return plan_doubles(f, local_view(f), mis, a, b);
+}
 
 // Prolongation plan of members `mis` restricted to fine rows [a, b) of
 // dimension 0 (the whole grid for a = 0, b = fine_ext[0]).  Prolongation is
@@ -1532,14 +1666,14 @@ long long plan_doubles(const sgwg_family* f, const std::vector<int>& mis, long l
 // the dimension-0 sweep every row of the finest grid is independent: a slab
 // of rows needs only its own rows of the intermediates.  Intermediates are
 // carved from `arena` (or one owned allocation when arena is null).
-int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long long b,
-               double* arena, ProlongPlan** out) {
+int build_plan(sgwg_family* f, const CombView& v, const std::vector<int>& mis, long long a,
+               long long b, double* arena, ProlongPlan** out) {
   ProlongPlan* pl = new ProlongPlan();
   const int d = f->d;
   std::vector<long long> coefs(d);
   for (int j = 0; j < d; ++j) coefs[j] = (j % 2 == 0 ? 1 : -1) * binomial(d - 1, j);
   if (arena == nullptr) {
-    const long long nd = plan_doubles(f, mis, a, b);
+    const long long nd = plan_doubles(f, v, mis, a, b);
     if (nd > 0) {
       CK(cudaMalloc(&arena, sizeof(double) * nd));
       pl->owned.push_back(arena);
@@ -1552,8 +1686,8 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long lo
   std::vector<const double*> cur(mis.size());
   std::vector<std::array<int, 4>> ext(mis.size());
   for (size_t s = 0; s < mis.size(); ++s) {
-    const MemberDesc& M = f->hmem[mis[s]];
-    cur[s] = f->u + M.offset;
+    const MemberDesc& M = (*v.hmem)[mis[s]];
+    cur[s] = v.u + M.offset;
     for (int q = 0; q < 4; ++q) ext[s][q] = (q < d) ? M.ext[q] : 1;
     if (d > 1 && f->nl - M.level[0] == 0) {  // dimension 0 already finest: row view
       cur[s] += a * (M.npts / M.ext[0]);
@@ -1569,7 +1703,7 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long lo
     long long nitems = 0;
     bool chunked = (arith_of(f) == SGWG_ARITH_FAST);
     for (size_t s = 0; s < mis.size(); ++s) {
-      const MemberDesc& M = f->hmem[mis[s]];
+      const MemberDesc& M = (*v.hmem)[mis[s]];
       if (f->nl - M.level[k] == 0) continue;  // interp.hpp:219
       if (f->nl - M.level[k] > 7) chunked = false;  // kInterpTabMaxM
       {  // chunked work items: 8-point chunks along k x 32-line blocks
@@ -1615,7 +1749,7 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long lo
   std::vector<double> fcoef;
   std::vector<int> fext, fref;
   for (size_t s = 0; s < mis.size(); ++s) {
-    const MemberDesc& M = f->hmem[mis[s]];
+    const MemberDesc& M = (*v.hmem)[mis[s]];
     int lsum = 0;
     for (int q = 0; q < d; ++q) lsum += M.level[q];
     fsrc.push_back(cur[s]);
@@ -1633,7 +1767,13 @@ int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long lo
   return SGWG_OK;
 }
 
-int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, double* out) {
+int build_plan(sgwg_family* f, const std::vector<int>& mis, long long a, long long b,
+               double* arena, ProlongPlan** out) {
+  return build_plan(f, local_view(f), mis, a, b, arena, out);
+}
+
+int run_plan(sgwg_family* f, const CombView& v, ProlongPlan* pl, int mode, double eps, int assign,
+             double* out) {
   const int d = f->d;
   const bool fast_mode = arith_of(f) == SGWG_ARITH_FAST;
   for (int k = 0; k + 1 < d; ++k) {
@@ -1641,7 +1781,7 @@ int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, 
     if (dm.ntasks == 0) continue;
     UpsampleParams p{};
     p.jrow0 = (k == 0) ? (int)pl->row_a : 0;
-    p.mem = f->dmem;
+    p.mem = v.dmem;
     p.tasks = dm.tasks;
     p.src = dm.src;
     p.dst = dm.dst;
@@ -1664,7 +1804,7 @@ int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, 
     f->stats.combine_launches++;
   }
   FinalParams fp{};
-  fp.mem = f->dmem;
+  fp.mem = v.dmem;
   fp.src = pl->fsrc;
   fp.coef = pl->fcoef;
   fp.msrc_ext = pl->fext;
@@ -1691,6 +1831,10 @@ int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, 
   return SGWG_OK;
 }
 
+int run_plan(sgwg_family* f, ProlongPlan* pl, int mode, double eps, int assign, double* out) {
+  return run_plan(f, local_view(f), pl, mode, eps, assign, out);
+}
+
 int copy_out(sgwg_family* f, const double* dev, double* out, size_t n, int out_is_device) {
   if (out_is_device) {
     if (out != dev)
@@ -1710,12 +1854,14 @@ long long combine_budget_doubles() {
 }
 
 // combination of fine rows [a, b) of dimension 0 into out (host or device)
-int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, double eps,
-                      long long a, long long b, double* out, int out_is_device) {
-  const long long need = plan_doubles(f, mis, a, b);
+int combine_rows_impl(sgwg_family* f, const CombView& v, const std::vector<int>& mis, int mode,
+                      double eps, long long a, long long b, double* out, int out_is_device) {
+  const long long need = plan_doubles(f, v, mis, a, b);
   if (f->slab_arena_doubles < need) {
-    for (auto& kv : f->slab_plans) free_plan(kv.second);  // carved from the old arena
-    f->slab_plans.clear();
+    for (auto* c : {&f->slab_plans, &f->gslab_plans}) {  // carved from the old arena
+      for (auto& kv : *c) free_plan(kv.second);
+      c->clear();
+    }
     cudaFree(f->slab_arena);
     f->slab_arena = nullptr;
     f->slab_arena_doubles = 0;
@@ -1733,18 +1879,18 @@ int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, dou
   }
   double* dst = out_is_device ? out : f->slab_out;
   ProlongPlan* pl = nullptr;
-  const bool cache = ((int)mis.size() == f->nm);
+  const bool cache = ((int)mis.size() == (int)v.hmem->size());
   if (cache) {
-    auto it = f->slab_plans.find(std::make_pair(a, b));
-    if (it != f->slab_plans.end()) pl = it->second;
+    auto it = v.cache->find(std::make_pair(a, b));
+    if (it != v.cache->end()) pl = it->second;
   }
   if (pl == nullptr) {
-    TRY(build_plan(f, mis, a, b, f->slab_arena, &pl));
-    if (cache) f->slab_plans[std::make_pair(a, b)] = pl;
+    TRY(build_plan(f, v, mis, a, b, f->slab_arena, &pl));
+    if (cache) (*v.cache)[std::make_pair(a, b)] = pl;
   }
   CK(cudaEventRecord(f->ev0, f->ctx->stream));
-  int st = run_plan(f, pl, mode, eps, 0, dst);
-  if (st == SGWG_OK && f->comm != nullptr && f->nranks > 1) {
+  int st = run_plan(f, v, pl, mode, eps, 0, dst);
+  if (st == SGWG_OK && v.partial && f->comm != nullptr && f->nranks > 1) {
     ncclResult_t r = ncclAllReduce(dst, dst, (size_t)nout, ncclDouble, ncclSum, f->comm,
                                    f->ctx->stream);
     if (r != ncclSuccess) st = fail_with(SGWG_ENCCL, ncclGetErrorString(r));
@@ -1759,6 +1905,11 @@ int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, dou
   }
   if (!cache) free_plan(pl);
   return st;
+}
+
+int combine_rows_impl(sgwg_family* f, const std::vector<int>& mis, int mode, double eps,
+                      long long a, long long b, double* out, int out_is_device) {
+  return combine_rows_impl(f, local_view(f), mis, mode, eps, a, b, out, out_is_device);
 }
 
 int ensure_fine_buf(sgwg_family* f) {
@@ -1862,6 +2013,10 @@ int sgwg_family_destroy(sgwg_family* f) {
   free_plan(f->full_plan);
   for (auto& kv : f->slab_plans) free_plan(kv.second);
   f->slab_plans.clear();
+  for (auto& kv : f->gslab_plans) free_plan(kv.second);
+  f->gslab_plans.clear();
+  cudaFree(f->gdmem);
+  cudaFree(f->gu);
   if (f->comm) ncclCommDestroy(f->comm);
   for (int k = 0; k < kMaxD; ++k) cudaFree(f->dtasks[k]);
   cudaFree(f->dmax_tasks);
@@ -2449,9 +2604,33 @@ int check_interp(int mode, double eps) {
 // fn(dev, first_linear_index, points).  One slab when the whole grid fits the
 // combination budget (or the family is a single grid).
 template <class Fn>
-int for_each_combined_slab(sgwg_family* f, int mode, double eps, Fn&& fn) {
+int for_each_combined_slab(sgwg_family* f, int mode, double eps, Fn&& fn, bool own_rows = false) {
   CK(cudaSetDevice(f->ctx->device));
   if (f->single) return fn((const double*)f->u, 0LL, f->finest);
+  if (own_rows && use_option_b(f)) {  // option B: this rank's rows, every member
+    TRY(gather_states(f));
+    const CombView v = gathered_view(f);
+    std::vector<int> gm(f->nfull);
+    for (int i = 0; i < f->nfull; ++i) gm[i] = i;
+    long long ra, rb;
+    option_b_rows(f, f->rank, &ra, &rb);
+    const long long per_row = (long long)(f->finest / f->fine_ext[0]);
+    long long slab = std::max(1LL, rb - ra);
+    while (slab > 1 && plan_doubles(f, v, gm, 0, slab) > combine_budget_doubles()) slab = (slab + 1) / 2;
+    if (f->diag_slab_doubles < slab * per_row) {
+      cudaFree(f->diag_slab);
+      f->diag_slab = nullptr;
+      f->diag_slab_doubles = 0;
+      CK(cudaMalloc(&f->diag_slab, sizeof(double) * slab * per_row));
+      f->diag_slab_doubles = slab * per_row;
+    }
+    for (long long a = ra; a < rb; a += slab) {
+      const long long b = std::min(rb, a + slab);
+      TRY(combine_rows_impl(f, v, gm, mode, eps, a, b, f->diag_slab, 1));
+      TRY(fn((const double*)f->diag_slab, a * per_row, (b - a) * per_row));
+    }
+    return SGWG_OK;
+  }
   if (f->nm == 0 && f->comm == nullptr) return fail_with(SGWG_EINVAL, "combine: empty family");
   std::vector<int> mis(f->nm);
   for (int i = 0; i < f->nm; ++i) mis[i] = i;
@@ -2536,7 +2715,21 @@ int sgwg_combined_stats(sgwg_family* f, int mode, double eps, int exact_preset, 
     l1 += h5[3];
     linf = std::max(linf, h5[4]);
     return SGWG_OK;
-  }));
+  }, /*own_rows=*/true));
+  if (use_option_b(f) && f->nranks > 1) {  // this rank's rows only: reduce across ranks
+    double h[5] = {mass, l1, -mn, mx, linf};
+    double* dh = f->diag_scratch;  // the stats partials are consumed
+    CK(cudaMemcpyAsync(dh, h, sizeof(h), cudaMemcpyHostToDevice, f->ctx->stream));
+    CKN(ncclAllReduce(dh, dh, 2, ncclDouble, ncclSum, f->comm, f->ctx->stream));
+    CKN(ncclAllReduce(dh + 2, dh + 2, 3, ncclDouble, ncclMax, f->comm, f->ctx->stream));
+    CK(cudaMemcpyAsync(h, dh, sizeof(h), cudaMemcpyDeviceToHost, f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    mass = h[0];
+    l1 = h[1];
+    mn = -h[2];
+    mx = h[3];
+    linf = h[4];
+  }
   CK(cudaEventRecord(f->evs1, f->ctx->stream));
   CK(cudaEventSynchronize(f->evs1));
   float cms = 0.f;
@@ -2595,28 +2788,41 @@ int sgwg_eval_points(sgwg_family* f, int mode, double eps, const int* idx, size_
   CK(cudaSetDevice(f->ctx->device));
   int* didx = nullptr;
   double *dcoef = nullptr, *dout = nullptr;
-  const std::vector<double> cf = member_coefs(f);
+  // option B: every rank evaluates every point from the gathered states (no all-reduce)
+  const bool optb = use_option_b(f);
+  if (optb) TRY(gather_states(f));
+  std::vector<double> cf = member_coefs(f);
+  if (optb) {
+    cf.clear();
+    for (const MemberDesc& M : f->ghmem) {
+      int ls = 0;
+      for (int k = 0; k < f->d; ++k) ls += M.level[k];
+      const int j = f->nl - ls;
+      cf.push_back((double)((j % 2 == 0 ? 1 : -1) * binomial(f->d - 1, j)));  // combine.hpp:116
+    }
+  }
+  const int nmv = optb ? f->nfull : f->nm;
   int st = SGWG_OK;
   auto fail_cuda = [&](cudaError_t e) {
     return (e == cudaSuccess) ? SGWG_OK : fail_with(SGWG_ECUDA, cudaGetErrorString(e));
   };
   st = fail_cuda(cudaMalloc(&didx, sizeof(int) * npoints * f->d));
-  if (st == SGWG_OK) st = fail_cuda(cudaMalloc(&dcoef, sizeof(double) * std::max(1, f->nm)));
+  if (st == SGWG_OK) st = fail_cuda(cudaMalloc(&dcoef, sizeof(double) * std::max(1, nmv)));
   if (st == SGWG_OK) st = fail_cuda(cudaMalloc(&dout, sizeof(double) * npoints));
   if (st == SGWG_OK)
     st = fail_cuda(cudaMemcpyAsync(didx, idx, sizeof(int) * npoints * f->d,
                                    cudaMemcpyHostToDevice, f->ctx->stream));
-  if (st == SGWG_OK && f->nm > 0)
-    st = fail_cuda(cudaMemcpyAsync(dcoef, cf.data(), sizeof(double) * f->nm,
+  if (st == SGWG_OK && nmv > 0)
+    st = fail_cuda(cudaMemcpyAsync(dcoef, cf.data(), sizeof(double) * nmv,
                                    cudaMemcpyHostToDevice, f->ctx->stream));
   if (st == SGWG_OK) {
     EvalParams p{};
-    p.mem = f->dmem;
-    p.u = f->u;
+    p.mem = optb ? f->gdmem : f->dmem;
+    p.u = optb ? f->gu : f->u;
     p.coef = dcoef;
     p.idx = didx;
     p.npts = (long long)npoints;
-    p.nm = f->nm;
+    p.nm = nmv;
     p.d = f->d;
     p.nl = f->single ? f->levels[0][0] : f->nl;
     p.mode = mode;
@@ -2625,7 +2831,7 @@ int sgwg_eval_points(sgwg_family* f, int mode, double eps, const int* idx, size_
     st = fail_cuda(arith_of(f) == SGWG_ARITH_FAST ? fast::launch_eval_points(p, f->ctx->stream)
                                                    : exact::launch_eval_points(p, f->ctx->stream));
   }
-  if (st == SGWG_OK && f->comm != nullptr && f->nranks > 1) {
+  if (st == SGWG_OK && !optb && f->comm != nullptr && f->nranks > 1) {
     const ncclResult_t r = ncclAllReduce(dout, dout, npoints, ncclDouble, ncclSum, f->comm,
                                          f->ctx->stream);
     if (r != ncclSuccess) st = fail_with(SGWG_ENCCL, ncclGetErrorString(r));
@@ -2764,6 +2970,38 @@ int sgwg_combine_rows(sgwg_family* f, int mode, double eps, long long row_begin,
   for (int i = 0; i < f->nm; ++i) mis[i] = i;
   f->stats.combine_launches = 0;
   return combine_rows_impl(f, mis, mode, eps, row_begin, row_end, out, out_is_device);
+}
+
+int sgwg_combine_local(sgwg_family* f, int mode, double eps, double* out, size_t n,
+                       int out_is_device, long long* row_begin, long long* row_end) {
+  if (f == nullptr || row_begin == nullptr || row_end == nullptr)
+    return fail_with(SGWG_EINVAL, "null argument");
+  TRY(check_interp(mode, eps));
+  if (f->d < 2) return fail_with(SGWG_EINVAL, "combine_local: needs d >= 2");
+  CK(cudaSetDevice(f->ctx->device));
+  long long a = 0, b = f->fine_ext[0];
+  if (use_option_b(f)) option_b_rows(f, f->rank, &a, &b);
+  *row_begin = a;
+  *row_end = b;
+  const long long per_row = (long long)(f->finest / f->fine_ext[0]);
+  if (out == nullptr) return SGWG_OK;  // query of the row range
+  if (n != (size_t)((b - a) * per_row))
+    return fail_with(SGWG_EINVAL, "combine_local: output size must equal this rank's rows x points per row");
+  if (!use_option_b(f)) return sgwg_combine(f, mode, eps, out, n, out_is_device);
+  TRY(gather_states(f));
+  const CombView v = gathered_view(f);
+  std::vector<int> gm(f->nfull);
+  for (int i = 0; i < f->nfull; ++i) gm[i] = i;
+  long long slab = std::max(1LL, b - a);
+  while (slab > 1 && plan_doubles(f, v, gm, 0, slab) > combine_budget_doubles()) slab = (slab + 1) / 2;
+  double ms = 0.0;
+  for (long long r0 = a; r0 < b; r0 += slab) {
+    const long long r1 = std::min(b, r0 + slab);
+    TRY(combine_rows_impl(f, v, gm, mode, eps, r0, r1, out + (r0 - a) * per_row, out_is_device));
+    ms += f->stats.combine_ms;
+  }
+  f->stats.combine_ms = ms;
+  return SGWG_OK;
 }
 
 int sgwg_prolong(sgwg_family* f, int mi, int mode, double eps, double* out, size_t n,

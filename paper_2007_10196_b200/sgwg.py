@@ -123,6 +123,8 @@ SIGNATURES = {
     "sgwg_time_stage": (C.c_int, [_VP, C.c_int, _DP, _DP, _DP]),
     "sgwg_combine_rows": (C.c_int, [_VP, C.c_int, C.c_double, C.c_longlong, C.c_longlong, _VP,
                                     C.c_size_t, C.c_int]),
+    "sgwg_combine_local": (C.c_int, [_VP, C.c_int, C.c_double, _VP, C.c_size_t, C.c_int,
+                                     C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "sgwg_vp_field": (C.c_int, [_VP, _DP, C.c_size_t, _DP, C.c_size_t]),
     "sgwg_field_energy": (C.c_int, [_VP, _DP, C.c_size_t, C.POINTER(C.c_size_t)]),
     "sgwg_combined_stats": (C.c_int, [_VP, C.c_int, C.c_double, C.c_int, C.c_double,
@@ -387,6 +389,18 @@ class Family:
         _check(load().sgwg_combine_rows(self.h, mode, eps, row_begin, row_end, out.ctypes.data,
                                         n, 0))
         return out
+
+    def combine_local(self, mode=1, eps=1e-6):
+        """this rank's dimension-0 rows of the combination (option B for a sharded
+        family: every member's state gathered, the result left sharded; bitwise the
+        one-GPU rows).  Returns (row_begin, row_end, values)."""
+        a, b = C.c_longlong(0), C.c_longlong(0)
+        _check(load().sgwg_combine_local(self.h, mode, eps, None, 0, 0, C.byref(a), C.byref(b)))
+        per_row = self.finest_points // self.fine_extent0
+        out = np.empty((b.value - a.value) * per_row)
+        _check(load().sgwg_combine_local(self.h, mode, eps, out.ctypes.data, out.size, 0,
+                                         C.byref(a), C.byref(b)))
+        return a.value, b.value, out
 
     @property
     def fine_extent0(self) -> int:

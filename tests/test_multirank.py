@@ -8,6 +8,12 @@ the collectives by gloo, checking that the sharded pipeline reproduces the
 single-process reference result: identical dt sequence and member states
 (members are independent given the shared dt), combination within 1e-13
 (summation order differs only across ranks).
+
+Option B (libsgwg's sgwg_combine_local / combined_stats / eval_points for a
+sharded family): every rank gathers all member states and combines its own
+dimension-0 rows [rows*r/N, rows*(r+1)/N) for every member -- the rows must be
+BITWISE those of the single-process combination (dimension-sequential
+prolongation, interp.hpp:217-244, makes row slabs independent).
 """
 import os
 import socket
@@ -94,10 +100,19 @@ def _worker(rank, world, port, cfg_name, over, T, q):
     del coef
     tp = torch.from_numpy(part)
     dist.all_reduce(tp, op=dist.ReduceOp.SUM)
+    # option B: gather every shard's states, combine this rank's dimension-0 rows
+    shards = [None] * world
+    dist.all_gather_object(shards, {int(m): states[m] for m in mine})
+    full = np.concatenate([next(sh[m] for sh in shards if m in sh) for m in range(len(pts))])
+    fine_ext = [(cfg["root"][k] << cfg["nl"]) + (1 if cfg["bc"][k] == 1 else 0)
+                for k in range(cfg["d"])]
+    a, b = fine_ext[0] * rank // world, fine_ext[0] * (rank + 1) // world
+    rows = orc.combine_box(dom, full, [a] + [0] * (cfg["d"] - 1), [b] + fine_ext[1:],
+                           cfg["interp"], cfg["epsilon"])
     if rank == 0:
-        q.put((np.array(dts), {int(m): states[m] for m in mine}, tp.numpy().copy()))
+        q.put((np.array(dts), {int(m): states[m] for m in mine}, tp.numpy().copy(), (a, b, rows)))
     else:
-        q.put((None, {int(m): states[m] for m in mine}, None))
+        q.put((None, {int(m): states[m] for m in mine}, None, (a, b, rows)))
     dist.destroy_process_group()
 
 
@@ -139,3 +154,8 @@ def test_two_rank_sharded_pipeline_matches_single(cfg_name, over, T):
         assert np.array_equal(states[m], s[offs[m]:offs[m + 1]])
     want = orc.combine(dom, s, cfg["interp"], cfg["epsilon"])
     assert np.max(np.abs(combined - want)) < 1e-13
+    # option B: the ranks' row slabs tile the finest grid and are bitwise the combination
+    slabs = sorted(r[3][:2] + (r[3][2],) for r in res)
+    assert slabs[0][0] == 0 and all(slabs[i][1] == slabs[i + 1][0] for i in range(world - 1))
+    rows = np.concatenate([sl[2].ravel() for sl in slabs])
+    assert np.array_equal(rows, want.ravel())
