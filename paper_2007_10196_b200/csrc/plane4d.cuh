@@ -742,33 +742,35 @@ __global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) vpass4d_kernel(const
 // density is a plain per-plane sum (4 accumulators per lane).
 // smem: [U0 | U1 | K | u^n | dv1 | dv2], each p.vpitch doubles.
 // ---------------------------------------------------------------------------
-struct VInfo {
-  long long gs, ga;  // tile start (doubles) and its 16-byte aligned floor
-  long long xoff;    // member's first x point in the packed x-grid buffers
-  double ih3, ih4, hh;
-  int mi, x0, G, n3, n4, V, NT, shift, nx;
-  unsigned nbytes;
-  __device__ void load(const Plane4Params& p, int t) {
-    const int4 tk = p.tiles[t];
-    const MemberDesc* M = p.mem + tk.x;
-    mi = tk.x;
-    x0 = tk.y;
-    G = tk.z;
-    n3 = M->ext[2];
-    n4 = M->ext[3];
-    V = n3 * n4;
-    NT = G * V;
-    gs = M->offset + (long long)x0 * V;
-    ga = gs & ~1LL;
-    shift = (int)(gs - ga);
-    nbytes = (unsigned)((((gs + NT + 1) & ~1LL) - ga) * 8);
-    xoff = M->xoff;
-    nx = M->nx;
-    ih3 = M->inv_h[2];
-    ih4 = M->inv_h[3];
-    hh = M->h[2] * M->h[3];
+using VInfo = P4VTile;
+
+// thread 0: the descriptor of tile t into a ring slot, async (16-byte pieces)
+__device__ __forceinline__ void vp_fetch_info(const Plane4Params& p, int t, VInfo* dst) {
+  const char* src = (const char*)(p.vtiles + t);
+  for (int q = 0; q < (int)sizeof(VInfo); q += 16) {
+    const unsigned sd = (unsigned)__cvta_generic_to_shared((char*)dst + q);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sd), "l"(src + q) : "memory");
   }
-};
+}
+
+// threads tid < G: the line coefficients of the tile's x points into ce1 / ce2 -- for
+// Vlasov-Poisson the raw E_j(x) by async copies (the sweeps apply the sign,
+// models.hpp:346-349), else line_coef (no memory dependence)
+__device__ __forceinline__ void vp_fetch_coefs(const Plane4Params& p, const VInfo* v, double* ce1,
+                                               double* ce2) {
+  const int tid = threadIdx.x;
+  if (tid >= v->G) return;
+  if (p.flux_a == kFluxKinVP) {
+    const double* E = p.efield + v->xoff * p.space_dim + v->x0 + tid;
+    cp_async8(ce1 + tid, E, true);
+    cp_async8(ce2 + tid, E + v->nx, true);
+  } else {
+    const MemberDesc* M = p.mem + v->mi;
+    ce1[tid] = line_coef(p.flux_a, M, 2, p.space_dim, v->x0 + tid, p.c_a, p.efield);
+    ce2[tid] = line_coef(p.flux_b, M, 3, p.space_dim, v->x0 + tid, p.c_b, p.efield);
+  }
+}
+
 
 __device__ __forceinline__ void bulk_g2s_noexpect(void* dst, const void* src, unsigned bytes,
                                                   unsigned long long* bar) {
@@ -794,7 +796,7 @@ __device__ __forceinline__ void vp_issue_ku(const Plane4Params& p, const VInfo& 
 template <bool LINEAR>
 __device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps, const double* U,
                                             double* DV1, double* DV2, const double* ce1,
-                                            const double* ce2) {
+                                            const double* ce2, double csign) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = vi->G, n3 = vi->n3, n4 = vi->n4, V = vi->V;
   P4Sweeps T;
@@ -810,7 +812,7 @@ __device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps
     if (sw == 0) {
       const int base = l * n4;
       SGWG_DCHECK(qdiv(l, i3f) == l / n3 && base + 8 * (r1 - 1) < G * V, "vpass row run");
-      const double cf = ce2[qdiv(l, i3f)];
+      const double cf = csign * ce2[qdiv(l, i3f)];
       for (int r = r0; r < r1; ++r)
         run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, cf, eps, ih4,
                                  DV2 + base + 8 * r);
@@ -818,7 +820,7 @@ __device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps
       const int gx = qdiv(l, i4f);
       const int base = gx * V + (l - gx * n4);
       SGWG_DCHECK(gx == l / n4 && gx < G && base + 8 * (r1 - 1) * n4 < G * V, "vpass column run");
-      const double cf = ce1[gx];
+      const double cf = csign * ce1[gx];
       for (int r = r0; r < r1; ++r)
         run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, cf, eps, ih3,
                                  DV1 + base + 8 * r * n4);
@@ -863,24 +865,35 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
   extern __shared__ __align__(16) double sm[];
   __shared__ unsigned long long bar[3];  // U0, U1, K/u^n
   __shared__ double ce1[2][kP4MaxG], ce2[2][kP4MaxG];
-  __shared__ VInfo info[3];              // tile `it` uses slot it % 3
+  // tiles in a 4-slot ring: tile `it` of this CTA is tix[it % 4] with descriptor
+  // info[it % 4] (async-filled two tiles ahead).  Tiles after the first two come
+  // from a global counter (dynamic scheduling: a static round robin left the
+  // slowest CTA ~17 % behind the median); the counter's value for tile it + 3
+  // is requested at tile it, so its latency is never waited for.
+  __shared__ VInfo info[4];
+  __shared__ int tix[4];
+  const double csign = (p.flux_a == kFluxKinVP) ? -1.0 : 1.0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pitch = p.vpitch;
   double* Ks = sm + 2 * pitch;
   double* UNs = sm + 3 * pitch;
   double* DV1 = sm + 4 * pitch;
   double* DV2 = sm + 5 * pitch;
-  const int stride = gridDim.x, nt = p.ntiles;
-  int t = blockIdx.x;
-  if (t >= nt) return;
+  const int G0 = gridDim.x, nt = p.ntiles;
+  if ((int)blockIdx.x >= nt) return;
   // static tile data before the dependency wait (overlaps the previous kernel under PDL)
   if (tid == 0) {
-    info[0].load(p, t);
-    if (t + stride < nt) info[1].load(p, t + stride);
+    tix[0] = blockIdx.x;
+    tix[1] = blockIdx.x + G0;
+    vp_fetch_info(p, tix[0], &info[0]);
+    if (tix[1] < nt) vp_fetch_info(p, tix[1], &info[1]);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
+  if (tid == 0) tix[2] = (tix[1] < nt) ? 2 * G0 + (int)atomicAdd(p.sched, 1u) : nt;
   const int stage = p.stage;
   const bool moment = (p.rho_parts != nullptr) && (stage > 0);
   __syncthreads();
@@ -891,14 +904,12 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
     bulk_g2s(sm, p.uin + info[0].ga, info[0].nbytes, &bar[0]);
     vp_issue_ku(p, info[0], Ks, UNs, &bar[2]);
   }
-  if (tid < info[0].G) {  // v_j lines at x point x0+tid: -E_j(x) (VP) or the advection speed
-    const MemberDesc* M = p.mem + info[0].mi;
-    ce1[0][tid] = line_coef(p.flux_a, M, 2, p.space_dim, info[0].x0 + tid, p.c_a, p.efield);
-    ce2[0][tid] = line_coef(p.flux_b, M, 3, p.space_dim, info[0].x0 + tid, p.c_b, p.efield);
-  }
+  vp_fetch_coefs(p, &info[0], ce1[0], ce2[0]);
+  cp_async_commit();
+  cp_async_wait<0>();
   const double dt = (ctl != nullptr) ? ctl->dt : 0.0;
 #ifdef SGWG_TRACE
-  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tc = clock64(), tn_;
 #define P4PH(k)                 \
   do {                          \
@@ -911,59 +922,53 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
   do {          \
   } while (0)
 #endif
-  for (int it = 0; t < nt; t += stride, ++it) {
+  for (int it = 0;; ++it) {
     // it: local tile counter -- U slot it & 1 (parity (it >> 1) & 1), K/u^n parity it & 1
     const int b = it & 1;
-    const int t1 = t + stride, t2 = t + 2 * stride;
-    const VInfo* vi = &info[it % 3];
-    // [A]: ce / info of this tile published (and, at it = 0, the mbarriers);
+    // [A]: ce / info / tix of this tile published (and, at it = 0, the mbarriers);
     // the previous tile is completely done with the other U slot and dv1
     __syncthreads();
     P4PH(0);
-    VInfo n2;
+    const int t = tix[it & 3];
+    if (t >= nt) break;
+    const int t1 = tix[(it + 1) & 3];
+    const VInfo* vi = &info[it & 3];
     if (tid == 0) {
       if (t1 < nt) {
-        const VInfo* v1 = &info[(it + 1) % 3];
+        const VInfo* v1 = &info[(it + 1) & 3];
         bulk_g2s(sm + (b ^ 1) * pitch, p.uin + v1->ga, v1->nbytes, &bar[b ^ 1]);
       }
-      if (t2 < nt) n2.load(p, t2);  // consumed after the sweeps
+      // the descriptor of the tile after next (its index came from the counter
+      // during the previous tile's epilogue) into its ring slot
+      const int t2 = tix[(it + 2) & 3];
+      if (t2 < nt) vp_fetch_info(p, t2, &info[(it + 2) & 3]);
     }
-    // the next tile's line coefficients: loads in flight during the sweeps
-    double nce1 = 0.0, nce2 = 0.0;
-    const VInfo* v1 = &info[(it + 1) % 3];
-    const bool ldce = (t1 < nt) && (tid < v1->G);
-    if (ldce) {
-      if (p.flux_a == kFluxKinVP) {  // -E_j(x) (models.hpp:346-349 with the Poisson field)
-        const double* E = p.efield + v1->xoff * p.space_dim + v1->x0 + tid;
-        nce1 = -E[0];
-        nce2 = -E[v1->nx];
-      } else {
-        const MemberDesc* M = p.mem + v1->mi;
-        nce1 = line_coef(p.flux_a, M, 2, p.space_dim, v1->x0 + tid, p.c_a, p.efield);
-        nce2 = line_coef(p.flux_b, M, 3, p.space_dim, v1->x0 + tid, p.c_b, p.efield);
-      }
-    }
+    P4PH(9);
+    // the next tile's line coefficients (its descriptor is in slot it + 1)
+    if (t1 < nt) vp_fetch_coefs(p, &info[(it + 1) & 3], ce1[b ^ 1], ce2[b ^ 1]);
+    cp_async_commit();
     const double* U = sm + b * pitch + vi->shift;
     SGWG_DCHECK(vi->shift + vi->NT <= pitch && (long long)vi->nbytes <= 8LL * pitch,
                 "vpass tile exceeds its shared-memory slot");
     SGWG_DCHECK(vi->gs + vi->NT <= p.mem[vi->mi].offset + p.mem[vi->mi].npts,
                 "vpass tile exceeds its member");
-    SGWG_DCHECK(vi->G <= kP4MaxG, "vpass tile has too many x points");
+    SGWG_DCHECK(vi->G <= kP4MaxG && p.vtiles[t].gs == vi->gs, "vpass tile descriptor");
+    P4PH(8);
     mbar_wait(&bar[b], (it >> 1) & 1);
     P4PH(1);
-    vp_tile_sweeps<LINEAR>(vi, p.rpt, p.eps, U, DV1, DV2, ce1[b], ce2[b]);
+    vp_tile_sweeps<LINEAR>(vi, p.rpt, p.eps, U, DV1, DV2, ce1[b], ce2[b], csign);
     P4PH(2);
-    if (ldce) {  // ce[b ^ 1] is not read before barrier A of the next tile
-      ce1[b ^ 1][tid] = nce1;
-      ce2[b ^ 1][tid] = nce2;
-    }
+    cp_async_wait<0>();  // this thread's async copies (descriptor, coefficients) landed
     mbar_wait(&bar[2], it & 1);
     P4PH(3);
     // [B]: dv1 / dv2 complete, K / u^n landed
     __syncthreads();
     P4PH(4);
-    if (tid == 0 && t2 < nt) info[(it + 2) % 3] = n2;
-
+    // the counter's tile for three iterations ahead: requested now, stored after
+    // the epilogue (the atomic's round trip hidden behind it)
+    const bool more = (tid == 0) && tix[(it + 2) & 3] < nt;
+    unsigned int got = 0u;
+    if (more) got = atomicAdd(p.sched, 1u);
     double* out = p.out + vi->gs;
     const double* Kt = Ks + vi->shift;
     const double* UNt = UNs + vi->shift;
@@ -983,12 +988,12 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
           (unsigned long long)ctl->cur_step * 4ull + (unsigned long long)stage;
       atomicMin(p.fail + vi->mi, code);
     }
-
+    if (tid == 0) tix[(it + 3) & 3] = more ? 2 * G0 + (int)got : nt;  // tile it - 1's slot
     P4PH(5);
     // [C]: K / u^n slots free, w f of the stage output in dv1
     __syncthreads();
     P4PH(6);
-    if (tid == 0 && t1 < nt) vp_issue_ku(p, info[(it + 1) % 3], Ks, UNs, &bar[2]);
+    if (tid == 0 && t1 < nt) vp_issue_ku(p, info[(it + 1) & 3], Ks, UNs, &bar[2]);
     if (moment) {
       // charge density of the stage output per x point (moment_density, models.hpp:294-306)
       const int V = vi->V;
@@ -1015,10 +1020,17 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
   }
 #ifdef SGWG_TRACE
   if (tid == 0 && blockIdx.x < kP4TraceCtas)
-    for (int k = 0; k < 8; ++k) sgwg_p4trace[1][blockIdx.x][k] = ph[k];
-  if (tid == 32 && blockIdx.x < kP4TraceCtas)  // warp 1's view of the same phases
-    for (int k = 0; k < 2; ++k) sgwg_p4trace[1][blockIdx.x][8 + k] = ph[2 + k];
+    for (int k = 0; k < 10; ++k) sgwg_p4trace[1][blockIdx.x][k] = ph[k];
 #endif
+  // the last CTA out resets the tile counter for the next launch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(p.sched + 1, 1u) == (unsigned)min(G0, nt) - 1) {
+      p.sched[0] = 0u;
+      p.sched[1] = 0u;
+      __threadfence();
+    }
+  }
   if (p.dtp != nullptr) fused_step_dt(p.dtp, p.counter);
 }
 

@@ -269,6 +269,8 @@ struct sgwg_family {
   int p4smem[2] = {0, 0};                  // dynamic shared memory (doubles) per pass
   int p4vpitch = 0;                        // > 0: persistent v pass, slot pitch (doubles)
   int p4xpitch = 0;                        // > 0: persistent x pass, slot pitch (doubles)
+  P4VTile* dp4vtiles = nullptr;            // persistent v pass: tile descriptors
+  unsigned int* dp4sched = nullptr;        // persistent v pass: dynamic tile counter (2 words)
   double* rho_parts = nullptr;      // Vlasov-Poisson charge-density partial sums
   double* twid = nullptr;           // FFT twiddle table (2 x hmax)
   int hmax = 1;
@@ -496,6 +498,8 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
       p.ntiles = nblk;
       if (pass == 1 && f->p4vpitch > 0) {
         p.vpitch = f->p4vpitch;
+        p.vtiles = f->dp4vtiles;
+        p.sched = f->dp4sched;
         nblk = std::min(nblk, 2 * f->ctx->sm_count);
       }
       if (pass == 0 && f->p4xpitch > 0) {
@@ -1407,6 +1411,38 @@ int build_plane4_tiles(sgwg_family* f) {
       f->p4smem[1] = 6 * pitch;
     }
   }
+  if (f->p4vpitch > 0) {  // persistent v pass: a descriptor per tile (plane4d.cuh VInfo)
+    std::vector<P4VTile> vt;
+    for (const int4& q : t[1]) {
+      const MemberDesc& M = f->hmem[q.x];
+      P4VTile v{};
+      v.mi = q.x;
+      v.x0 = q.y;
+      v.G = q.z;
+      v.n3 = M.ext[2];
+      v.n4 = M.ext[3];
+      v.V = v.n3 * v.n4;
+      v.NT = v.G * v.V;
+      v.gs = M.offset + (long long)v.x0 * v.V;
+      v.ga = v.gs & ~1LL;
+      v.shift = (int)(v.gs - v.ga);
+      v.nbytes = (unsigned)((((v.gs + v.NT + 1) & ~1LL) - v.ga) * 8);
+      v.xoff = M.xoff;
+      v.nx = M.nx;
+      v.ih3 = M.inv_h[2];
+      v.ih4 = M.inv_h[3];
+      v.hh = M.h[2] * M.h[3];
+      vt.push_back(v);
+    }
+    cudaFree(f->dp4vtiles);
+  cudaFree(f->dp4sched);
+    f->dp4vtiles = nullptr;
+    TRY(upload_vec(&f->dp4vtiles, vt));
+    if (f->dp4sched == nullptr) {
+      CK(cudaMalloc(&f->dp4sched, 2 * sizeof(unsigned int)));
+      CK(cudaMemset(f->dp4sched, 0, 2 * sizeof(unsigned int)));
+    }
+  }
   for (int mi = 0; mi < f->nm; ++mi) f->hmem[mi].rparts = 1;
   CK(cudaMemcpy(f->dmem, f->hmem.data(), sizeof(MemberDesc) * f->nm, cudaMemcpyHostToDevice));
   for (int pass = 0; pass < 2; ++pass) {
@@ -2039,6 +2075,7 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dptiles[1]);
   cudaFree(f->dp4tiles[0]);
   cudaFree(f->dp4tiles[1]);
+  cudaFree(f->dp4vtiles);
   cudaFree(f->rho_parts);
   cudaFree(f->twid);
   cudaFree(f->Fu);

@@ -187,6 +187,18 @@ struct PlaneParams {
   unsigned int* counter;
 };
 
+// v-pass tile descriptor of the persistent 4D v pass (plane4d.cuh), precomputed on the
+// host so a CTA prefetches it with one async copy (no dependent load chain)
+struct __align__(16) P4VTile {
+  long long gs, ga;  // tile start (doubles) and its 16-byte aligned floor
+  long long xoff;    // member's first x point in the packed x-grid buffers
+  double ih3, ih4, hh;
+  int mi, x0, G, n3, n4, V, NT, shift, nx;
+  unsigned nbytes;
+  int pad[2];
+};
+static_assert(sizeof(P4VTile) == 96, "P4VTile is copied in 16-byte pieces");
+
 // fast 4D stage on whole planes (plane4d.cuh): x pass tiles (mi, v0, nc, log2 C),
 // v pass tiles (mi, x0, G, -)
 struct Plane4Params {
@@ -210,6 +222,8 @@ struct Plane4Params {
   unsigned int* counter;
   int rpt;                 // runs per warp task (plane4d.cuh P4Sweeps)
   int xpitch;              // > 0: persistent x pass (xpass4d_persist_kernel), slot pitch in doubles
+  const P4VTile* vtiles;   // persistent v pass: descriptor per tile
+  unsigned int* sched;     // persistent v pass: [next tile counter, CTAs done] (self-resetting)
   int vpitch;              // > 0: persistent v pass (vpass4d_persist_kernel), slot pitch in doubles
   int ntiles;              // v-pass tiles (persistent form)
   int masked;              // 1: one sweep body with runtime ghost masks (default), 0: per-pattern bodies

@@ -17,8 +17,10 @@ lib = sgwg.load()
 buf = np.zeros((2, 8192, 10), dtype=np.int64)
 assert lib.sgwg_p4trace_dump(buf.ctypes.data_as(C.POINTER(C.c_longlong))) == 0
 t = buf[1][:296].astype(np.float64)
-names = ["bar A", "U wait", "sweeps(w0)", "KU wait", "bar B", "epilogue+ce", "bar C", "moment", "sweeps(w1)", "KUwait(w1)"]
-tot = t[:, :8].sum(axis=1)
+names = ["bar A", "U wait", "sweeps(w0)", "KU wait", "bar B", "epilogue", "bar C", "moment", "coefs", "tid0 issue"]
+tot = t[:, :10].sum(axis=1)
 print(f"CTAs {len(t)}, cycles per CTA median {np.median(tot):.0f} (max {tot.max():.0f})")
 for k, nm in enumerate(names):
+    if nm == "-":
+        continue
     print(f"  {nm:12s} median {np.median(t[:, k]):9.0f}  share {np.median(t[:, k]) / np.median(tot):.3f}")
