@@ -202,6 +202,9 @@ struct sgwg_family {
   int* degrp_mem = nullptr;
   int negrp = 0, ngx = 0;
   double* egrid = nullptr;
+  int egrp_tsum = 0;               // energy_rows_kernel: 2 x sum of group x2 extents
+  double* eparts = nullptr;        // energy_rows_kernel: per finest x row partial sums
+  unsigned int* edone = nullptr;   // energy_rows_kernel: CTAs done (self-resetting)
   // graphs: steps per chunk -> exec
   std::map<int, cudaGraphExec_t> graphs;
   long long graph_key_policy = -1;
@@ -404,15 +407,21 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
 // runs concurrently with stage 1
 int launch_energy_side(sgwg_family* f) {
   if (f->fe == nullptr) return SGWG_OK;
+  if (const char* e = std::getenv("SGWG_NO_ENERGY"))  // timing experiments only
+    if (e[0] == '1') return SGWG_OK;
   const FieldParams& fp = f->energy_fp;
   const int dx = f->model.space_dim;
   const int fine1 = (dx == 2) ? f->fine_ext[1] : 1;
   const double hvol = f->fine_h[0] * ((dx == 2) ? f->fine_h[1] : 1.0);
   CK(cudaEventRecord(f->evfork, f->ctx->stream));
   CK(cudaStreamWaitEvent(f->side, f->evfork, 0));
-  CK(launch_field_energy(fp, f->dcoef, f->fine_ext[0], fine1, hvol, f->fe, f->fe_cap, f->side));
+  // one-kernel row form for 2D x-grids with member groups (C5), else group + point kernels
+  const bool rows = (dx == 2 && fp.negrp > 0 && fp.negrp < 64 && f->egrp_tsum <= 4096 &&
+                     f->eparts != nullptr);
+  CK(launch_field_energy(fp, f->dcoef, f->fine_ext[0], fine1, hvol, f->fe, f->fe_cap, f->side,
+                         rows ? f->eparts : nullptr, rows ? f->edone : nullptr));
   CK(cudaEventRecord(f->evjoin, f->side));
-  f->stats.kernel_launches += (fp.negrp > 0) ? 2 : 1;
+  f->stats.kernel_launches += rows ? 1 : (fp.negrp > 0) ? 2 : 1;
   return SGWG_OK;
 }
 
@@ -1190,6 +1199,15 @@ int setup_vp(sgwg_family* f) {
     TRY(upload_vec(&f->degrp_m, gm));
     TRY(upload_vec(&f->degrp_mem, gmem));
     CK(cudaMalloc(&f->egrid, sizeof(double) * std::max(1, off)));
+    f->egrp_tsum = 0;  // doubles of one finest row's group interpolants (energy_rows_kernel)
+    for (size_t g = 0; g < keys.size(); ++g) f->egrp_tsum += 2 * keys[g].second;
+    cudaFree(f->eparts);
+    cudaFree(f->edone);
+    f->eparts = nullptr;
+    f->edone = nullptr;
+    CK(cudaMalloc(&f->eparts, sizeof(double) * std::max(1, f->fine_ext[0])));
+    CK(cudaMalloc(&f->edone, sizeof(unsigned int)));
+    CK(cudaMemset(f->edone, 0, sizeof(unsigned int)));
     f->negrp = (int)keys.size();
     f->ngx = gx;
   }
@@ -2086,6 +2104,8 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->degrp_m);
   cudaFree(f->degrp_mem);
   cudaFree(f->egrid);
+  cudaFree(f->eparts);
+  cudaFree(f->edone);
   cudaFree(f->fe);
   cudaFree(f->dcoef);
   cudaFreeHost(f->hctl);

@@ -394,7 +394,8 @@ cudaError_t configure_field();
 cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, cudaStream_t s);
 cudaError_t launch_twiddles(double* tw, int hmax, cudaStream_t s);
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
-                                double hvol, double* out_base, long long cap, cudaStream_t s);
+                                double hvol, double* out_base, long long cap, cudaStream_t s,
+                                double* part = nullptr, unsigned int* done = nullptr);
 cudaError_t launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t s);
 cudaError_t launch_vm_speeds(const VmParams& p, int nmembers, cudaStream_t s);
 int stats_partial_doubles();

@@ -76,13 +76,16 @@ def test_landau_damping_rate(ctx_fast):
     assert -0.18 < slope < -0.13, slope
 
 
-@pytest.mark.parametrize("groups", ["0", "1"])
+@pytest.mark.parametrize("groups", ["0", "1", "legacy"])
 def test_field_energy_record_2d2v(ctx_fast, oracle, monkeypatch, groups):
     """Same record for 2D2V (member by member, or members grouped by x-grid
-    on the device): step 0 against separable Lagrange upsampling of every
-    member's (E_1, E_2)."""
+    on the device: the one-kernel row form energy_rows_kernel, or the legacy
+    group + point kernels): step 0 against separable Lagrange upsampling of
+    every member's (E_1, E_2)."""
     from oracle import oracle as O
-    monkeypatch.setenv("SGWG_ENERGY_GROUPS", groups)
+    monkeypatch.setenv("SGWG_ENERGY_GROUPS", "0" if groups == "0" else "1")
+    if groups == "legacy":
+        monkeypatch.setenv("SGWG_ENERGY_LEGACY", "1")
     cfg = configs.config("C5", nl=3)
     fam = gpu_family(ctx_fast, cfg)
     fam.initialize(cfg["ic"])
