@@ -1045,30 +1045,33 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
 // memory (no d/dx2 array, no separate store phase).
 // smem: [U0 | U1 | d/dx1], each p.xpitch doubles.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void xp_issue_gather(const Plane4Params& p, int t, double* Ub) {
-  const int4 tk = p.tiles[t];
-  const MemberDesc* M = p.mem + tk.x;
-  const int v0 = tk.y, nc = tk.z, cs = tk.w, C = 1 << cs;
-  const int V = M->ext[2] * M->ext[3];
-  const int NT = (M->ext[0] * M->ext[1]) << cs;
-  const double* src = p.uin + M->offset + v0;
-  const int cm = nc - 1;
-  for (int e = threadIdx.x; e < NT; e += kP4Threads) {
-    const int c = e & (C - 1);
-    cp_async8(Ub + e, src + (e >> cs) * V + min(c, cm), c < nc);
+__device__ __forceinline__ void xp_fetch_info(const Plane4Params& p, int t, P4XTile* dst) {
+  const char* src = (const char*)(p.xtiles + t);
+  for (int q = 0; q < (int)sizeof(P4XTile); q += 16) {
+    const unsigned sd = (unsigned)__cvta_generic_to_shared((char*)dst + q);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sd), "l"(src + q) : "memory");
   }
 }
 
-__device__ __forceinline__ void xp_coefs(const Plane4Params& p, int t, double* ca, double* cb) {
-  const int4 tk = p.tiles[t];
-  const MemberDesc* M = p.mem + tk.x;
-  const int v0 = tk.y, nc = tk.z, C = 1 << tk.w, n4 = M->ext[3];
+// every thread: its share of the strided gather of tile x (X x-points x C velocity points)
+__device__ __forceinline__ void xp_issue_gather(const Plane4Params& p, const P4XTile* x, double* Ub) {
+  const int cs = x->cs, C = 1 << cs, V = x->V, cm = x->nc - 1;
+  const int NT = (x->n1 * x->n2) << cs;
+  const double* src = p.uin + x->src;
+  for (int e = threadIdx.x; e < NT; e += kP4Threads) {
+    const int c = e & (C - 1);
+    cp_async8(Ub + e, src + (e >> cs) * V + min(c, cm), c < x->nc);
+  }
+}
+
+// threads tid < C: x_j line coefficients at velocity point v0 + tid (models.hpp:341-344)
+__device__ __forceinline__ void xp_coefs(const P4XTile* x, double* ca, double* cb) {
   const int tid = threadIdx.x;
-  if (tid < C) {  // x_j lines at velocity point vl: coefficient v_j (models.hpp:341-344)
-    const int vl = v0 + min(tid, nc - 1);
-    const int i3 = vl / n4;
-    ca[tid] = line_coef(p.flux_a, M, 0, p.space_dim, i3, p.c_a, p.efield);
-    cb[tid] = line_coef(p.flux_b, M, 1, p.space_dim, vl - i3 * n4, p.c_b, p.efield);
+  if (tid < (1 << x->cs)) {
+    const int vl = x->v0 + min(tid, x->nc - 1);
+    const int i3 = vl / x->n4;
+    ca[tid] = x->ca0 + i3 * x->ca1;
+    cb[tid] = x->cb0 + (vl - i3 * x->n4) * x->cb1;
   }
 }
 
@@ -1076,43 +1079,80 @@ template <bool LINEAR>
 __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_persist_kernel(const Plane4Params p) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double ca[2][kP4MaxC], cb[2][kP4MaxC];
+  __shared__ P4XTile info[4];  // tile `it` of this CTA: tix[it % 4], info[it % 4]
+  __shared__ int tix[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pitch = p.xpitch;
   double* D1 = sm + 2 * pitch;
-  const int stride = gridDim.x, nt = p.ntiles;
-  int t = blockIdx.x;
-  if (t >= nt) return;
-  xp_coefs(p, t, ca[0], cb[0]);  // static (x coordinates / advection speeds)
+  const int G0 = gridDim.x, nt = p.ntiles;
+  if ((int)blockIdx.x >= nt) return;
+  if (tid == 0) {
+    tix[0] = blockIdx.x;
+    tix[1] = blockIdx.x + G0;
+    xp_fetch_info(p, tix[0], &info[0]);
+    if (tix[1] < nt) xp_fetch_info(p, tix[1], &info[1]);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  xp_coefs(&info[0], ca[0], cb[0]);  // static (x coordinates / advection speeds)
   pdl_wait();
   const StepCtl* ctl = p.ctl;
   if (ctl != nullptr && !ctl->active) return;
-  xp_issue_gather(p, t, sm);
+  if (tid == 0) tix[2] = (tix[1] < nt) ? 2 * G0 + (int)atomicAdd(p.sched, 1u) : nt;
+  xp_issue_gather(p, &info[0], sm);
   cp_async_commit();
   const double eps = p.eps;
-  for (int it = 0; t < nt; t += stride, ++it) {
+#ifdef SGWG_TRACE
+  long long xph[6] = {0, 0, 0, 0, 0, 0};
+  long long xtc = clock64(), xtn;
+#define XPH(k)             \
+  do {                     \
+    xtn = clock64();       \
+    xph[k] += xtn - xtc;   \
+    xtc = xtn;             \
+  } while (0)
+#else
+#define XPH(k) \
+  do {         \
+  } while (0)
+#endif
+  for (int it = 0;; ++it) {
     const int b = it & 1;
-    const int t1 = t + stride;
     cp_async_wait<0>();
-    // [A]: this tile's u (every thread's copies) and coefficients visible; the
-    // previous tile's x2 sweep is done with the other U slot and d/dx1
+    XPH(0);
+    // [A]: this tile's u (every thread's copies), coefficients, descriptors and
+    // indices visible; the previous tile's x2 sweep is done with the other U slot
     __syncthreads();
-    if (t1 < nt && !(p.dbg & 8)) {
-      xp_issue_gather(p, t1, sm + (b ^ 1) * pitch);
-      xp_coefs(p, t1, ca[b ^ 1], cb[b ^ 1]);
+    XPH(1);
+    const int t = tix[it & 3];
+    if (t >= nt) break;
+    const int t1 = tix[(it + 1) & 3];
+    const P4XTile* xi = &info[it & 3];
+    if (t1 < nt) {
+      const P4XTile* x1i = &info[(it + 1) & 3];
+      xp_issue_gather(p, x1i, sm + (b ^ 1) * pitch);
+      xp_coefs(x1i, ca[b ^ 1], cb[b ^ 1]);
     }
-    if (!(p.dbg & 8)) cp_async_commit();
-    const int4 tk = p.tiles[t];
-    const MemberDesc* M = p.mem + tk.x;
-    const int v0 = tk.y, cs = tk.w, C = 1 << cs, nc = tk.z;
-    const int n1 = M->ext[0], n2 = M->ext[1];
-    const int V = M->ext[2] * M->ext[3];
+    unsigned int got = 0u;
+    const bool more = (tid == 0) && tix[(it + 2) & 3] < nt;
+    if (tid == 0 && tix[(it + 2) & 3] < nt) xp_fetch_info(p, tix[(it + 2) & 3], &info[(it + 2) & 3]);
+    if (more) got = atomicAdd(p.sched, 1u);
+    cp_async_commit();
+    XPH(2);
+    const int cs = xi->cs, C = 1 << cs, nc = xi->nc;
+    const int n1 = xi->n1, n2 = xi->n2, V = xi->V;
+    SGWG_DCHECK(t >= 0 && t < nt && p.xtiles[t].src == xi->src && p.xtiles[t].cs == cs &&
+                    p.xtiles[t].nc == nc && p.xtiles[t].V == V,
+                "xpass tile descriptor");
+    SGWG_DCHECK(((n1 * n2) << cs) <= pitch, "xpass tile exceeds its slot");
     const double* U = sm + b * pitch;
     const double* cfa = ca[b];
     const double* cfb = cb[b];
     const int st0 = n2 << cs, wrap0 = n1 * st0, wrap1 = n2 << cs;
     // x1 sweep: lines (x2, c) = l, stride n2 C, n1 points -> d/dx1
     {
-      const double ih1 = M->inv_h[0];
+      const double ih1 = xi->ih1;
       const int nl = n2 << cs, m = n1 >> 3, nb = (nl + 31) >> 5, ntask = nb * m;
       const float inb = 1.0f / (float)nb;
       for (int q = warp; q < ntask; q += kP4Threads / 32) {
@@ -1122,21 +1162,17 @@ __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_persist_kernel(const Pl
                                   eps, ih1, D1 + l + 8 * r * st0);
       }
     }
+    XPH(3);
+    if (tid == 0) tix[(it + 3) & 3] = more ? 2 * G0 + (int)got : nt;  // tile it - 1's slot
     // [B]: d/dx1 complete
     __syncthreads();
-    if (p.dbg & 8) {  // experiment: gather of the next tile issued after the x1 sweep
-      if (t1 < nt) {
-        xp_issue_gather(p, t1, sm + (b ^ 1) * pitch);
-        xp_coefs(p, t1, ca[b ^ 1], cb[b ^ 1]);
-      }
-      cp_async_commit();
-    }
+    XPH(4);
     // x2 sweep: lines (x1, c), stride C, n2 points -> K to global
     {
-      const double ih2 = M->inv_h[1];
+      const double ih2 = xi->ih2;
       const int nl = n1 << cs, m = n2 >> 3, nb = (nl + 31) >> 5, ntask = nb * m;
       const float inb = 1.0f / (float)nb;
-      double* kb = p.kbuf + M->offset + v0;
+      double* kb = p.kbuf + xi->src;
       for (int q = warp; q < ntask; q += kP4Threads / 32) {
         const int r = qdiv(q, inb), l = ((q - r * nb) << 5) + lane;
         if (l >= nl) continue;
@@ -1149,8 +1185,21 @@ __global__ void __launch_bounds__(kP4Threads, 2) xpass4d_persist_kernel(const Pl
                              kb + ((long long)x1 * n2 + 8 * r) * V + c, V);
       }
     }
+    XPH(5);
   }
   cp_async_wait<0>();
+#ifdef SGWG_TRACE
+  if (tid == 0 && blockIdx.x < kP4TraceCtas)
+    for (int k = 0; k < 6; ++k) sgwg_p4trace[0][blockIdx.x][k] = xph[k];
+#endif
+  if (tid == 0) {  // the last CTA out resets the tile counter for the next launch
+    __threadfence();
+    if (atomicAdd(p.sched + 1, 1u) == (unsigned)min(G0, nt) - 1) {
+      p.sched[0] = 0u;
+      p.sched[1] = 0u;
+      __threadfence();
+    }
+  }
 }
 
 cudaError_t launch_plane4(const Plane4Params& p, int pass, int nblocks, size_t smem,

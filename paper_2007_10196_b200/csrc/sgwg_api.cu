@@ -274,6 +274,8 @@ struct sgwg_family {
   int p4xpitch = 0;                        // > 0: persistent x pass, slot pitch (doubles)
   P4VTile* dp4vtiles = nullptr;            // persistent v pass: tile descriptors
   unsigned int* dp4sched = nullptr;        // persistent v pass: dynamic tile counter (2 words)
+  P4XTile* dp4xtiles = nullptr;            // persistent x pass: tile descriptors
+  unsigned int* dp4xsched = nullptr;       // persistent x pass: dynamic tile counter
   double* rho_parts = nullptr;      // Vlasov-Poisson charge-density partial sums
   double* twid = nullptr;           // FFT twiddle table (2 x hmax)
   int hmax = 1;
@@ -513,6 +515,8 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
       }
       if (pass == 0 && f->p4xpitch > 0) {
         p.xpitch = f->p4xpitch;
+        p.xtiles = f->dp4xtiles;
+        p.sched = f->dp4xsched;
         nblk = std::min(nblk, 2 * f->ctx->sm_count);
       }
       CK(fast::launch_plane4(p, pass, nblk, (size_t)f->p4smem[pass] * sizeof(double),
@@ -1414,9 +1418,43 @@ int build_plane4_tiles(sgwg_family* f) {
     // Opt-in (SGWG_P4_XPERSIST=1): measured slower than the one-tile-per-CTA x pass
     // on C5 (150 vs 138 us per launch), unlike the v pass (209 vs 218 us)
     const char* xe = std::getenv("SGWG_P4_XPERSIST");
-    if (xe != nullptr && xe[0] == '1' && 3LL * xp * 8 + 1300 <= 115712) {
+    if (xe != nullptr && xe[0] == '1' && 3LL * xp * 8 + 1800 <= 115712) {
       f->p4xpitch = xp;
       f->p4smem[0] = 3 * xp;
+      std::vector<P4XTile> xt;
+      const int sd = m.space_dim;
+      for (const int4& q : t[0]) {
+        const MemberDesc& M = f->hmem[q.x];
+        P4XTile x{};
+        x.src = M.offset + q.y;
+        x.ih1 = M.inv_h[0];
+        x.ih2 = M.inv_h[1];
+        if (m.kind == SGWG_VLASOV_POISSON) {  // kinetic x lines: c = v_j (models.hpp:341-344)
+          x.ca0 = M.lower[sd + 0];
+          x.ca1 = M.h[sd + 0];
+          x.cb0 = M.lower[sd + 1];
+          x.cb1 = M.h[sd + 1];
+        } else {  // advection speeds of dims 0, 1
+          x.ca0 = m.speeds[0];
+          x.cb0 = m.speeds[1];
+        }
+        x.V = M.ext[2] * M.ext[3];
+        x.cs = q.w;
+        x.nc = q.z;
+        x.n1 = M.ext[0];
+        x.n2 = M.ext[1];
+        x.n4 = M.ext[3];
+        x.v0 = q.y;
+        x.mi = q.x;
+        xt.push_back(x);
+      }
+      cudaFree(f->dp4xtiles);
+      f->dp4xtiles = nullptr;
+      TRY(upload_vec(&f->dp4xtiles, xt));
+      if (f->dp4xsched == nullptr) {
+        CK(cudaMalloc(&f->dp4xsched, 2 * sizeof(unsigned int)));
+        CK(cudaMemset(f->dp4xsched, 0, 2 * sizeof(unsigned int)));
+      }
     }
     int pitch = 0;
     for (const int4& q : t[1]) {
@@ -1453,7 +1491,6 @@ int build_plane4_tiles(sgwg_family* f) {
       vt.push_back(v);
     }
     cudaFree(f->dp4vtiles);
-  cudaFree(f->dp4sched);
     f->dp4vtiles = nullptr;
     TRY(upload_vec(&f->dp4vtiles, vt));
     if (f->dp4sched == nullptr) {
@@ -2094,6 +2131,9 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->dp4tiles[0]);
   cudaFree(f->dp4tiles[1]);
   cudaFree(f->dp4vtiles);
+  cudaFree(f->dp4sched);
+  cudaFree(f->dp4xtiles);
+  cudaFree(f->dp4xsched);
   cudaFree(f->rho_parts);
   cudaFree(f->twid);
   cudaFree(f->Fu);

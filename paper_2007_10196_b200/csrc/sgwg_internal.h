@@ -199,6 +199,16 @@ struct __align__(16) P4VTile {
 };
 static_assert(sizeof(P4VTile) == 96, "P4VTile is copied in 16-byte pieces");
 
+// x-pass tile descriptor of the persistent 4D x pass (plane4d.cuh): the gather and
+// the line coefficients without dependent loads (host-precomputed)
+struct __align__(16) P4XTile {
+  long long src;           // member offset + v0 (doubles)
+  double ih1, ih2;
+  double ca0, ca1, cb0, cb1;  // x_j line coefficients: ca0 + i3 ca1, cb0 + i4 cb1 (KinX / advection)
+  int V, cs, nc, n1, n2, n4, v0, mi;
+};
+static_assert(sizeof(P4XTile) == 96, "P4XTile is copied in 16-byte pieces");
+
 // fast 4D stage on whole planes (plane4d.cuh): x pass tiles (mi, v0, nc, log2 C),
 // v pass tiles (mi, x0, G, -)
 struct Plane4Params {
@@ -223,6 +233,7 @@ struct Plane4Params {
   int rpt;                 // runs per warp task (plane4d.cuh P4Sweeps)
   int xpitch;              // > 0: persistent x pass (xpass4d_persist_kernel), slot pitch in doubles
   const P4VTile* vtiles;   // persistent v pass: descriptor per tile
+  const P4XTile* xtiles;   // persistent x pass: descriptor per tile
   unsigned int* sched;     // persistent v pass: [next tile counter, CTAs done] (self-resetting)
   int vpitch;              // > 0: persistent v pass (vpass4d_persist_kernel), slot pitch in doubles
   int ntiles;              // v-pass tiles (persistent form)
