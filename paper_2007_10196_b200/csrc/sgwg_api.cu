@@ -238,6 +238,9 @@ struct sgwg_family {
   cudaEvent_t evs0 = nullptr, evs1 = nullptr;  // whole combined_stats span (ev0/ev1 time each slab)
   cudaStream_t side = nullptr;                 // off-critical-path work (energy record)
   cudaEvent_t evfork = nullptr, evjoin = nullptr;
+  cudaStream_t side2 = nullptr;        // x pass concurrent with the VP field solve
+  cudaEvent_t evfork2 = nullptr, evjoin2 = nullptr;
+  bool p4x_forked = false;
   // current policy for graph building
   DtParams dtp{};
   DtParams* d_dtp = nullptr;       // device copy (fused dt)
@@ -436,11 +439,110 @@ double* fields_of(const sgwg_family* f, const double* state) {
 
 // One RK stage (stage 1..3) or a bare tendency evaluation (stage 0).
 // fuse_dt: the stage-3 kernel also computes the next step's dt (last CTA).
+// one pass of the whole-plane 4D stage (plane4d.cuh) on stream s
+int launch_p4_pass(sgwg_family* f, int stage, const StageBufs& b, int pass, cudaStream_t s,
+                   bool timed, const DtParams* dtp) {
+  const sgwg_model& m = f->model;
+  const bool vp = (m.kind == SGWG_VLASOV_POISSON);
+  Plane4Params p{};
+  p.mem = f->dmem;
+  p.stage = stage;
+  p.linear = (m.weno_mode == SGWG_WENO_LINEAR);
+  p.eps = m.epsilon;
+  p.space_dim = m.space_dim;
+  p.uin = b.uin;
+  p.un = b.un;
+  p.out = b.out;
+  p.kbuf = f->K;
+  p.efield = f->E;
+  p.ctl = f->ctl;
+  p.fail = f->fail;
+  p.counter = f->counter;
+  p.rpt = 1;
+  if (const char* e = std::getenv("SGWG_P4_RPT")) p.rpt = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SGWG_P4_DBG")) p.dbg = std::atoi(e);
+  p.masked = 1;
+  if (const char* e = std::getenv("SGWG_P4_MASKED")) p.masked = std::atoi(e);
+  p.tiles = f->dp4tiles[pass];
+  if (vp) {
+    p.flux_a = p.flux_b = (pass == 0) ? kFluxKinX : kFluxKinVP;
+  } else {
+    p.flux_a = p.flux_b = kFluxAdvect;
+    p.c_a = m.speeds[2 * pass];
+    p.c_b = m.speeds[2 * pass + 1];
+  }
+  p.rho_parts = (pass == 1 && vp) ? f->rho_parts : nullptr;
+  p.dtp = dtp;
+  if (timed) CK(cudaEventRecord(f->ev0, s));
+  int nblk = f->np4tiles[pass];
+  p.ntiles = nblk;
+  if (pass == 1 && f->p4vpitch > 0) {
+    p.vpitch = f->p4vpitch;
+    p.vtiles = f->dp4vtiles;
+    p.sched = f->dp4sched;
+    nblk = std::min(nblk, 2 * f->ctx->sm_count);
+  }
+  if (pass == 0 && f->p4xpitch > 0) {
+    p.xpitch = f->p4xpitch;
+    p.xtiles = f->dp4xtiles;
+    p.sched = f->dp4xsched;
+    nblk = std::min(nblk, 2 * f->ctx->sm_count);
+  }
+  CK(fast::launch_plane4(p, pass, nblk, (size_t)f->p4smem[pass] * sizeof(double), s));
+  if (timed) {
+    CK(cudaEventRecord(f->ev1, s));
+    CK(cudaEventSynchronize(f->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
+    account_timed(f, stage, 2, pass == 1, ms);
+    // algorithmic counts per launch: 70 flops per point and
+    // direction; x pass + K (1), v pass + accumulate (2) + RK stage (2/5/5) +
+    // charge density (2); HBM: u^(s) in, K out | u^(s), K, (u^n) in, out out
+    const double pts = (double)f->total;
+    const double rk = (stage == 0) ? 0.0 : (stage == 1 ? 2.0 : 5.0);
+    if (pass == 0)
+      account_kernel(f, "xpass4d_kernel", ms, pts * 141.0, pts * 16.0);
+    else
+      account_kernel(f, "vpass4d_kernel", ms, pts * (142.0 + rk + (vp ? 2.0 : 0.0)),
+                     pts * (stage > 1 ? 32.0 : 24.0));
+  }
+  f->stats.kernel_launches++;
+  return SGWG_OK;
+}
+
+// Vlasov-Poisson on the whole-plane 4D path: the stage's x pass does not read the
+// field, so it runs on a second stream concurrently with the field solve (and,
+// for stage 1, the dt and energy kernels); the v pass joins it.  Graph-captured
+// steps only (timed launches stay serial for the per-kernel clock).
+bool p4_overlap(const sgwg_family* f, bool timed) {
+  if (timed || !plane4_path(f) || f->model.kind != SGWG_VLASOV_POISSON) return false;
+  const char* e = std::getenv("SGWG_P4_OVERLAP");
+  return e == nullptr || e[0] != '0';
+}
+// the fork point (before the field solve), then -- after the field kernels have been
+// enqueued, so they are dispatched first -- the x pass on the low-priority stream
+int mark_x_fork(sgwg_family* f) {
+  CK(cudaEventRecord(f->evfork2, f->ctx->stream));
+  return SGWG_OK;
+}
+int fork_x_pass(sgwg_family* f, int stage, const StageBufs& b) {
+  CK(cudaStreamWaitEvent(f->side2, f->evfork2, 0));
+  TRY(launch_p4_pass(f, stage, b, 0, f->side2, false, nullptr));
+  CK(cudaEventRecord(f->evjoin2, f->side2));
+  f->p4x_forked = true;
+  return SGWG_OK;
+}
+
 int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool with_field = true,
                  bool fuse_dt = false) {
   const sgwg_model& m = f->model;
   const bool burgers = (m.kind == SGWG_BURGERS);
-  if (m.kind == SGWG_VLASOV_POISSON && with_field) TRY(launch_field_for(f, b.uin, stage));
+  if (m.kind == SGWG_VLASOV_POISSON && with_field) {
+    const bool ovl = p4_overlap(f, timed) && !f->p4x_forked;
+    if (ovl) TRY(mark_x_fork(f));
+    TRY(launch_field_for(f, b.uin, stage));
+    if (ovl) TRY(fork_x_pass(f, stage, b));
+  }
   const auto order = pass_order(f);
   const int in_slot = (stage == 0) ? 0 : stage - 1;
   const int out_slot = (stage == 0) ? 0 : stage % 3;
@@ -472,74 +574,11 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
   if (stage > 0 && !plane_path(f) && !plane4_path(f)) f->parts_of = nullptr;
   if (plane4_path(f)) {  // fast 4D on whole planes: x pass -> K, v pass + RK stage + rho
     const bool vp = (m.kind == SGWG_VLASOV_POISSON);
-    Plane4Params p{};
-    p.mem = f->dmem;
-    p.stage = stage;
-    p.linear = (m.weno_mode == SGWG_WENO_LINEAR);
-    p.eps = m.epsilon;
-    p.space_dim = m.space_dim;
-    p.uin = b.uin;
-    p.un = b.un;
-    p.out = b.out;
-    p.kbuf = f->K;
-    p.efield = f->E;
-    p.ctl = f->ctl;
-    p.fail = f->fail;
-    p.counter = f->counter;
-    p.rpt = 1;
-    if (const char* e = std::getenv("SGWG_P4_RPT")) p.rpt = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("SGWG_P4_DBG")) p.dbg = std::atoi(e);
-    p.masked = 1;
-    if (const char* e = std::getenv("SGWG_P4_MASKED")) p.masked = std::atoi(e);
-    for (int pass = 0; pass < 2; ++pass) {
-      p.tiles = f->dp4tiles[pass];
-      if (vp) {
-        p.flux_a = p.flux_b = (pass == 0) ? kFluxKinX : kFluxKinVP;
-      } else {
-        p.flux_a = p.flux_b = kFluxAdvect;
-        p.c_a = m.speeds[2 * pass];
-        p.c_b = m.speeds[2 * pass + 1];
-      }
-      p.rho_parts = (pass == 1 && vp) ? f->rho_parts : nullptr;
-      p.dtp = (pass == 1) ? dtp : nullptr;
-      if (timed) CK(cudaEventRecord(f->ev0, f->ctx->stream));
-      int nblk = f->np4tiles[pass];
-      p.vpitch = 0;
-      p.xpitch = 0;
-      p.ntiles = nblk;
-      if (pass == 1 && f->p4vpitch > 0) {
-        p.vpitch = f->p4vpitch;
-        p.vtiles = f->dp4vtiles;
-        p.sched = f->dp4sched;
-        nblk = std::min(nblk, 2 * f->ctx->sm_count);
-      }
-      if (pass == 0 && f->p4xpitch > 0) {
-        p.xpitch = f->p4xpitch;
-        p.xtiles = f->dp4xtiles;
-        p.sched = f->dp4xsched;
-        nblk = std::min(nblk, 2 * f->ctx->sm_count);
-      }
-      CK(fast::launch_plane4(p, pass, nblk, (size_t)f->p4smem[pass] * sizeof(double),
-                             f->ctx->stream));
-      if (timed) {
-        CK(cudaEventRecord(f->ev1, f->ctx->stream));
-        CK(cudaEventSynchronize(f->ev1));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, f->ev0, f->ev1));
-        account_timed(f, stage, 2, pass == 1, ms);
-        // algorithmic counts per launch: 70 flops per point and
-        // direction; x pass + K (1), v pass + accumulate (2) + RK stage (2/5/5) +
-        // charge density (2); HBM: u^(s) in, K out | u^(s), K, (u^n) in, out out
-        const double pts = (double)f->total;
-        const double rk = (stage == 0) ? 0.0 : (stage == 1 ? 2.0 : 5.0);
-        if (pass == 0)
-          account_kernel(f, "xpass4d_kernel", ms, pts * 141.0, pts * 16.0);
-        else
-          account_kernel(f, "vpass4d_kernel", ms, pts * (142.0 + rk + (vp ? 2.0 : 0.0)),
-                         pts * (stage > 1 ? 32.0 : 24.0));
-      }
-      f->stats.kernel_launches++;
-    }
+    const bool xdone = f->p4x_forked;  // the x pass already runs on the side stream
+    f->p4x_forked = false;
+    if (xdone) CK(cudaStreamWaitEvent(f->ctx->stream, f->evjoin2, 0));
+    for (int pass = xdone ? 1 : 0; pass < 2; ++pass)
+      TRY(launch_p4_pass(f, stage, b, pass, f->ctx->stream, timed, (pass == 1) ? dtp : nullptr));
     if (stage > 0) f->parts_of = vp ? b.out : nullptr;
     return SGWG_OK;
   }
@@ -784,6 +823,8 @@ int launch_step(sgwg_family* f, bool timed) {
   const bool vp = f->model.kind == SGWG_VLASOV_POISSON;
   const bool fused = dt_fusable(f);
   if (!fused) {
+    const bool ovl = vp && p4_overlap(f, timed);
+    if (ovl) TRY(mark_x_fork(f));
     if (vp) TRY(launch_field_for(f, f->u, 1, /*with_energy=*/true));
     if (f->model.kind == SGWG_VLASOV_MAXWELL) {  // family_wave_speeds of u^n
       VmParams sp{};
@@ -795,6 +836,7 @@ int launch_step(sgwg_family* f, bool timed) {
       f->stats.kernel_launches++;
     }
     TRY(launch_dt_step(f));
+    if (ovl) TRY(fork_x_pass(f, 1, StageBufs{f->u, f->u, f->A}));
     if (vp) TRY(launch_energy_side(f));
   }
   // stage 1: u -> A; stage 2: (A, u) -> B; stage 3: (B, u) -> u (timestep.hpp:91-103)
@@ -1098,6 +1140,13 @@ int family_create(sgwg_ctx* ctx, const sgwg_domain* dom, const int* members, int
   CK(cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&f->evfork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&f->evjoin, cudaEventDisableTiming));
+  {
+    int lo = 0, hi = 0;  // the x pass's stream at the lowest priority
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CK(cudaStreamCreateWithPriority(&f->side2, cudaStreamNonBlocking, lo));
+  }
+  CK(cudaEventCreateWithFlags(&f->evfork2, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&f->evjoin2, cudaEventDisableTiming));
   int st = build_tasks(f);
   if (st != SGWG_OK) return st;
   CK(cudaMalloc(&f->dmem, sizeof(MemberDesc) * std::max(1, f->nm)));
@@ -2166,6 +2215,9 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaEventDestroy(f->evfork);
   cudaEventDestroy(f->evjoin);
   cudaStreamDestroy(f->side);
+  cudaEventDestroy(f->evfork2);
+  cudaEventDestroy(f->evjoin2);
+  cudaStreamDestroy(f->side2);
   sgwg_ctx* ctx = f->ctx;
   delete f;
   if (--ctx->families == 0 && ctx->closing) {
