@@ -501,10 +501,11 @@ int launch_p4_pass(sgwg_family* f, int stage, const StageBufs& b, int pass, cuda
     const double pts = (double)f->total;
     const double rk = (stage == 0) ? 0.0 : (stage == 1 ? 2.0 : 5.0);
     if (pass == 0)
-      account_kernel(f, "xpass4d_kernel", ms, pts * 141.0, pts * 16.0);
+      account_kernel(f, f->p4xpitch > 0 ? "xpass4d_persist_kernel" : "xpass4d_kernel", ms,
+                     pts * 141.0, pts * 16.0);
     else
-      account_kernel(f, "vpass4d_kernel", ms, pts * (142.0 + rk + (vp ? 2.0 : 0.0)),
-                     pts * (stage > 1 ? 32.0 : 24.0));
+      account_kernel(f, f->p4vpitch > 0 ? "vpass4d_persist_kernel" : "vpass4d_kernel", ms,
+                     pts * (142.0 + rk + (vp ? 2.0 : 0.0)), pts * (stage > 1 ? 32.0 : 24.0));
   }
   f->stats.kernel_launches++;
   return SGWG_OK;
@@ -2914,7 +2915,10 @@ int sgwg_kernel_profile_reset(sgwg_family* f) {
 const char* sgwg_stage_kernels(const sgwg_family* f) {
   if (f == nullptr || !f->has_model) return "";
   const bool fast = arith_of(f) == SGWG_ARITH_FAST;
-  if (plane4_path(f)) return "xpass4d_kernel + vpass4d_kernel";
+  if (plane4_path(f))
+    return f->p4vpitch > 0 ? (f->p4xpitch > 0 ? "xpass4d_persist_kernel + vpass4d_persist_kernel"
+                                              : "xpass4d_kernel + vpass4d_persist_kernel")
+                           : "xpass4d_kernel + vpass4d_kernel";
   if (plane_path(f)) return "plane_fast_kernel (x2)";
   if (f->d == 3 && f->ntiles3d_fast > 0 && fast && f->model.kind == SGWG_ADVECTION)
     return "stage3d_small_kernel";
