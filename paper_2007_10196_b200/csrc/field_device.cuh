@@ -294,9 +294,15 @@ __device__ inline void field_member(const FieldParams& p, int mi, double* sh, do
   const double inv_n = 1.0 / (double)nx;
   for (int comp = 0; comp < dx; ++comp) {
     double* E = p.efield + M->xoff * dx + (long long)comp * nx;
+    // the ring copy of the step-start field (batched energy record)
+    double* E2 = (p.ering != nullptr)
+                     ? p.ering + (p.ctl->step % p.ering_slots) * p.ering_stride + M->xoff * dx +
+                           (long long)comp * nx
+                     : nullptr;
     for (int id = threadIdx.x; id < nx; id += blockDim.x) {
       const double e = er[comp][id] * inv_n;
       E[id] = e;
+      if (E2 != nullptr) E2[id] = e;
       lmax[comp] = fmax(lmax[comp], fabs(e));
     }
   }

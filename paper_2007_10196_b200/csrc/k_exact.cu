@@ -28,6 +28,18 @@ __global__ void dt_kernel(const DtParams p) {
   device_step_dt(p, p.use_reduced != 0);
 }
 
+// timing experiments only (SGWG_STAMPS): the device clock at a point of a stream
+__global__ void stamp_kernel(long long* tl, int slot) {
+  pdl_wait();
+  long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  tl[slot] = g;
+}
+
+cudaError_t launch_stamp(long long* tl, int slot, cudaStream_t s) {
+  return launch_k(stamp_kernel, dim3(1), dim3(1), 0, s, tl, slot);
+}
+
 cudaError_t launch_local_speeds(const DtParams& p, cudaStream_t s) {
   return launch_k(local_speeds_kernel, dim3(1), dim3(32), 0, s, p);
 }

@@ -205,6 +205,16 @@ struct sgwg_family {
   int egrp_tsum = 0;               // energy_rows_kernel: 2 x sum of group x2 extents
   double* eparts = nullptr;        // energy_rows_kernel: per finest x row partial sums
   unsigned int* edone = nullptr;   // energy_rows_kernel: CTAs done (self-resetting)
+  // batched energy record of captured step chunks (energy_rows_batch_kernel)
+  double* ering = nullptr;         // kEnergyRing step-start fields
+  long long ering_stride = 0;      // doubles of one field (space_dim x total x points)
+  long long* erecorded = nullptr;  // steps recorded so far
+  double* egrid_b = nullptr;       // the groups' combined fields of a chunk's steps
+  int ecls_n = 0;                  // groups classed by x2 extent (ascending), 0: not usable
+  int ecls_n1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned char egrp_cls[64] = {0};
+  long long egrid_stride = 0;
+  bool ering_step = false;         // the step being enqueued keeps its field in the ring
   // graphs: steps per chunk -> exec
   std::map<int, cudaGraphExec_t> graphs;
   long long graph_key_policy = -1;
@@ -239,6 +249,10 @@ struct sgwg_family {
   cudaStream_t side = nullptr;                 // off-critical-path work (energy record)
   cudaEvent_t evfork = nullptr, evjoin = nullptr;
   cudaStream_t side2 = nullptr;        // x pass concurrent with the VP field solve
+  // timing experiments only (SGWG_STAMPS=file): device-clock stamps between the kernels
+  // of the captured steps, dumped at the end of sgwg_evolve
+  long long* tl = nullptr;
+  std::vector<int> tl_labels;
   cudaEvent_t evfork2 = nullptr, evjoin2 = nullptr;
   bool p4x_forked = false;
   // current policy for graph building
@@ -399,11 +413,71 @@ int launch_field_for(sgwg_family* f, const double* state, int stage, bool with_e
   fp.negrp = groups ? f->negrp : 0;
   fp.ngx = f->ngx;
   fp.egrid = f->egrid;
+  if (with_energy && f->ering_step) {
+    fp.ering = f->ering;
+    fp.ering_stride = f->ering_stride;
+    fp.ering_slots = kEnergyRing;
+    fp.ncls = f->ecls_n;
+    for (int k = 0; k < 8; ++k) fp.cls_n1[k] = f->ecls_n1[k];
+    std::memcpy(fp.grp_cls, f->egrp_cls, sizeof(fp.grp_cls));
+  }
   const bool with_moment = (f->parts_of != state);
   CK(launch_field(fp, f->nm, with_moment, f->ctx->stream));
   f->parts_of = state;
   f->stats.kernel_launches += with_moment ? 2 : 1;
   if (with_energy) f->energy_fp = fp;  // recorded after the dt (launch_step)
+  return SGWG_OK;
+}
+
+constexpr int kStampSlots = 4096;
+int stamp(sgwg_family* f, cudaStream_t s, int label) {
+  static const bool on = std::getenv("SGWG_STAMPS") != nullptr;
+  if (!on) return SGWG_OK;
+  if (f->tl == nullptr) return SGWG_OK;
+  if ((int)f->tl_labels.size() >= kStampSlots) return SGWG_OK;
+  CK(launch_stamp(f->tl, (int)f->tl_labels.size(), s));
+  f->tl_labels.push_back(label);
+  return SGWG_OK;
+}
+int dump_stamps(sgwg_family* f) {
+  const char* path = std::getenv("SGWG_STAMPS");
+  if (path == nullptr || f->tl == nullptr) return SGWG_OK;
+  std::vector<long long> h(f->tl_labels.size());
+  CK(cudaMemcpy(h.data(), f->tl, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost));
+  if (FILE* fp = std::fopen(path, "w")) {
+    for (size_t i = 0; i < h.size(); ++i) std::fprintf(fp, "%d %lld\n", f->tl_labels[i], h[i]);
+    std::fclose(fp);
+  }
+  return SGWG_OK;
+}
+
+// The energy record of captured step chunks is batched: the step-start fields go to a ring
+// and one launch at the end of the chunk records all its steps (energy_rows_batch_kernel).
+// Eligible: the one-kernel row form's cases (2D x-grids with member groups, C5).
+bool energy_rows_form(const sgwg_family* f) {
+  const long long fine_x = (long long)f->fine_ext[0] * ((f->model.space_dim == 2) ? f->fine_ext[1] : 1);
+  bool groups = fine_x * f->nm > (1LL << 20);
+  if (const char* e = std::getenv("SGWG_ENERGY_GROUPS")) groups = (e[0] == '1');
+  return f->model.space_dim == 2 && groups && f->negrp > 0 && f->negrp < 64 &&
+         f->egrp_tsum <= 4096 && f->eparts != nullptr &&
+         std::getenv("SGWG_ENERGY_LEGACY") == nullptr;
+}
+bool energy_batched(const sgwg_family* f, bool timed) {
+  if (timed || f->fe == nullptr || f->ering == nullptr || f->comm != nullptr || f->ecls_n == 0 ||
+      f->model.kind != SGWG_VLASOV_POISSON || !energy_rows_form(f))
+    return false;
+  if (const char* e = std::getenv("SGWG_NO_ENERGY"))  // timing experiments only
+    if (e[0] == '1') return false;
+  const char* e = std::getenv("SGWG_ENERGY_BATCH");
+  return e == nullptr || e[0] != '0';
+}
+int launch_energy_batch(sgwg_family* f, int nsteps) {
+  const FieldParams& fp = f->energy_fp;
+  const double hvol = f->fine_h[0] * f->fine_h[1];
+  CK(launch_field_energy_batch(fp, f->dcoef, f->fine_ext[0], f->fine_ext[1], hvol, f->fe, f->fe_cap,
+                               nsteps, f->eparts, f->edone, f->erecorded, f->egrid_b,
+                               f->egrid_stride, f->ctx->stream));
+  f->stats.kernel_launches += 2;
   return SGWG_OK;
 }
 
@@ -425,6 +499,7 @@ int launch_energy_side(sgwg_family* f) {
                      f->eparts != nullptr);
   CK(launch_field_energy(fp, f->dcoef, f->fine_ext[0], fine1, hvol, f->fe, f->fe_cap, f->side,
                          rows ? f->eparts : nullptr, rows ? f->edone : nullptr));
+  TRY(stamp(f, f->side, 11));
   CK(cudaEventRecord(f->evjoin, f->side));
   f->stats.kernel_launches += rows ? 1 : (fp.negrp > 0) ? 2 : 1;
   return SGWG_OK;
@@ -529,6 +604,7 @@ int mark_x_fork(sgwg_family* f) {
 int fork_x_pass(sgwg_family* f, int stage, const StageBufs& b) {
   CK(cudaStreamWaitEvent(f->side2, f->evfork2, 0));
   TRY(launch_p4_pass(f, stage, b, 0, f->side2, false, nullptr));
+  TRY(stamp(f, f->side2, 20 + stage));
   CK(cudaEventRecord(f->evjoin2, f->side2));
   f->p4x_forked = true;
   return SGWG_OK;
@@ -542,6 +618,7 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     const bool ovl = p4_overlap(f, timed) && !f->p4x_forked;
     if (ovl) TRY(mark_x_fork(f));
     TRY(launch_field_for(f, b.uin, stage));
+    TRY(stamp(f, f->ctx->stream, 30 + stage));
     if (ovl) TRY(fork_x_pass(f, stage, b));
   }
   const auto order = pass_order(f);
@@ -578,8 +655,10 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
     const bool xdone = f->p4x_forked;  // the x pass already runs on the side stream
     f->p4x_forked = false;
     if (xdone) CK(cudaStreamWaitEvent(f->ctx->stream, f->evjoin2, 0));
+    if (!timed) TRY(stamp(f, f->ctx->stream, 40 + stage));
     for (int pass = xdone ? 1 : 0; pass < 2; ++pass)
       TRY(launch_p4_pass(f, stage, b, pass, f->ctx->stream, timed, (pass == 1) ? dtp : nullptr));
+    if (!timed) TRY(stamp(f, f->ctx->stream, 50 + stage));
     if (stage > 0) f->parts_of = vp ? b.out : nullptr;
     return SGWG_OK;
   }
@@ -825,8 +904,11 @@ int launch_step(sgwg_family* f, bool timed) {
   const bool fused = dt_fusable(f);
   if (!fused) {
     const bool ovl = vp && p4_overlap(f, timed);
+    f->ering_step = vp && energy_batched(f, timed);
+    if (!timed) TRY(stamp(f, f->ctx->stream, 0));
     if (ovl) TRY(mark_x_fork(f));
     if (vp) TRY(launch_field_for(f, f->u, 1, /*with_energy=*/true));
+    if (!timed) TRY(stamp(f, f->ctx->stream, 31));
     if (f->model.kind == SGWG_VLASOV_MAXWELL) {  // family_wave_speeds of u^n
       VmParams sp{};
       sp.mem = f->dmem;
@@ -837,14 +919,16 @@ int launch_step(sgwg_family* f, bool timed) {
       f->stats.kernel_launches++;
     }
     TRY(launch_dt_step(f));
+    if (!timed) TRY(stamp(f, f->ctx->stream, 1));
     if (ovl) TRY(fork_x_pass(f, 1, StageBufs{f->u, f->u, f->A}));
-    if (vp) TRY(launch_energy_side(f));
+    if (vp && !f->ering_step) TRY(launch_energy_side(f));
   }
   // stage 1: u -> A; stage 2: (A, u) -> B; stage 3: (B, u) -> u (timestep.hpp:91-103)
   StageBufs s1{f->u, f->u, f->A}, s2{f->A, f->u, f->B}, s3{f->B, f->u, f->u};
   // VP: the stage-1 field was computed above (it feeds dt); stages 2, 3 recompute it
   TRY(launch_stage(f, 1, s1, timed, /*with_field=*/!vp));
-  if (vp && !fused && f->fe != nullptr) CK(cudaStreamWaitEvent(f->ctx->stream, f->evjoin, 0));
+  if (vp && !fused && f->fe != nullptr && !f->ering_step)
+    CK(cudaStreamWaitEvent(f->ctx->stream, f->evjoin, 0));
   TRY(launch_stage(f, 2, s2, timed));
   TRY(launch_stage(f, 3, s3, timed, true, fused));
   return SGWG_OK;
@@ -1259,9 +1343,40 @@ int setup_vp(sgwg_family* f) {
     cudaFree(f->edone);
     f->eparts = nullptr;
     f->edone = nullptr;
-    CK(cudaMalloc(&f->eparts, sizeof(double) * std::max(1, f->fine_ext[0])));
-    CK(cudaMalloc(&f->edone, sizeof(unsigned int)));
-    CK(cudaMemset(f->edone, 0, sizeof(unsigned int)));
+    CK(cudaMalloc(&f->eparts, sizeof(double) * std::max(1, f->fine_ext[0]) * kEnergyRing));
+    CK(cudaMalloc(&f->edone, sizeof(unsigned int) * (kEnergyRing + 1)));
+    CK(cudaMemset(f->edone, 0, sizeof(unsigned int) * (kEnergyRing + 1)));
+    cudaFree(f->ering);
+    cudaFree(f->erecorded);
+    f->ering = nullptr;
+    f->erecorded = nullptr;
+    f->ering_stride = (long long)xoff * dx;
+    CK(cudaMalloc(&f->ering, sizeof(double) * std::max<long long>(1, f->ering_stride) * kEnergyRing));
+    CK(cudaMalloc(&f->erecorded, sizeof(long long)));
+    CK(cudaMemset(f->erecorded, 0, sizeof(long long)));
+    {  // classes of groups sharing the x2 extent (energy_row_cls)
+      std::vector<int> ext;
+      for (const auto& k : keys) ext.push_back(k.second);
+      std::sort(ext.begin(), ext.end());
+      ext.erase(std::unique(ext.begin(), ext.end()), ext.end());
+      int tsum = 0;
+      bool ok = ext.size() <= 8 && keys.size() < 64 && dx == 2;
+      for (int e : ext) {
+        tsum += 2 * e;
+        ok = ok && e > 0 && (e & (e - 1)) == 0 && f->fine_ext[1] % e == 0 && f->fine_ext[1] / e <= 128;
+      }
+      ok = ok && tsum <= 1024;
+      f->ecls_n = ok ? (int)ext.size() : 0;
+      if (ok) {
+        for (size_t k = 0; k < ext.size(); ++k) f->ecls_n1[k] = ext[k];
+        for (size_t g = 0; g < keys.size(); ++g)
+          f->egrp_cls[g] = (unsigned char)(std::find(ext.begin(), ext.end(), keys[g].second) - ext.begin());
+      }
+    }
+    cudaFree(f->egrid_b);
+    f->egrid_b = nullptr;
+    f->egrid_stride = std::max(1, off);
+    CK(cudaMalloc(&f->egrid_b, sizeof(double) * f->egrid_stride * kEnergyRing));
     f->negrp = (int)keys.size();
     f->ngx = gx;
   }
@@ -1571,6 +1686,10 @@ int get_graph(sgwg_family* f, int nsteps, cudaGraphExec_t* exec) {
   }
   cudaGraph_t g;
   const long long saved = f->stats.kernel_launches;
+  if (f->tl == nullptr && std::getenv("SGWG_STAMPS") != nullptr) {
+    CK(cudaMalloc(&f->tl, sizeof(long long) * kStampSlots));
+    CK(cudaMemset(f->tl, 0, sizeof(long long) * kStampSlots));
+  }
   CK(cudaStreamBeginCapture(f->ctx->stream, cudaStreamCaptureModeThreadLocal));
   for (int s = 0; s < nsteps; ++s) {
     int st = launch_step(f, false);
@@ -1579,10 +1698,19 @@ int get_graph(sgwg_family* f, int nsteps, cudaGraphExec_t* exec) {
       return st;
     }
   }
+  if (f->ering_step) {  // the chunk's energy records in one launch
+    int st = launch_energy_batch(f, nsteps);
+    if (st != SGWG_OK) {
+      cudaStreamEndCapture(f->ctx->stream, &g);
+      return st;
+    }
+  }
   CK(cudaStreamEndCapture(f->ctx->stream, &g));
   f->stats.kernel_launches = saved;
   cudaGraphExec_t e;
-  CK(cudaGraphInstantiate(&e, g, 0));
+  // per-node priorities (the side streams' kernels below the critical path's): without the
+  // flag every node runs at the priority of the stream the graph is launched into
+  CK(cudaGraphInstantiate(&e, g, std::getenv("SGWG_NO_NODE_PRIO") ? 0 : cudaGraphInstantiateFlagUseNodePriority));
   CK(cudaGraphDestroy(g));
   f->graphs[nsteps] = e;
   *exec = e;
@@ -2087,7 +2215,14 @@ int sgwg_init(int device, sgwg_ctx** out) {
   sgwg_ctx* c = new sgwg_ctx();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
-  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  {
+    // the main stream above the default priority: kernels forked to the family's side
+    // streams (default = lowest priority) must not be dispatched ahead of the critical path
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (const char* e = std::getenv("SGWG_MAIN_PRIO")) hi = std::atoi(e);
+    CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+  }
   CK(exact::configure());
   CK(fast::configure());
   CK(configure_field());
@@ -2196,6 +2331,9 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaFree(f->egrid);
   cudaFree(f->eparts);
   cudaFree(f->edone);
+  cudaFree(f->ering);
+  cudaFree(f->erecorded);
+  cudaFree(f->egrid_b);
   cudaFree(f->fe);
   cudaFree(f->dcoef);
   cudaFreeHost(f->hctl);
@@ -2216,6 +2354,7 @@ int sgwg_family_destroy(sgwg_family* f) {
   cudaEventDestroy(f->evfork);
   cudaEventDestroy(f->evjoin);
   cudaStreamDestroy(f->side);
+  cudaFree(f->tl);
   cudaEventDestroy(f->evfork2);
   cudaEventDestroy(f->evjoin2);
   cudaStreamDestroy(f->side2);
@@ -2447,6 +2586,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
       clear_graphs(f);
     }
     CK(cudaMemsetAsync(f->fe, 0, sizeof(double) * f->fe_cap, s));
+    if (f->erecorded != nullptr) CK(cudaMemsetAsync(f->erecorded, 0, sizeof(long long), s));
   }
   dp.dts = f->dts;
   dp.dts_cap = f->dts_cap;
@@ -2604,6 +2744,7 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
   }
   CK(cudaMemcpyAsync(f->hctl, f->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  TRY(dump_stamps(f));
   f->stats.steps = f->hctl->step;
   if (nsteps) *nsteps = (size_t)f->hctl->step;
   if (dts && cap > 0) {

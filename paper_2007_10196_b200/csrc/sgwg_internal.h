@@ -352,7 +352,18 @@ struct FieldParams {
   int ngx;                 // total group x points
   double* egrid;           // per group: sum_m c_m E_m on the group's x-grid
   const double* ecoef;     // combination coefficient per member (negrp == 0: no groups)
+  // batched energy record (captured step chunks): the step-start field of step k is also
+  // kept in slot k % ering_slots of a ring, and one launch per chunk records every step
+  double* ering;           // ering_slots x ering_stride doubles (nullptr: off)
+  long long ering_stride;
+  int ering_slots;
+  // groups classed by their x2 extent (the batched record sums a class's groups before the
+  // x2 interpolation they share): class extents, each group's class
+  int ncls;
+  int cls_n1[8];
+  unsigned char grp_cls[64];
 };
+constexpr int kEnergyRing = 64;  // >= the steps of a captured chunk
 
 // launchers: one set per arithmetic TU (k_exact.cu, k_fast.cu)
 #define SGWG_DECLARE_LAUNCHERS(NS)                                                        \
@@ -399,11 +410,16 @@ struct DtParams {
 };
 cudaError_t launch_local_speeds(const DtParams& p, cudaStream_t s);
 cudaError_t launch_dt(const DtParams& p, cudaStream_t s);
+cudaError_t launch_stamp(long long* tl, int slot, cudaStream_t s);
 cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* tasks, int ntasks,
                               const double* u, unsigned long long* amax, cudaStream_t s);
 cudaError_t configure_field();
 cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, cudaStream_t s);
 cudaError_t launch_twiddles(double* tw, int hmax, cudaStream_t s);
+cudaError_t launch_field_energy_batch(const FieldParams& p, const double* coef, int fine0, int fine1,
+                                      double hvol, double* out_base, long long cap, int nbatch,
+                                      double* part, unsigned int* done, long long* recorded,
+                                      double* egrid_b, long long egrid_stride, cudaStream_t s);
 cudaError_t launch_field_energy(const FieldParams& p, const double* coef, int fine0, int fine1,
                                 double hvol, double* out_base, long long cap, cudaStream_t s,
                                 double* part = nullptr, unsigned int* done = nullptr);

@@ -1,5 +1,5 @@
 set -u
-mkdir -p gpurun_out/g1
-nvidia-smi --query-gpu=name,clocks.sm,memory.total --format=csv > gpurun_out/g1/smi.txt 2>&1
-timeout 600 python tools/c5_combine.py fast > gpurun_out/g1/c5_combine.log 2>&1; echo "c5comb rc=$?"
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/g1/pytest.log 2>&1; echo "pytest rc=$?"
+O=gpurun_out/r3d; mkdir -p $O
+python tools/energy_ab.py > $O/energy_ab.log 2>&1; cat $O/energy_ab.log
+python tools/stamps.py $O/stamps.txt > $O/stamps.log 2>&1; echo "stamps rc=$?"; cat $O/stamps.log
+python tools/profile_evolve.py --config C5 --tfinal 0.52 > $O/plain.log 2>&1; cat $O/plain.log
