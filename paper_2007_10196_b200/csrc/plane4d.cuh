@@ -99,110 +99,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       : "memory");
 }
 
-// Reference-form fallback of adv_run (recon_ref: weno5_flux_positive /
-// _negative, weno.hpp:60-80): taken only when the fast form overflowed
-// (|u| >~ 1e36 makes the common-denominator weights infinite, the reference's
-// separate divides do not).
-template <int RUN, int GL, int GR, bool ZERO>
-__device__ __forceinline__ void adv_run_ref(const double* __restrict__ P, int st, int wrap, double c,
-                                         double eps, int linear, double inv_h,
-                                         double* __restrict__ out, int ost) {
-  constexpr int NV = RUN + 6;
-  double f[NV];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    if (q < GL)
-      f[q] = ZERO ? 0.0 : c * P[q * st + wrap];
-    else if (q >= NV - GR)
-      f[q] = ZERO ? 0.0 : c * P[q * st - wrap];
-    else
-      f[q] = c * P[q * st];
-  }
-  const bool rev = c < 0.0;
-  double Fp = 0.0;
-#pragma unroll
-  for (int t = 0; t <= RUN; ++t) {
-    const int i = t + 2, m = t + 3;
-    const double F = rev ? recon_ref(f[m + 2], f[m + 1], f[m], f[m - 1], f[m - 2], eps, linear)
-                         : recon_ref(f[i - 2], f[i - 1], f[i], f[i + 1], f[i + 2], eps, linear);
-    if (t > 0) out[(t - 1) * ost] = (F - Fp) * inv_h;
-    Fp = F;
-  }
-}
-
 // du/dx of c*u (upwind WENO5-JS, advect_derivative_line weno.hpp:160-192) for
 // RUN consecutive points of one line.  P: the window's first value (physical
-// point 8r - 3 of the line), st: smem stride along the line.  GL / GR values at
-// the window ends are ghosts: zeros (ZERO) or the periodic image at -/+ wrap.
-// Writes out[k*ost] = du.  Downwind lines (c < 0) use
-// the mirrored reconstruction on the same physically ordered window.
-template <int RUN, int GL, int GR, bool ZERO, bool LINEAR>
-__device__ __noinline__ bool adv_run_fast(const double* __restrict__ P, int st, int wrap, double c,
-                                          double eps, double inv_h, double* __restrict__ out,
-                                          int ost) {
-  constexpr int NV = RUN + 6;
-  double f[NV];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    if (q < GL)
-      f[q] = ZERO ? 0.0 : c * P[q * st + wrap];
-    else if (q >= NV - GR)
-      f[q] = ZERO ? 0.0 : c * P[q * st - wrap];
-    else
-      f[q] = c * P[q * st];
-  }
-  const double eps4 = 4.0 * eps;
-  double D[NV], K[NV], dd[NV];
-#pragma unroll
-  for (int q = 1; q < NV - 1; ++q) {
-    D[q] = fma(-2.0, f[q], f[q - 1] + f[q + 1]);
-    K[q] = fma(13.0 / 3.0 * D[q], D[q], eps4);
-  }
-#pragma unroll
-  for (int q = 1; q < NV; ++q) dd[q] = f[q] - f[q - 1];
-  double Fp = 0.0;
-  int ex = 0;  // max exponent field of the outputs (overflow guard)
-  if (!(c < 0.0)) {
-#pragma unroll
-    for (int t = 0; t <= RUN; ++t) {
-      const int i = t + 2;
-      const double F = recon_roles<LINEAR>(f[i], D[i - 1], D[i], D[i + 1], K[i - 1], K[i],
-                                           K[i + 1], dd[i], dd[i + 1]);
-      if (t > 0) {
-        const double du = (F - Fp) * inv_h;
-        ex = max(ex, __double2hiint(du) & 0x7ff00000);
-        out[(t - 1) * ost] = du;
-      }
-      Fp = F;
-    }
-  } else {
-#pragma unroll
-    for (int t = 0; t <= RUN; ++t) {
-      const int m = t + 3;
-      const double F = recon_roles<LINEAR>(f[m], D[m + 1], D[m], D[m - 1], K[m + 1], K[m],
-                                           K[m - 1], -dd[m + 1], -dd[m]);
-      if (t > 0) {
-        const double du = (F - Fp) * inv_h;
-        ex = max(ex, __double2hiint(du) & 0x7ff00000);
-        out[(t - 1) * ost] = du;
-      }
-      Fp = F;
-    }
-  }
-  // overflow guard: a non-finite du (all exponent bits set, tracked on the
-  // integer pipe) re-runs the window in the reference form, overwriting the
-  // outputs (inlined: the run stays a leaf function)
-  if (ex == 0x7ff00000) adv_run_ref<RUN, GL, GR, ZERO>(P, st, wrap, c, eps, LINEAR, inv_h, out, ost);
-  return false;
-}
-
-template <int RUN, int GL, int GR, bool ZERO, bool LINEAR>
-__device__ __forceinline__ void adv_run(const double* __restrict__ P, int st, int wrap, double c,
-                                        double eps, double inv_h, double* __restrict__ out,
-                                        int ost) {
-  adv_run_fast<RUN, GL, GR, ZERO, LINEAR>(P, st, wrap, c, eps, inv_h, out, ost);
-}
-
+// point 8r - 3 of the line), st: smem stride along the line.  Writes
+// out[k*ost] = du.  Downwind lines (c < 0) use the mirrored reconstruction on
+// the same physically ordered window.
 // Masked form: one instantiation per (RUN, ghost kind) -- the ghost counts
 // gl (left) / gr (right) of the run are runtime values (integer selects on the
 // six window ends), so every full run of a sweep shares one body: a small hot
@@ -385,79 +286,57 @@ __device__ __noinline__ void adv_run_kout(const double* __restrict__ P, int st, 
 }
 
 // ---------------------------------------------------------------------------
-// Warp tasks.  A task is 32 consecutive lines of one sweep (one per lane) and
-// a range of <= rpt consecutive runs along them (rpt = 1 by default: equal-cost
-// tasks, so the round-robin assignment to warps is balanced to one run): the
-// line address is decoded once per task, the runs follow by pointer steps,
-// and the run position -- first (left ghosts), middle, last (right ghosts),
-// the tail point of a zero-ghost line of 8m + 1 points -- is warp-uniform, so
-// the ghost pattern is a compile-time property of the adv_run instantiation
-// each run calls.  Tasks are decoded arithmetically by every warp (no table,
-// no serial set-up before the CTA's first barrier).
+// Warp tasks.  The work items of a sweep are its (line, full run of 8 points)
+// pairs, numbered run-major (item = r * nlines + l) and packed 32 to a warp
+// task, so every lane of every task but a sweep's last has a run whatever the
+// line count (a velocity plane of 9 x 257 points has 9 rows: with a task = 32
+// lines of one run, 9 lanes of 32 worked).  A lane's run position -- first /
+// middle / last of its line -- is a runtime value: the masked run body selects
+// the ghosts per lane.  The tail points of zero-ghost lines of 8m + 1 points
+// are separate, cheap tasks (32 lines each) dealt last.  Tasks are decoded
+// arithmetically by every warp (no table, no serial set-up) and dealt round
+// robin: full runs of sweep 0, of sweep 1, then the tails.
 // ---------------------------------------------------------------------------
 struct P4Sweeps {
   // per sweep s = 0, 1 as scalars (a runtime-indexed array would live in local memory)
-  int nl0, nl1, m0, m1, nb0, nb1, nr0, nr1, nt0, ntask, rpt;
-  float inb0, inb1;
+  int nl0, nl1, m0, m1, nf0, nf1, nt0, nt1;
+  float inl0, inl1;
   __device__ void set(int s, int nlines_, int m_, bool zero) {
-    const int nb = (nlines_ + 31) >> 5, nr = m_ + (zero ? 1 : 0);
+    const int nf = (nlines_ * m_ + 31) >> 5, nt = zero ? (nlines_ + 31) >> 5 : 0;
     if (s == 0) {
-      nl0 = nlines_, m0 = m_, nb0 = nb, nr0 = nr, inb0 = 1.0f / (float)nb;
+      nl0 = nlines_, m0 = m_, nf0 = nf, nt0 = nt, inl0 = 1.0f / (float)nlines_;
     } else {
-      nl1 = nlines_, m1 = m_, nb1 = nb, nr1 = nr, inb1 = 1.0f / (float)nb;
+      nl1 = nlines_, m1 = m_, nf1 = nf, nt1 = nt, inl1 = 1.0f / (float)nlines_;
     }
   }
-  __device__ void finish(int rpt_) {
-    rpt = rpt_;
-    const int c0 = (nr0 + rpt - 1) / rpt, c1 = (nr1 + rpt - 1) / rpt;
-    nt0 = nb0 * c0;
-    ntask = nt0 + nb1 * c1;
-  }
-  // task t -> sweep, line (lane's), run range [r0, r1), the sweep's line count and runs
-  __device__ __forceinline__ void decode(int t, int lane, int& sw, int& l, int& r0, int& r1,
-                                         int& nlines, int& m) const {
-    sw = (t >= nt0) ? 1 : 0;
-    const int u = sw ? t - nt0 : t;
-    const int nb = sw ? nb1 : nb0;
-    const int q = qdiv(u, sw ? inb1 : inb0);
-    l = ((u - q * nb) << 5) + lane;
-    r0 = q * rpt;
-    r1 = min(sw ? nr1 : nr0, r0 + rpt);
-    nlines = sw ? nl1 : nl0;
+  __device__ __forceinline__ int ntask() const { return nf0 + nf1 + nt0 + nt1; }
+  // task t, lane -> sweep, line l, run r (r == m: the tail point), m; false: no item
+  __device__ __forceinline__ bool decode(int t, int lane, int& sw, int& l, int& r, int& m) const {
+    int u = t;
+    bool tail = false;
+    if (u < nf0) {
+      sw = 0;
+    } else if ((u -= nf0) < nf1) {
+      sw = 1;
+    } else if ((u -= nf1) < nt0) {
+      sw = 0, tail = true;
+    } else {
+      u -= nt0;
+      sw = 1, tail = true;
+    }
+    const int nl = sw ? nl1 : nl0;
     m = sw ? m1 : m0;
+    const int idx = (u << 5) + lane;
+    if (tail) {
+      l = idx;
+      r = m;
+      return idx < nl;
+    }
+    r = qdiv(idx, sw ? inl1 : inl0);
+    l = idx - r * nl;
+    return r < m;
   }
 };
-
-// adv_run instantiation of run r of a line with m full runs: 0 middle, 1 first,
-// 2 last, 3 single (both ends), 4 zero-ghost tail point
-__device__ __forceinline__ int run_inst(int r, int m) {
-  if (r == m) return 4;
-  if (m == 1) return 3;
-  if (r == 0) return 1;
-  if (r == m - 1) return 2;
-  return 0;
-}
-
-template <bool ZERO, bool LINEAR>
-__device__ __forceinline__ void run_dispatch(int inst, const double* P, int st, int wrap, double c,
-                                             double eps, double inv_h, double* out) {
-  if constexpr (ZERO) {
-    switch (inst) {
-      case 0: adv_run<8, 0, 0, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
-      case 1: adv_run<8, 3, 0, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
-      case 2: adv_run<8, 0, 2, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
-      case 3: adv_run<8, 3, 2, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
-      default: adv_run<1, 0, 3, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
-    }
-  } else {
-    switch (inst) {
-      case 0: adv_run<8, 0, 0, true, LINEAR>(P, st, 0, c, eps, inv_h, out, st); break;
-      case 1: adv_run<8, 3, 0, false, LINEAR>(P, st, wrap, c, eps, inv_h, out, st); break;
-      case 2: adv_run<8, 0, 3, false, LINEAR>(P, st, wrap, c, eps, inv_h, out, st); break;
-      default: adv_run<8, 3, 3, false, LINEAR>(P, st, wrap, c, eps, inv_h, out, st); break;
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // x pass: dims (0, 1) of C velocity points over the whole periodic x-plane
@@ -501,7 +380,6 @@ __global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) xpass4d_kernel(const
   P4Sweeps T;
   T.set(0, n2 << cs, n1 >> 3, false);
   T.set(1, n1 << cs, n2 >> 3, false);
-  T.finish(p.rpt);
   P4MARK(0, 1);
   cp_async_wait<0>();
   __syncthreads();
@@ -509,30 +387,18 @@ __global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) xpass4d_kernel(const
   const int lane = tid & 31, warp = tid >> 5;
   const int st0 = n2 << cs, wrap0 = n1 * st0, wrap1 = n2 << cs;
   const double ih1 = M->inv_h[0], ih2 = M->inv_h[1], eps = p.eps;
-  for (int t = (p.dbg & 1) ? T.ntask : warp; t < T.ntask; t += kP4Threads / 32) {
-    int sw, l, r0, r1, nlines, m;
-    T.decode(t, lane, sw, l, r0, r1, nlines, m);
-    if (l >= nlines) continue;
+  const int ntask = T.ntask();
+  for (int t = (p.dbg & 1) ? ntask : warp; t < ntask; t += kP4Threads / 32) {
+    int sw, l, r, m;
+    if (!T.decode(t, lane, sw, l, r, m)) continue;
     const int c = l & (C - 1);
     if (sw == 0) {
-      const double cf = ca[c];
-      for (int r = r0; r < r1; ++r)
-        if (p.masked)
-          run_masked<false, LINEAR>(r, m, U + l + (8 * r - 3) * st0, st0, wrap0, cf, eps, ih1,
-                                    D1 + l + 8 * r * st0);
-        else
-          run_dispatch<false, LINEAR>(run_inst(r, m), U + l + (8 * r - 3) * st0, st0, wrap0,
-                                      cf, eps, ih1, D1 + l + 8 * r * st0);
+      run_masked<false, LINEAR>(r, m, U + l + (8 * r - 3) * st0, st0, wrap0, ca[c], eps, ih1,
+                                D1 + l + 8 * r * st0);
     } else {
       const int base = (l >> cs) * wrap1 + c;
-      const double cf = cb[c];
-      for (int r = r0; r < r1; ++r)
-        if (p.masked)
-          run_masked<false, LINEAR>(r, m, U + base + (8 * r - 3) * C, C, wrap1, cf, eps, ih2,
-                                    D2 + base + 8 * r * C);
-        else
-          run_dispatch<false, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * C, C, wrap1,
-                                      cf, eps, ih2, D2 + base + 8 * r * C);
+      run_masked<false, LINEAR>(r, m, U + base + (8 * r - 3) * C, C, wrap1, cb[c], eps, ih2,
+                                D2 + base + 8 * r * C);
     }
   }
   P4MARK(0, 3);
@@ -629,7 +495,6 @@ __global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) vpass4d_kernel(const
   P4Sweeps T;
   T.set(0, G * n3, n4 >> 3, true);
   T.set(1, G * n4, n3 >> 3, true);
-  T.finish(p.rpt);
   if (tid < G) {  // v_j lines at x point x0+tid: -E_j(x) (VP) or the advection speed
     ce1[tid] = line_coef(p.flux_a, M, 2, p.space_dim, x0 + tid, p.c_a, p.efield);
     ce2[tid] = line_coef(p.flux_b, M, 3, p.space_dim, x0 + tid, p.c_b, p.efield);
@@ -642,31 +507,19 @@ __global__ void __launch_bounds__(kP4Threads, SGWG_P4_MINB) vpass4d_kernel(const
   {
     const float i3f = 1.0f / (float)n3, i4f = 1.0f / (float)n4;
     const double ih3 = M->inv_h[2], ih4 = M->inv_h[3], eps = p.eps;
-    for (int t = (p.dbg & 1) ? T.ntask : warp; t < T.ntask; t += kP4Threads / 32) {
-      int sw, l, r0, r1, nlines, m;
-      T.decode(t, lane, sw, l, r0, r1, nlines, m);
-      if (l >= nlines) continue;
+    const int ntask = T.ntask();
+    for (int t = (p.dbg & 1) ? ntask : warp; t < ntask; t += kP4Threads / 32) {
+      int sw, l, r, m;
+      if (!T.decode(t, lane, sw, l, r, m)) continue;
       if (sw == 0) {
         const int base = l * n4;
-        const double cf = ce2[qdiv(l, i3f)];
-        for (int r = r0; r < r1; ++r)
-          if (p.masked)
-            run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, cf, eps, ih4,
-                                     DV2 + base + 8 * r);
-          else
-            run_dispatch<true, LINEAR>(run_inst(r, m), U + base + 8 * r - 3, 1, 0, cf, eps,
-                                       ih4, DV2 + base + 8 * r);
+        run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, ce2[qdiv(l, i3f)], eps, ih4,
+                                 DV2 + base + 8 * r);
       } else {
         const int gx = qdiv(l, i4f);
         const int base = gx * V + (l - gx * n4);
-        const double cf = ce1[gx];
-        for (int r = r0; r < r1; ++r)
-          if (p.masked)
-            run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, cf, eps, ih3,
-                                     DV1 + base + 8 * r * n4);
-          else
-            run_dispatch<true, LINEAR>(run_inst(r, m), U + base + (8 * r - 3) * n4, n4, 0, cf,
-                                       eps, ih3, DV1 + base + 8 * r * n4);
+        run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, ce1[gx], eps, ih3,
+                                 DV1 + base + 8 * r * n4);
       }
     }
   }
@@ -794,7 +647,7 @@ __device__ __forceinline__ void vp_issue_ku(const Plane4Params& p, const VInfo& 
 
 // the sweeps of one tile (both directions, all warps); U = the tile's u^(s)
 template <bool LINEAR>
-__device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps, const double* U,
+__device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, double eps, const double* U,
                                             double* DV1, double* DV2, const double* ce1,
                                             const double* ce2, double csign) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -802,28 +655,23 @@ __device__ __noinline__ void vp_tile_sweeps(const VInfo* vi, int rpt, double eps
   P4Sweeps T;
   T.set(0, G * n3, n4 >> 3, true);
   T.set(1, G * n4, n3 >> 3, true);
-  T.finish(rpt);
   const float i3f = 1.0f / (float)n3, i4f = 1.0f / (float)n4;
   const double ih3 = vi->ih3, ih4 = vi->ih4;
-  for (int q = warp; q < T.ntask; q += kP4Threads / 32) {
-    int sw, l, r0, r1, nlines, m;
-    T.decode(q, lane, sw, l, r0, r1, nlines, m);
-    if (l >= nlines) continue;
+  const int ntask = T.ntask();
+  for (int q = warp; q < ntask; q += kP4Threads / 32) {
+    int sw, l, r, m;
+    if (!T.decode(q, lane, sw, l, r, m)) continue;
     if (sw == 0) {
       const int base = l * n4;
-      SGWG_DCHECK(qdiv(l, i3f) == l / n3 && base + 8 * (r1 - 1) < G * V, "vpass row run");
-      const double cf = csign * ce2[qdiv(l, i3f)];
-      for (int r = r0; r < r1; ++r)
-        run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, cf, eps, ih4,
-                                 DV2 + base + 8 * r);
+      SGWG_DCHECK(qdiv(l, i3f) == l / n3 && l < G * n3 && base + 8 * r < G * V, "vpass row run");
+      run_masked<true, LINEAR>(r, m, U + base + 8 * r - 3, 1, 0, csign * ce2[qdiv(l, i3f)], eps,
+                               ih4, DV2 + base + 8 * r);
     } else {
       const int gx = qdiv(l, i4f);
       const int base = gx * V + (l - gx * n4);
-      SGWG_DCHECK(gx == l / n4 && gx < G && base + 8 * (r1 - 1) * n4 < G * V, "vpass column run");
-      const double cf = csign * ce1[gx];
-      for (int r = r0; r < r1; ++r)
-        run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, cf, eps, ih3,
-                                 DV1 + base + 8 * r * n4);
+      SGWG_DCHECK(gx == l / n4 && gx < G && base + 8 * r * n4 < G * V, "vpass column run");
+      run_masked<true, LINEAR>(r, m, U + base + (8 * r - 3) * n4, n4, 0, csign * ce1[gx], eps, ih3,
+                               DV1 + base + 8 * r * n4);
     }
   }
 }
@@ -956,7 +804,7 @@ __global__ void __launch_bounds__(kP4Threads, 2) vpass4d_persist_kernel(const Pl
     P4PH(8);
     mbar_wait(&bar[b], (it >> 1) & 1);
     P4PH(1);
-    vp_tile_sweeps<LINEAR>(vi, p.rpt, p.eps, U, DV1, DV2, ce1[b], ce2[b], csign);
+    vp_tile_sweeps<LINEAR>(vi, p.eps, U, DV1, DV2, ce1[b], ce2[b], csign);
     P4PH(2);
     cp_async_wait<0>();  // this thread's async copies (descriptor, coefficients) landed
     mbar_wait(&bar[2], it & 1);
