@@ -111,3 +111,24 @@ def test_field_energy_record_2d2v(ctx_fast, oracle, monkeypatch, groups):
     assert len(fe) > 3
     assert abs(fe[0] - want0) <= 1e-12 * want0
     assert np.all(np.isfinite(fe)) and np.all(fe > 0)
+
+
+def test_field_energy_batched_matches_per_step(ctx_fast, monkeypatch):
+    """The batched record of captured step chunks (step-start fields in a ring, one
+    group + one row launch per chunk: energy_rows_batch_kernel) against the per-step
+    kernel (SGWG_ENERGY_BATCH=0) on the same run, with stops that cut chunks short:
+    the same steps recorded, equal to rounding (the batched rows sum the groups of an
+    x2 class before interpolating)."""
+    monkeypatch.setenv("SGWG_ENERGY_GROUPS", "1")
+    cfg = configs.config("C5", nl=3)
+    rec = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SGWG_ENERGY_BATCH", mode)
+        fam = gpu_family(ctx_fast, cfg)
+        fam.initialize(cfg["ic"])
+        dts = fam.evolve(cfg["dt_mode"], 0.9, cfl=cfg["cfl"], stops=[0.13, 0.5, 0.9])
+        fe = np.asarray(fam.field_energy())
+        assert len(fe) == len(dts) > 70  # more than one 64-step chunk
+        rec[mode] = fe
+    assert np.all(rec["1"] > 0)
+    assert np.max(np.abs(rec["1"] - rec["0"]) / rec["0"]) < 1e-13

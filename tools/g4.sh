@@ -1,5 +1,4 @@
 set -u
-O=gpurun_out/g4; mkdir -p $O
-timeout 300 python tools/profile_c5.py C5 0.02 > $O/prof.json 2> $O/prof.err; echo "prof rc=$?"
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:"xpass4d|vpass4d" -s 6 -c 2 -o $O/p4 python tools/profile_c5.py C5 0.01 > $O/ncu.log 2>&1; echo "ncu rc=$?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python tools/profile_evolve.py --config C5 --tfinal 0.01 > $O/ncu_l.log 2>&1; echo "ncu launches rc=$?"
+O=gpurun_out/r3m; mkdir -p $O
+timeout 2400 python -m pytest tests -x -q -m gpu > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -8 $O/pytest_gpu.log
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "default rc=$?"; cat $O/bench_default.json | cut -c1-700
