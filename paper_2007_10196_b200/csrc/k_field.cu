@@ -338,6 +338,56 @@ __global__ void __launch_bounds__(256) energy_rows_batch_kernel(const FieldParam
   }
 }
 
+// Batched record of small families without member groups (1D1V C4: 11 members, 1,024
+// finest x points): one CTA per step of the chunk, a thread per finest point over all
+// members (energy_point), the block sum in a fixed order.
+__global__ void __launch_bounds__(256) energy_direct_batch_kernel(const FieldParams p, int fine0,
+                                                                  int fine1, double hvol,
+                                                                  double* out_base, long long cap,
+                                                                  unsigned int* done,
+                                                                  long long* recorded) {
+  pdl_wait();
+  __shared__ double red[8];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const long long taken = p.ctl->step;
+  const long long k = *recorded + b;
+  if (k < taken && k < cap) {  // block-uniform
+    FieldParams q = p;
+    q.efield = p.ering + (k % p.ering_slots) * p.ering_stride;
+    double acc = 0.0;
+    for (int x = tid; x < fine0 * fine1; x += blockDim.x)
+      acc += energy_point<false, false>(q, x, fine0, fine1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+      out_base[k] = tot * hvol;
+    }
+  }
+  if (tid == 0) {  // every CTA has read *recorded before the last one out rewrites it
+    __threadfence();
+    if (atomicAdd(done + kEnergyRing, 1u) == gridDim.x - 1) {
+      done[kEnergyRing] = 0u;
+      *recorded = taken;
+      __threadfence();
+    }
+  }
+}
+
+cudaError_t launch_field_energy_batch_direct(const FieldParams& p, const double* coef, int fine0,
+                                             int fine1, double hvol, double* out_base,
+                                             long long cap, int nbatch, unsigned int* done,
+                                             long long* recorded, cudaStream_t s) {
+  FieldParams q = p;
+  q.ecoef = coef;
+  q.negrp = 0;
+  return launch_k(energy_direct_batch_kernel, dim3(nbatch), dim3(256), 0, s, q, fine0, fine1, hvol,
+                  out_base, cap, done, recorded);
+}
+
 cudaError_t launch_field_energy_batch(const FieldParams& p, const double* coef, int fine0, int fine1,
                                       double hvol, double* out_base, long long cap, int nbatch,
                                       double* part, unsigned int* done, long long* recorded,

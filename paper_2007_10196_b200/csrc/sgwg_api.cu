@@ -462,10 +462,18 @@ bool energy_rows_form(const sgwg_family* f) {
          f->egrp_tsum <= 4096 && f->eparts != nullptr &&
          std::getenv("SGWG_ENERGY_LEGACY") == nullptr;
 }
+// small families without member groups: a CTA per step (energy_direct_batch_kernel)
+bool energy_direct_form(const sgwg_family* f) {
+  const long long fine_x = (long long)f->fine_ext[0] * ((f->model.space_dim == 2) ? f->fine_ext[1] : 1);
+  bool groups = fine_x * f->nm > (1LL << 20);
+  if (const char* e = std::getenv("SGWG_ENERGY_GROUPS")) groups = (e[0] == '1');
+  return !groups && fine_x * f->nm <= (1LL << 17);
+}
 bool energy_batched(const sgwg_family* f, bool timed) {
-  if (timed || f->fe == nullptr || f->ering == nullptr || f->comm != nullptr || f->ecls_n == 0 ||
-      f->model.kind != SGWG_VLASOV_POISSON || !energy_rows_form(f))
+  if (timed || f->fe == nullptr || f->ering == nullptr || f->comm != nullptr ||
+      f->model.kind != SGWG_VLASOV_POISSON)
     return false;
+  if (!(energy_rows_form(f) && f->ecls_n > 0) && !energy_direct_form(f)) return false;
   if (const char* e = std::getenv("SGWG_NO_ENERGY"))  // timing experiments only
     if (e[0] == '1') return false;
   const char* e = std::getenv("SGWG_ENERGY_BATCH");
@@ -473,6 +481,15 @@ bool energy_batched(const sgwg_family* f, bool timed) {
 }
 int launch_energy_batch(sgwg_family* f, int nsteps) {
   const FieldParams& fp = f->energy_fp;
+  if (!(energy_rows_form(f) && f->ecls_n > 0)) {
+    const int dx = f->model.space_dim;
+    const int fine1 = (dx == 2) ? f->fine_ext[1] : 1;
+    const double hv = f->fine_h[0] * ((dx == 2) ? f->fine_h[1] : 1.0);
+    CK(launch_field_energy_batch_direct(fp, f->dcoef, f->fine_ext[0], fine1, hv, f->fe, f->fe_cap,
+                                        nsteps, f->edone, f->erecorded, f->ctx->stream));
+    f->stats.kernel_launches++;
+    return SGWG_OK;
+  }
   const double hvol = f->fine_h[0] * f->fine_h[1];
   CK(launch_field_energy_batch(fp, f->dcoef, f->fine_ext[0], f->fine_ext[1], hvol, f->fe, f->fe_cap,
                                nsteps, f->eparts, f->edone, f->erecorded, f->egrid_b,
@@ -1729,7 +1746,10 @@ int launches_per_step(const sgwg_family* f) {
   if (f->model.kind == SGWG_VLASOV_POISSON) {  // (moment +) field per stage, energy per step
     const long long fine_x = (long long)f->fine_ext[0] *
                              ((f->model.space_dim == 2) ? f->fine_ext[1] : 1);
-    n += ((plane_path(f) || plane4_path(f)) ? 3 : 6) + ((fine_x * f->nm > (1LL << 20)) ? 2 : 1);
+    n += (plane_path(f) || plane4_path(f)) ? 3 : 6;
+    // the energy record: per step, or (captured chunks) batched per chunk -- counted there
+    if (!energy_batched(f, false))
+      n += energy_rows_form(f) ? 1 : ((fine_x * f->nm > (1LL << 20)) ? 2 : 1);
   }
   if (f->comm != nullptr) n += 1;
   return n;
@@ -2715,6 +2735,8 @@ int sgwg_evolve(sgwg_family* f, const sgwg_policy* pol, double tfinal, const dou
           TRY(get_graph(f, chunk, &ge));
           CK(cudaGraphLaunch(ge, s));
           f->stats.kernel_launches += (long long)chunk * lps;
+          if (energy_batched(f, false))
+            f->stats.kernel_launches += (energy_rows_form(f) && f->ecls_n > 0) ? 2 : 1;
           left -= chunk;
         }
       }

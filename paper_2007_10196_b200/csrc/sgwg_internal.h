@@ -416,6 +416,10 @@ cudaError_t launch_member_max(const MemberDesc* mem, int nmembers, const int2* t
 cudaError_t configure_field();
 cudaError_t launch_field(const FieldParams& p, int nmembers, bool with_moment, cudaStream_t s);
 cudaError_t launch_twiddles(double* tw, int hmax, cudaStream_t s);
+cudaError_t launch_field_energy_batch_direct(const FieldParams& p, const double* coef, int fine0,
+                                             int fine1, double hvol, double* out_base,
+                                             long long cap, int nbatch, unsigned int* done,
+                                             long long* recorded, cudaStream_t s);
 cudaError_t launch_field_energy_batch(const FieldParams& p, const double* coef, int fine0, int fine1,
                                       double hvol, double* out_base, long long cap, int nbatch,
                                       double* part, unsigned int* done, long long* recorded,

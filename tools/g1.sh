@@ -1,5 +1,4 @@
 set -u
-O=gpurun_out/r3d; mkdir -p $O
-python tools/energy_ab.py > $O/energy_ab.log 2>&1; cat $O/energy_ab.log
+O=gpurun_out/r3n; mkdir -p $O
 python tools/stamps.py $O/stamps.txt > $O/stamps.log 2>&1; echo "stamps rc=$?"; cat $O/stamps.log
-python tools/profile_evolve.py --config C5 --tfinal 0.52 > $O/plain.log 2>&1; cat $O/plain.log
+SGWG_P4_OVERLAP=0 python tools/stamps.py $O/stamps_noovl.txt > $O/stamps_noovl.log 2>&1; cat $O/stamps_noovl.log
