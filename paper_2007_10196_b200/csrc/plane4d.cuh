@@ -150,50 +150,148 @@ __device__ __noinline__ void adv_run_ref_masked(const double* __restrict__ P, in
   }
 }
 
+// Window load of the fast run: the values in upwind order (a downwind line, c < 0, is the
+// positive reconstruction of the reversed line, weno.hpp:178-183, so only the addressing
+// depends on the direction -- per lane, no divergent branch when the lines of a warp
+// differ in sign).
+template <int RUN, bool ZERO>
+__device__ __forceinline__ void load_window_dir(double* f, const double* __restrict__ P, int st,
+                                                int wrap, int gl, int gr, double c, bool rev) {
+  constexpr int NV = RUN + 6;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    // physical window position of upwind position q: q or NV - 1 - q; only the three
+    // positions at each end can be ghosts
+    const bool endl = (q < 3), endr = (q >= NV - 3);
+    int idx = (rev ? NV - 1 - q : q) * st;
+    bool ghost = false;
+    if (endl || endr) {
+      const int pq = rev ? NV - 1 - q : q;
+      const bool lg = pq < gl, rg = pq >= NV - gr;
+      ghost = lg || rg;
+      if (ZERO) {
+        if (ghost) idx = 3 * st;
+      } else {
+        if (lg) idx += wrap;
+        if (rg) idx -= wrap;
+      }
+    }
+    const double v = c * P[idx];
+    f[q] = (ZERO && ghost) ? 0.0 : v;
+  }
+}
+
+// Three reconstructions side by side (recon_roles step by step over k = 0, 1, 2): three
+// independent dependency chains in flight.  A single reconstruction is a chain ~14 DP
+// operations deep of ~32, and a DFMA result takes ~8 cycles (tools/probe/dfma_ilp.cu), so
+// one chain at a time leaves the DP pipe half idle at four warps per scheduler.
+template <bool LINEAR>
+__device__ __forceinline__ void recon_roles3(const double* fc, const double* A, const double* B,
+                                             const double* C, const double* KA, const double* KB,
+                                             const double* KC, const double* a, const double* b,
+                                             double* F) {
+  double g0[3], c0[3], c1[3], c2[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g0[k] = fma(2.0, a[k], A[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c0[k] = fma(2.0, g0[k], -a[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c1[k] = fma(3.0, b[k], -B[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c2[k] = fma(3.0, b[k], -C[k]);
+  if (LINEAR) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      F[k] = fc[k] + kSixth * fma(0.1, c0[k], fma(0.6, c1[k], 0.3 * c2[k]));
+    return;
+  }
+  double g1[3], g2[3], e0[3], e1[3], e2[3], q0[3], q1[3], q2[3], w0[3], w1[3], w2[3], num[3], den[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g1[k] = a[k] + b[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g2[k] = fma(-2.0, b[k], C[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) e0[k] = fma(g0[k], g0[k], KA[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) e1[k] = fma(g1[k], g1[k], KB[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) e2[k] = fma(g2[k], g2[k], KC[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) q0[k] = e0[k] * e0[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) q1[k] = e1[k] * e1[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) q2[k] = e2[k] * e2[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) w0[k] = q1[k] * q2[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) w1[k] = (6.0 * q0[k]) * q2[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) w2[k] = (3.0 * q0[k]) * q1[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) num[k] = fma(w0[k], c0[k], fma(w1[k], c1[k], w2[k] * c2[k]));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) den[k] = 6.0 * (w0[k] + w1[k] + w2[k]);
+  double r[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r[k]) : "d"(den[k]));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) F[k] = fc[k] + num[k] * r[k];
+}
+
 template <int RUN, bool ZERO, bool LINEAR>
 __device__ __noinline__ void adv_run_masked(const double* __restrict__ P, int st, int wrap, int gl,
                                             int gr, double c, double eps, double inv_h,
                                             double* __restrict__ out, int ost) {
   constexpr int NV = RUN + 6;
+  const bool rev = c < 0.0;
   double f[NV];
-  load_window_masked<RUN, ZERO>(f, P, st, wrap, gl, gr, c);
+  load_window_dir<RUN, ZERO>(f, P, st, wrap, gl, gr, c, rev);
   const double eps4 = 4.0 * eps;
-  double D[NV], K[NV], dd[NV];
+  auto Dq = [&](int q) { return fma(-2.0, f[q], f[q - 1] + f[q + 1]); };
+  auto Kq = [&](int q) {
+    const double d = Dq(q);
+    return fma(13.0 / 3.0 * d, d, eps4);
+  };
+  // interface t (left point i = t + 2 of the upwind-ordered window) -> F[t]
+  double F[RUN + 1];
+  constexpr int NG = (RUN + 1) / 3, REM = (RUN + 1) - 3 * NG;
 #pragma unroll
-  for (int q = 1; q < NV - 1; ++q) {
-    D[q] = fma(-2.0, f[q], f[q - 1] + f[q + 1]);
-    K[q] = fma(13.0 / 3.0 * D[q], D[q], eps4);
+  for (int g = 0; g < NG; ++g) {
+    double fc[3], A[3], B[3], C[3], KA[3], KB[3], KC[3], a[3], b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int i = 3 * g + k + 2;
+      fc[k] = f[i];
+      A[k] = Dq(i - 1);
+      B[k] = Dq(i);
+      C[k] = Dq(i + 1);
+      KA[k] = Kq(i - 1);
+      KB[k] = Kq(i);
+      KC[k] = Kq(i + 1);
+      a[k] = f[i] - f[i - 1];
+      b[k] = f[i + 1] - f[i];
+    }
+    recon_roles3<LINEAR>(fc, A, B, C, KA, KB, KC, a, b, F + 3 * g);
   }
 #pragma unroll
-  for (int q = 1; q < NV; ++q) dd[q] = f[q] - f[q - 1];
-  double Fp = 0.0;
+  for (int k = 0; k < REM; ++k) {
+    const int i = 3 * NG + k + 2;
+    F[3 * NG + k] = recon_roles<LINEAR>(f[i], Dq(i - 1), Dq(i), Dq(i + 1), Kq(i - 1), Kq(i),
+                                        Kq(i + 1), f[i] - f[i - 1], f[i + 1] - f[i]);
+  }
+  // reversed: interface t is the flux left of point RUN - t, so du(RUN - t) = (F[t-1] - F[t]) / h
   int ex = 0;  // max exponent field of the outputs (overflow guard)
-  if (!(c < 0.0)) {
+  const double sh = rev ? -inv_h : inv_h;
 #pragma unroll
-    for (int t = 0; t <= RUN; ++t) {
-      const int i = t + 2;
-      const double F = recon_roles<LINEAR>(f[i], D[i - 1], D[i], D[i + 1], K[i - 1], K[i],
-                                           K[i + 1], dd[i], dd[i + 1]);
-      if (t > 0) {
-        const double du = (F - Fp) * inv_h;
-        ex = max(ex, __double2hiint(du) & 0x7ff00000);
-        out[(t - 1) * ost] = du;
-      }
-      Fp = F;
-    }
-  } else {
-#pragma unroll
-    for (int t = 0; t <= RUN; ++t) {
-      const int m = t + 3;
-      const double F = recon_roles<LINEAR>(f[m], D[m + 1], D[m], D[m - 1], K[m + 1], K[m],
-                                           K[m - 1], -dd[m + 1], -dd[m]);
-      if (t > 0) {
-        const double du = (F - Fp) * inv_h;
-        ex = max(ex, __double2hiint(du) & 0x7ff00000);
-        out[(t - 1) * ost] = du;
-      }
-      Fp = F;
-    }
+  for (int t = 1; t <= RUN; ++t) {
+    const double du = (F[t] - F[t - 1]) * sh;
+    ex = max(ex, __double2hiint(du) & 0x7ff00000);
+    out[(rev ? RUN - t : t - 1) * ost] = du;
   }
   if (ex == 0x7ff00000)
     adv_run_ref_masked<RUN, ZERO, LINEAR>(P, st, wrap, gl, gr, c, eps, inv_h, out, ost);

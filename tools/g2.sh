@@ -1,8 +1,6 @@
 set -u
-O=gpurun_out/r3q; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_landau.py tests/test_gpu_vp.py -x -q -m gpu > $O/pytest_l.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_l.log
-timeout 900 python -m pytest tests/test_gpu_fullsize_parity.py -x -q -m gpu -k "c4" > $O/pytest_c4.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_c4.log
-for b in 1 0; do
-SGWG_ENERGY_BATCH=$b timeout 600 python bench.py --config C4 --steps 2 --warmup 3 --no-cpu-baseline > $O/bench_C4_b$b.json 2> $O/bench_C4_b$b.err; echo "C4 batch=$b rc=$?"; python -c "
-import json;d=json.load(open('$O/bench_C4_b$b.json'));print(d['ms_per_step'],d['value'],d['gpu_launches'])"
-done
+O=gpurun_out/r4d; mkdir -p $O
+timeout 120 python tools/profile_c5.py C5 0.02 > $O/kprof.json 2>&1; echo "rc=$?"; grep -A8 '"name"' $O/kprof.json | grep "name\|avg_us"
+timeout 600 python -m pytest tests/test_gpu_vp.py tests/test_gpu_hardening.py -x -q -m gpu > $O/pytest_vp.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_vp.log
+timeout 300 python -m pytest tests/test_gpu_fullsize_parity.py -x -q -m gpu -k "c5" > $O/pytest_c5.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_c5.log
+timeout 120 python tools/profile_evolve.py --config C5 --tfinal 2.0 > $O/plain2.log 2>&1; cat $O/plain2.log
