@@ -471,8 +471,11 @@ def run_b200(args):
                         "share_ms": k["ms_sum"]})
     per_pt_step = 3 * (142.0 if cfg["kind"] == 1 else 70.0) * cfg["d"] + 2 + 5 + 5
     evolve_flops = total_pts * per_pt_step * nsteps
+    # the persistent cooperative kernel ran iff the evolve needed fewer launches than RK
+    # steps (families that are not co-resident -- S2 -- fall back to one launch per stage)
     persistent = (args.arith == "fast" and cfg["d"] == 2 and cfg["kind"] in (0, 1)
-                  and world == 1 and not os.environ.get("SGWG_NO_PERSIST"))
+                  and world == 1 and not os.environ.get("SGWG_NO_PERSIST")
+                  and st["kernel_launches"] < nsteps)
     if kernels:
         dom_k = max(kernels, key=lambda k: k["share_ms"])
         achieved = dom_k["achieved_tflops"]

@@ -181,66 +181,93 @@ __device__ __forceinline__ void load_window_dir(double* f, const double* __restr
   }
 }
 
-// Three reconstructions side by side (recon_roles step by step over k = 0, 1, 2): three
-// independent dependency chains in flight.  A single reconstruction is a chain ~14 DP
+// N reconstructions side by side (recon_roles step by step over k < N): N independent
+// dependency chains in flight.  A single reconstruction is a chain ~14 DP
 // operations deep of ~32, and a DFMA result takes ~8 cycles (tools/probe/dfma_ilp.cu), so
 // one chain at a time leaves the DP pipe half idle at four warps per scheduler.
-template <bool LINEAR>
-__device__ __forceinline__ void recon_roles3(const double* fc, const double* A, const double* B,
+template <int N, bool LINEAR>
+__device__ __forceinline__ void recon_rolesN(const double* fc, const double* A, const double* B,
                                              const double* C, const double* KA, const double* KB,
                                              const double* KC, const double* a, const double* b,
                                              double* F) {
-  double g0[3], c0[3], c1[3], c2[3];
+  double g0[N], c0[N], c1[N], c2[N];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) g0[k] = fma(2.0, a[k], A[k]);
+  for (int k = 0; k < N; ++k) g0[k] = fma(2.0, a[k], A[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) c0[k] = fma(2.0, g0[k], -a[k]);
+  for (int k = 0; k < N; ++k) c0[k] = fma(2.0, g0[k], -a[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) c1[k] = fma(3.0, b[k], -B[k]);
+  for (int k = 0; k < N; ++k) c1[k] = fma(3.0, b[k], -B[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) c2[k] = fma(3.0, b[k], -C[k]);
+  for (int k = 0; k < N; ++k) c2[k] = fma(3.0, b[k], -C[k]);
   if (LINEAR) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
+    for (int k = 0; k < N; ++k)
       F[k] = fc[k] + kSixth * fma(0.1, c0[k], fma(0.6, c1[k], 0.3 * c2[k]));
     return;
   }
-  double g1[3], g2[3], e0[3], e1[3], e2[3], q0[3], q1[3], q2[3], w0[3], w1[3], w2[3], num[3], den[3];
+  double g1[N], g2[N], e0[N], e1[N], e2[N], q0[N], q1[N], q2[N], w0[N], w1[N], w2[N], num[N], den[N];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) g1[k] = a[k] + b[k];
+  for (int k = 0; k < N; ++k) g1[k] = a[k] + b[k];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) g2[k] = fma(-2.0, b[k], C[k]);
+  for (int k = 0; k < N; ++k) g2[k] = fma(-2.0, b[k], C[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) e0[k] = fma(g0[k], g0[k], KA[k]);
+  for (int k = 0; k < N; ++k) e0[k] = fma(g0[k], g0[k], KA[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) e1[k] = fma(g1[k], g1[k], KB[k]);
+  for (int k = 0; k < N; ++k) e1[k] = fma(g1[k], g1[k], KB[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) e2[k] = fma(g2[k], g2[k], KC[k]);
+  for (int k = 0; k < N; ++k) e2[k] = fma(g2[k], g2[k], KC[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) q0[k] = e0[k] * e0[k];
+  for (int k = 0; k < N; ++k) q0[k] = e0[k] * e0[k];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) q1[k] = e1[k] * e1[k];
+  for (int k = 0; k < N; ++k) q1[k] = e1[k] * e1[k];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) q2[k] = e2[k] * e2[k];
+  for (int k = 0; k < N; ++k) q2[k] = e2[k] * e2[k];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) w0[k] = q1[k] * q2[k];
+  for (int k = 0; k < N; ++k) w0[k] = q1[k] * q2[k];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) w1[k] = (6.0 * q0[k]) * q2[k];
+  for (int k = 0; k < N; ++k) w1[k] = (6.0 * q0[k]) * q2[k];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) w2[k] = (3.0 * q0[k]) * q1[k];
+  for (int k = 0; k < N; ++k) w2[k] = (3.0 * q0[k]) * q1[k];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) num[k] = fma(w0[k], c0[k], fma(w1[k], c1[k], w2[k] * c2[k]));
+  for (int k = 0; k < N; ++k) num[k] = fma(w0[k], c0[k], fma(w1[k], c1[k], w2[k] * c2[k]));
 #pragma unroll
-  for (int k = 0; k < 3; ++k) den[k] = 6.0 * (w0[k] + w1[k] + w2[k]);
-  double r[3];
+  for (int k = 0; k < N; ++k) den[k] = 6.0 * (w0[k] + w1[k] + w2[k]);
+  double r[N];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r[k]) : "d"(den[k]));
+  for (int k = 0; k < N; ++k) asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r[k]) : "d"(den[k]));
 #pragma unroll
-  for (int k = 0; k < 3; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
+  for (int k = 0; k < N; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
+  for (int k = 0; k < N; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) F[k] = fc[k] + num[k] * r[k];
+  for (int k = 0; k < N; ++k) F[k] = fc[k] + num[k] * r[k];
+}
+
+// interfaces T0 .. T0 + NLEFT - 1 in groups of GS side by side
+#ifndef SGWG_P4_GS
+#define SGWG_P4_GS 3
+#endif
+template <int T0, int NLEFT, int GS, bool LINEAR, class DQ, class KQ>
+__device__ __forceinline__ void recon_groups(const double* f, DQ Dq, KQ Kq, double* F) {
+  if constexpr (NLEFT > 0) {
+    constexpr int N = NLEFT < GS ? NLEFT : GS;
+    double fc[N], A[N], B[N], C[N], KA[N], KB[N], KC[N], a[N], b[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int i = T0 + k + 2;
+      fc[k] = f[i];
+      A[k] = Dq(i - 1);
+      B[k] = Dq(i);
+      C[k] = Dq(i + 1);
+      KA[k] = Kq(i - 1);
+      KB[k] = Kq(i);
+      KC[k] = Kq(i + 1);
+      a[k] = f[i] - f[i - 1];
+      b[k] = f[i + 1] - f[i];
+    }
+    recon_rolesN<N, LINEAR>(fc, A, B, C, KA, KB, KC, a, b, F + T0);
+    recon_groups<T0 + N, NLEFT - N, GS, LINEAR>(f, Dq, Kq, F);
+  }
 }
 
 template <int RUN, bool ZERO, bool LINEAR>
@@ -259,31 +286,7 @@ __device__ __noinline__ void adv_run_masked(const double* __restrict__ P, int st
   };
   // interface t (left point i = t + 2 of the upwind-ordered window) -> F[t]
   double F[RUN + 1];
-  constexpr int NG = (RUN + 1) / 3, REM = (RUN + 1) - 3 * NG;
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    double fc[3], A[3], B[3], C[3], KA[3], KB[3], KC[3], a[3], b[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int i = 3 * g + k + 2;
-      fc[k] = f[i];
-      A[k] = Dq(i - 1);
-      B[k] = Dq(i);
-      C[k] = Dq(i + 1);
-      KA[k] = Kq(i - 1);
-      KB[k] = Kq(i);
-      KC[k] = Kq(i + 1);
-      a[k] = f[i] - f[i - 1];
-      b[k] = f[i + 1] - f[i];
-    }
-    recon_roles3<LINEAR>(fc, A, B, C, KA, KB, KC, a, b, F + 3 * g);
-  }
-#pragma unroll
-  for (int k = 0; k < REM; ++k) {
-    const int i = 3 * NG + k + 2;
-    F[3 * NG + k] = recon_roles<LINEAR>(f[i], Dq(i - 1), Dq(i), Dq(i + 1), Kq(i - 1), Kq(i),
-                                        Kq(i + 1), f[i] - f[i - 1], f[i + 1] - f[i]);
-  }
+  recon_groups<0, RUN + 1, SGWG_P4_GS, LINEAR>(f, Dq, Kq, F);
   // reversed: interface t is the flux left of point RUN - t, so du(RUN - t) = (F[t-1] - F[t]) / h
   int ex = 0;  // max exponent field of the outputs (overflow guard)
   const double sh = rev ? -inv_h : inv_h;
