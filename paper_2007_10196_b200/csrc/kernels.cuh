@@ -601,9 +601,9 @@ __global__ void __launch_bounds__(256) stage2d_kernel(const Stage2DParams p) {
 __device__ __forceinline__ double fast_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  r = fma(r, fma(-x, r, 1.0), r);
-  r = fma(r, fma(-x, r, 1.0), r);
-  return r;
+  // one third-order step from the ~2^-20 seed: r (1 + e + e^2), e = 1 - x r (error e^3)
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 // generic role form: A,B,C = D at the three substencil centres, a,b = the two

@@ -235,10 +235,14 @@ __device__ __forceinline__ void recon_rolesN(const double* fc, const double* A, 
   double r[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r[k]) : "d"(den[k]));
+  // one third-order step from the ~2^-20 seed: r (1 + e + e^2), e = 1 - den r (fast_rcp)
+  double e[N];
 #pragma unroll
-  for (int k = 0; k < N; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
+  for (int k = 0; k < N; ++k) e[k] = fma(-den[k], r[k], 1.0);
 #pragma unroll
-  for (int k = 0; k < N; ++k) r[k] = fma(r[k], fma(-den[k], r[k], 1.0), r[k]);
+  for (int k = 0; k < N; ++k) e[k] = fma(e[k], e[k], e[k]);
+#pragma unroll
+  for (int k = 0; k < N; ++k) r[k] = fma(r[k], e[k], r[k]);
 #pragma unroll
   for (int k = 0; k < N; ++k) F[k] = fc[k] + num[k] * r[k];
 }
@@ -279,7 +283,8 @@ __device__ __noinline__ void adv_run_masked(const double* __restrict__ P, int st
   double f[NV];
   load_window_dir<RUN, ZERO>(f, P, st, wrap, gl, gr, c, rev);
   const double eps4 = 4.0 * eps;
-  auto Dq = [&](int q) { return fma(-2.0, f[q], f[q - 1] + f[q + 1]); };
+  // second difference as the difference of the first differences (shared with a, b)
+  auto Dq = [&](int q) { return (f[q + 1] - f[q]) - (f[q] - f[q - 1]); };
   auto Kq = [&](int q) {
     const double d = Dq(q);
     return fma(13.0 / 3.0 * d, d, eps4);

@@ -1,6 +1,5 @@
 set -u
-O=gpurun_out/r4e; mkdir -p $O
-echo "== gs 3"; timeout 120 python tools/profile_c5.py C5 0.02 > $O/kprof_3.json 2>&1; grep -A8 '"name"' $O/kprof_3.json | grep "avg_us"
-for g in 2 4 5; do
-echo "== gs $g"; SGWG_LIB=$PWD/tracelib/libsgwg_gs$g.so timeout 120 python tools/profile_c5.py C5 0.02 > $O/kprof_$g.json 2>&1; grep -A8 '"name"' $O/kprof_$g.json | grep "avg_us"
-done
+O=gpurun_out/r4f; mkdir -p $O
+timeout 120 python tools/profile_c5.py C5 0.02 > $O/kprof.json 2>&1; echo "rc=$?"; grep -A8 '"name"' $O/kprof.json | grep "name\|avg_us"
+timeout 900 python -m pytest tests/test_gpu_vp.py tests/test_gpu_hardening.py tests/test_gpu_fast.py -x -q -m gpu > $O/pytest_vp.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_vp.log
+timeout 600 python -m pytest tests/test_gpu_fullsize_parity.py -x -q -m gpu > $O/pytest_full.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_full.log
