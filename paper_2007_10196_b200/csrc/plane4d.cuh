@@ -154,12 +154,12 @@ __device__ __noinline__ void adv_run_ref_masked(const double* __restrict__ P, in
 // positive reconstruction of the reversed line, weno.hpp:178-183, so only the addressing
 // depends on the direction -- per lane, no divergent branch when the lines of a warp
 // differ in sign).
-template <int RUN, bool ZERO>
+template <int RUN, bool ZERO, int Q0 = 0, int Q1 = RUN + 6>
 __device__ __forceinline__ void load_window_dir(double* f, const double* __restrict__ P, int st,
                                                 int wrap, int gl, int gr, double c, bool rev) {
   constexpr int NV = RUN + 6;
 #pragma unroll
-  for (int q = 0; q < NV; ++q) {
+  for (int q = Q0; q < Q1; ++q) {
     // physical window position of upwind position q: q or NV - 1 - q; only the three
     // positions at each end can be ghosts
     const bool endl = (q < 3), endr = (q >= NV - 3);
@@ -251,6 +251,7 @@ __device__ __forceinline__ void recon_rolesN(const double* fc, const double* A, 
 #ifndef SGWG_P4_GS
 #define SGWG_P4_GS 3
 #endif
+
 template <int T0, int NLEFT, int GS, bool LINEAR, class DQ, class KQ>
 __device__ __forceinline__ void recon_groups(const double* f, DQ Dq, KQ Kq, double* F) {
   if constexpr (NLEFT > 0) {
@@ -281,7 +282,6 @@ __device__ __noinline__ void adv_run_masked(const double* __restrict__ P, int st
   constexpr int NV = RUN + 6;
   const bool rev = c < 0.0;
   double f[NV];
-  load_window_dir<RUN, ZERO>(f, P, st, wrap, gl, gr, c, rev);
   const double eps4 = 4.0 * eps;
   // second difference as the difference of the first differences (shared with a, b)
   auto Dq = [&](int q) { return (f[q + 1] - f[q]) - (f[q] - f[q - 1]); };
@@ -289,17 +289,21 @@ __device__ __noinline__ void adv_run_masked(const double* __restrict__ P, int st
     const double d = Dq(q);
     return fma(13.0 / 3.0 * d, d, eps4);
   };
-  // interface t (left point i = t + 2 of the upwind-ordered window) -> F[t]
+  // interface t (left point i = t + 2 of the upwind-ordered window) -> F[t]; the upwind
+  // reconstructions of interfaces 0 .. RUN read window positions 0 .. RUN + 4 only
   double F[RUN + 1];
-  recon_groups<0, RUN + 1, SGWG_P4_GS, LINEAR>(f, Dq, Kq, F);
-  // reversed: interface t is the flux left of point RUN - t, so du(RUN - t) = (F[t-1] - F[t]) / h
   int ex = 0;  // max exponent field of the outputs (overflow guard)
   const double sh = rev ? -inv_h : inv_h;
+  // reversed: interface t is the flux left of point RUN - t, so du(RUN - t) = (F[t-1] - F[t]) / h
+  {
+    load_window_dir<RUN, ZERO, 0, RUN + 5>(f, P, st, wrap, gl, gr, c, rev);
+    recon_groups<0, RUN + 1, SGWG_P4_GS, LINEAR>(f, Dq, Kq, F);
 #pragma unroll
-  for (int t = 1; t <= RUN; ++t) {
-    const double du = (F[t] - F[t - 1]) * sh;
-    ex = max(ex, __double2hiint(du) & 0x7ff00000);
-    out[(rev ? RUN - t : t - 1) * ost] = du;
+    for (int t = 1; t <= RUN; ++t) {
+      const double du = (F[t] - F[t - 1]) * sh;
+      ex = max(ex, __double2hiint(du) & 0x7ff00000);
+      out[(rev ? RUN - t : t - 1) * ost] = du;
+    }
   }
   if (ex == 0x7ff00000)
     adv_run_ref_masked<RUN, ZERO, LINEAR>(P, st, wrap, gl, gr, c, eps, inv_h, out, ost);
