@@ -656,22 +656,22 @@ __device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
     fp[q] = sc * P[(p0 + (rev ? NV - 1 - q : q)) * st];
     if (BURGERS) fm[q] = Mv[(p0 + q) * st];
   }
-  auto Dof = [](const double* f, int q) { return fma(-2.0, f[q], f[q - 1] + f[q + 1]); };
+  // second differences from the first differences they share a, b with
   auto Kof = [&](double Dq) { return fma(13.0 / 3.0 * Dq, Dq, eps4); };
   double Dp[NV], Kp[NV], dp[NV], Dm[NV], Km[NV], dm[NV];
-#pragma unroll
-  for (int q = 1; q < NV - 1; ++q) {
-    Dp[q] = Dof(fp, q);
-    Kp[q] = Kof(Dp[q]);
-    if (BURGERS) {
-      Dm[q] = Dof(fm, q);
-      Km[q] = Kof(Dm[q]);
-    }
-  }
 #pragma unroll
   for (int q = 1; q < NV; ++q) {
     dp[q] = fp[q] - fp[q - 1];
     if (BURGERS) dm[q] = fm[q] - fm[q - 1];
+  }
+#pragma unroll
+  for (int q = 1; q < NV - 1; ++q) {
+    Dp[q] = dp[q + 1] - dp[q];
+    Kp[q] = Kof(Dp[q]);
+    if (BURGERS) {
+      Dm[q] = dm[q + 1] - dm[q];
+      Km[q] = Kof(Dm[q]);
+    }
   }
   double fprev = 0.0;
 #pragma unroll
