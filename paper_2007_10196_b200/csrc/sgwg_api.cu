@@ -1570,7 +1570,8 @@ int build_plane4_tiles(sgwg_family* f) {
   // persistent v pass (SGWG_P4_PERSIST, default on): six tile slots per CTA, two CTAs per SM
   bool persist = true;
   if (const char* e = std::getenv("SGWG_P4_PERSIST")) persist = (e[0] != '0');
-  int vtarget = persist ? 2300 : 2400;
+  // (2,330: two planes of the 9 x 129 / 17 x 65 / 33 x 33 shapes -- 2 x 1,161 points -- fit)
+  int vtarget = persist ? 2330 : 2400;
   if (const char* e = std::getenv("SGWG_P4_VTARGET")) vtarget = std::max(64, std::atoi(e));
   int xtarget = 4096;
   if (const char* e = std::getenv("SGWG_P4_XTARGET")) xtarget = std::max(128, std::atoi(e));
