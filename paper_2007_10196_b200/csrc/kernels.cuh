@@ -95,7 +95,7 @@ __device__ __forceinline__ double warp_max(double v) {
 #ifndef SGWG_SWEEP_ATTR
 #define SGWG_SWEEP_ATTR __noinline__
 #endif
-template <bool BURGERS, int RUN, bool LINEAR>
+template <bool BURGERS, int RUN, bool LINEAR, bool NEWTON = false>
 __device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
                                        const double* __restrict__ Mv, int st, int p0, double c,
                                        double eps4, double inv_h, double* __restrict__ out,
@@ -598,9 +598,19 @@ __global__ void __launch_bounds__(256) stage2d_kernel(const Stage2DParams p) {
 // reconstruction (rcp.approx + Newton).  Rounding differs from the reference
 // at the 1e-16 level; the parity bar for this build is 1e-10.
 
+// NEWTON: two Newton steps (4 DFMA) instead of one third-order step (3 DFMA) -- measured
+// faster in the Burgers stage kernel of large families (S2 evolve 25.8 vs 27.3 ms), slower
+// everywhere else (C2 persistent 34.3 vs 33.5 ms, C3 144.3 vs 143.3 ms, the C5 planes, the
+// combination).
+template <bool NEWTON = false>
 __device__ __forceinline__ double fast_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  if (NEWTON) {
+    r = fma(r, fma(-x, r, 1.0), r);
+    r = fma(r, fma(-x, r, 1.0), r);
+    return r;
+  }
   // one third-order step from the ~2^-20 seed: r (1 + e + e^2), e = 1 - x r (error e^3)
   const double e = fma(-x, r, 1.0);
   return fma(r, fma(e, e, e), r);
@@ -608,7 +618,7 @@ __device__ __forceinline__ double fast_rcp(double x) {
 
 // generic role form: A,B,C = D at the three substencil centres, a,b = the two
 // first differences, fc = centre value; returns the reconstruction.
-template <bool LINEAR>
+template <bool LINEAR, bool NEWTON = false>
 __device__ __forceinline__ double recon_roles(double fc, double A, double B, double C, double KA,
                                               double KB, double KC, double a, double b) {
   const double g0 = fma(2.0, a, A);
@@ -625,7 +635,7 @@ __device__ __forceinline__ double recon_roles(double fc, double A, double B, dou
   const double w2 = (3.0 * q0) * q1;
   const double num = fma(w0, c0, fma(w1, c1, w2 * c2));
   const double den = 6.0 * (w0 + w1 + w2);
-  return fc + num * fast_rcp(den);
+  return fc + num * fast_rcp<NEWTON>(den);
 }
 
 // du = (F(i+1/2) - F(i-1/2)) / h for RUN consecutive points of one line held
@@ -635,7 +645,7 @@ __device__ __forceinline__ double recon_roles(double fc, double A, double B, dou
 // Not inlined: one copy of the (large, fully unrolled) line sweep serves the
 // x and y sweeps of every tile shape, keeping the hot code in the i-cache.
 // du[t] is written to out[t * ost] (shared memory).
-template <bool BURGERS, int RUN, bool LINEAR>
+template <bool BURGERS, int RUN, bool LINEAR, bool NEWTON = false>
 __device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
                                           const double* __restrict__ Mv, int st, int p0,
                                           double c, double eps4, double inv_h,
@@ -666,10 +676,12 @@ __device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
   }
 #pragma unroll
   for (int q = 1; q < NV - 1; ++q) {
-    Dp[q] = dp[q + 1] - dp[q];
+    // (NEWTON -- the Burgers stage kernel of large families -- keeps the direct form: with
+    // both splittings' differences live first it was 8 % slower on S2)
+    Dp[q] = NEWTON ? fma(-2.0, fp[q], fp[q - 1] + fp[q + 1]) : dp[q + 1] - dp[q];
     Kp[q] = Kof(Dp[q]);
     if (BURGERS) {
-      Dm[q] = dm[q + 1] - dm[q];
+      Dm[q] = NEWTON ? fma(-2.0, fm[q], fm[q - 1] + fm[q + 1]) : dm[q + 1] - dm[q];
       Km[q] = Kof(Dm[q]);
     }
   }
@@ -677,11 +689,11 @@ __device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
 #pragma unroll
   for (int t = 0; t <= RUN; ++t) {
     const int i = t + 2, m = t + 3;
-    double F = recon_roles<LINEAR>(fp[i], Dp[i - 1], Dp[i], Dp[i + 1], Kp[i - 1], Kp[i],
-                                   Kp[i + 1], dp[i], dp[i + 1]);
+    double F = recon_roles<LINEAR, NEWTON>(fp[i], Dp[i - 1], Dp[i], Dp[i + 1], Kp[i - 1], Kp[i],
+                                           Kp[i + 1], dp[i], dp[i + 1]);
     if (BURGERS)
-      F += recon_roles<LINEAR>(fm[m], Dm[m + 1], Dm[m], Dm[m - 1], Km[m + 1], Km[m], Km[m - 1],
-                               -dm[m + 1], -dm[m]);
+      F += recon_roles<LINEAR, NEWTON>(fm[m], Dm[m + 1], Dm[m], Dm[m - 1], Km[m + 1], Km[m],
+                                       Km[m - 1], -dm[m + 1], -dm[m]);
     if (t > 0) {
       // reversed: step t yields the flux left of padded point RUN+3-t, so
       // du(local RUN-t) = (F_{t-1} - F_t) / h
@@ -847,23 +859,26 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   __syncthreads();
   if (PERSIST) SGWG_MARK(p.trace_ss, 1);
   const double eps4 = 4.0 * p.eps;
+  // reciprocal form of the reconstructions (fast_rcp): Newton steps in the Burgers stage
+  // kernel of large families, the third-order step in the latency-bound persistent kernel
+  constexpr bool NWT = BURGERS && !PERSIST;
   if (tid < NS) {  // x-sweep warps: thread = (column j, run of RUN rows)
     const int j = tid % TY, r = tid / TY;
     const double c = BURGERS ? 0.0 : cx[j];
     if (p.linear)
-      sweep_run<BURGERS, RUN, true>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
+      sweep_run<BURGERS, RUN, true, NWT>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
                                     eps4, M->inv_h[0], DX + r * RUN * DP + j, DP);
     else
-      sweep_run<BURGERS, RUN, false>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
+      sweep_run<BURGERS, RUN, false, NWT>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
                                      eps4, M->inv_h[0], DX + r * RUN * DP + j, DP);
   } else {  // y-sweep warps: thread = (row i, run of RUN columns)
     const int i = (tid - NS) % TX, r = (tid - NS) / TX;
     const double c = BURGERS ? 0.0 : cy[i];
     if (p.linear)
-      sweep_run<BURGERS, RUN, true>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
+      sweep_run<BURGERS, RUN, true, NWT>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
                                     r * RUN, c, eps4, M->inv_h[1], DY + i * DP + r * RUN, 1);
     else
-      sweep_run<BURGERS, RUN, false>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
+      sweep_run<BURGERS, RUN, false, NWT>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
                                      r * RUN, c, eps4, M->inv_h[1], DY + i * DP + r * RUN, 1);
   }
   __syncthreads();
