@@ -352,47 +352,37 @@ __device__ __noinline__ void adv_run_kout(const double* __restrict__ P, int st, 
                                           const double* __restrict__ d1, int ost,
                                           double* __restrict__ gout, long long gst) {
   constexpr int RUN = 8, NV = RUN + 6;
+  const bool rev = c < 0.0;
   double f[NV];
-  load_window_masked<RUN, false>(f, P, st, wrap, gl, gr, c);
+  load_window_dir<RUN, false, 0, RUN + 5>(f, P, st, wrap, gl, gr, c, rev);
   const double eps4 = 4.0 * eps;
-  double D[NV], K[NV], dd[NV];
-#pragma unroll
-  for (int q = 1; q < NV - 1; ++q) {
-    D[q] = fma(-2.0, f[q], f[q - 1] + f[q + 1]);
-    K[q] = fma(13.0 / 3.0 * D[q], D[q], eps4);
-  }
-#pragma unroll
-  for (int q = 1; q < NV; ++q) dd[q] = f[q] - f[q - 1];
+  auto Dq = [&](int q) { return (f[q + 1] - f[q]) - (f[q] - f[q - 1]); };
+  auto Kq = [&](int q) {
+    const double d = Dq(q);
+    return fma(13.0 / 3.0 * d, d, eps4);
+  };
+  double F[RUN + 1];
+  recon_groups<0, RUN + 1, SGWG_P4_GS, LINEAR>(f, Dq, Kq, F);
+  // du of point k of the run (adv_run_masked: reversed, interface t is left of point RUN - t)
   double du[RUN];
-  double Fp = 0.0;
+  const double sh = rev ? -inv_h : inv_h;
   int ex = 0;
-  if (!(c < 0.0)) {
 #pragma unroll
-    for (int t = 0; t <= RUN; ++t) {
-      const int i = t + 2;
-      const double F = recon_roles<LINEAR>(f[i], D[i - 1], D[i], D[i + 1], K[i - 1], K[i],
-                                           K[i + 1], dd[i], dd[i + 1]);
-      if (t > 0) du[t - 1] = (F - Fp) * inv_h;
-      Fp = F;
-    }
-  } else {
-#pragma unroll
-    for (int t = 0; t <= RUN; ++t) {
-      const int m = t + 3;
-      const double F = recon_roles<LINEAR>(f[m], D[m + 1], D[m], D[m - 1], K[m + 1], K[m],
-                                           K[m - 1], -dd[m + 1], -dd[m]);
-      if (t > 0) du[t - 1] = (F - Fp) * inv_h;
-      Fp = F;
-    }
+  for (int t = 1; t <= RUN; ++t) {
+    const double v = (F[t] - F[t - 1]) * sh;
+    ex = max(ex, __double2hiint(v) & 0x7ff00000);
+    du[t - 1] = v;
   }
-#pragma unroll
-  for (int t = 0; t < RUN; ++t) ex = max(ex, __double2hiint(du[t]) & 0x7ff00000);
   if (ex == 0x7ff00000) {
     adv_run_kout_ref<LINEAR>(P, st, wrap, gl, gr, c, eps, inv_h, d1, ost, gout, gst);
     return;
   }
+  // du[t - 1] belongs to point rev ? RUN - t : t - 1
 #pragma unroll
-  for (int t = 0; t < RUN; ++t) gout[t * gst] = (0.0 - d1[t * ost]) - du[t];
+  for (int t = 0; t < RUN; ++t) {
+    const int k = rev ? RUN - 1 - t : t;
+    gout[k * gst] = (0.0 - d1[k * ost]) - du[t];
+  }
 }
 
 // ---------------------------------------------------------------------------
