@@ -645,7 +645,7 @@ __device__ __forceinline__ double recon_roles(double fc, double A, double B, dou
 // Not inlined: one copy of the (large, fully unrolled) line sweep serves the
 // x and y sweeps of every tile shape, keeping the hot code in the i-cache.
 // du[t] is written to out[t * ost] (shared memory).
-template <bool BURGERS, int RUN, bool LINEAR, bool NEWTON = false>
+template <bool BURGERS, int RUN, bool LINEAR, bool NEWTON>
 __device__ SGWG_SWEEP_ATTR void sweep_run(const double* __restrict__ P,
                                           const double* __restrict__ Mv, int st, int p0,
                                           double c, double eps4, double inv_h,
