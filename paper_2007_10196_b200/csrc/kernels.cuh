@@ -859,27 +859,46 @@ __device__ __forceinline__ void stage2d_fast_body(const Stage2DParams& p, const 
   __syncthreads();
   if (PERSIST) SGWG_MARK(p.trace_ss, 1);
   const double eps4 = 4.0 * p.eps;
-  // reciprocal form of the reconstructions (fast_rcp): Newton steps in the Burgers stage
-  // kernel of large families, the third-order step in the latency-bound persistent kernel
-  constexpr bool NWT = BURGERS && !PERSIST;
+  // Arithmetic form of the reconstructions (fast_rcp / second differences): a property of
+  // the FAMILY (p.newton: Burgers families too large for the persistent kernel), not of the
+  // kernel -- the stage kernel and the persistent kernel of one family stay bitwise equal
+  // (a sharded small family runs the stage kernel: option B compares it with the
+  // unsharded run).
+  const bool nw = BURGERS && !PERSIST && p.newton;
   if (tid < NS) {  // x-sweep warps: thread = (column j, run of RUN rows)
     const int j = tid % TY, r = tid / TY;
     const double c = BURGERS ? 0.0 : cx[j];
-    if (p.linear)
-      sweep_run<BURGERS, RUN, true, NWT>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
-                                    eps4, M->inv_h[0], DX + r * RUN * DP + j, DP);
-    else
-      sweep_run<BURGERS, RUN, false, NWT>(FP + j + 3, (BURGERS ? FM : FP) + j + 3, PY, r * RUN, c,
-                                     eps4, M->inv_h[0], DX + r * RUN * DP + j, DP);
+    const double* P = FP + j + 3;
+    const double* Mv = (BURGERS ? FM : FP) + j + 3;
+    double* o = DX + r * RUN * DP + j;
+    if (p.linear) {
+      if (nw)
+        sweep_run<BURGERS, RUN, true, true>(P, Mv, PY, r * RUN, c, eps4, M->inv_h[0], o, DP);
+      else
+        sweep_run<BURGERS, RUN, true, false>(P, Mv, PY, r * RUN, c, eps4, M->inv_h[0], o, DP);
+    } else {
+      if (nw)
+        sweep_run<BURGERS, RUN, false, true>(P, Mv, PY, r * RUN, c, eps4, M->inv_h[0], o, DP);
+      else
+        sweep_run<BURGERS, RUN, false, false>(P, Mv, PY, r * RUN, c, eps4, M->inv_h[0], o, DP);
+    }
   } else {  // y-sweep warps: thread = (row i, run of RUN columns)
     const int i = (tid - NS) % TX, r = (tid - NS) / TX;
     const double c = BURGERS ? 0.0 : cy[i];
-    if (p.linear)
-      sweep_run<BURGERS, RUN, true, NWT>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
-                                    r * RUN, c, eps4, M->inv_h[1], DY + i * DP + r * RUN, 1);
-    else
-      sweep_run<BURGERS, RUN, false, NWT>(FP + (i + 3) * PY, (BURGERS ? FM : FP) + (i + 3) * PY, 1,
-                                     r * RUN, c, eps4, M->inv_h[1], DY + i * DP + r * RUN, 1);
+    const double* P = FP + (i + 3) * PY;
+    const double* Mv = (BURGERS ? FM : FP) + (i + 3) * PY;
+    double* o = DY + i * DP + r * RUN;
+    if (p.linear) {
+      if (nw)
+        sweep_run<BURGERS, RUN, true, true>(P, Mv, 1, r * RUN, c, eps4, M->inv_h[1], o, 1);
+      else
+        sweep_run<BURGERS, RUN, true, false>(P, Mv, 1, r * RUN, c, eps4, M->inv_h[1], o, 1);
+    } else {
+      if (nw)
+        sweep_run<BURGERS, RUN, false, true>(P, Mv, 1, r * RUN, c, eps4, M->inv_h[1], o, 1);
+      else
+        sweep_run<BURGERS, RUN, false, false>(P, Mv, 1, r * RUN, c, eps4, M->inv_h[1], o, 1);
+    }
   }
   __syncthreads();
   if (PERSIST) SGWG_MARK(p.trace_ss, 2);

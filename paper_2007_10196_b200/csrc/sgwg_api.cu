@@ -775,6 +775,9 @@ int launch_stage(sgwg_family* f, int stage, const StageBufs& b, bool timed, bool
       smem = (size_t)f->smem2d_half * sizeof(double);
     }
     p.burgers = burgers;
+    // large Burgers families (never co-resident: no persistent kernel) take the Newton /
+    // direct-difference form of the reconstructions (fast_rcp); a property of the family
+    p.newton = (burgers && f->total > (1LL << 21)) ? 1 : 0;
     p.flux0 = order[0].flux;
     p.flux1 = order[1].flux;
     p.c0 = order[0].c_const;

@@ -147,6 +147,7 @@ struct Stage2DParams {
   int resident_load;  // first stage of the launch: fill the resident copy from HBM
   int trace_ss;       // step * 3 + stage - 1 (phase-trace experiment builds)
   int half_tiles;     // fast stage kernel on 1024-point tiles (two CTAs per SM)
+  int newton;         // Burgers families too large for the persistent kernel: fast_rcp<NEWTON> form
 };
 
 struct PersistParams {
