@@ -44,17 +44,36 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _digest(deps, cmd):
+    """Content hash of a unit's sources and command line (file times are not trusted: an
+    object that looked fresh once hid a source change from the GPU runs)."""
+    import hashlib
+    h = hashlib.sha256(" ".join(cmd).encode())
+    for d in deps:
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def _compile(src, flags, verbose):
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(ROOT, "include", "sgwg.h"), __file__]
-    if not _stale(obj, deps):
-        return obj, ""
     cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + COMMON + flags
+    want = _digest(deps, cmd)
+    stamp = obj + ".sha256"
+    if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read().strip() == want:
+        return obj, "", False
+    if os.path.exists(stamp):
+        os.remove(stamp)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
+        if os.path.exists(obj):
+            os.remove(obj)
         raise RuntimeError(f"nvcc failed for {src}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-    return obj, (r.stdout + r.stderr) if verbose else ""
+    with open(stamp, "w") as f:
+        f.write(want)
+    return obj, (r.stdout + r.stderr) if verbose else "", True
 
 
 def build(verbose: bool = False) -> str:
@@ -63,11 +82,11 @@ def build(verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
         futs = [ex.submit(_compile, s, f, verbose) for s, f in UNITS.items()]
         results = [f.result() for f in futs]
-    objs = [o for o, _ in results]
-    for _, log in results:
+    objs = [o for o, _, _ in results]
+    for _, log, _ in results:
         if log:
             sys.stdout.write(log)
-    if _stale(LIB, objs):
+    if any(c for _, _, c in results) or _stale(LIB, objs):
         cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + ["-lnccl", "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
